@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 balance-and-redistribute path (KnapFormer, arXiv 2508.06001).
+
+One step = one pass of the hot path over one batch of the synthetic stream:
+  plan_routing (device knapsack planner) -> route (forward all-to-all) ->
+  pre_attn + post_attn (Ulysses seq<->head all-to-all, every multi-GPU bag) ->
+  reverse_route (reverse all-to-all restoring the original packing).
+Rows carry 6144 B of payload (== 3072 bf16 hidden == 768 reference doubles)
+plus the reference's 16 B {sample_id, position} metadata.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  `value` is device-timed with inputs resident
+in HBM; `e2e` times the same step through the C-ABI with pinned HOST buffers
+(H2D of metadata + world image, D2H of the restored world inside the timed
+region).  `--impl reference` times the unmodified reference C++ library
+(oracle/_ref/ref_harness, built from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "balanced tokens/s + all-to-all GB/s at 1/2/4/8 B200; max/mean load ratio"
+C2_CODES = ["g2b8i256f1s0", "g2b4i512f1s0", "g2b2i768f1s0", "g2b1i1024f1s0"]
+C3_CODES = ["g1b1i1024f51s1", "g1b1i512f85s1", "g2b2i512f1s0", "g2b4i256f1s0", "g2b1i1024f1s0"]
+PAYLOAD_BYTES = 6144  # 3072 x bf16 per token row (== 768 doubles in the reference)
+META_BYTES = 16       # {sample_id u64, position i64} per row (exchange.hpp:28-29)
+
+CONFIGS = {
+    "c2": dict(workload="C2: FLUX-like mixed-resolution stream (data_sim g2b8i256f1s0,g2b4i512f1s0,"
+                        "g2b2i768f1s0,g2b1i1024f1s0; T5 text U[0,392]), 8 ranks, bags of 1 and 2 "
+                        "(g1n4+g2n2), hidden 3072 bf16 rows + 16 B position metadata",
+               world=8, topology="g1n4+g2n2", meta=dict(kind="scenario", codes=C2_CODES, step=0, seed=7)),
+    "c1": dict(workload="C1: 8 ranks x 32 seqs, text U[64,512] + image U[256,4096], g1n8, hidden 3072 bf16",
+               world=8, topology="g1n8", meta=dict(kind="c1", seed=1, step=0, per_rank=32)),
+    "c3": dict(workload="C3: image-video joint stream (<=64K-token videos), bags of 4 (g4n2), 24x128 heads",
+               world=8, topology="g4n2", meta=dict(kind="scenario", codes=C3_CODES, step=0, seed=7)),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--topology", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    def __init__(self, index=0, period=0.01):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.period = period
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or
+                 k.startswith("nvmlClocksThrottleReason")}
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80, "sync_boost": 0x10,
+                "applications_clocks_setting": 0x2, "gpu_idle": 0x1}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, b in bits.items():
+                    if r & b and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+        del names
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ---------------------------------------------------------- reference arm
+def ref_case(cfg, topology, steps, warmup, budget_s):
+    return {"world": cfg["world"], "topology": topology, "model": {},
+            "meta": dict(cfg["meta"], group_size=cfg["world"]) if cfg["meta"]["kind"] == "scenario" else cfg["meta"],
+            "payload_width": PAYLOAD_BYTES // 8, "steps": steps, "warmup": warmup, "budget_s": budget_s,
+            "ulysses": True}
+
+
+def run_reference(cfg, topology, steps, warmup, budget_s, threads=None):
+    """Time the unmodified reference CPU path (oracle/_ref/ref_harness)."""
+    harness = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+    env = dict(os.environ)
+    nthreads = threads or os.cpu_count() or 1
+    env["OMP_NUM_THREADS"] = str(nthreads)
+    if os.path.exists(harness):
+        p = subprocess.run([harness, "bench"], input=json.dumps(ref_case(cfg, topology, steps, warmup, budget_s)).encode(),
+                           capture_output=True, env=env, timeout=1800)
+        if p.returncode == 0:
+            d = json.loads(p.stdout)
+            d["kind"] = "reference"
+            d["cores"] = int(d.get("threads", nthreads))
+            return d
+        err = p.stderr.decode()[-300:]
+    else:
+        err = "oracle/_ref/ref_harness not built"
+    return {"unavailable": err}
+
+
+# ------------------------------------------------------------ our arm
+def main():
+    args = parse_args()
+    cfg = CONFIGS[args.config]
+    topology = args.topology or cfg["topology"]
+    rank = int(os.environ.get("RANK", "0"))
+    world_procs = int(os.environ.get("WORLD_SIZE", "1"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        r = run_reference(cfg, topology, args.steps, args.warmup, budget_s=120.0)
+        if "unavailable" in r:
+            print(json.dumps({"impl": "reference", "unavailable": r["unavailable"]}))
+            return 0
+        line = {"impl": "reference", "metric": METRIC, "value": r["tokens_per_s"], "unit": "tokens/s",
+                "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
+                "ms_per_step": 1000 * r["s_per_step"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": cfg["world"]},
+                "cpu_baseline": {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"],
+                                 "kind": "reference",
+                                 "sample": f"{r['steps']} full steps of the config (budget-bounded), "
+                                           "payload 768 doubles/row == 6144 B"},
+                "e2e": {"value": r["tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "phases_s": {k: r[k] for k in ("plan_s", "route_s", "ulysses_s", "reverse_s")}}
+        print(json.dumps(line))
+        return 0
+
+    import numpy as np
+    import torch
+
+    import paper_2508_06001_b200 as sb
+    from paper_2508_06001_b200 import datagen
+
+    if world_procs > 1:
+        from paper_2508_06001_b200 import multigpu
+        return multigpu.bench_main(args, cfg, topology, METRIC)
+
+    torch.cuda.set_device(0)
+    W = cfg["world"]
+    ids, lens = datagen.metadata(cfg["meta"]["kind"], W, **{k: v for k, v in cfg["meta"].items() if k != "kind"})
+    tokens = int(sum(int(l.sum()) for l in lens))
+    n_seqs = int(sum(len(l) for l in lens))
+    dm = sb.DeviceMeta.from_lists(ids, lens)
+    planner = sb.Planner(topology, W, max_seqs=max(n_seqs, 1))
+    G = planner.max_bag
+    mk = lambda: sb.World(W, 24, [PAYLOAD_BYTES], capacity_rows=tokens, max_bag=G)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        planner.plan(dm)
+        sb.route(planner, A, B)
+        if planner.topology.bag_sizes and max(planner.topology.bag_sizes) > 1:
+            sb.pre_attn(planner, B, Cw)
+            sb.post_attn(planner, Cw, D)
+            sb.reverse_route(planner, D, E)
+        else:
+            sb.reverse_route(planner, B, E)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    E.status()
+    # correctness of what we time: E == A byte for byte
+    for r in range(W):
+        assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r)), "round trip not bit-exact"
+    hp = planner.download()
+    per = hp.per_gpu_workload
+    max_mean = float(per.max() / per.mean()) if per.mean() > 0 else 1.0
+
+    # ---- device-timed steps (inputs resident in HBM; worlds >> 126 MB L2)
+    planner.enable_timing(True)
+    planner.copy_timing_reset()
+    launches0 = sb.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler() as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = sb.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    ms_per_step = ms / args.steps
+    n_route, us_route = planner.copy_timing(0)
+    n_rev, us_rev = planner.copy_timing(1)
+    n_pre, us_pre = planner.copy_timing(2)
+    n_post, us_post = planner.copy_timing(3)
+    planner.enable_timing(False)
+    planner.copy_timing_reset()
+
+    # plan latency alone (device events)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(20):
+        planner.plan(dm)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    plan_us = 1000 * t0.elapsed_time(t1) / 20
+
+    row_bytes = PAYLOAD_BYTES + META_BYTES
+    route_bytes = 2 * tokens * row_bytes  # every row read once and written once (out-of-place)
+    hbm_peak, peak_kind = load_peaks()
+    route_kernel_us = us_route / max(1, n_route)
+    achieved = route_bytes / (route_kernel_us * 1e-6) / 1e9
+    # Ulysses: rows of multi-GPU bags; metadata replicated to every member
+    multi = [b for b in planner.topology.bag_sizes]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        if pj.get("config") == args.config:
+            traffic = pj.get("route_copy_dram_bytes")
+
+    # ---- e2e through the C-ABI with pinned host buffers
+    host_meta = torch.empty(tokens * META_BYTES, dtype=torch.uint8, pin_memory=True)
+    host_pay = torch.empty(tokens * PAYLOAD_BYTES, dtype=torch.uint8, pin_memory=True)
+    out_meta = torch.empty_like(host_meta)
+    out_pay = torch.empty_like(host_pay)
+    A.download([host_meta.data_ptr(), host_pay.data_ptr()], [host_meta.numel(), host_pay.numel()])
+    torch.cuda.synchronize()
+    flat_ids = np.concatenate(ids).view(np.int64)
+    flat_lens = np.concatenate(lens)
+    off = np.zeros(W + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in ids])
+    h_ids = torch.from_numpy(flat_ids.copy()).pin_memory()
+    h_lens = torch.from_numpy(flat_lens.copy()).pin_memory()
+    h_off = torch.from_numpy(off).pin_memory()
+    A2 = mk()
+    e2e_meta = sb.DeviceMeta.from_lists(ids, lens)
+    h2d = host_meta.numel() + host_pay.numel() + 8 * (len(flat_ids) * 2 + W + 1)
+    d2h = out_meta.numel() + out_pay.numel()
+
+    def e2e_step():
+        e2e_meta.ids.copy_(h_ids, non_blocking=True)
+        e2e_meta.lens.copy_(h_lens, non_blocking=True)
+        e2e_meta.rank_off.copy_(h_off, non_blocking=True)
+        A2.layout_origin(e2e_meta)
+        A2.upload([host_meta.data_ptr(), host_pay.data_ptr()], [host_meta.numel(), host_pay.numel()])
+        planner.plan(e2e_meta)
+        sb.route(planner, A2, B)
+        if max(planner.topology.bag_sizes) > 1:
+            sb.pre_attn(planner, B, Cw)
+            sb.post_attn(planner, Cw, D)
+            sb.reverse_route(planner, D, E)
+        else:
+            sb.reverse_route(planner, B, E)
+        E.download([out_meta.data_ptr(), out_pay.data_ptr()], [out_meta.numel(), out_pay.numel()])
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    assert torch.equal(out_pay, host_pay) and torch.equal(out_meta, host_meta), "e2e round trip not bit-exact"
+    e2e_steps = max(3, min(args.steps, 50))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+
+    line = {
+        "metric": METRIC, "value": tokens / (ms_per_step * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": W, "tokens_per_step": tokens,
+                   "sequences": n_seqs, "row_bytes": row_bytes,
+                   "l2": "inputs larger than L2 (world payload %.0f MB per buffer > 126 MB)" % (
+                       tokens * PAYLOAD_BYTES / 1e6), "parallelism": "world of 8 ranks on 1 GPU"},
+        "max_mean": max_mean, "wir": hp.wir, "plan_us": plan_us,
+        "phases_us": {"route_copy": route_kernel_us, "reverse_copy": us_rev / max(1, n_rev),
+                      "pre_attn_copy": us_pre / max(1, n_pre), "post_attn_copy": us_post / max(1, n_post)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_copy (route)", "algorithmic_bytes_per_launch": route_bytes},
+        "a2a_gbs": None,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms},
+    }
+    if not args.no_cpu_baseline:
+        r = run_reference(cfg, topology, steps=1000, warmup=1, budget_s=args.cpu_budget_s)
+        if "unavailable" in r:
+            line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "unavailable": r["unavailable"]}
+        else:
+            line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"],
+                                    "kind": "reference",
+                                    "sample": f"{r['steps']} full C2 steps (~{args.cpu_budget_s:.0f} s budget), "
+                                              "reference plan_routing+route+pre/post_attn+reverse_route, "
+                                              "Exec::Parallel, 768 doubles/row"}
+    print(json.dumps(line))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

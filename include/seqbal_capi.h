@@ -1,0 +1,247 @@
+/*
+ * seqbal_capi.h -- C-ABI of libseqbal_cuda.so, the B200-native
+ * balance-and-redistribute path (KnapFormer, arXiv 2508.06001).
+ *
+ * Plain C: integers, pointers and sizes only; no CUDA, torch or C++ types in
+ * any signature (a stream is passed as an opaque pointer, i.e. a
+ * cudaStream_t).  Every call returns an sb_status; on failure
+ * sb_last_error() holds a thread-local message.  Status values mirror the
+ * reference's exception classes (/root/reference/proj/include/seqbal/error.hpp)
+ * and the CLI exit-code mapping (proj/tools/main.cpp:369-387):
+ *   SB_ERR_CONFIG    <-> ConfigError    (error.hpp:24-27)
+ *   SB_ERR_INTEGRITY <-> IntegrityError (error.hpp:31-34)
+ *   SB_ERR_PARSE     <-> ParseError     (error.hpp:10-21)
+ *
+ * The C++ host API in include/seqbal/*.hpp (same names and signatures as the
+ * reference headers) is layered on these entry points; INTEGRATION.md shows
+ * the binding a reference maintainer would add.
+ *
+ * Everything device-side is asynchronous and stream-ordered: a plan computed
+ * by sb_plan() lives in device memory owned by the planner and is consumed by
+ * sb_route()/sb_pre_attn()/... without a host round trip, so a whole step
+ * can be captured in one CUDA graph.  Only the *_download / *_status calls
+ * synchronise.
+ */
+#ifndef SEQBAL_CAPI_H
+#define SEQBAL_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SB_API __attribute__((visibility("default")))
+#else
+#define SB_API
+#endif
+
+typedef int sb_status;
+enum {
+  SB_OK = 0,
+  SB_ERR_CONFIG = 1,    /* ConfigError */
+  SB_ERR_INTEGRITY = 2, /* IntegrityError */
+  SB_ERR_PARSE = 3,     /* ParseError */
+  SB_ERR_CAPACITY = 4,  /* a caller-sized buffer/capacity was too small */
+  SB_ERR_CUDA = 5,      /* CUDA runtime failure (no device, launch failure, ...) */
+  SB_ERR_COMM = 6       /* peer-memory / multi-process exchange failure */
+};
+
+typedef void* sb_stream; /* cudaStream_t; NULL = legacy default stream */
+
+SB_API const char* sb_last_error(void);
+SB_API int sb_abi_version(void);
+/* Number of CUDA kernels this library has launched in this process (the
+ * bench's gpu_launches evidence). */
+SB_API int64_t sb_kernel_launches(void);
+
+/* ------------------------------------------------------------ planner -- */
+/* Replaces plan_routing / identity_plan / reverse_plan
+ * (proj/include/seqbal/balancer.hpp:95-104) and gamma_weighted_workload
+ * (workload_model.hpp:63).  One planner per (model, topology, world).       */
+typedef struct sb_planner sb_planner;
+
+typedef struct sb_planner_desc {
+  int world_size;            /* W: global ranks (WorldLayout::world_size)          */
+  int unit_size;             /* ranks per replica (Topology::unit_size)            */
+  int n_bags;                /* bags per replica (Topology::bags.size())           */
+  const int32_t* bag_offsets;/* host, n_bags+1: CSR into bag_ranks                 */
+  const int32_t* bag_ranks;  /* host, unit-local ranks of each bag (ComputeBag)    */
+  int d_model, n_heads, d_head, n_blocks; /* ModelShape (workload_model.hpp:13-24) */
+  double gamma;              /* WorkloadModel::gamma                               */
+  double k;                  /* WorkloadModel::k (validated only)                  */
+  int64_t max_seqs;          /* capacity: sequences over all ranks                 */
+} sb_planner_desc;
+
+/* Validates like WorkloadModel::validate (workload_model.cpp:15-31),
+ * replicate (topology.cpp:81-93) and plan_routing's head check
+ * (balancer.cpp:114-120); SB_ERR_CONFIG with the reference's message. */
+SB_API sb_status sb_planner_create(const sb_planner_desc* desc, sb_planner** out);
+SB_API sb_status sb_planner_destroy(sb_planner* p);
+
+/* Metadata all-gather result in gather order (exchange.cpp:68-77): rank r's
+ * sequences are [rank_off[r], rank_off[r+1]).  All three arrays are DEVICE
+ * pointers.  Computes the plan on the device (no host synchronisation). */
+SB_API sb_status sb_plan(sb_planner* p, const uint64_t* d_ids, const int64_t* d_lens,
+                  const int64_t* d_rank_off, sb_stream stream);
+/* identity_plan (balancer.cpp:227-240) into the same planner slots. */
+SB_API sb_status sb_plan_identity(sb_planner* p, const uint64_t* d_ids, const int64_t* d_lens,
+                           const int64_t* d_rank_off, sb_stream stream);
+
+/* Device view of the current plan.  Counts live in device memory; arrays are
+ * sized for the planner's capacity. */
+typedef struct sb_plan_dev {
+  int world_size;
+  int64_t max_chunks;
+  const int64_t* n_chunks;      /* device scalar                                   */
+  const uint64_t* chunk_id;     /* ChunkAssignment SoA (balancer.hpp:38-47)        */
+  const int32_t* chunk_index;
+  const int64_t* chunk_start;
+  const int64_t* chunk_end;
+  const int32_t* chunk_src;
+  const int32_t* chunk_dst;
+  const int64_t* chunk_src_row; /* row of the chunk's first token in origin packing */
+  const int64_t* chunk_dst_row; /* row in target packing                           */
+  const int64_t* send_off;      /* W+1: RoutingPlan::send as CSR                   */
+  const int32_t* send_idx;
+  const int64_t* recv_off;      /* W+1: RoutingPlan::recv                          */
+  const int32_t* recv_idx;
+  const int32_t* rev_recv_idx;  /* reverse_plan(plan).recv; offsets = send_off     */
+  const int64_t* origin_rows;   /* W: rows per rank before the exchange            */
+  const int64_t* target_rows;   /* W: rows per rank after                          */
+  const double* per_gpu_workload;  /* BalanceReport (balancer.hpp:78-84)           */
+  const double* per_bag_occupancy; /* replicas * n_bags                            */
+  const int32_t* capacity_violations;
+  const double* total_workload;
+  const double* wir;
+  const int32_t* status;        /* device error word (0 = ok)                      */
+} sb_plan_dev;
+SB_API sb_status sb_plan_get(const sb_planner* p, sb_plan_dev* out);
+
+/* Synchronises `stream`, checks the device status word and returns the plan
+ * sizes.  n_seqs is the sequence count the plan was built from. */
+SB_API sb_status sb_plan_sizes(sb_planner* p, sb_stream stream, int64_t* n_chunks, int64_t* n_seqs);
+
+/* Host copy of the plan (caller-allocated arrays; NULL entries are skipped). */
+typedef struct sb_plan_host {
+  uint64_t* chunk_id;
+  int32_t* chunk_index;
+  int64_t* chunk_start;
+  int64_t* chunk_end;
+  int32_t* chunk_src;
+  int32_t* chunk_dst;
+  int64_t* send_off;     /* W+1 */
+  int32_t* send_idx;     /* n_chunks */
+  int64_t* recv_off;     /* W+1 */
+  int32_t* recv_idx;     /* n_chunks */
+  int32_t* rev_recv_idx; /* n_chunks */
+  int64_t* target_rows;  /* W */
+  double* per_gpu_workload;  /* W */
+  double* per_bag_occupancy; /* replicas * n_bags */
+  int32_t capacity_violations;
+  double total_workload;
+  double wir;
+} sb_plan_host;
+SB_API sb_status sb_plan_download(sb_planner* p, sb_plan_host* out, sb_stream stream);
+
+/* Plan latency breakdown of the last sb_plan (device time, microseconds,
+ * measured with events when timing is enabled; zeros otherwise). */
+SB_API sb_status sb_planner_enable_timing(sb_planner* p, int enable);
+SB_API sb_status sb_planner_timing(sb_planner* p, double* us_prep, double* us_sort, double* us_greedy,
+                            double* us_emit, double* us_lists);
+
+/* -------------------------------------------------------------- world -- */
+/* Device-resident rank buffers (RankBuffer, exchange.hpp:22-44) laid out for
+ * HBM: one arena per tensor, ranks packed back to back, plus per-rank tables
+ * (row count, base pointer, row pitch) that the kernels read.  Tensor 0 is
+ * the 16-byte row metadata {uint64 sample_id, int64 position}; tensors
+ * 1..n_payload are head-sliced payloads (hidden states, q/k/v ...); the
+ * remaining n_aux tensors are whole-row auxiliaries (e.g. RoPE ids). */
+typedef struct sb_world sb_world;
+
+typedef struct sb_world_desc {
+  int world_size;          /* global ranks W                                    */
+  int n_local;             /* ranks hosted by this process                      */
+  int first_local;         /* global rank of the first hosted rank              */
+  int n_heads;             /* World::n_heads                                    */
+  int n_payload;           /* >= 1 head-sliced tensors                          */
+  int n_aux;               /* whole-row tensors besides the metadata            */
+  const int64_t* row_bytes;/* n_payload + n_aux full-width row sizes            */
+  int64_t capacity_rows;   /* rows per tensor arena (all hosted ranks)          */
+  int max_bag;             /* largest bag size (sizes the metadata arena)       */
+} sb_world_desc;
+
+SB_API sb_status sb_world_create(const sb_world_desc* desc, sb_world** out);
+SB_API sb_status sb_world_destroy(sb_world* w);
+/* Arena base of tensor t (0 = metadata) -- for peer export / host copies. */
+SB_API sb_status sb_world_arena(const sb_world* w, int tensor, void** base, int64_t* bytes);
+/* Per-rank tables (device pointers, W entries). */
+SB_API sb_status sb_world_tables(const sb_world* w, int tensor, const uint64_t** d_base,
+                          const int64_t** d_pitch, const int64_t** d_rows);
+/* Multi-process: arena bases of every process's world for tensor t
+ * (peer-mapped device pointers), index = process; n_procs = W / n_local.   */
+SB_API sb_status sb_world_set_peers(sb_world* w, int tensor, const uint64_t* host_bases, int n_procs);
+
+/* Origin layout from gathered metadata: rank r holds its sequences packed in
+ * gather order (exchange.cpp:31-66 shells).  Device arrays as in sb_plan. */
+SB_API sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, const int64_t* d_rank_off,
+                                 sb_stream stream);
+/* Fill hosted ranks with the reference witness: metadata (id, pos) and
+ * payload doubles payload_value(id, pos, col) (exchange.cpp:18-23,52-63).
+ * Fixture generator for tests/bench; payload tensors must be 8*W_d bytes. */
+SB_API sb_status sb_world_fill_witness(sb_world* w, const uint64_t* d_ids, const int64_t* d_lens,
+                                const int64_t* d_rank_off, sb_stream stream);
+/* payload[r][c] += block_perturbation(id, pos) on hosted ranks
+ * (simulator.cpp:128-136) -- stands in for a transformer block. */
+SB_API sb_status sb_world_perturb(sb_world* w, sb_stream stream);
+/* content_checksum (exchange.cpp:438-457) over the hosted ranks' payload
+ * tensor 1, accumulated into *d_acc (device uint64, caller zeroes it). */
+SB_API sb_status sb_world_checksum(sb_world* w, uint64_t* d_acc, sb_stream stream);
+
+/* ------------------------------------------------------------ exchange -- */
+/* route (exchange.cpp:127-194): every chunk of the current plan moves to its
+ * target rank, packed in receive order; out-of-place from `src` to `dst`.
+ * reverse != 0 executes reverse_route (exchange.cpp:196-198), i.e. the plan
+ * with source and target swapped.  Each process pushes the chunks whose
+ * source it hosts (peer stores when the target is remote).                */
+SB_API sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_world* dst, sb_stream stream);
+/* Ulysses seq->head all-to-all for every multi-GPU bag of every replica
+ * (pre_attn, exchange.cpp:255-331); ranks in single-GPU bags alias `src`.  */
+SB_API sb_status sb_pre_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream);
+/* Inverse (post_attn, exchange.cpp:333-436).                               */
+SB_API sb_status sb_post_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream);
+/* Synchronises and returns the world's device status (layout capacity). */
+SB_API sb_status sb_world_status(sb_world* w, sb_stream stream);
+
+/* Copy the hosted ranks' packed image of every tensor between host and
+ * device (pinned host memory is fastest): bytes[t] from/to the start of
+ * tensor t's arena, where k_layout packs the hosted ranks back to back in
+ * rank order.  Asynchronous; NULL host[t] skips tensor t. */
+SB_API sb_status sb_world_upload(sb_world* w, void* const* host, const int64_t* bytes, sb_stream stream);
+SB_API sb_status sb_world_download(sb_world* w, void* const* host, const int64_t* bytes, sb_stream stream);
+/* One rank's tensor t (rows x pitch bytes, current layout) to/from host
+ * memory; synchronises.  *bytes returns the rank's byte size (pass
+ * host == NULL to query). */
+SB_API sb_status sb_world_read_rank(sb_world* w, int tensor, int rank, void* host, int64_t capacity,
+                                    int64_t* bytes, sb_stream stream);
+SB_API sb_status sb_world_write_rank(sb_world* w, int tensor, int rank, const void* host, int64_t bytes,
+                                     sb_stream stream);
+/* Current per-rank rows/pitch as host arrays (synchronises). */
+SB_API sb_status sb_world_shape(sb_world* w, int tensor, int64_t* rows, int64_t* pitch, sb_stream stream);
+
+/* Device time of the copy kernels launched while timing was enabled
+ * (sb_planner_enable_timing): op 0 route, 1 reverse_route, 2 pre_attn,
+ * 3 post_attn, -1 all.  Synchronises on the recorded events. */
+SB_API sb_status sb_copy_timing(sb_planner* p, int op, int64_t* count, double* total_us);
+SB_API sb_status sb_copy_timing_reset(sb_planner* p);
+
+/* Bytes the last exchange call moved (algorithmic, read + write) and the
+ * number of copy jobs it issued; for roofline accounting. */
+SB_API sb_status sb_last_exchange_bytes(const sb_planner* p, int64_t* bytes_read, int64_t* bytes_written);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

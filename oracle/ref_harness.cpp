@@ -337,9 +337,12 @@ int cmd_bench() {
   for (const auto& r : info)
     for (const auto& s : r) tokens += s.length;
 
+  const double budget_s = c.value("budget_s", 1e30);  // bound the sample's wall time
   double t_plan = 0, t_route = 0, t_uly = 0, t_rev = 0;
   std::vector<double> step_s;
+  const double t_begin = now_s();
   for (int it = 0; it < warmup + steps; ++it) {
+    if (it > warmup && now_s() - t_begin > budget_s) break;
     const double a = now_s();
     const PlanResult pr = plan_routing(info, model, layout);
     const double b = now_s();
@@ -370,14 +373,15 @@ int cmd_bench() {
   json out;
   double total = 0;
   for (double s : step_s) total += s;
-  out["steps"] = steps;
+  const double ns = step_s.empty() ? 1.0 : static_cast<double>(step_s.size());
+  out["steps"] = step_s.size();
   out["tokens_per_step"] = tokens;
-  out["s_per_step"] = total / steps;
-  out["tokens_per_s"] = tokens / (total / steps);
-  out["plan_s"] = t_plan / steps;
-  out["route_s"] = t_route / steps;
-  out["ulysses_s"] = t_uly / steps;
-  out["reverse_s"] = t_rev / steps;
+  out["s_per_step"] = total / ns;
+  out["tokens_per_s"] = tokens / (total / ns);
+  out["plan_s"] = t_plan / ns;
+  out["route_s"] = t_route / ns;
+  out["ulysses_s"] = t_uly / ns;
+  out["reverse_s"] = t_rev / ns;
   out["threads"] = omp_get_max_threads();
   out["bytes_per_row"] = width * 8;
   std::cout << out.dump() << "\n";

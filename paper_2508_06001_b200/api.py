@@ -1,0 +1,395 @@
+"""Python host mirror of the reference plan/route/reverse API over the C-ABI.
+
+Mirrors /root/reference/proj/include/seqbal/{balancer,exchange,topology}.hpp:
+``parse_topology`` / ``Planner.plan`` (plan_routing) / ``Planner.plan_identity``
+(identity_plan) / ``route`` / ``reverse_route`` / ``pre_attn`` / ``post_attn``.
+Device memory and streams come from torch (plumbing only); every byte of
+planning and data movement runs in libseqbal_cuda.so's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from ._capi import ConfigError, ParseError, call
+
+__all__ = ["Topology", "parse_topology", "Model", "Planner", "World", "DeviceMeta", "HostPlan",
+           "route", "reverse_route", "pre_attn", "post_attn", "kernel_launches"]
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise _capi.CudaError("no CUDA device: the redistribute path runs only on the GPU")
+    return torch
+
+
+def _stream(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def kernel_launches() -> int:
+    return int(_capi.load().sb_kernel_launches())
+
+
+# ---------------------------------------------------------------- topology
+@dataclass
+class Topology:
+    """topology.hpp:16-34: bags of contiguous unit-local ranks, textual order."""
+    bag_sizes: list
+
+    @property
+    def unit_size(self) -> int:
+        return sum(self.bag_sizes)
+
+    def bag_ranks(self, b: int) -> list:
+        s = sum(self.bag_sizes[:b])
+        return list(range(s, s + self.bag_sizes[b]))
+
+    def format(self) -> str:  # format_topology (topology.cpp:67-79)
+        out, i = [], 0
+        while i < len(self.bag_sizes):
+            j = i
+            while j < len(self.bag_sizes) and self.bag_sizes[j] == self.bag_sizes[i]:
+                j += 1
+            out.append(f"g{self.bag_sizes[i]}n{j - i}")
+            i = j
+        return "+".join(out)
+
+
+def parse_topology(spec: str) -> Topology:
+    """Grammar of topology.cpp:31-65: term ('+' term)*, term := 'g' INT 'n' INT."""
+    if not spec:
+        raise ParseError("empty topology spec (at offset 0)")
+    sizes, pos = [], 0
+
+    def num(p, what):
+        q, v = p, 0
+        while q < len(spec) and spec[q].isdigit():
+            v = v * 10 + ord(spec[q]) - 48
+            if v > (1 << 20):
+                raise ParseError(f"{what} value too large (at offset {p})")
+            q += 1
+        if q == p:
+            raise ParseError(f"expected digits for {what} (at offset {p})")
+        if v < 1:
+            raise ParseError(f"{what} must be >= 1 (at offset {p})")
+        return v, q
+
+    while True:
+        if pos >= len(spec) or spec[pos] != "g":
+            raise ParseError(f"expected 'g' (at offset {pos})")
+        g, pos = num(pos + 1, "bag size")
+        if pos >= len(spec) or spec[pos] != "n":
+            raise ParseError(f"expected 'n' (at offset {pos})")
+        n, pos = num(pos + 1, "bag count")
+        sizes += [g] * n
+        if pos == len(spec):
+            break
+        if spec[pos] != "+":
+            raise ParseError(f"expected '+' or end of spec (at offset {pos})")
+        pos += 1
+    return Topology(sizes)
+
+
+@dataclass
+class Model:
+    """WorkloadModel (workload_model.hpp:13-42); FLUX defaults."""
+    d_model: int = 3072
+    n_heads: int = 24
+    d_head: int = 128
+    n_blocks: int = 57
+    gamma: float = 0.49
+    k: float = 4.0e-15
+
+
+# ---------------------------------------------------------------- metadata
+class DeviceMeta:
+    """Gathered per-rank (sample_id, length) metadata resident in HBM
+    (the all-gather result, gather order; exchange.cpp:68-77)."""
+
+    def __init__(self, ids, lens, rank_off, device=None):
+        torch = _torch()
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        # at least one element so empty worlds still pass valid device pointers
+        n = len(ids)
+        self.ids = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+        self.lens = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+        if n:
+            self.ids[:n].copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(ids, np.uint64).view(np.int64))))
+            self.lens[:n].copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(lens, np.int64))))
+        self.rank_off = torch.as_tensor(np.asarray(rank_off, np.int64), device=dev)
+        self.world = len(rank_off) - 1
+        self.n = int(rank_off[-1])
+
+    @classmethod
+    def from_lists(cls, ids_per_rank, lens_per_rank, device=None):
+        ids = np.concatenate([np.asarray(x, np.uint64) for x in ids_per_rank]) if ids_per_rank else np.zeros(0, np.uint64)
+        lens = np.concatenate([np.asarray(x, np.int64) for x in lens_per_rank]) if lens_per_rank else np.zeros(0, np.int64)
+        off = np.zeros(len(ids_per_rank) + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in ids_per_rank])
+        return cls(ids, lens, off, device)
+
+    def ptrs(self):
+        return (C.c_void_p(self.ids.data_ptr()), C.c_void_p(self.lens.data_ptr()),
+                C.c_void_p(self.rank_off.data_ptr()))
+
+
+@dataclass
+class HostPlan:
+    """RoutingPlan + BalanceReport downloaded from the device (balancer.hpp:38-89)."""
+    world: int
+    c_id: np.ndarray
+    c_idx: np.ndarray
+    c_start: np.ndarray
+    c_end: np.ndarray
+    c_src: np.ndarray
+    c_dst: np.ndarray
+    send_off: np.ndarray
+    send_idx: np.ndarray
+    recv_off: np.ndarray
+    recv_idx: np.ndarray
+    rev_recv_idx: np.ndarray
+    target_rows: np.ndarray
+    per_gpu_workload: np.ndarray
+    per_bag_occupancy: np.ndarray
+    capacity_violations: int
+    total_workload: float
+    wir: float
+
+    @property
+    def n_chunks(self) -> int:
+        return len(self.c_id)
+
+    def _lists(self, off, idx):
+        return [idx[off[r]:off[r + 1]].astype(np.int64).tolist() for r in range(self.world)]
+
+    @property
+    def send(self):
+        return self._lists(self.send_off, self.send_idx)
+
+    @property
+    def recv(self):
+        return self._lists(self.recv_off, self.recv_idx)
+
+    @property
+    def rev_send(self):  # reverse_plan(plan).send == plan.recv (balancer.cpp:256-258)
+        return self.recv
+
+    @property
+    def rev_recv(self):
+        return self._lists(self.send_off, self.rev_recv_idx)
+
+
+# ----------------------------------------------------------------- planner
+class Planner:
+    """Device planner for one (model, topology, world): plan_routing on the GPU."""
+
+    def __init__(self, topology, world_size: int, model: Model | None = None, max_seqs: int = 1 << 16):
+        _torch()
+        self.topology = parse_topology(topology) if isinstance(topology, str) else (
+            topology if isinstance(topology, Topology) else Topology(list(topology)))
+        self.model = model or Model()
+        self.world_size = world_size
+        self.max_seqs = max_seqs
+        sizes = self.topology.bag_sizes
+        self._bag_off = np.zeros(len(sizes) + 1, np.int32)
+        self._bag_off[1:] = np.cumsum(sizes)
+        self._bag_ranks = np.arange(self.topology.unit_size, dtype=np.int32)
+        d = _capi.PlannerDesc(world_size, self.topology.unit_size, len(sizes),
+                              self._bag_off.ctypes.data, self._bag_ranks.ctypes.data, self.model.d_model,
+                              self.model.n_heads, self.model.d_head, self.model.n_blocks, self.model.gamma,
+                              self.model.k, max_seqs)
+        h = C.c_void_p()
+        call("sb_planner_create", C.byref(d), C.byref(h))
+        self._h = h
+        self.replicas = world_size // self.topology.unit_size
+        self.max_bag = max(sizes)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _capi.load().sb_planner_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def plan(self, meta: DeviceMeta, stream=None):
+        call("sb_plan", self._h, *meta.ptrs(), _stream(stream))
+        self._meta = meta
+        return self
+
+    def plan_identity(self, meta: DeviceMeta, stream=None):
+        call("sb_plan_identity", self._h, *meta.ptrs(), _stream(stream))
+        self._meta = meta
+        return self
+
+    def enable_timing(self, on: bool = True):
+        call("sb_planner_enable_timing", self._h, int(on))
+
+    def timing(self) -> dict:
+        v = [C.c_double() for _ in range(5)]
+        call("sb_planner_timing", self._h, *[C.byref(x) for x in v])
+        return dict(zip(["prep_us", "sort_us", "greedy_us", "emit_us", "lists_us"], [x.value for x in v]))
+
+    def sizes(self, stream=None):
+        nc, ns = C.c_int64(), C.c_int64()
+        call("sb_plan_sizes", self._h, _stream(stream), C.byref(nc), C.byref(ns))
+        return nc.value, ns.value
+
+    def device_view(self) -> _capi.PlanDev:
+        v = _capi.PlanDev()
+        call("sb_plan_get", self._h, C.byref(v))
+        return v
+
+    def download(self, stream=None) -> HostPlan:
+        nc, _ = self.sizes(stream)
+        W = self.world_size
+        nb = self.replicas * len(self.topology.bag_sizes)
+        a = dict(c_id=np.zeros(nc, np.uint64), c_idx=np.zeros(nc, np.int32), c_start=np.zeros(nc, np.int64),
+                 c_end=np.zeros(nc, np.int64), c_src=np.zeros(nc, np.int32), c_dst=np.zeros(nc, np.int32),
+                 send_off=np.zeros(W + 1, np.int64), send_idx=np.zeros(nc, np.int32),
+                 recv_off=np.zeros(W + 1, np.int64), recv_idx=np.zeros(nc, np.int32),
+                 rev_recv_idx=np.zeros(nc, np.int32), target_rows=np.zeros(W, np.int64),
+                 per_gpu_workload=np.zeros(W, np.float64), per_bag_occupancy=np.zeros(nb, np.float64))
+        h = _capi.PlanHost(*[x.ctypes.data for x in a.values()])
+        call("sb_plan_download", self._h, C.byref(h), _stream(stream))
+        return HostPlan(W, *a.values(), capacity_violations=int(h.capacity_violations),
+                        total_workload=float(h.total_workload), wir=float(h.wir))
+
+    def copy_timing(self, op: int = -1):
+        """(count, total_us) of copy kernels recorded while timing was on."""
+        n, us = C.c_int64(), C.c_double()
+        call("sb_copy_timing", self._h, op, C.byref(n), C.byref(us))
+        return n.value, us.value
+
+    def copy_timing_reset(self):
+        call("sb_copy_timing_reset", self._h)
+
+    def exchange_bytes(self) -> int:
+        r, w = C.c_int64(), C.c_int64()
+        call("sb_last_exchange_bytes", self._h, C.byref(r), C.byref(w))
+        return r.value
+
+
+# ------------------------------------------------------------------- world
+class World:
+    """Device-resident rank buffers (RankBuffer/World, exchange.hpp:22-44).
+
+    Tensor 0 is the 16-byte row metadata {sample_id, position}; tensors
+    1..n_payload are head-sliced payloads of ``payload_row_bytes[i]`` bytes per
+    row; aux tensors are whole-row extras (e.g. RoPE position ids)."""
+
+    def __init__(self, world_size: int, n_heads: int, payload_row_bytes, capacity_rows: int,
+                 aux_row_bytes=(), n_local: int | None = None, first_local: int = 0, max_bag: int = 1):
+        _torch()
+        self.world_size = world_size
+        self.n_local = n_local or world_size
+        self.first_local = first_local
+        self.n_payload = len(payload_row_bytes)
+        self.n_aux = len(aux_row_bytes)
+        self.row_bytes = [16] + list(payload_row_bytes) + list(aux_row_bytes)
+        rb = np.asarray(list(payload_row_bytes) + list(aux_row_bytes), np.int64)
+        d = _capi.WorldDesc(world_size, self.n_local, first_local, n_heads, self.n_payload, self.n_aux,
+                            rb.ctypes.data, capacity_rows, max_bag)
+        h = C.c_void_p()
+        call("sb_world_create", C.byref(d), C.byref(h))
+        self._h = h
+        self.n_heads = n_heads
+        self.T = 1 + self.n_payload + self.n_aux
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _capi.load().sb_world_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def arena(self, t: int):
+        base, nbytes = C.c_void_p(), C.c_int64()
+        call("sb_world_arena", self._h, t, C.byref(base), C.byref(nbytes))
+        return base.value, nbytes.value
+
+    def set_peers(self, t: int, bases):
+        a = np.asarray(bases, np.uint64)
+        call("sb_world_set_peers", self._h, t, a.ctypes.data, len(a))
+
+    def layout_origin(self, meta: DeviceMeta, stream=None):
+        _, lens, off = meta.ptrs()
+        call("sb_world_layout_origin", self._h, lens, off, _stream(stream))
+
+    def fill_witness(self, meta: DeviceMeta, stream=None):
+        call("sb_world_fill_witness", self._h, *meta.ptrs(), _stream(stream))
+
+    def perturb(self, stream=None):
+        call("sb_world_perturb", self._h, _stream(stream))
+
+    def checksum(self, stream=None) -> int:
+        torch = _torch()
+        acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+        call("sb_world_checksum", self._h, C.c_void_p(acc.data_ptr()), _stream(stream))
+        return int(acc.cpu().numpy().view(np.uint64)[0])
+
+    def status(self, stream=None):
+        call("sb_world_status", self._h, _stream(stream))
+
+    def shape(self, t: int = 0, stream=None):
+        W = self.world_size
+        rows, pitch = np.zeros(W, np.int64), np.zeros(W, np.int64)
+        call("sb_world_shape", self._h, t, rows.ctypes.data, pitch.ctypes.data, _stream(stream))
+        return rows, pitch
+
+    def read_rank(self, t: int, rank: int, stream=None) -> np.ndarray:
+        n = C.c_int64()
+        call("sb_world_read_rank", self._h, t, rank, None, 0, C.byref(n), _stream(stream))
+        buf = np.zeros(n.value, np.uint8)
+        call("sb_world_read_rank", self._h, t, rank, buf.ctypes.data, n.value, C.byref(n), _stream(stream))
+        return buf
+
+    def write_rank(self, t: int, rank: int, data: np.ndarray, stream=None):
+        data = np.ascontiguousarray(data).view(np.uint8)
+        call("sb_world_write_rank", self._h, t, rank, data.ctypes.data, data.nbytes, _stream(stream))
+
+    def upload(self, host_ptrs, nbytes, stream=None):
+        p = (C.c_void_p * self.T)(*host_ptrs)
+        b = np.asarray(nbytes, np.int64)
+        call("sb_world_upload", self._h, p, b.ctypes.data, _stream(stream))
+
+    def download(self, host_ptrs, nbytes, stream=None):
+        p = (C.c_void_p * self.T)(*host_ptrs)
+        b = np.asarray(nbytes, np.int64)
+        call("sb_world_download", self._h, p, b.ctypes.data, _stream(stream))
+
+
+# --------------------------------------------------------------- exchange
+def route(planner: Planner, src: World, dst: World, stream=None, reverse: bool = False):
+    """route (exchange.cpp:127-194): out-of-place, src (origin layout) -> dst."""
+    call("sb_route", planner.handle, int(reverse), src.handle, dst.handle, _stream(stream))
+    return dst
+
+
+def reverse_route(planner: Planner, src: World, dst: World, stream=None):
+    """reverse_route (exchange.cpp:196-198)."""
+    return route(planner, src, dst, stream, reverse=True)
+
+
+def pre_attn(planner: Planner, src: World, dst: World, stream=None):
+    """pre_attn (exchange.cpp:255-331) for every multi-GPU bag at once."""
+    call("sb_pre_attn", planner.handle, src.handle, dst.handle, _stream(stream))
+    return dst
+
+
+def post_attn(planner: Planner, src: World, dst: World, stream=None):
+    """post_attn (exchange.cpp:333-436) for every multi-GPU bag at once."""
+    call("sb_post_attn", planner.handle, src.handle, dst.handle, _stream(stream))
+    return dst

@@ -1,0 +1,920 @@
+// Exchange engine: device worlds, plan -> copy-job builders for route /
+// reverse_route / pre_attn / post_attn, and the batched strided copy kernel
+// that moves the rows (the pack, the all-to-all and the unpack fused into one
+// pass: each row is read once from its source buffer and written once into
+// its final slot, local or peer-mapped).
+//
+// Reference data movement being replaced: exchange.cpp:127-198 (route),
+// :255-436 (pre_attn / post_attn), exchange_kernels.cpp:15-56 (the
+// OpenMP memcpy of BlockMoves).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace sb {
+
+thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+constexpr int64_t kPieceBytes = 32768;  // work unit of the copy kernel
+constexpr int kCopyThreads = 256;
+
+// --------------------------------------------------------------- layouts
+struct WorldArgs {
+  int W, T, n_local, first_local, n_procs;
+  uint64_t* base;     // T*W
+  int64_t* pitch;     // T*W
+  int64_t* rows;      // W
+  int32_t* headcol;   // W
+  const uint64_t* peer_arena;  // T*n_procs
+  const int64_t* arena_bytes;  // T
+  int32_t* status;
+};
+
+static WorldArgs wargs(sb_world* w) {
+  WorldArgs a;
+  a.W = w->W; a.T = w->T; a.n_local = w->n_local; a.first_local = w->first_local; a.n_procs = w->n_procs;
+  a.base = w->d_base; a.pitch = w->d_pitch; a.rows = w->d_rows; a.headcol = w->d_headcol;
+  a.peer_arena = w->d_peer_arena; a.arena_bytes = w->d_arena_bytes; a.status = w->d_status;
+  return a;
+}
+
+struct TensorInfo {
+  int64_t row_bytes[16];
+  int kind[16];  // 0 meta, 1 payload (head-sliced), 2 aux
+};
+
+static TensorInfo tinfo(sb_world* w) {
+  TensorInfo t;
+  for (int i = 0; i < w->T && i < 16; ++i) {
+    t.row_bytes[i] = w->row_bytes[i];
+    t.kind[i] = (int)w->tensor_desc[i];
+  }
+  return t;
+}
+
+// Packs ranks back to back per owner process.  mode 0: every rank gets
+// rows_src[r] full-width rows (route / reverse_route / origin).  mode 1:
+// ranks of multi-GPU bags get the Ulysses (full sequence, H/G heads) layout,
+// others alias `src`.  mode 2: ranks of multi-GPU bags get the chunk layout
+// again (post_attn), others alias `src`.
+struct LayoutPlan {
+  const int64_t* rows_src;  // mode 0: rows per rank
+  const int32_t* rank_bag;  // U
+  const int32_t* rank_member;
+  const int32_t* bag_size;
+  const int64_t* bag_rows;  // R*M
+  const int64_t* target_rows;
+  int U, M;
+};
+
+__global__ void k_layout(WorldArgs d, WorldArgs s, LayoutPlan lp, TensorInfo ti, int mode) {
+  const int t = threadIdx.x;
+  if (t >= d.T) return;
+  int owner = -1;
+  int64_t off = 0;
+  for (int r = 0; r < d.W; ++r) {
+    const int o = r / d.n_local;
+    if (o != owner) {
+      owner = o;
+      off = 0;
+    }
+    int g = 1, k = 0;
+    int64_t rows;
+    if (mode == 0) {
+      rows = lp.rows_src[r];
+    } else {
+      const int u = r % lp.U, rep = r / lp.U;
+      const int b = lp.rank_bag[u];
+      g = lp.bag_size[b];
+      k = lp.rank_member[u];
+      if (g == 1) {  // alias the source world's buffers (pre/post are no-ops)
+        d.base[t * d.W + r] = s.base[t * s.W + r];
+        d.pitch[t * d.W + r] = s.pitch[t * s.W + r];
+        if (t == 0) {
+          d.rows[r] = s.rows[r];
+          d.headcol[r] = s.headcol[r];
+        }
+        continue;
+      }
+      rows = mode == 1 ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
+    }
+    int64_t pitch = ti.row_bytes[t];
+    if (mode == 1 && ti.kind[t] == 1) pitch = ti.row_bytes[t] / g;
+    d.base[t * d.W + r] = d.peer_arena[t * d.n_procs + owner] + (uint64_t)off;
+    d.pitch[t * d.W + r] = pitch;
+    off += rows * pitch;
+    if (off > d.arena_bytes[t]) atomicOr(d.status, ST_LAYOUT);
+    if (t == 0) {
+      d.rows[r] = rows;
+      d.headcol[r] = (mode == 1) ? (int32_t)(k * (ti.row_bytes[1] / 8 / g)) : 0;
+    }
+  }
+}
+
+// ----------------------------------------------------------- job builders
+struct JobArgs {
+  const int64_t* n_chunks;
+  const int32_t *c_idx, *c_src, *c_dst, *bag_of_rank, *bag_size;
+  const int64_t *c_start, *c_end, *c_src_row, *c_dst_row, *c_seq_base;
+  int U;
+  int max_bag;
+  SbJob* jobs;
+  int64_t* n_jobs;
+};
+
+__device__ __forceinline__ bool is_local(const WorldArgs& w, int r) {
+  return r >= w.first_local && r < w.first_local + w.n_local;
+}
+
+__global__ void k_jobs_route(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti, int reverse) {
+  const int64_t nc = *j.n_chunks;
+  const int T = s.T;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *j.n_jobs = nc * T;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nc * T; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = x / T;
+    const int t = (int)(x % T);
+    const int sr = reverse ? j.c_dst[c] : j.c_src[c];
+    const int dr = reverse ? j.c_src[c] : j.c_dst[c];
+    const int64_t srow = reverse ? j.c_dst_row[c] : j.c_src_row[c];
+    const int64_t drow = reverse ? j.c_src_row[c] : j.c_dst_row[c];
+    SbJob job;
+    const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
+    job.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp);
+    job.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp);
+    job.n_rows = is_local(s, sr) ? j.c_end[c] - j.c_start[c] : 0;
+    job.width = ti.row_bytes[t];
+    job.spitch = sp;
+    job.dpitch = dp;
+    j.jobs[x] = job;
+  }
+}
+
+// pre_attn (exchange.cpp:298-325): chunk c = (seq q, member m) held by bag
+// rank m moves, for each destination member d, its column slice d (payload)
+// or its whole rows (metadata / aux) to row seq_base(q) + start on rank d.
+// post_attn (exchange.cpp:406-431) is the transpose: destination chunk
+// c = (q, d) gathers slice m from every member m; metadata from m = 0 only.
+__global__ void k_jobs_ulysses(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti, int post) {
+  const int64_t nc = *j.n_chunks;
+  const int T = s.T, G = j.max_bag;
+  const int64_t total = nc * G * T;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *j.n_jobs = total;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x % T);
+    const int64_t y = x / T;
+    const int other = (int)(y % G);  // d for pre, m for post
+    const int64_t c = y / G;
+    SbJob job;
+    job.src = job.dst = 0;
+    job.n_rows = 0;
+    job.width = 16;
+    job.spitch = job.dpitch = 16;
+    const int dst_rank_of_chunk = j.c_dst[c];
+    const int g = j.bag_size[j.bag_of_rank[dst_rank_of_chunk % j.U]];
+    const int mine = j.c_idx[c];
+    if (g > 1 && other < g) {
+      const int64_t cq0 = c - mine;
+      const int64_t full_row = j.c_seq_base[cq0] + j.c_start[c];
+      const int64_t n = j.c_end[c] - j.c_start[c];
+      const int kind = ti.kind[t];
+      const int64_t slice = ti.row_bytes[t] / g;
+      int sr, dr;
+      int64_t srow, drow, scol = 0, dcol = 0, width;
+      bool active = true;
+      if (!post) {
+        sr = dst_rank_of_chunk;               // member m = mine holds chunk c
+        dr = j.c_dst[cq0 + other];            // member d
+        srow = j.c_dst_row[c];
+        drow = full_row;
+        if (kind == 1) {
+          scol = other * slice;
+          width = slice;
+        } else {
+          width = ti.row_bytes[t];
+        }
+      } else {
+        sr = j.c_dst[cq0 + other];            // member m holds slice m of the full seq
+        dr = dst_rank_of_chunk;               // member d = mine gets chunk c back
+        srow = full_row;
+        drow = j.c_dst_row[c];
+        if (kind == 1) {
+          dcol = other * slice;
+          width = slice;
+        } else {
+          width = ti.row_bytes[t];
+          active = other == 0;  // metadata once per destination row (exchange.cpp:424)
+        }
+      }
+      if (active && is_local(s, sr)) {
+        const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
+        job.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp + scol);
+        job.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp + dcol);
+        job.n_rows = n;
+        job.width = width;
+        job.spitch = sp;
+        job.dpitch = dp;
+      }
+    }
+    j.jobs[x] = job;
+  }
+}
+
+// Piece decomposition + exclusive scan (single CTA).  A job whose rows are
+// contiguous on both sides is split into kPieceBytes spans of the flat byte
+// range; otherwise into groups of kPieceBytes/width rows.
+__device__ __forceinline__ bool job_flat(const SbJob& j) { return j.width == j.spitch && j.width == j.dpitch; }
+__device__ __forceinline__ int64_t job_rows_per_piece(const SbJob& j) {
+  const int64_t r = kPieceBytes / (j.width > 0 ? j.width : 1);
+  return r > 0 ? r : 1;
+}
+__device__ __forceinline__ int64_t job_pieces(const SbJob& j) {
+  if (j.n_rows <= 0 || j.width <= 0) return 0;
+  if (job_flat(j)) return (j.n_rows * j.width + kPieceBytes - 1) / kPieceBytes;
+  const int64_t rp = job_rows_per_piece(j);
+  return (j.n_rows + rp - 1) / rp;
+}
+
+__global__ void __launch_bounds__(1024) k_pieces(const SbJob* jobs, const int64_t* n_jobs_p, int64_t* piece_off,
+                                                 int64_t* bytes_moved) {
+  __shared__ int64_t sh[33];
+  const int64_t n = *n_jobs_p;
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int64_t per = (n + nt - 1) / nt;
+  const int64_t b = tid * per, e = b + per < n ? b + per : n;
+  int64_t cnt = 0, bytes = 0;
+  for (int64_t i = b; i < e; ++i) {
+    const SbJob jb = jobs[i];
+    cnt += job_pieces(jb);
+    if (jb.n_rows > 0) bytes += jb.n_rows * jb.width;
+  }
+  int64_t tot, tb;
+  const int64_t ex = block_excl_scan<int64_t>(cnt, sh, &tot);
+  block_excl_scan<int64_t>(bytes, sh, &tb);
+  int64_t run = ex;
+  for (int64_t i = b; i < e; ++i) {
+    piece_off[i] = run;
+    run += job_pieces(jobs[i]);
+  }
+  if (tid == 0) {
+    piece_off[n] = tot;
+    *bytes_moved = tb;
+  }
+}
+
+// ------------------------------------------------------------ copy kernel
+__device__ __forceinline__ int4 ld_stream(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+constexpr int kUnroll = 8;
+
+// Warp copies `len` contiguous bytes (16-B aligned) with kUnroll 128-bit
+// loads in flight per lane before the matching stores.
+__device__ __forceinline__ void warp_copy_flat(const char* src, char* dst, int64_t len, int lane) {
+  const int64_t step = 32 * 16 * kUnroll;
+  int64_t off = (int64_t)lane * 16;
+  for (; off + (kUnroll - 1) * 512 < len; off += step) {
+    int4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(src + off + u * 512);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_stream(dst + off + u * 512, v[u]);
+  }
+  int4 v[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (off + u * 512 < len) v[u] = ld_stream(src + off + u * 512);
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (off + u * 512 < len) st_stream(dst + off + u * 512, v[u]);
+}
+
+// Warp copies rows [r0, r1) of a strided job: flat index over (row, vec).
+__device__ __forceinline__ void warp_copy_rows(const SbJob& j, int64_t r0, int64_t r1, int lane) {
+  const int vpr = (int)(j.width >> 4);
+  const int total = (int)(r1 - r0) * vpr;
+  const float inv = 1.0f / (float)vpr;
+  const char* src = reinterpret_cast<const char*>(j.src) + r0 * j.spitch;
+  char* dst = reinterpret_cast<char*>(j.dst) + r0 * j.dpitch;
+  for (int base = 0; base < total; base += 32 * kUnroll) {
+    int4 v[kUnroll];
+    int rr[kUnroll], cc[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int f = base + u * 32 + lane;
+      int row = (int)((float)f * inv);
+      if (row * vpr > f) --row;
+      else if ((row + 1) * vpr <= f) ++row;
+      rr[u] = row;
+      cc[u] = f - row * vpr;
+      if (f < total) v[u] = ld_stream(src + rr[u] * j.spitch + cc[u] * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int f = base + u * 32 + lane;
+      if (f < total) st_stream(dst + rr[u] * j.dpitch + cc[u] * 16, v[u]);
+    }
+  }
+}
+
+// Unaligned fallback (never hit by the bench layouts; kept for generality).
+__device__ void warp_copy_bytes(const SbJob& j, int64_t r0, int64_t r1, int lane) {
+  for (int64_t r = r0; r < r1; ++r) {
+    const char* s = reinterpret_cast<const char*>(j.src) + r * j.spitch;
+    char* d = reinterpret_cast<char*>(j.dst) + r * j.dpitch;
+    for (int64_t b = lane; b < j.width; b += 32) d[b] = s[b];
+  }
+}
+
+__global__ void __launch_bounds__(kCopyThreads) k_copy(const SbJob* __restrict__ jobs,
+                                                       const int64_t* __restrict__ piece_off,
+                                                       const int64_t* __restrict__ n_jobs_p) {
+  const int64_t n_jobs = *n_jobs_p;
+  const int64_t total = piece_off[n_jobs];
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (kCopyThreads / 32);
+  const int64_t wid = (int64_t)blockIdx.x * (kCopyThreads / 32) + (threadIdx.x >> 5);
+  // contiguous block of pieces per warp: one job search, then walk
+  const int64_t g0 = total * wid / nwarps, g1 = total * (wid + 1) / nwarps;
+  if (g0 >= g1) return;
+  int64_t lo = 0, hi = n_jobs;  // find last job with piece_off[j] <= g0
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (piece_off[mid] <= g0) lo = mid;
+    else hi = mid;
+  }
+  int64_t jb = lo;
+  for (int64_t g = g0; g < g1; ++g) {
+    while (piece_off[jb + 1] <= g) ++jb;
+    const SbJob j = jobs[jb];
+    const int64_t k = g - piece_off[jb];
+    const bool aligned = ((j.src | j.dst | (uint64_t)j.width | (uint64_t)j.spitch | (uint64_t)j.dpitch) & 15) == 0;
+    if (job_flat(j)) {
+      const int64_t len = j.n_rows * j.width;
+      const int64_t b = k * kPieceBytes;
+      const int64_t e = b + kPieceBytes < len ? b + kPieceBytes : len;
+      if (aligned) {
+        warp_copy_flat(reinterpret_cast<const char*>(j.src) + b, reinterpret_cast<char*>(j.dst) + b, e - b, lane);
+      } else {
+        const char* s = reinterpret_cast<const char*>(j.src);
+        char* d = reinterpret_cast<char*>(j.dst);
+        for (int64_t x = b + lane; x < e; x += 32) d[x] = s[x];
+      }
+    } else {
+      const int64_t rp = job_rows_per_piece(j);
+      const int64_t r0 = k * rp, r1 = r0 + rp < j.n_rows ? r0 + rp : j.n_rows;
+      if (aligned) warp_copy_rows(j, r0, r1, lane);
+      else warp_copy_bytes(j, r0, r1, lane);
+    }
+  }
+}
+
+// rows per rank = sum of its sequence lengths (origin packing).
+__global__ void k_rank_rows(const int64_t* lens, const int64_t* off, int64_t* rows) {
+  __shared__ int64_t sh[33];
+  const int r = blockIdx.x;
+  int64_t local = 0;
+  for (int64_t i = off[r] + threadIdx.x; i < off[r + 1]; i += blockDim.x) local += lens[i] > 0 ? lens[i] : 0;
+  int64_t tot;
+  block_excl_scan<int64_t>(local, sh, &tot);
+  if (threadIdx.x == 0) rows[r] = tot;
+}
+
+static int g_num_sms = 0;
+static int copy_grid() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms * 8;  // 8 CTAs x 8 warps per SM: ~64 KB+ of loads in flight per SM
+}
+
+// ----------------------------------------------------- witness / checksum
+// Witness fill for hosted ranks (exchange.cpp:18-23, 52-63): one warp per
+// row; metadata {id, pos} and payload doubles payload_value(id, pos, col).
+__global__ void k_witness(WorldArgs w, TensorInfo ti, const uint64_t* ids, const int64_t* rank_off,
+                          const int64_t* lens) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int lr = 0; lr < w.n_local; ++lr) {
+    const int r = w.first_local + lr;
+    const int64_t rows = w.rows[r];
+    const int64_t s0 = rank_off[r], s1 = rank_off[r + 1];
+    for (int64_t row = warp; row < rows; row += nwarps) {
+      // sequence containing `row` (fixture path: linear walk over the rank's lengths)
+      int64_t acc = 0, s = s0;
+      for (; s < s1; ++s) {
+        const int64_t l = lens[s] > 0 ? lens[s] : 0;
+        if (row < acc + l) break;
+        acc += l;
+      }
+      const uint64_t id = ids[s];
+      const int64_t pos = row - acc;
+      if (lane == 0) {
+        uint64_t* m = reinterpret_cast<uint64_t*>(w.base[r] + row * w.pitch[r]);
+        m[0] = id;
+        m[1] = (uint64_t)pos;
+      }
+      for (int t = 1; t < w.T; ++t) {
+        if (ti.kind[t] != 1) continue;
+        double* pl = reinterpret_cast<double*>(w.base[t * w.W + r] + row * w.pitch[t * w.W + r]);
+        const int wd = (int)(ti.row_bytes[t] / 8);
+        for (int c = lane; c < wd; c += 32) {
+          const uint64_t h = derive_key4(0x7061796c6f6164ULL, id, (uint64_t)pos, (uint64_t)c);
+          pl[c] = (double)(h >> 11) * 0x1.0p-53;
+        }
+      }
+    }
+  }
+}
+
+// simulator.cpp:128-136 on hosted full-width ranks.
+__global__ void k_perturb(WorldArgs w, TensorInfo ti) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int lr = 0; lr < w.n_local; ++lr) {
+    const int r = w.first_local + lr;
+    const int64_t rows = w.rows[r];
+    for (int64_t row = warp; row < rows; row += nwarps) {
+      const uint64_t* m = reinterpret_cast<const uint64_t*>(w.base[r] + row * w.pitch[r]);
+      const uint64_t h = derive_key3(0x706572747572ULL, m[0], m[1]);
+      const double delta = (double)(h >> 11) * 0x1.0p-53;
+      for (int t = 1; t < w.T; ++t) {
+        if (ti.kind[t] != 1) continue;
+        double* pl = reinterpret_cast<double*>(w.base[t * w.W + r] + row * w.pitch[t * w.W + r]);
+        const int wd = (int)(w.pitch[t * w.W + r] / 8);
+        for (int c = lane; c < wd; c += 32) pl[c] = __dadd_rn(pl[c], delta);
+      }
+    }
+  }
+}
+
+// content_checksum (exchange.cpp:438-457) over payload tensor 1.
+__global__ void k_checksum(WorldArgs w, unsigned long long* acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long sum = 0;
+  for (int lr = 0; lr < w.n_local; ++lr) {
+    const int r = w.first_local + lr;
+    const int64_t rows = w.rows[r];
+    const int wd = (int)(w.pitch[1 * w.W + r] / 8);
+    const int hc = w.headcol[r];
+    for (int64_t row = warp; row < rows; row += nwarps) {
+      const uint64_t* m = reinterpret_cast<const uint64_t*>(w.base[r] + row * w.pitch[r]);
+      const uint64_t id = m[0], pos = m[1];
+      const uint64_t* pl = reinterpret_cast<const uint64_t*>(w.base[1 * w.W + r] + row * w.pitch[1 * w.W + r]);
+      for (int c = lane; c < wd; c += 32) sum += derive_key4(id, pos, (uint64_t)(hc + c), pl[c]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0 && sum) atomicAdd(acc, sum);
+}
+
+void ensure_jobs(sb_planner* p, int64_t cap) {
+  if (cap <= p->job_cap) return;
+  if (p->jobs) cudaFree(p->jobs);
+  if (p->piece_off) cudaFree(p->piece_off);
+  p->jobs = nullptr;
+  p->piece_off = nullptr;
+  SB_CUDA(cudaMalloc(&p->jobs, sizeof(SbJob) * (size_t)cap));
+  SB_CUDA(cudaMalloc(&p->piece_off, sizeof(int64_t) * (size_t)(cap + 1)));
+  if (!p->n_jobs) SB_CUDA(cudaMalloc(&p->n_jobs, sizeof(int64_t) * 2));
+  p->job_cap = cap;
+}
+
+static JobArgs jargs(sb_planner* p) {
+  JobArgs j;
+  j.n_chunks = p->n_chunks;
+  j.c_idx = p->c_idx; j.c_src = p->c_src; j.c_dst = p->c_dst;
+  j.bag_of_rank = p->d_rank_bag; j.bag_size = p->d_bag_size;
+  j.c_start = p->c_start; j.c_end = p->c_end; j.c_src_row = p->c_src_row; j.c_dst_row = p->c_dst_row;
+  j.c_seq_base = p->c_seq_base;
+  j.U = p->U;
+  j.max_bag = p->max_bag;
+  j.jobs = p->jobs;
+  j.n_jobs = p->n_jobs;
+  return j;
+}
+
+static void check_compatible(sb_planner* p, sb_world* a, sb_world* b) {
+  if (a->W != p->W || b->W != p->W)
+    throw Error{SB_ERR_INTEGRITY, "route: plan world size " + std::to_string(p->W) + " != world ranks " +
+                                      std::to_string(a->W)};
+  if (a->T != b->T || a->row_bytes != b->row_bytes || a->n_local != b->n_local || a->first_local != b->first_local)
+    throw Error{SB_ERR_CONFIG, "exchange: source and destination worlds have different tensors"};
+  if (a->T > 16) throw Error{SB_ERR_CONFIG, "at most 16 tensors per world"};
+}
+
+static void run_copy(sb_planner* p, cudaStream_t s) {
+  k_pieces<<<1, 1024, 0, s>>>(p->jobs, p->n_jobs, p->piece_off, p->n_jobs + 1);
+  SB_CHECK_LAUNCH();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->timing) {
+    if (p->copy_used + 2 > p->copy_ev.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        SB_CUDA(cudaEventCreate(&e));
+        p->copy_ev.push_back(e);
+      }
+      p->copy_op.resize(p->copy_ev.size() / 2);
+    }
+    e0 = p->copy_ev[p->copy_used];
+    e1 = p->copy_ev[p->copy_used + 1];
+    p->copy_op[p->copy_used / 2] = p->current_op;
+    p->copy_used += 2;
+    SB_CUDA(cudaEventRecord(e0, s));
+  }
+  k_copy<<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs);
+  SB_CHECK_LAUNCH();
+  if (e1) SB_CUDA(cudaEventRecord(e1, s));
+  count_launch(2);
+}
+
+}  // namespace sb
+
+// ============================================================== C-ABI
+using sb::Error;
+
+#define SB_API_BEGIN try {
+#define SB_API_END                              \
+  return SB_OK;                                 \
+  }                                             \
+  catch (const Error& e) {                      \
+    sb::set_error(e.msg);                       \
+    return e.code;                              \
+  }                                             \
+  catch (const std::bad_alloc&) {               \
+    sb::set_error("host allocation failed");    \
+    return SB_ERR_CAPACITY;                     \
+  }
+
+extern "C" const char* sb_last_error(void) { return sb::g_last_error.c_str(); }
+extern "C" int sb_abi_version(void) { return 1; }
+extern "C" int64_t sb_kernel_launches(void) { return sb::g_launches.load(); }
+
+extern "C" sb_status sb_world_create(const sb_world_desc* d, sb_world** out) {
+  SB_API_BEGIN
+  if (!d || !out) throw Error{SB_ERR_CONFIG, "sb_world_create: null argument"};
+  *out = nullptr;
+  if (d->world_size < 1 || d->n_local < 1 || d->world_size % d->n_local != 0 || d->first_local % d->n_local != 0 ||
+      d->first_local + d->n_local > d->world_size)
+    throw Error{SB_ERR_CONFIG, "sb_world_create: hosted ranks must be a contiguous block dividing the world"};
+  if (d->n_payload < 1 || d->n_aux < 0 || d->n_heads < 1 || 1 + d->n_payload + d->n_aux > 16)
+    throw Error{SB_ERR_CONFIG, "sb_world_create: need 1..15 tensors and n_heads >= 1"};
+  auto* w = new sb_world();
+  w->W = d->world_size;
+  w->n_local = d->n_local;
+  w->first_local = d->first_local;
+  w->n_heads = d->n_heads;
+  w->n_payload = d->n_payload;
+  w->n_aux = d->n_aux;
+  w->T = 1 + d->n_payload + d->n_aux;
+  w->max_bag = std::max(1, d->max_bag);
+  w->n_procs = d->world_size / d->n_local;
+  w->capacity_rows = std::max<int64_t>(1, d->capacity_rows);
+  w->row_bytes.push_back(16);
+  w->tensor_desc.push_back(0);
+  for (int i = 0; i < d->n_payload + d->n_aux; ++i) {
+    const int64_t rb = d->row_bytes[i];
+    if (rb < 1) {
+      delete w;
+      throw Error{SB_ERR_CONFIG, "row bytes must be >= 1"};
+    }
+    if (i < d->n_payload && rb % d->n_heads != 0) {
+      delete w;
+      throw Error{SB_ERR_CONFIG, "payload width must be a positive multiple of n_heads"};
+    }
+    w->row_bytes.push_back(rb);
+    w->tensor_desc.push_back(i < d->n_payload ? 1 : 2);
+  }
+  try {
+    w->arena.assign(w->T, nullptr);
+    w->arena_bytes.assign(w->T, 0);
+    for (int t = 0; t < w->T; ++t) {
+      // metadata is replicated G-fold in the Ulysses layout
+      int64_t bytes = w->capacity_rows * w->row_bytes[t];
+      if (t == 0 || w->tensor_desc[t] == 2) bytes *= w->max_bag;
+      w->arena_bytes[t] = bytes;
+      SB_CUDA(cudaMalloc(&w->arena[t], (size_t)bytes));
+    }
+    SB_CUDA(cudaMalloc(&w->d_base, sizeof(uint64_t) * w->T * w->W));
+    SB_CUDA(cudaMalloc(&w->d_pitch, sizeof(int64_t) * w->T * w->W));
+    SB_CUDA(cudaMalloc(&w->d_rows, sizeof(int64_t) * w->W));
+    SB_CUDA(cudaMalloc(&w->d_headcol, sizeof(int32_t) * w->W));
+    SB_CUDA(cudaMalloc(&w->d_peer_arena, sizeof(uint64_t) * w->T * w->n_procs));
+    SB_CUDA(cudaMalloc(&w->d_arena_bytes, sizeof(int64_t) * w->T));
+    SB_CUDA(cudaMalloc(&w->d_status, sizeof(int32_t)));
+    SB_CUDA(cudaMemset(w->d_status, 0, sizeof(int32_t)));
+    SB_CUDA(cudaMemset(w->d_rows, 0, sizeof(int64_t) * w->W));
+    SB_CUDA(cudaMemset(w->d_headcol, 0, sizeof(int32_t) * w->W));
+    SB_CUDA(cudaMemset(w->d_base, 0, sizeof(uint64_t) * w->T * w->W));
+    SB_CUDA(cudaMemset(w->d_pitch, 0, sizeof(int64_t) * w->T * w->W));
+    SB_CUDA(cudaMemcpy(w->d_arena_bytes, w->arena_bytes.data(), sizeof(int64_t) * w->T, cudaMemcpyHostToDevice));
+    // single process: every "peer" slot is this process's arena
+    std::vector<uint64_t> pa((size_t)w->T * w->n_procs, 0);
+    const int me = w->first_local / w->n_local;
+    for (int t = 0; t < w->T; ++t) pa[(size_t)t * w->n_procs + me] = (uint64_t)w->arena[t];
+    SB_CUDA(cudaMemcpy(w->d_peer_arena, pa.data(), sizeof(uint64_t) * pa.size(), cudaMemcpyHostToDevice));
+  } catch (...) {
+    for (void* q : w->arena)
+      if (q) cudaFree(q);
+    delete w;
+    throw;
+  }
+  *out = w;
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_destroy(sb_world* w) {
+  SB_API_BEGIN
+  if (w) {
+    for (void* q : w->arena)
+      if (q) cudaFree(q);
+    void* ptrs[] = {w->d_base, w->d_pitch, w->d_rows, w->d_headcol, w->d_peer_arena, w->d_arena_bytes, w->d_status};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    delete w;
+  }
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_arena(const sb_world* w, int t, void** base, int64_t* bytes) {
+  SB_API_BEGIN
+  if (!w || t < 0 || t >= w->T) throw Error{SB_ERR_CONFIG, "sb_world_arena: bad tensor"};
+  if (base) *base = w->arena[t];
+  if (bytes) *bytes = w->arena_bytes[t];
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_tables(const sb_world* w, int t, const uint64_t** b, const int64_t** pitch,
+                                     const int64_t** rows) {
+  SB_API_BEGIN
+  if (!w || t < 0 || t >= w->T) throw Error{SB_ERR_CONFIG, "sb_world_tables: bad tensor"};
+  if (b) *b = w->d_base + (size_t)t * w->W;
+  if (pitch) *pitch = w->d_pitch + (size_t)t * w->W;
+  if (rows) *rows = w->d_rows;
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_set_peers(sb_world* w, int t, const uint64_t* host_bases, int n_procs) {
+  SB_API_BEGIN
+  if (!w || t < 0 || t >= w->T || n_procs != w->n_procs || !host_bases)
+    throw Error{SB_ERR_CONFIG, "sb_world_set_peers: bad arguments"};
+  SB_CUDA(cudaMemcpy(w->d_peer_arena + (size_t)t * w->n_procs, host_bases, sizeof(uint64_t) * n_procs,
+                     cudaMemcpyHostToDevice));
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, const int64_t* d_rank_off,
+                                            sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !d_lens || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_world_layout_origin: null argument"};
+  (void)d_lens;
+  cudaStream_t s = (cudaStream_t)stream;
+  sb::k_rank_rows<<<w->W, 256, 0, s>>>(d_lens, d_rank_off, w->d_rows);
+  SB_CHECK_LAUNCH();
+  sb::LayoutPlan lp{};
+  lp.rows_src = w->d_rows;
+  sb::WorldArgs a = sb::wargs(w);
+  sb::k_layout<<<1, 32, 0, s>>>(a, a, lp, sb::tinfo(w), 0);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(2);
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_fill_witness(sb_world* w, const uint64_t* d_ids, const int64_t* d_lens,
+                                           const int64_t* d_rank_off, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !d_ids || !d_lens || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_world_fill_witness: null argument"};
+  for (int t = 1; t < w->T; ++t)
+    if (w->tensor_desc[t] == 1 && w->row_bytes[t] % 8 != 0)
+      throw Error{SB_ERR_CONFIG, "witness payload must be whole doubles"};
+  sb::k_witness<<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w), d_ids, d_rank_off,
+                                                                   d_lens);
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_perturb(sb_world* w, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w) throw Error{SB_ERR_CONFIG, "null world"};
+  sb::k_perturb<<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w));
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_checksum(sb_world* w, uint64_t* d_acc, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !d_acc) throw Error{SB_ERR_CONFIG, "null argument"};
+  sb::k_checksum<<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w),
+                                                                    reinterpret_cast<unsigned long long*>(d_acc));
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
+  SB_API_END
+}
+
+extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_world* dst, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_route: null argument"};
+  if (src == dst) throw Error{SB_ERR_CONFIG, "sb_route is out-of-place: src and dst must differ"};
+  sb::check_compatible(p, src, dst);
+  cudaStream_t s = (cudaStream_t)stream;
+  sb::ensure_jobs(p, p->max_chunks * src->T);
+  p->current_op = reverse ? 1 : 0;
+  sb::LayoutPlan lp{};
+  lp.rows_src = reverse ? p->origin_rows : p->target_rows;
+  sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
+  SB_CHECK_LAUNCH();
+  sb::k_jobs_route<<<std::min<int64_t>(1184, (p->max_chunks * src->T + 255) / 256), 256, 0, s>>>(
+      sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), reverse);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(2);
+  sb::run_copy(p, s);
+  SB_API_END
+}
+
+static void ulysses(sb_planner* p, sb_world* src, sb_world* dst, cudaStream_t s, int post) {
+  if (p->identity) throw Error{SB_ERR_CONFIG, "Ulysses transforms need a balanced plan (not identity_plan)"};
+  sb::check_compatible(p, src, dst);
+  if (src == dst) throw Error{SB_ERR_CONFIG, "Ulysses transforms are out-of-place: src and dst must differ"};
+  if (p->n_heads % p->max_bag != 0 || src->n_heads % p->max_bag != 0)
+    throw Error{SB_ERR_CONFIG, "pre_attn: bag of " + std::to_string(p->max_bag) +
+                                   " GPUs does not divide n_heads " + std::to_string(src->n_heads)};
+  for (int b = 0; b < p->M; ++b)
+    if (src->n_heads % p->bag_size[b] != 0)
+      throw Error{SB_ERR_CONFIG, "pre_attn: bag of " + std::to_string(p->bag_size[b]) +
+                                     " GPUs does not divide n_heads " + std::to_string(src->n_heads)};
+  if (dst->max_bag < p->max_bag) throw Error{SB_ERR_CONFIG, "world max_bag smaller than the topology's bags"};
+  sb::ensure_jobs(p, p->max_chunks * p->max_bag * src->T);
+  p->current_op = post ? 3 : 2;
+  sb::LayoutPlan lp{};
+  lp.rank_bag = p->d_rank_bag;
+  lp.rank_member = p->d_rank_member;
+  lp.bag_size = p->d_bag_size;
+  lp.bag_rows = p->bag_rows;
+  lp.target_rows = p->target_rows;
+  lp.U = p->U;
+  lp.M = p->M;
+  sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), post ? 2 : 1);
+  SB_CHECK_LAUNCH();
+  const int64_t total = p->max_chunks * p->max_bag * src->T;
+  sb::k_jobs_ulysses<<<std::min<int64_t>(1184, (total + 255) / 256), 256, 0, s>>>(
+      sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), post);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(2);
+  sb::run_copy(p, s);
+}
+
+extern "C" sb_status sb_pre_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_pre_attn: null argument"};
+  ulysses(p, src, dst, (cudaStream_t)stream, 0);
+  SB_API_END
+}
+
+extern "C" sb_status sb_post_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_post_attn: null argument"};
+  ulysses(p, src, dst, (cudaStream_t)stream, 1);
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_status(sb_world* w, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w) throw Error{SB_ERR_CONFIG, "null world"};
+  SB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int32_t st = 0;
+  SB_CUDA(cudaMemcpy(&st, w->d_status, sizeof st, cudaMemcpyDeviceToHost));
+  if (st & sb::ST_LAYOUT) throw Error{SB_ERR_CAPACITY, "world arena too small for the requested layout"};
+  if (st) throw Error{SB_ERR_INTEGRITY, "world status " + std::to_string(st)};
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_upload(sb_world* w, void* const* host, const int64_t* bytes, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !host || !bytes) throw Error{SB_ERR_CONFIG, "sb_world_upload: null argument"};
+  for (int t = 0; t < w->T; ++t) {
+    if (bytes[t] > w->arena_bytes[t]) throw Error{SB_ERR_CAPACITY, "sb_world_upload: image larger than arena"};
+    if (host[t] && bytes[t] > 0)
+      SB_CUDA(cudaMemcpyAsync(w->arena[t], host[t], (size_t)bytes[t], cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  }
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_download(sb_world* w, void* const* host, const int64_t* bytes, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !host || !bytes) throw Error{SB_ERR_CONFIG, "sb_world_download: null argument"};
+  for (int t = 0; t < w->T; ++t) {
+    if (bytes[t] > w->arena_bytes[t]) throw Error{SB_ERR_CAPACITY, "sb_world_download: image larger than arena"};
+    if (host[t] && bytes[t] > 0)
+      SB_CUDA(cudaMemcpyAsync(host[t], w->arena[t], (size_t)bytes[t], cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  }
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_shape(sb_world* w, int t, int64_t* rows, int64_t* pitch, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || t < 0 || t >= w->T) throw Error{SB_ERR_CONFIG, "sb_world_shape: bad tensor"};
+  SB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (rows) SB_CUDA(cudaMemcpy(rows, w->d_rows, sizeof(int64_t) * w->W, cudaMemcpyDeviceToHost));
+  if (pitch) SB_CUDA(cudaMemcpy(pitch, w->d_pitch + (size_t)t * w->W, sizeof(int64_t) * w->W, cudaMemcpyDeviceToHost));
+  SB_API_END
+}
+
+static void rank_span(sb_world* w, int t, int rank, cudaStream_t s, uint64_t* base, int64_t* bytes) {
+  if (!w || t < 0 || t >= w->T || rank < 0 || rank >= w->W) throw Error{SB_ERR_CONFIG, "bad tensor or rank"};
+  SB_CUDA(cudaStreamSynchronize(s));
+  int64_t rows = 0, pitch = 0;
+  SB_CUDA(cudaMemcpy(&rows, w->d_rows + rank, sizeof rows, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(&pitch, w->d_pitch + (size_t)t * w->W + rank, sizeof pitch, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(base, w->d_base + (size_t)t * w->W + rank, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  *bytes = rows * pitch;
+}
+
+extern "C" sb_status sb_world_read_rank(sb_world* w, int t, int rank, void* host, int64_t capacity, int64_t* bytes,
+                                        sb_stream stream) {
+  SB_API_BEGIN
+  uint64_t base = 0;
+  int64_t n = 0;
+  rank_span(w, t, rank, (cudaStream_t)stream, &base, &n);
+  if (bytes) *bytes = n;
+  if (host) {
+    if (capacity < n) throw Error{SB_ERR_CAPACITY, "sb_world_read_rank: host buffer too small"};
+    if (n > 0) SB_CUDA(cudaMemcpy(host, reinterpret_cast<void*>(base), (size_t)n, cudaMemcpyDeviceToHost));
+  }
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_write_rank(sb_world* w, int t, int rank, const void* host, int64_t bytes,
+                                         sb_stream stream) {
+  SB_API_BEGIN
+  uint64_t base = 0;
+  int64_t n = 0;
+  rank_span(w, t, rank, (cudaStream_t)stream, &base, &n);
+  if (bytes != n) throw Error{SB_ERR_INTEGRITY, "sb_world_write_rank: byte count does not match the layout"};
+  if (n > 0) SB_CUDA(cudaMemcpy(reinterpret_cast<void*>(base), host, (size_t)n, cudaMemcpyHostToDevice));
+  SB_API_END
+}
+
+extern "C" sb_status sb_copy_timing(sb_planner* p, int op, int64_t* count, double* total_us) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  int64_t n = 0;
+  double us = 0;
+  for (size_t i = 0; i + 1 < p->copy_used; i += 2) {
+    if (op >= 0 && p->copy_op[i / 2] != op) continue;
+    SB_CUDA(cudaEventSynchronize(p->copy_ev[i + 1]));
+    float ms = 0.f;
+    SB_CUDA(cudaEventElapsedTime(&ms, p->copy_ev[i], p->copy_ev[i + 1]));
+    us += 1000.0 * ms;
+    ++n;
+  }
+  if (count) *count = n;
+  if (total_us) *total_us = us;
+  SB_API_END
+}
+
+extern "C" sb_status sb_copy_timing_reset(sb_planner* p) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  p->copy_used = 0;
+  SB_API_END
+}
+
+extern "C" sb_status sb_last_exchange_bytes(const sb_planner* p, int64_t* bytes_read, int64_t* bytes_written) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  int64_t b = 0;
+  if (p->n_jobs) SB_CUDA(cudaMemcpy(&b, p->n_jobs + 1, sizeof b, cudaMemcpyDeviceToHost));
+  if (bytes_read) *bytes_read = b;
+  if (bytes_written) *bytes_written = b;
+  SB_API_END
+}

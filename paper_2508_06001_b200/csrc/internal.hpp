@@ -1,0 +1,117 @@
+// Host-side objects behind the opaque C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "seqbal_capi.h"
+
+// One copy job: n_rows rows of `width` bytes from src (row pitch spitch) to
+// dst (row pitch dpitch).  Built on the device from a plan.
+struct SbJob {
+  uint64_t src;
+  uint64_t dst;
+  int64_t n_rows;
+  int64_t width;
+  int64_t spitch;
+  int64_t dpitch;
+};
+
+struct sb_planner {
+  int W = 0, U = 0, M = 0, R = 0;
+  int d_model = 0, n_heads = 0, d_head = 0, n_blocks = 0;
+  double gamma = 0, k = 0;
+  int64_t max_seqs = 0, max_chunks = 0;
+  int max_bag = 1;
+  std::vector<int32_t> bag_off, bag_ranks, bag_size, rank_bag, rank_member;
+  bool identity = false;
+  bool any_multi_bag = false;
+
+  // constant topology tables (device)
+  int32_t *d_bag_off = nullptr, *d_bag_ranks = nullptr, *d_bag_size = nullptr;
+  int32_t *d_rank_bag = nullptr, *d_rank_member = nullptr;
+
+  // inputs of the last plan (device, caller-owned)
+  const uint64_t* ids = nullptr;
+  const int64_t* lens = nullptr;
+  const int64_t* rank_off = nullptr;
+
+  // per-sequence scratch (max_seqs)
+  double* w = nullptr;
+  int32_t* seq_rank = nullptr;
+  int64_t* seq_off = nullptr;
+  uint64_t* hash = nullptr;  // 2*max_seqs
+  uint64_t *sk_hi = nullptr, *sk_lo = nullptr, *tk_hi = nullptr, *tk_lo = nullptr;
+  uint32_t *sk_v = nullptr, *tk_v = nullptr;
+  double* sorted_w = nullptr;
+  int32_t* sorted_idx = nullptr;
+  int32_t* pick = nullptr;
+  int32_t* seq_bag = nullptr;
+  int32_t* seq_G = nullptr;
+  int64_t* seq_chunk_base = nullptr;
+
+  // per replica / bag / rank
+  double* rep_total = nullptr;       // R
+  int32_t* sentinel = nullptr;       // R
+  int32_t* bag_count = nullptr;      // R*M
+  int64_t* bag_rows = nullptr;       // R*M
+  int64_t* rep_chunks = nullptr;     // R
+  unsigned long long* send_count = nullptr;  // W
+
+  // plan (device)
+  int64_t* n_chunks = nullptr;
+  int64_t* n_seqs = nullptr;
+  uint64_t* c_id = nullptr;
+  int32_t *c_idx = nullptr, *c_src = nullptr, *c_dst = nullptr;
+  int64_t *c_start = nullptr, *c_end = nullptr, *c_src_row = nullptr, *c_dst_row = nullptr;
+  int64_t* c_seq_base = nullptr;  // per chunk (q,0): row base of the sequence in its bag's full layout
+  int64_t *send_off = nullptr, *recv_off = nullptr;
+  int32_t *send_idx = nullptr, *recv_idx = nullptr, *rev_recv_idx = nullptr;
+  int64_t *origin_rows = nullptr, *target_rows = nullptr;
+  double *per_gpu = nullptr, *per_bag_occ = nullptr, *total = nullptr, *wir = nullptr;
+  int32_t* violations = nullptr;
+  int32_t* status = nullptr;
+
+  // exchange job scratch (grown on demand)
+  SbJob* jobs = nullptr;
+  int64_t* piece_off = nullptr;
+  int64_t* n_jobs = nullptr;
+  int64_t job_cap = 0;
+  int64_t last_bytes_read = 0, last_bytes_written = 0;
+
+  // copy-kernel event pairs recorded while timing is on: (start, stop, op)
+  std::vector<cudaEvent_t> copy_ev;
+  std::vector<int> copy_op;
+  size_t copy_used = 0;
+  int current_op = 0;
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
+  float last_ms[5] = {};
+};
+
+struct sb_world {
+  int W = 0, n_local = 0, first_local = 0, n_heads = 0, n_payload = 0, n_aux = 0, T = 0, max_bag = 1;
+  int n_procs = 1;
+  int64_t capacity_rows = 0;
+  std::vector<int64_t> row_bytes;    // T (tensor 0 = 16-byte metadata)
+  std::vector<void*> arena;          // T
+  std::vector<int64_t> arena_bytes;  // T
+  uint64_t* d_base = nullptr;        // T*W
+  int64_t* d_pitch = nullptr;        // T*W
+  int64_t* d_rows = nullptr;         // W
+  int32_t* d_headcol = nullptr;      // W: first global payload column held (doubles)
+  uint64_t* d_peer_arena = nullptr;  // T*n_procs
+  int64_t* d_arena_bytes = nullptr;  // T
+  int32_t* d_status = nullptr;
+  std::vector<int64_t> tensor_desc;  // flags: 0 meta, 1 payload, 2 aux
+};
+
+namespace sb {
+void ensure_jobs(sb_planner* p, int64_t cap);
+}

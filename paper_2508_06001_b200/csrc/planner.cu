@@ -1,0 +1,916 @@
+// Device planner: the reference's plan_routing (balancer.cpp:105-225),
+// identity_plan (:227-240) and the receive order of reverse_plan (:242-287),
+// reproduced bit-exactly on the GPU.
+//
+// Pipeline (one stream, no host synchronisation, graph-capturable):
+//   k_prep      W CTAs     workloads (FP64, reference operation order), per
+//                          rank row offsets (block scan), duplicate-id hash
+//   k_sort      2R+1 CTAs  per replica sort by (workload desc, id asc);
+//                          serial per-replica and global FP64 totals
+//   k_greedy    R warps    the multi-knapsack greedy: lane = bag, warp
+//                          argmin via REDUX, speculative division
+//   k_emit      R CTAs     stable bag partition (match_any + scan) and
+//                          chunk emission in the reference's chunk order
+//   k_lists     W CTAs     send/recv manifests, receive-side row offsets,
+//                          reverse receive order, Ulysses sequence bases
+//   k_finalize  1 CTA      WIR, chunk count
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <new>
+
+#include "block_sort.cuh"
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace sb {
+
+constexpr int kMaxBags = 64;  // bags per replica handled by k_emit's shared tables
+
+struct PlanArgs {
+  int W, U, M, R;
+  double d_model, gamma;
+  int64_t max_seqs;
+  const int32_t *bag_off, *bag_ranks, *bag_size, *rank_bag, *rank_member;
+  const uint64_t* ids;
+  const int64_t* lens;
+  const int64_t* rank_off;
+  double* w;
+  int32_t* seq_rank;
+  int64_t* seq_off;
+  uint64_t* hash;
+  uint64_t *sk_hi, *sk_lo, *tk_hi, *tk_lo;
+  uint32_t *sk_v, *tk_v;
+  double* sorted_w;
+  int32_t* sorted_idx;
+  int32_t* pick;
+  int32_t *seq_bag, *seq_G;
+  int64_t* seq_chunk_base;
+  double* rep_total;
+  int32_t* sentinel;
+  int32_t* bag_count;
+  int64_t* bag_rows;
+  int64_t* rep_chunks;
+  unsigned long long* send_count;
+  int64_t *n_chunks, *n_seqs;
+  uint64_t* c_id;
+  int32_t *c_idx, *c_src, *c_dst;
+  int64_t *c_start, *c_end, *c_src_row, *c_dst_row, *c_seq_base;
+  int64_t *send_off, *recv_off;
+  int32_t *send_idx, *recv_idx, *rev_recv_idx;
+  int64_t *origin_rows, *target_rows;
+  double *per_gpu, *per_bag_occ, *total, *wir;
+  int32_t* violations;
+  int32_t* status;
+};
+
+__device__ __forceinline__ bool seqs_ok(const PlanArgs& a) { return a.rank_off[a.W] <= a.max_seqs; }
+
+__device__ __forceinline__ double occupancy(double asg, double cap) {  // balancer.cpp:32-35
+  if (cap > 0.0) return __ddiv_rn(asg, cap);
+  return asg > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
+}
+
+__device__ __forceinline__ uint64_t hash_slot(uint64_t id) { return splitmix64(id ^ 0x5eedULL); }
+
+// ------------------------------------------------------------------ k_prep
+__global__ void __launch_bounds__(256) k_prep(PlanArgs a) {
+  __shared__ int64_t sh[33];
+  const int r = blockIdx.x;
+  if (!seqs_ok(a)) {
+    if (r == 0 && threadIdx.x == 0) atomicOr(a.status, ST_CAPACITY);
+    return;
+  }
+  const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
+  const int rep = r / a.U;
+  const int64_t rlo = a.rank_off[rep * a.U], rhi = a.rank_off[rep * a.U + a.U];
+  const int64_t tsize = 2 * (rhi - rlo);
+  uint64_t* tab = a.hash + 2 * rlo;
+  int64_t carry = 0;
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < hi;
+    int64_t len = 0;
+    if (valid) {
+      len = a.lens[i];
+      if (len < 0) {
+        atomicOr(a.status, ST_NEG_LENGTH);
+        len = 0;
+      }
+      a.w[i] = gamma_weighted_workload(len, a.d_model, a.gamma);  // balancer.cpp:144
+      a.seq_rank[i] = r;
+      // duplicate sample_id detection inside the replica (open addressing)
+      const uint64_t id = a.ids[i];
+      if (id == ~0ull) {
+        if (atomicAdd(&a.sentinel[rep], 1) > 0) atomicOr(a.status, ST_DUP_ID);
+      } else {
+        uint64_t s = hash_slot(id) % (uint64_t)tsize;
+        while (true) {
+          const unsigned long long old =
+              atomicCAS(reinterpret_cast<unsigned long long*>(tab + s), ~0ull, (unsigned long long)id);
+          if (old == ~0ull) break;
+          if (old == id) {
+            atomicOr(a.status, ST_DUP_ID);
+            break;
+          }
+          s = (s + 1 == (uint64_t)tsize) ? 0 : s + 1;
+        }
+      }
+    }
+    int64_t tot;
+    const int64_t ex = block_excl_scan<int64_t>(len, sh, &tot);
+    if (valid) a.seq_off[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    a.origin_rows[r] = carry;
+    a.send_count[r] = 0;
+  }
+}
+
+// ------------------------------------------------------------------ k_sort
+__global__ void __launch_bounds__(1024) k_sort(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (!seqs_ok(a)) return;
+  const int b = blockIdx.x;
+  if (b < a.R) {
+    const int64_t lo = a.rank_off[b * a.U], hi = a.rank_off[b * a.U + a.U];
+    const int64_t n = hi - lo;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      // (workload desc, sample_id asc) == ascending (~bits(w), id): w >= 0,
+      // so its IEEE bits are monotone in value (balancer.cpp:37-40).
+      a.sk_hi[lo + i] = ~(uint64_t)__double_as_longlong(a.w[lo + i]);
+      a.sk_lo[lo + i] = a.ids[lo + i];
+      a.sk_v[lo + i] = (uint32_t)i;
+    }
+    __syncthreads();
+    block_sort(n, a.sk_hi + lo, a.sk_lo + lo, a.sk_v + lo, a.tk_hi + lo, a.tk_lo + lo, a.tk_v + lo, smem);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const int64_t s = lo + a.sk_v[lo + i];
+      a.sorted_idx[lo + i] = (int32_t)s;
+      a.sorted_w[lo + i] = a.w[s];
+    }
+  } else if (b < 2 * a.R) {
+    // per-replica total in gather order (balancer.cpp:24-25): a dependent
+    // FP64 chain, so one lane; loads are issued ahead of the adds.
+    if (threadIdx.x != 0) return;
+    const int rep = b - a.R;
+    const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+    double s = 0.0;
+    int64_t i = lo;
+    for (; i + 8 <= hi; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = a.w[i + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
+    }
+    for (; i < hi; ++i) s = __dadd_rn(s, a.w[i]);
+    a.rep_total[rep] = s;
+  } else {
+    // BalanceReport::total_workload: one running sum over every replica in
+    // gather order (balancer.cpp:147).
+    if (threadIdx.x != 0) return;
+    const int64_t n = a.rank_off[a.W];
+    double s = 0.0;
+    int64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = a.w[i + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
+    }
+    for (; i < n; ++i) s = __dadd_rn(s, a.w[i]);
+    *a.total = s;
+    *a.n_seqs = n;
+  }
+}
+
+// ---------------------------------------------------------------- k_greedy
+// balancer.cpp:44-62.  One warp per replica; bag j lives in lane j%32, slot
+// j/32.  Per sequence every lane forms key = (infeasible << 63 | bits(occ))
+// for its bags; the warp takes the lexicographic minimum of (key, j), which
+// is exactly "feasible bag with minimum occupancy, else global minimum, ties
+// to the lowest bag id".  The winner's next occupancy is computed
+// speculatively by every lane so the division is off the critical path.
+template <int BPL>
+__global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  const int rep = blockIdx.x, lane = threadIdx.x;
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  const int64_t n = hi - lo;
+  const double target = __ddiv_rn(a.rep_total[rep], (double)a.U);  // balancer.cpp:26
+  double cap[BPL], asg[BPL], occ[BPL], rem[BPL];
+  int cnt[BPL];
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    const int j = lane + 32 * i;
+    const int size = j < a.M ? a.bag_size[j] : 0;
+    cap[i] = __dmul_rn((double)size, target);  // balancer.cpp:30
+    asg[i] = 0.0;
+    occ[i] = occupancy(0.0, cap[i]);
+    rem[i] = __dsub_rn(cap[i], 0.0);
+    cnt[i] = 0;
+  }
+  int viol = 0;
+  for (int64_t p0 = 0; p0 < n; p0 += 32) {
+    const double w_lane = (p0 + lane < n) ? a.sorted_w[lo + p0 + lane] : 0.0;
+    const int steps = (n - p0) < 32 ? (int)(n - p0) : 32;
+    int my_pick = 0;
+    for (int t = 0; t < steps; ++t) {
+      const double w = __shfl_sync(0xffffffffu, w_lane, t);
+      double nasg[BPL], nocc[BPL], nrem[BPL];
+      uint64_t best_key = ~0ull;
+      uint32_t best_j = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < BPL; ++i) {
+        nasg[i] = __dadd_rn(asg[i], w);
+        nocc[i] = occupancy(nasg[i], cap[i]);
+        nrem[i] = __dsub_rn(cap[i], nasg[i]);
+        const uint32_t j = lane + 32 * i;
+        if (j < (uint32_t)a.M) {
+          const bool feasible = rem[i] >= w;  // cap - asg >= w (balancer.cpp:50)
+          const uint64_t key = (feasible ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ[i]);
+          if (key < best_key) {
+            best_key = key;
+            best_j = j;
+          }
+        }
+      }
+      const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
+      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      const uint32_t pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+      viol += (int)(m1 >> 31);  // no feasible bag -> fallback -> capacity violation
+#pragma unroll
+      for (int i = 0; i < BPL; ++i) {
+        if ((uint32_t)(lane + 32 * i) == pick) {
+          asg[i] = nasg[i];
+          occ[i] = nocc[i];
+          rem[i] = nrem[i];
+          cnt[i]++;
+        }
+      }
+      if (lane == t) my_pick = (int)pick;
+    }
+    if (p0 + lane < n) a.pick[lo + p0 + lane] = my_pick;
+  }
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < a.M) {
+      a.bag_count[rep * a.M + j] = cnt[i];
+      a.per_bag_occ[rep * a.M + j] = occ[i];  // balancer.cpp:170-175 (replay == greedy)
+      const int g = a.bag_size[j];
+      const double per = __ddiv_rn(asg[i], (double)g);  // balancer.cpp:199-202
+      for (int k = 0; k < g; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[j] + k]] = per;
+    }
+  }
+  if (lane == 0) atomicAdd(a.violations, viol);
+}
+
+// ------------------------------------------------------------------ k_emit
+// balancer.cpp:178-218.  Sequences of bag b in assignment order get index q
+// (a stable partition of the greedy order by bag); chunk k of (b, q) is
+// global chunk rep_base + bag_base[b] + q*G_b + k and targets the bag's k-th
+// rank.
+__device__ void replica_bases(const PlanArgs& a, int rep, int64_t* rep_base, int64_t* bag_base) {
+  // rep_base = chunks of earlier replicas; bag_base[b] within this replica.
+  int64_t rb = 0;
+  for (int r = 0; r < rep; ++r)
+    for (int b = 0; b < a.M; ++b) rb += (int64_t)a.bag_count[r * a.M + b] * a.bag_size[b];
+  *rep_base = rb;
+  int64_t acc = 0;
+  for (int b = 0; b < a.M; ++b) {
+    bag_base[b] = acc;
+    acc += (int64_t)a.bag_count[rep * a.M + b] * a.bag_size[b];
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
+  __shared__ int warp_cnt[32][kMaxBags];
+  __shared__ int running[kMaxBags];
+  __shared__ int64_t bag_base[kMaxBags];
+  __shared__ int64_t rep_base;
+  if (!seqs_ok(a)) return;
+  const int rep = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    replica_bases(a, rep, &rep_base, bag_base);
+    int64_t c = 0;
+    for (int b = 0; b < a.M; ++b) c += (int64_t)a.bag_count[rep * a.M + b] * a.bag_size[b];
+    a.rep_chunks[rep] = c;
+  }
+  if (tid < a.M) running[tid] = 0;
+  __syncthreads();
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t tile = lo; tile < hi; tile += blockDim.x) {
+    for (int e = tid; e < 32 * a.M; e += blockDim.x) warp_cnt[e / a.M][e % a.M] = 0;
+    __syncthreads();
+    const int64_t p = tile + tid;
+    const bool valid = p < hi;
+    const int b = valid ? a.pick[p] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int rank_in = __popc(peers & lt_mask);
+    if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
+    __syncthreads();
+    if (tid < a.M) {
+      int run = running[tid];
+      for (int w = 0; w < 32; ++w) {
+        const int c = warp_cnt[w][tid];
+        warp_cnt[w][tid] = run;
+        run += c;
+      }
+      running[tid] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      const int q = warp_cnt[warp][b] + rank_in;
+      const int s = a.sorted_idx[p];
+      const int64_t l = a.lens[s] < 0 ? 0 : a.lens[s];
+      const int g = a.bag_size[b];
+      const int64_t cb = rep_base + bag_base[b] + (int64_t)q * g;
+      const uint64_t id = a.ids[s];
+      const int src = a.seq_rank[s];
+      const int64_t soff = a.seq_off[s];
+      for (int k = 0; k < g; ++k) {
+        const int64_t c = cb + k;
+        const int64_t st = chunk_start(l, g, k);
+        a.c_id[c] = id;
+        a.c_idx[c] = k;
+        a.c_start[c] = st;
+        a.c_end[c] = st + chunk_len(l, g, k);
+        a.c_src[c] = src;
+        a.c_dst[c] = rep * a.U + a.bag_ranks[a.bag_off[b] + k];
+        a.c_src_row[c] = soff + st;
+      }
+      a.seq_bag[s] = b;
+      a.seq_G[s] = g;
+      a.seq_chunk_base[s] = cb;
+      atomicAdd(&a.send_count[src], (unsigned long long)g);
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------- k_lists
+// One CTA per global rank r.  Builds
+//   recv[r]      = chunks (q, k) of r's bag member slot k, q ascending
+//                  (finalize_manifests, balancer.cpp:84-91), plus the
+//                  receive-side row offsets (target packing, :93-101);
+//   send[r]      = chunks with source r in chunk order: r's sequences sorted
+//                  by their first chunk index, each expanded to G chunks;
+//   rev_recv[r]  = reverse_plan's receive order (:259-285): r's sequences in
+//                  buffer order, chunks by start (chunk index breaks the
+//                  zero-length ties);
+//   c_seq_base   = row base of each sequence in its bag's full-sequence
+//                  layout (pre_attn shells, exchange.cpp:291-295).
+__global__ void __launch_bounds__(1024) k_lists(PlanArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t sh[33];
+  __shared__ int64_t s_recv_off, s_send_off, s_rep_base;
+  __shared__ int64_t s_bag_base[kMaxBags];
+  if (!seqs_ok(a)) return;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const int rep = r / a.U, u = r % a.U;
+  const int b = a.rank_bag[u], k = a.rank_member[u];
+  const int g = a.bag_size[b];
+  const int n_b = a.bag_count[rep * a.M + b];
+  if (tid == 0) {
+    replica_bases(a, rep, &s_rep_base, s_bag_base);
+    int64_t ro = 0, so = 0;
+    for (int x = 0; x < r; ++x) {
+      const int xr = x / a.U, xu = x % a.U;
+      ro += a.bag_count[xr * a.M + a.rank_bag[xu]];
+      so += (int64_t)a.send_count[x];
+    }
+    s_recv_off = ro;
+    s_send_off = so;
+    a.recv_off[r] = ro;
+    a.send_off[r] = so;
+    if (r == a.W - 1) {
+      a.recv_off[a.W] = ro + n_b;
+      a.send_off[a.W] = so + (int64_t)a.send_count[r];
+    }
+  }
+  __syncthreads();
+  const int64_t cb0 = s_rep_base + s_bag_base[b];
+  // recv list and target row offsets
+  int64_t carry = 0;
+  for (int64_t q0 = 0; q0 < n_b; q0 += blockDim.x) {
+    const int64_t q = q0 + tid;
+    const bool valid = q < n_b;
+    const int64_t c = cb0 + q * g + k;
+    const int64_t len = valid ? a.c_end[c] - a.c_start[c] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan<int64_t>(len, sh, &tot);
+    if (valid) {
+      a.c_dst_row[c] = carry + ex;
+      a.recv_idx[s_recv_off + q] = (int32_t)c;
+    }
+    carry += tot;
+  }
+  if (tid == 0) a.target_rows[r] = carry;
+  // Ulysses: per-sequence base rows in the bag's full layout (member 0 only)
+  if (k == 0) {
+    int64_t c2 = 0;
+    for (int64_t q0 = 0; q0 < n_b; q0 += blockDim.x) {
+      const int64_t q = q0 + tid;
+      const bool valid = q < n_b;
+      const int64_t c = cb0 + q * g;
+      const int64_t full = valid ? a.c_end[c + g - 1] : 0;  // last chunk ends at l
+      int64_t tot;
+      const int64_t ex = block_excl_scan<int64_t>(full, sh, &tot);
+      if (valid) a.c_seq_base[c] = c2 + ex;
+      c2 += tot;
+    }
+    if (tid == 0) a.bag_rows[rep * a.M + b] = c2;
+  }
+  // send list: rank r's sequences ordered by first chunk index
+  const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
+  const int64_t n = hi - lo;
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    a.sk_hi[lo + i] = (uint64_t)a.seq_chunk_base[lo + i];
+    a.sk_lo[lo + i] = 0;
+    a.sk_v[lo + i] = (uint32_t)i;
+  }
+  __syncthreads();
+  block_sort(n, a.sk_hi + lo, a.sk_lo + lo, a.sk_v + lo, a.tk_hi + lo, a.tk_lo + lo, a.tk_v + lo, smem);
+  int64_t c3 = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int64_t i = i0 + tid;
+    const bool valid = i < n;
+    const int64_t s = valid ? lo + a.sk_v[lo + i] : 0;
+    const int gs = valid ? a.seq_G[s] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
+    if (valid) {
+      const int64_t cb = a.seq_chunk_base[s];
+      for (int kk = 0; kk < gs; ++kk) a.send_idx[s_send_off + c3 + ex + kk] = (int32_t)(cb + kk);
+    }
+    c3 += tot;
+  }
+  // reverse receive order: sequences in buffer order, chunks ascending
+  int64_t c4 = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int64_t i = i0 + tid;
+    const bool valid = i < n;
+    const int gs = valid ? a.seq_G[lo + i] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
+    if (valid) {
+      const int64_t cb = a.seq_chunk_base[lo + i];
+      for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[s_send_off + c4 + ex + kk] = (int32_t)(cb + kk);
+    }
+    c4 += tot;
+  }
+}
+
+// -------------------------------------------------------------- k_finalize
+__global__ void k_finalize(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  if (threadIdx.x == 0) {
+    int64_t c = 0;
+    for (int r = 0; r < a.R; ++r) c += a.rep_chunks[r];
+    *a.n_chunks = c;
+    // workload_imbalance_ratio (metrics.cpp:20-31)
+    double lo = a.per_gpu[0], hi = a.per_gpu[0];
+    for (int r = 0; r < a.W; ++r) {
+      lo = fmin(lo, a.per_gpu[r]);
+      hi = fmax(hi, a.per_gpu[r]);
+    }
+    double wir;
+    if (hi == 0.0) wir = 1.0;
+    else if (lo == 0.0) wir = __longlong_as_double(0x7ff0000000000000ll);
+    else wir = __ddiv_rn(hi, lo);
+    *a.wir = wir;
+  }
+}
+
+// -------------------------------------------------------- identity kernels
+// identity_plan (balancer.cpp:227-240): chunk i = sequence i, src = dst.
+__global__ void k_identity(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  const int64_t n = a.rank_off[a.W];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = a.lens[i] < 0 ? 0 : a.lens[i];
+    const int r = a.seq_rank[i];
+    a.c_id[i] = a.ids[i];
+    a.c_idx[i] = 0;
+    a.c_start[i] = 0;
+    a.c_end[i] = l;
+    a.c_src[i] = r;
+    a.c_dst[i] = r;
+    a.c_src_row[i] = a.seq_off[i];
+    a.c_dst_row[i] = a.seq_off[i];
+    a.send_idx[i] = (int32_t)i;
+    a.recv_idx[i] = (int32_t)i;
+    a.rev_recv_idx[i] = (int32_t)i;
+    a.seq_G[i] = 1;
+    a.seq_chunk_base[i] = i;
+  }
+  if (blockIdx.x == 0) {
+    for (int r = threadIdx.x; r <= a.W; r += blockDim.x) {
+      a.send_off[r] = a.rank_off[r];
+      a.recv_off[r] = a.rank_off[r];
+      if (r < a.W) a.target_rows[r] = a.origin_rows[r];
+    }
+  }
+}
+
+// Report for the no-balancer case, as simulator.cpp:76-86 computes it:
+// per-rank sums in gather order, then WIR.
+__global__ void k_identity_report(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < a.W) {
+    double s = 0.0;
+    for (int64_t i = a.rank_off[r]; i < a.rank_off[r + 1]; ++i) s = __dadd_rn(s, a.w[i]);
+    a.per_gpu[r] = s;
+  }
+}
+
+__global__ void k_identity_finalize(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  if (threadIdx.x == 0) {
+    *a.n_chunks = a.rank_off[a.W];
+    double lo = a.per_gpu[0], hi = a.per_gpu[0];
+    for (int r = 0; r < a.W; ++r) {
+      lo = fmin(lo, a.per_gpu[r]);
+      hi = fmax(hi, a.per_gpu[r]);
+    }
+    *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
+  }
+}
+
+// ------------------------------------------------------------------ host
+template <typename T>
+static void dalloc(T** p, int64_t n) {
+  SB_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (size_t)(n > 0 ? n : 1)));
+}
+
+static PlanArgs make_args(sb_planner* p) {
+  PlanArgs a;
+  a.W = p->W; a.U = p->U; a.M = p->M; a.R = p->R;
+  a.d_model = (double)p->d_model; a.gamma = p->gamma; a.max_seqs = p->max_seqs;
+  a.bag_off = p->d_bag_off; a.bag_ranks = p->d_bag_ranks; a.bag_size = p->d_bag_size;
+  a.rank_bag = p->d_rank_bag; a.rank_member = p->d_rank_member;
+  a.ids = p->ids; a.lens = p->lens; a.rank_off = p->rank_off;
+  a.w = p->w; a.seq_rank = p->seq_rank; a.seq_off = p->seq_off; a.hash = p->hash;
+  a.sk_hi = p->sk_hi; a.sk_lo = p->sk_lo; a.tk_hi = p->tk_hi; a.tk_lo = p->tk_lo;
+  a.sk_v = p->sk_v; a.tk_v = p->tk_v;
+  a.sorted_w = p->sorted_w; a.sorted_idx = p->sorted_idx; a.pick = p->pick;
+  a.seq_bag = p->seq_bag; a.seq_G = p->seq_G; a.seq_chunk_base = p->seq_chunk_base;
+  a.rep_total = p->rep_total; a.sentinel = p->sentinel; a.bag_count = p->bag_count;
+  a.bag_rows = p->bag_rows; a.rep_chunks = p->rep_chunks; a.send_count = p->send_count;
+  a.n_chunks = p->n_chunks; a.n_seqs = p->n_seqs;
+  a.c_id = p->c_id; a.c_idx = p->c_idx; a.c_src = p->c_src; a.c_dst = p->c_dst;
+  a.c_start = p->c_start; a.c_end = p->c_end; a.c_src_row = p->c_src_row; a.c_dst_row = p->c_dst_row;
+  a.c_seq_base = p->c_seq_base;
+  a.send_off = p->send_off; a.recv_off = p->recv_off; a.send_idx = p->send_idx;
+  a.recv_idx = p->recv_idx; a.rev_recv_idx = p->rev_recv_idx;
+  a.origin_rows = p->origin_rows; a.target_rows = p->target_rows;
+  a.per_gpu = p->per_gpu; a.per_bag_occ = p->per_bag_occ; a.total = p->total; a.wir = p->wir;
+  a.violations = p->violations; a.status = p->status;
+  return a;
+}
+
+static void planner_alloc(sb_planner* p) {
+  const int64_t N = p->max_seqs, C = p->max_chunks, W = p->W, R = p->R, M = p->M;
+  dalloc(&p->d_bag_off, M + 1); dalloc(&p->d_bag_ranks, p->U); dalloc(&p->d_bag_size, M);
+  dalloc(&p->d_rank_bag, p->U); dalloc(&p->d_rank_member, p->U);
+  dalloc(&p->w, N); dalloc(&p->seq_rank, N); dalloc(&p->seq_off, N); dalloc(&p->hash, 2 * N);
+  dalloc(&p->sk_hi, N); dalloc(&p->sk_lo, N); dalloc(&p->tk_hi, N); dalloc(&p->tk_lo, N);
+  dalloc(&p->sk_v, N); dalloc(&p->tk_v, N);
+  dalloc(&p->sorted_w, N); dalloc(&p->sorted_idx, N); dalloc(&p->pick, N);
+  dalloc(&p->seq_bag, N); dalloc(&p->seq_G, N); dalloc(&p->seq_chunk_base, N);
+  dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
+  dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
+  dalloc(&p->n_chunks, 1); dalloc(&p->n_seqs, 1);
+  dalloc(&p->c_id, C); dalloc(&p->c_idx, C); dalloc(&p->c_src, C); dalloc(&p->c_dst, C);
+  dalloc(&p->c_start, C); dalloc(&p->c_end, C); dalloc(&p->c_src_row, C); dalloc(&p->c_dst_row, C);
+  dalloc(&p->c_seq_base, C);
+  dalloc(&p->send_off, W + 1); dalloc(&p->recv_off, W + 1);
+  dalloc(&p->send_idx, C); dalloc(&p->recv_idx, C); dalloc(&p->rev_recv_idx, C);
+  dalloc(&p->origin_rows, W); dalloc(&p->target_rows, W);
+  dalloc(&p->per_gpu, W); dalloc(&p->per_bag_occ, R * M); dalloc(&p->total, 1); dalloc(&p->wir, 1);
+  dalloc(&p->violations, 1); dalloc(&p->status, 1);
+  SB_CUDA(cudaMemcpy(p->d_bag_off, p->bag_off.data(), sizeof(int32_t) * (M + 1), cudaMemcpyHostToDevice));
+  SB_CUDA(cudaMemcpy(p->d_bag_ranks, p->bag_ranks.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
+  SB_CUDA(cudaMemcpy(p->d_bag_size, p->bag_size.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
+  SB_CUDA(cudaMemcpy(p->d_rank_bag, p->rank_bag.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
+  SB_CUDA(cudaMemcpy(p->d_rank_member, p->rank_member.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
+  SB_CUDA(cudaFuncSetAttribute(k_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
+  SB_CUDA(cudaFuncSetAttribute(k_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
+  for (int i = 0; i < 6; ++i) SB_CUDA(cudaEventCreate(&p->ev[i]));
+}
+
+static void planner_free(sb_planner* p) {
+  void* ptrs[] = {p->d_bag_off, p->d_bag_ranks, p->d_bag_size, p->d_rank_bag, p->d_rank_member,
+                  p->w, p->seq_rank, p->seq_off, p->hash, p->sk_hi, p->sk_lo, p->tk_hi, p->tk_lo,
+                  p->sk_v, p->tk_v, p->sorted_w, p->sorted_idx, p->pick, p->seq_bag, p->seq_G,
+                  p->seq_chunk_base, p->rep_total, p->sentinel, p->bag_count, p->bag_rows,
+                  p->rep_chunks, p->send_count, p->n_chunks, p->n_seqs, p->c_id, p->c_idx, p->c_src,
+                  p->c_dst, p->c_start, p->c_end, p->c_src_row, p->c_dst_row, p->c_seq_base,
+                  p->send_off, p->recv_off, p->send_idx, p->recv_idx, p->rev_recv_idx,
+                  p->origin_rows, p->target_rows, p->per_gpu, p->per_bag_occ, p->total, p->wir,
+                  p->violations, p->status, p->jobs, p->piece_off, p->n_jobs};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (int i = 0; i < 6; ++i)
+    if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  for (cudaEvent_t e : p->copy_ev) cudaEventDestroy(e);
+}
+
+static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
+  SB_CUDA(cudaMemsetAsync(p->hash, 0xff, sizeof(uint64_t) * 2 * (size_t)p->max_seqs, s));
+  SB_CUDA(cudaMemsetAsync(p->sentinel, 0, sizeof(int32_t) * p->R, s));
+  SB_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int32_t), s));
+  SB_CUDA(cudaMemsetAsync(p->violations, 0, sizeof(int32_t), s));
+}
+
+static void run_plan(sb_planner* p, cudaStream_t s) {
+  PlanArgs a = make_args(p);
+  plan_common_prologue(p, s);
+  if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
+  k_prep<<<p->W, 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  if (p->timing) SB_CUDA(cudaEventRecord(p->ev[1], s));
+  k_sort<<<2 * p->R + 1, 1024, kSortSmemBytes, s>>>(a);
+  SB_CHECK_LAUNCH();
+  if (p->timing) SB_CUDA(cudaEventRecord(p->ev[2], s));
+  const int bpl = (p->M + 31) / 32;
+  if (bpl <= 1) k_greedy<1><<<p->R, 32, 0, s>>>(a);
+  else k_greedy<2><<<p->R, 32, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  if (p->timing) SB_CUDA(cudaEventRecord(p->ev[3], s));
+  k_emit<<<p->R, 1024, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  if (p->timing) SB_CUDA(cudaEventRecord(p->ev[4], s));
+  k_lists<<<p->W, 1024, kSortSmemBytes, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_finalize<<<1, 32, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
+  count_launch(6);
+}
+
+static void run_identity(sb_planner* p, cudaStream_t s) {
+  PlanArgs a = make_args(p);
+  plan_common_prologue(p, s);
+  k_prep<<<p->W, 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_sort<<<2 * p->R + 1, 1024, kSortSmemBytes, s>>>(a);  // totals (sorted order unused)
+  SB_CHECK_LAUNCH();
+  k_identity<<<148, 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_identity_report<<<(p->W + 127) / 128, 128, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_identity_finalize<<<1, 32, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  count_launch(5);
+}
+
+}  // namespace sb
+
+// ============================================================== C-ABI
+using sb::Error;
+
+#define SB_API_BEGIN try {
+#define SB_API_END                              \
+  return SB_OK;                                 \
+  }                                             \
+  catch (const Error& e) {                      \
+    sb::set_error(e.msg);                       \
+    return e.code;                              \
+  }                                             \
+  catch (const std::bad_alloc&) {               \
+    sb::set_error("host allocation failed");    \
+    return SB_ERR_CAPACITY;                     \
+  }
+
+extern "C" sb_status sb_planner_create(const sb_planner_desc* d, sb_planner** out) {
+  SB_API_BEGIN
+  if (!d || !out) throw Error{SB_ERR_CONFIG, "sb_planner_create: null argument"};
+  *out = nullptr;
+  // WorkloadModel::validate (workload_model.cpp:15-31)
+  if (d->d_model < 1 || d->n_heads < 1 || d->d_head < 1 || d->n_blocks < 1)
+    throw Error{SB_ERR_CONFIG, "model shape fields must be >= 1"};
+  if ((int64_t)d->n_heads * d->d_head != d->d_model)
+    throw Error{SB_ERR_CONFIG, "n_heads * d_head must equal d_model (" + std::to_string(d->n_heads) + " * " +
+                                   std::to_string(d->d_head) + " != " + std::to_string(d->d_model) + ")"};
+  if (!(d->gamma > 0.0)) throw Error{SB_ERR_CONFIG, "gamma must be positive"};
+  if (!(d->k > 0.0)) throw Error{SB_ERR_CONFIG, "k must be positive"};
+  if (d->n_bags < 1 || !d->bag_offsets || !d->bag_ranks) throw Error{SB_ERR_CONFIG, "topology has no GPUs"};
+  if (d->unit_size < 1) throw Error{SB_ERR_CONFIG, "topology has no GPUs"};
+  // replicate (topology.cpp:81-93)
+  if (d->world_size < d->unit_size)
+    throw Error{SB_ERR_CONFIG, "world_size " + std::to_string(d->world_size) +
+                                   " is smaller than the sharding unit " + std::to_string(d->unit_size)};
+  if (d->world_size % d->unit_size != 0)
+    throw Error{SB_ERR_CONFIG, "world_size " + std::to_string(d->world_size) +
+                                   " is not a multiple of the sharding unit " + std::to_string(d->unit_size)};
+  if (d->n_bags > sb::kMaxBags)
+    throw Error{SB_ERR_CONFIG, "more than " + std::to_string(sb::kMaxBags) + " bags per replica"};
+  auto* p = new sb_planner();
+  p->W = d->world_size;
+  p->U = d->unit_size;
+  p->M = d->n_bags;
+  p->R = d->world_size / d->unit_size;
+  p->d_model = d->d_model;
+  p->n_heads = d->n_heads;
+  p->d_head = d->d_head;
+  p->n_blocks = d->n_blocks;
+  p->gamma = d->gamma;
+  p->k = d->k;
+  p->bag_off.assign(d->bag_offsets, d->bag_offsets + d->n_bags + 1);
+  if (p->bag_off[0] != 0 || p->bag_off[p->M] != p->U) {
+    delete p;
+    throw Error{SB_ERR_CONFIG, "bag ranks must cover the unit exactly once"};
+  }
+  p->bag_ranks.assign(d->bag_ranks, d->bag_ranks + p->U);
+  p->rank_bag.assign(p->U, -1);
+  p->rank_member.assign(p->U, -1);
+  for (int b = 0; b < p->M; ++b) {
+    const int g = p->bag_off[b + 1] - p->bag_off[b];
+    if (g < 1) {
+      delete p;
+      throw Error{SB_ERR_CONFIG, "empty bag"};
+    }
+    // plan_routing head check (balancer.cpp:114-120)
+    if (d->n_heads % g != 0) {
+      delete p;
+      throw Error{SB_ERR_CONFIG, "bag of " + std::to_string(g) + " GPUs does not divide n_heads " +
+                                     std::to_string(d->n_heads)};
+    }
+    p->bag_size.push_back(g);
+    p->max_bag = std::max(p->max_bag, g);
+    if (g > 1) p->any_multi_bag = true;
+    for (int k = 0; k < g; ++k) {
+      const int u = p->bag_ranks[p->bag_off[b] + k];
+      if (u < 0 || u >= p->U || p->rank_bag[u] != -1) {
+        delete p;
+        throw Error{SB_ERR_CONFIG, "bag ranks must cover the unit exactly once"};
+      }
+      p->rank_bag[u] = b;
+      p->rank_member[u] = k;
+    }
+  }
+  p->max_seqs = std::max<int64_t>(1, d->max_seqs);
+  if (p->max_seqs > (int64_t)1 << 30) {
+    delete p;
+    throw Error{SB_ERR_CONFIG, "max_seqs too large"};
+  }
+  p->max_chunks = p->max_seqs * p->max_bag;
+  try {
+    sb::planner_alloc(p);
+  } catch (...) {
+    sb::planner_free(p);
+    delete p;
+    throw;
+  }
+  *out = p;
+  SB_API_END
+}
+
+extern "C" sb_status sb_planner_destroy(sb_planner* p) {
+  SB_API_BEGIN
+  if (p) {
+    sb::planner_free(p);
+    delete p;
+  }
+  SB_API_END
+}
+
+extern "C" sb_status sb_plan(sb_planner* p, const uint64_t* d_ids, const int64_t* d_lens,
+                             const int64_t* d_rank_off, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_plan: null argument"};
+  p->ids = d_ids;
+  p->lens = d_lens;
+  p->rank_off = d_rank_off;
+  p->identity = false;
+  sb::run_plan(p, (cudaStream_t)stream);
+  SB_API_END
+}
+
+extern "C" sb_status sb_plan_identity(sb_planner* p, const uint64_t* d_ids, const int64_t* d_lens,
+                                      const int64_t* d_rank_off, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_plan_identity: null argument"};
+  p->ids = d_ids;
+  p->lens = d_lens;
+  p->rank_off = d_rank_off;
+  p->identity = true;
+  sb::run_identity(p, (cudaStream_t)stream);
+  SB_API_END
+}
+
+extern "C" sb_status sb_plan_get(const sb_planner* p, sb_plan_dev* o) {
+  SB_API_BEGIN
+  if (!p || !o) throw Error{SB_ERR_CONFIG, "sb_plan_get: null argument"};
+  o->world_size = p->W;
+  o->max_chunks = p->max_chunks;
+  o->n_chunks = p->n_chunks;
+  o->chunk_id = p->c_id;
+  o->chunk_index = p->c_idx;
+  o->chunk_start = p->c_start;
+  o->chunk_end = p->c_end;
+  o->chunk_src = p->c_src;
+  o->chunk_dst = p->c_dst;
+  o->chunk_src_row = p->c_src_row;
+  o->chunk_dst_row = p->c_dst_row;
+  o->send_off = p->send_off;
+  o->send_idx = p->send_idx;
+  o->recv_off = p->recv_off;
+  o->recv_idx = p->recv_idx;
+  o->rev_recv_idx = p->rev_recv_idx;
+  o->origin_rows = p->origin_rows;
+  o->target_rows = p->target_rows;
+  o->per_gpu_workload = p->per_gpu;
+  o->per_bag_occupancy = p->per_bag_occ;
+  o->capacity_violations = p->violations;
+  o->total_workload = p->total;
+  o->wir = p->wir;
+  o->status = p->status;
+  SB_API_END
+}
+
+static void check_plan_status(sb_planner* p, cudaStream_t s) {
+  SB_CUDA(cudaStreamSynchronize(s));
+  int32_t st = 0;
+  SB_CUDA(cudaMemcpy(&st, p->status, sizeof st, cudaMemcpyDeviceToHost));
+  if (st & sb::ST_CAPACITY)
+    throw Error{SB_ERR_CAPACITY, "plan_routing: more sequences than the planner capacity"};
+  if (st & sb::ST_NEG_LENGTH) throw Error{SB_ERR_CONFIG, "seq_len must be >= 0"};
+  if (st & sb::ST_DUP_ID)
+    throw Error{SB_ERR_CONFIG, "plan_routing: duplicate sample_id within a replica"};
+  if (st) throw Error{SB_ERR_INTEGRITY, "plan_routing: device status " + std::to_string(st)};
+}
+
+extern "C" sb_status sb_plan_sizes(sb_planner* p, sb_stream stream, int64_t* n_chunks, int64_t* n_seqs) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "sb_plan_sizes: null planner"};
+  check_plan_status(p, (cudaStream_t)stream);
+  int64_t c = 0, n = 0;
+  SB_CUDA(cudaMemcpy(&c, p->n_chunks, sizeof c, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(&n, p->rank_off + p->W, sizeof n, cudaMemcpyDeviceToHost));
+  if (n_chunks) *n_chunks = c;
+  if (n_seqs) *n_seqs = n;
+  SB_API_END
+}
+
+template <typename T>
+static void d2h(T* dst, const T* src, int64_t n, cudaStream_t s) {
+  if (dst && n > 0) SB_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost, s));
+}
+
+extern "C" sb_status sb_plan_download(sb_planner* p, sb_plan_host* o, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !o) throw Error{SB_ERR_CONFIG, "sb_plan_download: null argument"};
+  cudaStream_t s = (cudaStream_t)stream;
+  check_plan_status(p, s);
+  int64_t c = 0;
+  SB_CUDA(cudaMemcpy(&c, p->n_chunks, sizeof c, cudaMemcpyDeviceToHost));
+  d2h(o->chunk_id, p->c_id, c, s);
+  d2h(o->chunk_index, p->c_idx, c, s);
+  d2h(o->chunk_start, p->c_start, c, s);
+  d2h(o->chunk_end, p->c_end, c, s);
+  d2h(o->chunk_src, p->c_src, c, s);
+  d2h(o->chunk_dst, p->c_dst, c, s);
+  d2h(o->send_off, p->send_off, p->W + 1, s);
+  d2h(o->send_idx, p->send_idx, c, s);
+  d2h(o->recv_off, p->recv_off, p->W + 1, s);
+  d2h(o->recv_idx, p->recv_idx, c, s);
+  d2h(o->rev_recv_idx, p->rev_recv_idx, c, s);
+  d2h(o->target_rows, p->target_rows, p->W, s);
+  d2h(o->per_gpu_workload, p->per_gpu, p->W, s);
+  if (!p->identity) d2h(o->per_bag_occupancy, p->per_bag_occ, (int64_t)p->R * p->M, s);
+  SB_CUDA(cudaMemcpyAsync(&o->capacity_violations, p->violations, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaMemcpyAsync(&o->total_workload, p->total, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaMemcpyAsync(&o->wir, p->wir, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaStreamSynchronize(s));
+  SB_API_END
+}
+
+extern "C" sb_status sb_planner_enable_timing(sb_planner* p, int enable) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  p->timing = enable != 0;
+  SB_API_END
+}
+
+extern "C" sb_status sb_planner_timing(sb_planner* p, double* a, double* b, double* c, double* d, double* e) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  double* outs[5] = {a, b, c, d, e};
+  for (int i = 0; i < 5; ++i) {
+    float ms = 0.f;
+    if (p->timing) SB_CUDA(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
+    if (outs[i]) *outs[i] = 1000.0 * ms;
+  }
+  SB_API_END
+}

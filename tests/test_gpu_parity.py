@@ -1,0 +1,215 @@
+"""Parity of the CUDA path (libseqbal_cuda.so through the C-ABI) against the
+reference fixtures (tests/golden/cases.json, produced by the unmodified
+reference) and the CPU oracle.  Integer/byte work: bit-exact everywhere;
+the FP64 BalanceReport is compared bit for bit as well."""
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import case_by_name, check_plan, check_report, dbits, hexd, load_cases, meta_for, model_for
+
+pytestmark = pytest.mark.gpu
+
+sb = pytest.importorskip("paper_2508_06001_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def device_meta(meta: oracle.Meta):
+    return sb.DeviceMeta.from_lists(meta.ids, meta.lens)
+
+
+def host_plan_as_oracle(hp, meta: oracle.Meta) -> oracle.Plan:
+    """Reassemble a device plan into the oracle's Plan record for comparison."""
+    W = hp.world
+    recv = hp.recv
+    target = [[(int(hp.c_id[c]), int(hp.c_start[c]), int(hp.c_end[c] - hp.c_start[c])) for c in recv[r]]
+              for r in range(W)]
+    origin = [[(int(i), 0, int(l)) for i, l in zip(meta.ids[r], meta.lens[r])] for r in range(W)]
+    return oracle.Plan(W, hp.c_id, hp.c_idx, hp.c_start, hp.c_end, hp.c_src, hp.c_dst, hp.send, recv,
+                       origin, target)
+
+
+def reverse_as_oracle(hp, fwd: oracle.Plan) -> oracle.Plan:
+    return oracle.Plan(hp.world, hp.c_id, hp.c_idx, hp.c_start, hp.c_end, hp.c_dst, hp.c_src, hp.rev_send,
+                       hp.rev_recv, origin=fwd.target, target=fwd.origin)
+
+
+def report_as_oracle(hp) -> oracle.Report:
+    return oracle.Report(hp.per_gpu_workload, hp.per_bag_occupancy, hp.capacity_violations, hp.total_workload,
+                         hp.wir)
+
+
+def rank_digests(world, r):
+    meta = world.read_rank(0, r).view(np.uint64).reshape(-1, 2)
+    ids = np.ascontiguousarray(meta[:, 0])
+    pos = np.ascontiguousarray(meta[:, 1])
+    pay = world.read_rank(1, r)
+    return len(ids), hexd(oracle.digest(ids)), hexd(oracle.digest(pos)), hexd(oracle.digest(pay)), pay.nbytes
+
+
+def check_dev_world(world, ref, ranks=None):
+    for r, rr in enumerate(ref["ranks"]):
+        if ranks is not None and r not in ranks:
+            continue
+        rows, di, dp, dpl, nbytes = rank_digests(world, r)
+        assert rows == rr["rows"], f"rank {r} rows"
+        assert di == rr["ids_digest"], f"rank {r} ids"
+        assert dp == rr["pos_digest"], f"rank {r} positions"
+        assert dpl == rr["payload_digest"], f"rank {r} payload"
+        if rows:
+            assert nbytes // rows == rr["width"] * 8, f"rank {r} width"
+
+
+def make_planner(case, meta):
+    d, h, g = model_for(case)
+    md = case["model"]
+    model = sb.Model(d_model=d, n_heads=h, d_head=md["d_head"], n_blocks=md["n_blocks"], gamma=g)
+    return sb.Planner(case["topology"], case["world"], model, max_seqs=max(1, sum(len(x) for x in meta.ids)))
+
+
+CASES = [c["name"] for c in load_cases()]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_device_plan_and_exchange_match_reference(name):
+    c = case_by_name(name)
+    case, ref = c["case"], c["result"]
+    meta = oracle_meta = meta_for(case)
+    if "error" in ref:
+        with pytest.raises(sb.ConfigError):
+            make_planner(case, meta)
+        return
+    planner = make_planner(case, meta)
+    dm = device_meta(meta)
+    planner.plan(dm)
+    hp = planner.download()
+    fwd = host_plan_as_oracle(hp, meta)
+    check_plan(fwd, ref["plan"])
+    check_report(report_as_oracle(hp), ref["report"])
+    check_plan(reverse_as_oracle(hp, fwd), ref["reverse"], recv_ties_ok=True)
+
+    # identity_plan on the same planner slots
+    planner.plan_identity(dm)
+    ident = planner.download()
+    check_plan(host_plan_as_oracle(ident, meta), ref["identity"])
+    planner.plan(dm)
+
+    if not case.get("route"):
+        return
+    W, width = case["world"], case["payload_width"]
+    _, h, _ = model_for(case)
+    rows = max(1, int(sum(int(x.sum()) for x in meta.lens)))
+    mk = lambda: sb.World(W, h, [width * 8], capacity_rows=rows, max_bag=planner.max_bag)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    check_dev_world(A, ref["world0"])
+    assert hexd(A.checksum()) == ref["world0"]["checksum"]
+    sb.route(planner, A, B)
+    B.status()
+    check_dev_world(B, ref["routed"])
+    assert hexd(B.checksum()) == ref["routed"]["checksum"]
+    if ref.get("ulysses"):
+        sb.pre_attn(planner, B, Cw)
+        Cw.status()
+        topo = oracle.parse_topology(case["topology"])
+        for u in ref["ulysses"]:
+            bag = [x + u["replica"] * topo.unit_size for x in topo.bag_ranks(u["bag"])]
+            check_dev_world(Cw, u["pre"], ranks=set(bag))
+        assert hexd(Cw.checksum()) == ref["routed"]["checksum"]
+        sb.post_attn(planner, Cw, D)
+        D.status()
+        for r in range(W):
+            assert rank_digests(D, r) == rank_digests(B, r), f"post(pre(x)) != x on rank {r}"
+    B.perturb()
+    check_dev_world(B, ref["mutated"])
+    sb.reverse_route(planner, B, E)
+    E.status()
+    check_dev_world(E, ref["returned"])
+
+
+def test_duplicate_ids_rejected():
+    meta = oracle.meta_explicit([[10, 20], [30]], ids=[[5, 6], [5]])
+    planner = sb.Planner("g1n2", 2, max_seqs=8)
+    planner.plan(device_meta(meta))
+    with pytest.raises(sb.ConfigError):
+        planner.sizes()
+
+
+def test_negative_length_rejected():
+    meta = oracle.meta_explicit([[10, -1], [30]])
+    planner = sb.Planner("g1n2", 2, max_seqs=8)
+    planner.plan(device_meta(meta))
+    with pytest.raises(sb.ConfigError):
+        planner.sizes()
+
+
+def test_capacity_exceeded_is_loud():
+    meta = oracle.meta_explicit([[1, 2, 3], [4, 5]])
+    planner = sb.Planner("g1n2", 2, max_seqs=4)
+    planner.plan(device_meta(meta))
+    with pytest.raises(sb.CapacityError):
+        planner.sizes()
+
+
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2", "g8n1", "g1n2+g2n1+g4n1"])
+def test_random_plans_vs_oracle(topo):
+    rng = np.random.default_rng(hash(topo) % 2**32)
+    planner = sb.Planner(topo, 16 if "+" in topo else 8, max_seqs=4096)
+    W = planner.world_size
+    for trial in range(20):
+        lens = [rng.integers(0, 5000, size=rng.integers(0, 40)).tolist() for _ in range(W)]
+        meta = oracle.meta_explicit(lens)
+        planner.plan(device_meta(meta))
+        hp = planner.download()
+        plan, rep = oracle.plan_routing(meta, oracle.parse_topology(topo))
+        got = host_plan_as_oracle(hp, meta)
+        assert got.chunk_rows() == plan.chunk_rows()
+        assert got.send == plan.send and got.recv == plan.recv
+        assert [dbits(x) for x in hp.per_gpu_workload] == [dbits(x) for x in rep.per_gpu_workload]
+        assert [dbits(x) for x in hp.per_bag_occupancy] == [dbits(x) for x in rep.per_bag_occupancy]
+        assert hp.capacity_violations == rep.capacity_violations
+        assert dbits(hp.total_workload) == dbits(rep.total_workload)
+        assert dbits(hp.wir) == dbits(rep.wir)
+        rev = oracle.reverse_plan(plan)
+        assert hp.rev_recv == rev.recv
+
+
+def test_full_width_c1_roundtrip_bit_exact():
+    """C1 at the bench width (768 doubles == 3072 bf16 == 6144 B/row)."""
+    meta = oracle.meta_c1(8, 32, seed=1, step=0)
+    planner = sb.Planner("g2n4", 8, max_seqs=256)
+    dm = device_meta(meta)
+    planner.plan(dm)
+    rows = int(sum(int(x.sum()) for x in meta.lens))
+    mk = lambda: sb.World(8, 24, [6144], capacity_rows=rows, max_bag=2)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    cs = A.checksum()
+    sb.route(planner, A, B)
+    sb.pre_attn(planner, B, Cw)
+    sb.post_attn(planner, Cw, D)
+    sb.reverse_route(planner, D, E)
+    E.status()
+    assert B.checksum() == cs and Cw.checksum() == cs
+    for r in range(8):
+        assert rank_digests(E, r) == rank_digests(A, r)
+        assert rank_digests(D, r) == rank_digests(B, r)
+    # routed bytes equal the oracle's route of the same world
+    plan, _ = oracle.plan_routing(meta, oracle.parse_topology("g2n4"))
+    w0 = oracle.make_world(meta, 768, 24)
+    routed = oracle.route(w0, plan)
+    for r in range(8):
+        rows_r, di, dp, dpl, _ = rank_digests(B, r)
+        ob = routed.ranks[r]
+        assert rows_r == ob.rows
+        assert dpl == hexd(oracle.digest(np.ascontiguousarray(ob.payload)))
+        assert di == hexd(oracle.digest(ob.ids)) and dp == hexd(oracle.digest(ob.pos))
