@@ -231,6 +231,41 @@ SB_API sb_status sb_world_write_rank(sb_world* w, int tensor, int rank, const vo
 /* Current per-rank rows/pitch as host arrays (synchronises). */
 SB_API sb_status sb_world_shape(sb_world* w, int tensor, int64_t* rows, int64_t* pitch, sb_stream stream);
 
+/* ------------------------------------------------- multi-process / peer -- */
+/* One process per GPU.  Device buffers are shared once through CUDA IPC
+ * (handles travel over the caller's control plane, e.g. torch.distributed);
+ * the exchange kernels then store straight into peer memory over NVLink.  */
+#define SB_IPC_HANDLE_BYTES 64
+SB_API sb_status sb_ipc_export(const void* dptr, void* handle /* SB_IPC_HANDLE_BYTES */);
+SB_API sb_status sb_ipc_import(const void* handle, void** dptr);
+SB_API sb_status sb_ipc_close(void* dptr);
+
+/* Metadata all-gather (gather_sequence_info, exchange.cpp:68-77, made a real
+ * collective): every process pushes its hosted ranks' (id, len) records into
+ * slot [rank] of every process's gather buffer (peer stores), then -- after a
+ * barrier -- compacts its own buffer into gather order for sb_plan.        */
+typedef struct sb_gather sb_gather;
+SB_API sb_status sb_gather_create(int world_size, int n_local, int first_local, int64_t cap_per_rank,
+                                  sb_gather** out);
+SB_API sb_status sb_gather_destroy(sb_gather* g);
+SB_API sb_status sb_gather_buffer(const sb_gather* g, void** buf, int64_t* bytes);
+SB_API sb_status sb_gather_set_peers(sb_gather* g, const uint64_t* bases, int n_procs);
+/* d_local_off: n_local+1 offsets of the hosted ranks' records in d_ids/d_lens. */
+SB_API sb_status sb_gather_push(sb_gather* g, const uint64_t* d_ids, const int64_t* d_lens,
+                                const int64_t* d_local_off, sb_stream stream);
+SB_API sb_status sb_gather_compact(sb_gather* g, uint64_t* d_ids, int64_t* d_lens, int64_t* d_rank_off,
+                                   sb_stream stream);
+SB_API sb_status sb_gather_status(sb_gather* g, sb_stream stream);
+
+/* Device-side barrier over system-scope flags in peer memory: closes an
+ * exchange phase on every process without a host round trip.            */
+typedef struct sb_barrier sb_barrier;
+SB_API sb_status sb_barrier_create(int n_procs, int me, sb_barrier** out);
+SB_API sb_status sb_barrier_destroy(sb_barrier* b);
+SB_API sb_status sb_barrier_buffer(const sb_barrier* b, void** buf, int64_t* bytes);
+SB_API sb_status sb_barrier_set_peers(sb_barrier* b, const uint64_t* bases, int n_procs);
+SB_API sb_status sb_barrier_wait(sb_barrier* b, sb_stream stream);
+
 /* Device time of the copy kernels launched while timing was enabled
  * (sb_planner_enable_timing): op 0 route, 1 reverse_route, 2 pre_attn,
  * 3 post_attn, -1 all.  Synchronises on the recorded events. */

@@ -112,6 +112,21 @@ _SIGS = {
     "sb_last_exchange_bytes": (C.c_int, [C.c_void_p] * 3),
     "sb_copy_timing": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "sb_copy_timing_reset": (C.c_int, [C.c_void_p]),
+    "sb_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sb_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sb_ipc_close": (C.c_int, [C.c_void_p]),
+    "sb_gather_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_void_p]),
+    "sb_gather_destroy": (C.c_int, [C.c_void_p]),
+    "sb_gather_buffer": (C.c_int, [C.c_void_p] * 3),
+    "sb_gather_set_peers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "sb_gather_push": (C.c_int, [C.c_void_p] * 5),
+    "sb_gather_compact": (C.c_int, [C.c_void_p] * 5),
+    "sb_gather_status": (C.c_int, [C.c_void_p] * 2),
+    "sb_barrier_create": (C.c_int, [C.c_int, C.c_int, C.c_void_p]),
+    "sb_barrier_destroy": (C.c_int, [C.c_void_p]),
+    "sb_barrier_buffer": (C.c_int, [C.c_void_p] * 3),
+    "sb_barrier_set_peers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "sb_barrier_wait": (C.c_int, [C.c_void_p] * 2),
 }
 
 

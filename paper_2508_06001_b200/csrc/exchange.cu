@@ -348,7 +348,7 @@ __device__ void warp_copy_bytes(const SbJob& j, int64_t r0, int64_t r1, int lane
 
 __global__ void __launch_bounds__(kCopyThreads) k_copy(const SbJob* __restrict__ jobs,
                                                        const int64_t* __restrict__ piece_off,
-                                                       const int64_t* __restrict__ n_jobs_p) {
+                                                       const int64_t* __restrict__ n_jobs_p, int fence_sys) {
   const int64_t n_jobs = *n_jobs_p;
   const int64_t total = piece_off[n_jobs];
   const int lane = threadIdx.x & 31;
@@ -387,6 +387,9 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy(const SbJob* __restrict__
       else warp_copy_bytes(j, r0, r1, lane);
     }
   }
+  // Peer (NVLink) stores must be visible system-wide before the barrier
+  // kernel that follows publishes this phase as complete.
+  if (fence_sys) __threadfence_system();
 }
 
 // rows per rank = sum of its sequence lengths (origin packing).
@@ -531,7 +534,7 @@ static void check_compatible(sb_planner* p, sb_world* a, sb_world* b) {
   if (a->T > 16) throw Error{SB_ERR_CONFIG, "at most 16 tensors per world"};
 }
 
-static void run_copy(sb_planner* p, cudaStream_t s) {
+static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys) {
   k_pieces<<<1, 1024, 0, s>>>(p->jobs, p->n_jobs, p->piece_off, p->n_jobs + 1);
   SB_CHECK_LAUNCH();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -550,7 +553,7 @@ static void run_copy(sb_planner* p, cudaStream_t s) {
     p->copy_used += 2;
     SB_CUDA(cudaEventRecord(e0, s));
   }
-  k_copy<<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs);
+  k_copy<<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
   SB_CHECK_LAUNCH();
   if (e1) SB_CUDA(cudaEventRecord(e1, s));
   count_launch(2);
@@ -757,7 +760,7 @@ extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_worl
       sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), reverse);
   SB_CHECK_LAUNCH();
   sb::count_launch(2);
-  sb::run_copy(p, s);
+  sb::run_copy(p, s, dst->n_procs > 1);
   SB_API_END
 }
 
@@ -790,7 +793,7 @@ static void ulysses(sb_planner* p, sb_world* src, sb_world* dst, cudaStream_t s,
       sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), post);
   SB_CHECK_LAUNCH();
   sb::count_launch(2);
-  sb::run_copy(p, s);
+  sb::run_copy(p, s, dst->n_procs > 1);
 }
 
 extern "C" sb_status sb_pre_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream) {

@@ -1,0 +1,303 @@
+"""One process per GPU: the redistribute path over peer memory.
+
+Each process hosts a contiguous block of the world's logical ranks.  Device
+buffers (world arenas, the metadata gather buffer, barrier flags) are shared
+once through CUDA IPC, the handles travelling over torch.distributed (the
+control plane only).  Per step:
+
+  1. metadata all-gather  -- every process pushes its ranks' (id, len)
+     records into every process's gather buffer (peer stores), barrier,
+     local compaction into gather order;
+  2. plan                 -- every process runs the identical device planner
+     (deterministic, bit-exact), so no plan broadcast is needed;
+  3. route / pre_attn / post_attn / reverse_route -- the copy engine writes
+     each chunk from its source rank straight into its final slot in the
+     destination process's arena (NVLink stores), then a device barrier.
+
+Reference counterparts: gather_sequence_info (exchange.cpp:68-77),
+plan_routing (balancer.cpp:105-225), route/reverse_route
+(exchange.cpp:127-198), pre_attn/post_attn (exchange.cpp:255-436).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import socket
+
+import numpy as np
+
+from . import _capi
+from ._capi import call
+from .api import DeviceMeta, Planner, World, post_attn, pre_attn, reverse_route, route
+
+
+def partition(world_size: int, n_procs: int, proc: int):
+    """(n_local, first_local) of process `proc` -- contiguous blocks of ranks."""
+    if n_procs < 1 or world_size % n_procs:
+        raise _capi.ConfigError(f"world of {world_size} ranks does not split over {n_procs} processes")
+    n_local = world_size // n_procs
+    return n_local, proc * n_local
+
+
+def owner_of(rank: int, world_size: int, n_procs: int) -> int:
+    return rank // (world_size // n_procs)
+
+
+def exchange_bytes(c_src, c_dst, c_start, c_end, world_size, n_procs, row_bytes):
+    """Bytes each process sends to / receives from OTHER processes in one
+    exchange direction (the busiest-GPU convention of metrics.cpp:42-50)."""
+    n = np.asarray(c_end, np.int64) - np.asarray(c_start, np.int64)
+    per = world_size // n_procs
+    so = np.asarray(c_src, np.int64) // per
+    do = np.asarray(c_dst, np.int64) // per
+    cross = so != do
+    sent = np.bincount(so[cross], weights=n[cross], minlength=n_procs) * row_bytes
+    recv = np.bincount(do[cross], weights=n[cross], minlength=n_procs) * row_bytes
+    return sent.astype(np.int64), recv.astype(np.int64)
+
+
+class PeerGroup:
+    """Control plane over torch.distributed plus device-buffer sharing."""
+
+    def __init__(self, barrier_mode: str = "auto"):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        dev = torch.cuda.current_device()
+        props = torch.cuda.get_device_properties(dev)
+        key = (socket.gethostname(), str(getattr(props, "uuid", "")) or f"{props.pci_bus_id}")
+        keys = self.all_gather_object(key)
+        self.same_device = len(set(keys)) < self.size
+        self.mode = ("host" if self.same_device else "device") if barrier_mode == "auto" else barrier_mode
+        self._opened = []
+        self._barrier = None
+        if self.mode == "device":
+            h = C.c_void_p()
+            call("sb_barrier_create", self.size, self.rank, C.byref(h))
+            self._barrier = h
+            buf, nb = C.c_void_p(), C.c_int64()
+            call("sb_barrier_buffer", h, C.byref(buf), C.byref(nb))
+            peers = np.asarray(self.share(buf.value), np.uint64)
+            call("sb_barrier_set_peers", h, peers.ctypes.data, self.size)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def share(self, dptr: int) -> list:
+        """IPC-export dptr; return every process's pointer as mapped here."""
+        h = (C.c_ubyte * 64)()
+        call("sb_ipc_export", C.c_void_p(dptr), h)
+        handles = self.all_gather_object(bytes(h))
+        out = []
+        for q, hb in enumerate(handles):
+            if q == self.rank:
+                out.append(dptr)
+                continue
+            p = C.c_void_p()
+            buf = (C.c_ubyte * 64).from_buffer_copy(hb)
+            call("sb_ipc_import", buf, C.byref(p))
+            self._opened.append(p.value)
+            out.append(p.value)
+        return out
+
+    def barrier(self, stream=None):
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        if self.mode == "device":
+            call("sb_barrier_wait", self._barrier, C.c_void_p(s.cuda_stream))
+        else:
+            s.synchronize()
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        t = self.torch.tensor([x], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_u64(self, x: int) -> int:
+        t = self.torch.tensor([np.uint64(x).astype(np.int64)], dtype=self.torch.int64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return int(np.int64(t.item()).astype(np.uint64))
+
+    def close(self):
+        for p in self._opened:
+            _capi.load().sb_ipc_close(C.c_void_p(p))
+        self._opened = []
+        if self._barrier is not None:
+            _capi.load().sb_barrier_destroy(self._barrier)
+            self._barrier = None
+
+
+def make_world(group: PeerGroup, world_size: int, n_heads: int, payload_row_bytes, capacity_rows: int,
+               max_bag: int = 1, aux_row_bytes=()) -> World:
+    n_local, first = partition(world_size, group.size, group.rank)
+    w = World(world_size, n_heads, payload_row_bytes, capacity_rows, aux_row_bytes, n_local=n_local,
+              first_local=first, max_bag=max_bag)
+    for t in range(w.T):
+        base, _ = w.arena(t)
+        w.set_peers(t, group.share(base))
+    return w
+
+
+class MetaGather:
+    """The metadata all-gather over peer memory; result is a DeviceMeta in
+    gather order with capacity world_size * cap_per_rank."""
+
+    def __init__(self, group: PeerGroup, world_size: int, cap_per_rank: int):
+        import torch
+        self.group, self.W = group, world_size
+        self.n_local, self.first = partition(world_size, group.size, group.rank)
+        h = C.c_void_p()
+        call("sb_gather_create", world_size, self.n_local, self.first, cap_per_rank, C.byref(h))
+        self._h = h
+        buf, nb = C.c_void_p(), C.c_int64()
+        call("sb_gather_buffer", h, C.byref(buf), C.byref(nb))
+        peers = np.asarray(group.share(buf.value), np.uint64)
+        call("sb_gather_set_peers", h, peers.ctypes.data, group.size)
+        cap = world_size * cap_per_rank
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.out = DeviceMeta(np.zeros(cap, np.uint64), np.zeros(cap, np.int64), np.zeros(world_size + 1, np.int64),
+                              dev)
+        self.local_ids = torch.zeros(max(1, self.n_local * cap_per_rank), dtype=torch.int64, device=dev)
+        self.local_lens = torch.zeros_like(self.local_ids)
+        self.local_off = torch.zeros(self.n_local + 1, dtype=torch.int64, device=dev)
+
+    def set_local(self, ids_per_rank, lens_per_rank):
+        """Stage this process's ranks' metadata in HBM (host -> device)."""
+        torch = self.group.torch
+        ids = np.concatenate([np.asarray(x, np.uint64) for x in ids_per_rank]).view(np.int64)
+        lens = np.concatenate([np.asarray(x, np.int64) for x in lens_per_rank])
+        off = np.zeros(self.n_local + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in ids_per_rank])
+        n = len(ids)
+        if n:
+            self.local_ids[:n].copy_(torch.from_numpy(ids.copy()))
+            self.local_lens[:n].copy_(torch.from_numpy(lens.copy()))
+        self.local_off.copy_(torch.from_numpy(off))
+
+    def gather(self, stream=None) -> DeviceMeta:
+        torch = self.group.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        sp = C.c_void_p(s.cuda_stream)
+        call("sb_gather_push", self._h, C.c_void_p(self.local_ids.data_ptr()), C.c_void_p(self.local_lens.data_ptr()),
+             C.c_void_p(self.local_off.data_ptr()), sp)
+        self.group.barrier(s)
+        ids, lens, off = self.out.ptrs()
+        call("sb_gather_compact", self._h, ids, lens, off, sp)
+        return self.out
+
+    def status(self, stream=None):
+        torch = self.group.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        call("sb_gather_status", self._h, C.c_void_p(s.cuda_stream))
+
+    def close(self):
+        if self._h is not None:
+            _capi.load().sb_gather_destroy(self._h)
+            self._h = None
+
+
+def step(group: PeerGroup, gather: MetaGather, planner: Planner, A, B, Cw, D, E, ulysses: bool, stream=None):
+    """One pass of the hot path on every process (all phases peer-closed)."""
+    meta = gather.gather(stream)
+    planner.plan(meta, stream)
+    route(planner, A, B, stream)
+    group.barrier(stream)
+    if ulysses:
+        pre_attn(planner, B, Cw, stream)
+        group.barrier(stream)
+        post_attn(planner, Cw, D, stream)
+        group.barrier(stream)
+        reverse_route(planner, D, E, stream)
+    else:
+        reverse_route(planner, B, E, stream)
+    group.barrier(stream)
+    return meta
+
+
+def bench_main(args, cfg, topology, metric):
+    """bench.py --gpus N under torchrun: N processes, one GPU each."""
+    import torch
+    import torch.distributed as dist
+
+    from . import datagen
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    if not dist.is_initialized():
+        dist.init_process_group("gloo")
+    group = PeerGroup()
+    W = cfg["world"]
+    n_local, first = partition(W, group.size, group.rank)
+    meta_kw = {k: v for k, v in cfg["meta"].items() if k != "kind"}
+    all_ids, all_lens = datagen.metadata(cfg["meta"]["kind"], W, **meta_kw)
+    tokens = int(sum(int(l.sum()) for l in all_lens))
+    n_seqs = int(sum(len(l) for l in all_lens))
+    cap = max(len(x) for x in all_ids) + 1
+    gather = MetaGather(group, W, cap)
+    gather.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
+    planner = Planner(topology, W, max_seqs=max(1, W * cap))
+    G = planner.max_bag
+    ulysses = G > 1
+    payload, meta_b = 6144, 16
+    mk = lambda: make_world(group, W, 24, [payload], capacity_rows=tokens, max_bag=G)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    meta = gather.gather()
+    gather.status()
+    A.layout_origin(meta)
+    A.fill_witness(meta)
+    group.barrier()
+    for _ in range(max(3, args.warmup)):
+        step(group, gather, planner, A, B, Cw, D, E, ulysses)
+    torch.cuda.synchronize()
+    E.status()
+    for r in range(first, first + n_local):
+        assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r)), "round trip not bit-exact"
+    cs = group.sum_u64(B.checksum()) == group.sum_u64(A.checksum())
+    hp = planner.download()
+    sent, recv = exchange_bytes(hp.c_src, hp.c_dst, hp.c_start, hp.c_end, W, group.size, payload + meta_b)
+    busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
+
+    stream = torch.cuda.current_stream()
+    planner.enable_timing(True)
+    planner.copy_timing_reset()
+    n0 = _capi.load().sb_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    group.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(group, gather, planner, A, B, Cw, D, E, ulysses)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = _capi.load().sb_kernel_launches() - n0
+    ms = group.max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    nr, us_r = planner.copy_timing(0)
+    route_us = group.max_over_ranks(us_r / max(1, nr))
+    planner.enable_timing(False)
+    per = hp.per_gpu_workload
+    line = {
+        "metric": metric, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": group.size,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": W,
+                   "tokens_per_step": tokens, "sequences": n_seqs, "row_bytes": payload + meta_b,
+                   "parallelism": f"{W} ranks over {group.size} GPUs (peer-store all-to-all)",
+                   "barrier": group.mode},
+        "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
+        "a2a_gbs": busiest / (route_us * 1e-6) / 1e9 if route_us > 0 else None,
+        "a2a_busiest_bytes": busiest, "route_copy_us": route_us,
+        "roofline": {"bound": "nvlink", "achieved": busiest / (route_us * 1e-6) / 1e9 if route_us > 0 else None,
+                     "peak": 900.0, "unit": "GB/s",
+                     "frac": (busiest / (route_us * 1e-6) / 1e9 / 900.0) if route_us > 0 else None,
+                     "traffic": None},
+        "gpu_launches": int(launches), "checksum_conserved": bool(cs),
+    }
+    if group.rank == 0:
+        print(json.dumps(line))
+    group.close()
+    gather.close()
+    return 0
