@@ -231,6 +231,50 @@ SB_API sb_status sb_world_write_rank(sb_world* w, int tensor, int rank, const vo
 /* Current per-rank rows/pitch as host arrays (synchronises). */
 SB_API sb_status sb_world_shape(sb_world* w, int tensor, int64_t* rows, int64_t* pitch, sb_stream stream);
 
+/* ------------------------------------- host-buffer drop-in entry points -- */
+/* assign_to_bags (balancer.hpp:30-31, balancer.cpp:15-64) on caller
+ * workloads; the planner must describe exactly one replica.  Host arrays;
+ * outputs in assignment (sorted) order; out_bag = bag INDEX.  Synchronises. */
+SB_API sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t* ids, const double* workloads,
+                                   uint64_t* out_ids, double* out_w, int32_t* out_bag, sb_stream stream);
+
+/* A RoutingPlan that did not come from sb_plan (host arrays): chunks plus
+ * the origin/target layouts as per-rank segment CSR.  Chunk rows are located
+ * on the device (route's locate, exchange.cpp:156-167); SB_ERR_INTEGRITY
+ * names the sample when a chunk has no containing segment.  The uploaded
+ * plan drives sb_route (both directions).  Synchronises. */
+SB_API sb_status sb_plan_upload(sb_planner* p, int64_t n_chunks, const uint64_t* chunk_id, const int32_t* chunk_index,
+                                const int64_t* chunk_start, const int64_t* chunk_end, const int32_t* chunk_src,
+                                const int32_t* chunk_dst, const int64_t* origin_off, const uint64_t* origin_id,
+                                const int64_t* origin_first, const int64_t* origin_len, const int64_t* target_off,
+                                const uint64_t* target_id, const int64_t* target_first, const int64_t* target_len,
+                                sb_stream stream);
+
+/* finalize_manifests (balancer.cpp:84-91) and reverse_plan's receive order
+ * (balancer.cpp:259-285) for the uploaded plan, on the device; results in
+ * the planner's send/recv/rev_recv arrays (sb_plan_download).  Synchronises. */
+SB_API sb_status sb_plan_manifests(sb_planner* p, sb_stream stream);
+
+/* Host-chosen layout: rows[W] and pitch[T*W] (bytes per row per tensor);
+ * ranks packed back to back in each arena.  Single-process worlds. */
+SB_API sb_status sb_world_set_layout(sb_world* w, const int64_t* rows, const int64_t* pitch, sb_stream stream);
+/* First global payload column (in doubles) held per rank (checksum). */
+SB_API sb_status sb_world_set_headcol(sb_world* w, const int32_t* headcol, sb_stream stream);
+
+/* BlockMove (exchange.hpp:86-96) with columns in bytes of payload tensor 1;
+ * copy_meta also moves the 16-byte metadata rows. */
+typedef struct sb_block_move {
+  int32_t src_rank, dst_rank;
+  int64_t src_row, dst_row, n_rows;
+  int64_t src_col_bytes, dst_col_bytes, n_col_bytes;
+  int32_t copy_meta, reserved;
+} sb_block_move;
+/* apply_block_moves (exchange.hpp:98-105, exchange_kernels.cpp:35-56) on
+ * the device copy engine; destinations must be disjoint (as the reference
+ * requires), so the result equals the serial reference bit for bit. */
+SB_API sb_status sb_apply_moves(sb_world* src, sb_world* dst, const sb_block_move* moves, int64_t n,
+                                sb_stream stream);
+
 /* ------------------------------------------------- multi-process / peer -- */
 /* One process per GPU.  Device buffers are shared once through CUDA IPC
  * (handles travel over the caller's control plane, e.g. torch.distributed);

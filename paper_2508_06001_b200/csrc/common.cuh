@@ -24,6 +24,7 @@ struct Error {
   do {                                                                                \
     cudaError_t _e = (expr);                                                          \
     if (_e != cudaSuccess) {                                                          \
+      cudaGetLastError(); /* clear the non-sticky error so later calls start clean */ \
       throw ::sb::Error{SB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
     }                                                                                 \
   } while (0)

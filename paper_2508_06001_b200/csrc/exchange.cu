@@ -766,6 +766,8 @@ extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_worl
 
 static void ulysses(sb_planner* p, sb_world* src, sb_world* dst, cudaStream_t s, int post) {
   if (p->identity) throw Error{SB_ERR_CONFIG, "Ulysses transforms need a balanced plan (not identity_plan)"};
+  if (p->uploaded)
+    throw Error{SB_ERR_CONFIG, "Ulysses transforms need a device-built plan (sb_plan); use sb_apply_moves"};
   sb::check_compatible(p, src, dst);
   if (src == dst) throw Error{SB_ERR_CONFIG, "Ulysses transforms are out-of-place: src and dst must differ"};
   if (p->n_heads % p->max_bag != 0 || src->n_heads % p->max_bag != 0)
@@ -919,5 +921,282 @@ extern "C" sb_status sb_last_exchange_bytes(const sb_planner* p, int64_t* bytes_
   if (p->n_jobs) SB_CUDA(cudaMemcpy(&b, p->n_jobs + 1, sizeof b, cudaMemcpyDeviceToHost));
   if (bytes_read) *bytes_read = b;
   if (bytes_written) *bytes_written = b;
+  SB_API_END
+}
+
+// ====================================================================
+// Host-buffer entry points used by the C++ drop-in API (include/seqbal/):
+// a RoutingPlan that did not come from sb_plan (e.g. user-built or
+// deserialised) is uploaded and its chunk rows located on the device; a
+// world layout can be set from host row counts; and the reference's
+// BlockMove lists (exchange.hpp:86-105) run on the same copy engine.
+// ====================================================================
+namespace sb {
+
+struct UploadArgs {
+  int W;
+  int64_t n;
+  const int64_t *o_off, *t_off;      // W+1 segment CSR (origin, target)
+  const uint64_t *o_id, *t_id;
+  const int64_t *o_first, *o_len, *t_first, *t_len;
+  const int64_t *o_row, *t_row;      // per-segment row offsets (prefix of lens within rank)
+  const uint64_t* c_id;
+  const int32_t *c_src, *c_dst;
+  const int64_t *c_start, *c_end;
+  int64_t *c_src_row, *c_dst_row;
+  unsigned long long* first_bad;     // smallest failing chunk index
+  int32_t* status;
+};
+
+// route's locate (exchange.cpp:156-167): the first segment of the holding
+// rank that contains the chunk's token range, on both sides.
+__device__ __forceinline__ int64_t locate_row(const int64_t* off, const uint64_t* id, const int64_t* first,
+                                              const int64_t* len, const int64_t* row, int rank, uint64_t cid,
+                                              int64_t st, int64_t en) {
+  for (int64_t s = off[rank]; s < off[rank + 1]; ++s)
+    if (id[s] == cid && st >= first[s] && en <= first[s] + len[s]) return row[s] + (st - first[s]);
+  return -1;
+}
+
+__global__ void k_locate(UploadArgs a) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < a.n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t st = a.c_start[c], en = a.c_end[c];
+    if (en == st) {  // empty transfers are skipped (exchange.cpp:172)
+      a.c_src_row[c] = 0;
+      a.c_dst_row[c] = 0;
+      continue;
+    }
+    const int64_t sr = locate_row(a.o_off, a.o_id, a.o_first, a.o_len, a.o_row, a.c_src[c], a.c_id[c], st, en);
+    const int64_t dr = locate_row(a.t_off, a.t_id, a.t_first, a.t_len, a.t_row, a.c_dst[c], a.c_id[c], st, en);
+    if (sr < 0 || dr < 0) {
+      atomicOr(a.status, sr < 0 ? 32 : 64);
+      atomicMin(a.first_bad, (unsigned long long)c);
+    }
+    a.c_src_row[c] = sr < 0 ? 0 : sr;
+    a.c_dst_row[c] = dr < 0 ? 0 : dr;
+  }
+}
+
+struct Scratch {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t n) {
+    if (n > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      SB_CUDA(cudaMalloc(&p, n));
+      cap = n;
+    }
+    return p;
+  }
+};
+
+static thread_local Scratch g_move_jobs, g_move_pieces, g_move_n, g_upload, g_bad;
+
+}  // namespace sb
+
+extern "C" sb_status sb_plan_upload(sb_planner* p, int64_t n, const uint64_t* c_id, const int32_t* c_idx,
+                                    const int64_t* c_start, const int64_t* c_end, const int32_t* c_src,
+                                    const int32_t* c_dst, const int64_t* origin_off, const uint64_t* origin_id,
+                                    const int64_t* origin_first, const int64_t* origin_len, const int64_t* target_off,
+                                    const uint64_t* target_id, const int64_t* target_first, const int64_t* target_len,
+                                    sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || n < 0) throw Error{SB_ERR_CONFIG, "sb_plan_upload: bad arguments"};
+  if (n > p->max_chunks) throw Error{SB_ERR_CAPACITY, "sb_plan_upload: more chunks than planner capacity"};
+  const int W = p->W;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t c = 0; c < n; ++c)
+    if (c_src[c] < 0 || c_src[c] >= W || c_dst[c] < 0 || c_dst[c] >= W || c_end[c] < c_start[c])
+      throw Error{SB_ERR_INTEGRITY, "route: chunk " + std::to_string(c) + " has an invalid rank or range"};
+  const int64_t so = origin_off[W], sd = target_off[W];
+  // per-segment row offsets and per-rank rows, host side (cheap prefix sums)
+  std::vector<int64_t> o_row(so), t_row(sd), orows(W), trows(W);
+  for (int r = 0; r < W; ++r) {
+    int64_t acc = 0;
+    for (int64_t q = origin_off[r]; q < origin_off[r + 1]; ++q) { o_row[q] = acc; acc += origin_len[q]; }
+    orows[r] = acc;
+    acc = 0;
+    for (int64_t q = target_off[r]; q < target_off[r + 1]; ++q) { t_row[q] = acc; acc += target_len[q]; }
+    trows[r] = acc;
+  }
+  // one staging allocation for the segment tables
+  const size_t segb = sizeof(int64_t) * (size_t)(2 * (W + 1) + 4 * (so + sd)) + sizeof(uint64_t) * (size_t)(so + sd) + 64;
+  char* st = static_cast<char*>(sb::g_upload.get(segb));
+  auto put = [&](const void* src, size_t bytes) {
+    char* at = st;
+    if (bytes) SB_CUDA(cudaMemcpyAsync(at, src, bytes, cudaMemcpyHostToDevice, s));
+    st += (bytes + 7) & ~size_t(7);
+    return at;
+  };
+  sb::UploadArgs a;
+  a.W = W;
+  a.n = n;
+  a.o_off = (const int64_t*)put(origin_off, sizeof(int64_t) * (W + 1));
+  a.t_off = (const int64_t*)put(target_off, sizeof(int64_t) * (W + 1));
+  a.o_id = (const uint64_t*)put(origin_id, sizeof(uint64_t) * so);
+  a.t_id = (const uint64_t*)put(target_id, sizeof(uint64_t) * sd);
+  a.o_first = (const int64_t*)put(origin_first, sizeof(int64_t) * so);
+  a.o_len = (const int64_t*)put(origin_len, sizeof(int64_t) * so);
+  a.t_first = (const int64_t*)put(target_first, sizeof(int64_t) * sd);
+  a.t_len = (const int64_t*)put(target_len, sizeof(int64_t) * sd);
+  a.o_row = (const int64_t*)put(o_row.data(), sizeof(int64_t) * so);
+  a.t_row = (const int64_t*)put(t_row.data(), sizeof(int64_t) * sd);
+  if (n > 0) {
+    SB_CUDA(cudaMemcpyAsync(p->c_id, c_id, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->c_idx, c_idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->c_start, c_start, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->c_end, c_end, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->c_src, c_src, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->c_dst, c_dst, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+  }
+  // keep the origin layout for reverse_plan's receive order (sb_plan_manifests)
+  if (so > p->seg_cap || !p->seg_off) {
+    cudaFree(p->seg_id);
+    cudaFree(p->seg_first);
+    cudaFree(p->seg_len);
+    if (!p->seg_off) SB_CUDA(cudaMalloc(&p->seg_off, sizeof(int64_t) * (W + 1)));
+    const int64_t cap = std::max<int64_t>(1, so);
+    SB_CUDA(cudaMalloc(&p->seg_id, sizeof(uint64_t) * cap));
+    SB_CUDA(cudaMalloc(&p->seg_first, sizeof(int64_t) * cap));
+    SB_CUDA(cudaMalloc(&p->seg_len, sizeof(int64_t) * cap));
+    p->seg_cap = cap;
+  }
+  SB_CUDA(cudaMemcpyAsync(p->seg_off, origin_off, sizeof(int64_t) * (W + 1), cudaMemcpyHostToDevice, s));
+  if (so) {
+    SB_CUDA(cudaMemcpyAsync(p->seg_id, origin_id, sizeof(uint64_t) * so, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->seg_first, origin_first, sizeof(int64_t) * so, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->seg_len, origin_len, sizeof(int64_t) * so, cudaMemcpyHostToDevice, s));
+  }
+  SB_CUDA(cudaMemcpyAsync(p->n_chunks, &n, sizeof n, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemcpyAsync(p->origin_rows, orows.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemcpyAsync(p->target_rows, trows.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int32_t), s));
+  unsigned long long* bad = static_cast<unsigned long long*>(sb::g_bad.get(sizeof(unsigned long long)));
+  SB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+  a.c_id = p->c_id;
+  a.c_src = p->c_src;
+  a.c_dst = p->c_dst;
+  a.c_start = p->c_start;
+  a.c_end = p->c_end;
+  a.c_src_row = p->c_src_row;
+  a.c_dst_row = p->c_dst_row;
+  a.first_bad = bad;
+  a.status = p->status;
+  if (n > 0) {
+    sb::k_locate<<<(int)std::min<int64_t>(1184, (n + 255) / 256), 256, 0, s>>>(a);
+    SB_CHECK_LAUNCH();
+    sb::count_launch();
+  }
+  SB_CUDA(cudaStreamSynchronize(s));  // staging tables are reused by the next call
+  int32_t stt = 0;
+  unsigned long long fb = 0;
+  SB_CUDA(cudaMemcpy(&stt, p->status, sizeof stt, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(&fb, bad, sizeof fb, cudaMemcpyDeviceToHost));
+  if (stt) {
+    const int64_t c = (int64_t)fb;
+    throw Error{SB_ERR_INTEGRITY, "route: sample " + std::to_string(c_id[c]) + " chunk [" +
+                                      std::to_string(c_start[c]) + "," + std::to_string(c_end[c]) +
+                                      ") has no containing " + ((stt & 32) ? "origin" : "target") + " segment"};
+  }
+  p->identity = false;
+  p->uploaded = true;
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_set_layout(sb_world* w, const int64_t* rows, const int64_t* pitch, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !rows || !pitch) throw Error{SB_ERR_CONFIG, "sb_world_set_layout: null argument"};
+  if (w->n_procs != 1) throw Error{SB_ERR_CONFIG, "sb_world_set_layout: single-process worlds only"};
+  const int W = w->W, T = w->T;
+  std::vector<uint64_t> base((size_t)T * W);
+  for (int t = 0; t < T; ++t) {
+    int64_t off = 0;
+    for (int r = 0; r < W; ++r) {
+      const int64_t pt = pitch[(size_t)t * W + r];
+      if (rows[r] < 0 || pt < 0) throw Error{SB_ERR_CONFIG, "sb_world_set_layout: negative size"};
+      base[(size_t)t * W + r] = (uint64_t)w->arena[t] + (uint64_t)off;
+      off += rows[r] * pt;
+      if (off > w->arena_bytes[t]) throw Error{SB_ERR_CAPACITY, "world arena too small for the requested layout"};
+    }
+  }
+  std::vector<int32_t> hc(W, 0);
+  cudaStream_t s = (cudaStream_t)stream;
+  SB_CUDA(cudaMemcpyAsync(w->d_base, base.data(), sizeof(uint64_t) * base.size(), cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemcpyAsync(w->d_pitch, pitch, sizeof(int64_t) * (size_t)T * W, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemcpyAsync(w->d_rows, rows, sizeof(int64_t) * W, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemcpyAsync(w->d_headcol, hc.data(), sizeof(int32_t) * W, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaStreamSynchronize(s));
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_set_headcol(sb_world* w, const int32_t* headcol, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !headcol) throw Error{SB_ERR_CONFIG, "null argument"};
+  SB_CUDA(cudaMemcpyAsync(w->d_headcol, headcol, sizeof(int32_t) * w->W, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  SB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  SB_API_END
+}
+
+extern "C" sb_status sb_apply_moves(sb_world* src, sb_world* dst, const sb_block_move* moves, int64_t n,
+                                    sb_stream stream) {
+  SB_API_BEGIN
+  if (!src || !dst || (n > 0 && !moves)) throw Error{SB_ERR_CONFIG, "sb_apply_moves: bad arguments"};
+  if (src->W != dst->W || src->T < 2 || dst->T < 2) throw Error{SB_ERR_CONFIG, "sb_apply_moves: incompatible worlds"};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = src->W;
+  std::vector<uint64_t> sb0(W), sb1(W), db0(W), db1(W);
+  std::vector<int64_t> sp0(W), sp1(W), dp0(W), dp1(W), srows(W), drows(W);
+  SB_CUDA(cudaStreamSynchronize(s));
+  SB_CUDA(cudaMemcpy(sb0.data(), src->d_base, sizeof(uint64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(sb1.data(), src->d_base + W, sizeof(uint64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(db0.data(), dst->d_base, sizeof(uint64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(db1.data(), dst->d_base + W, sizeof(uint64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(sp0.data(), src->d_pitch, sizeof(int64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(sp1.data(), src->d_pitch + W, sizeof(int64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(dp0.data(), dst->d_pitch, sizeof(int64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(dp1.data(), dst->d_pitch + W, sizeof(int64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(srows.data(), src->d_rows, sizeof(int64_t) * W, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(drows.data(), dst->d_rows, sizeof(int64_t) * W, cudaMemcpyDeviceToHost));
+  std::vector<SbJob> jobs;
+  jobs.reserve((size_t)n * 2);
+  for (int64_t i = 0; i < n; ++i) {
+    const sb_block_move& m = moves[i];
+    if (m.src_rank < 0 || m.src_rank >= W || m.dst_rank < 0 || m.dst_rank >= W || m.n_rows < 0 ||
+        m.src_row < 0 || m.dst_row < 0 || m.src_row + m.n_rows > srows[m.src_rank] ||
+        m.dst_row + m.n_rows > drows[m.dst_rank] || m.src_col_bytes < 0 || m.dst_col_bytes < 0 ||
+        m.src_col_bytes + m.n_col_bytes > sp1[m.src_rank] || m.dst_col_bytes + m.n_col_bytes > dp1[m.dst_rank])
+      throw Error{SB_ERR_INTEGRITY, "apply_block_moves: move " + std::to_string(i) + " outside its buffers"};
+    SbJob j;
+    j.src = sb1[m.src_rank] + (uint64_t)(m.src_row * sp1[m.src_rank] + m.src_col_bytes);
+    j.dst = db1[m.dst_rank] + (uint64_t)(m.dst_row * dp1[m.dst_rank] + m.dst_col_bytes);
+    j.n_rows = m.n_rows;
+    j.width = m.n_col_bytes;
+    j.spitch = sp1[m.src_rank];
+    j.dpitch = dp1[m.dst_rank];
+    jobs.push_back(j);
+    if (m.copy_meta) {
+      SbJob k;
+      k.src = sb0[m.src_rank] + (uint64_t)(m.src_row * sp0[m.src_rank]);
+      k.dst = db0[m.dst_rank] + (uint64_t)(m.dst_row * dp0[m.dst_rank]);
+      k.n_rows = m.n_rows;
+      k.width = 16;
+      k.spitch = sp0[m.src_rank];
+      k.dpitch = dp0[m.dst_rank];
+      jobs.push_back(k);
+    }
+  }
+  const int64_t nj = (int64_t)jobs.size();
+  SbJob* dj = static_cast<SbJob*>(sb::g_move_jobs.get(sizeof(SbJob) * (size_t)std::max<int64_t>(1, nj)));
+  int64_t* dpo = static_cast<int64_t*>(sb::g_move_pieces.get(sizeof(int64_t) * (size_t)(nj + 1)));
+  int64_t* dn = static_cast<int64_t*>(sb::g_move_n.get(sizeof(int64_t) * 2));
+  if (nj) SB_CUDA(cudaMemcpyAsync(dj, jobs.data(), sizeof(SbJob) * nj, cudaMemcpyHostToDevice, s));
+  SB_CUDA(cudaMemcpyAsync(dn, &nj, sizeof nj, cudaMemcpyHostToDevice, s));
+  sb::k_pieces<<<1, 1024, 0, s>>>(dj, dn, dpo, dn + 1);
+  SB_CHECK_LAUNCH();
+  sb::k_copy<<<sb::copy_grid(), sb::kCopyThreads, 0, s>>>(dj, dpo, dn, 0);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(2);
+  SB_CUDA(cudaStreamSynchronize(s));  // host job vector and staging are reused
   SB_API_END
 }

@@ -30,6 +30,13 @@ struct sb_planner {
   std::vector<int32_t> bag_off, bag_ranks, bag_size, rank_bag, rank_member;
   bool identity = false;
   bool any_multi_bag = false;
+  bool uploaded = false;  // current plan came from sb_plan_upload (no bag tables)
+  // origin layout of an uploaded plan (segment CSR), kept for reverse_plan
+  int64_t seg_cap = 0;
+  int64_t* seg_off = nullptr;  // W+1
+  uint64_t* seg_id = nullptr;
+  int64_t* seg_first = nullptr;
+  int64_t* seg_len = nullptr;
 
   // constant topology tables (device)
   int32_t *d_bag_off = nullptr, *d_bag_ranks = nullptr, *d_bag_size = nullptr;
@@ -39,6 +46,11 @@ struct sb_planner {
   const uint64_t* ids = nullptr;
   const int64_t* lens = nullptr;
   const int64_t* rank_off = nullptr;
+  const double* w_in = nullptr;  // assign_to_bags mode: caller workloads
+  uint64_t* stage_ids = nullptr;  // staging for host-array entry points
+  int64_t* stage_lens = nullptr;
+  double* stage_w = nullptr;
+  int64_t* stage_off = nullptr;
 
   // per-sequence scratch (max_seqs)
   double* w = nullptr;
@@ -61,6 +73,10 @@ struct sb_planner {
   int64_t* bag_rows = nullptr;       // R*M
   int64_t* rep_chunks = nullptr;     // R
   unsigned long long* send_count = nullptr;  // W
+  unsigned long long* recv_count = nullptr;  // W (generic manifests)
+  // chunk-sized sort scratch for the generic reverse order (lazy)
+  uint64_t *ck_hi = nullptr, *ck_lo = nullptr, *ck_thi = nullptr, *ck_tlo = nullptr;
+  uint32_t *ck_v = nullptr, *ck_tv = nullptr;
 
   // plan (device)
   int64_t* n_chunks = nullptr;

@@ -37,6 +37,7 @@ struct PlanArgs {
   const uint64_t* ids;
   const int64_t* lens;
   const int64_t* rank_off;
+  const double* w_in;  // non-null: caller-supplied workloads (assign_to_bags)
   double* w;
   int32_t* seq_rank;
   int64_t* seq_off;
@@ -99,12 +100,18 @@ __global__ void __launch_bounds__(256) k_prep(PlanArgs a) {
         atomicOr(a.status, ST_NEG_LENGTH);
         len = 0;
       }
-      a.w[i] = gamma_weighted_workload(len, a.d_model, a.gamma);  // balancer.cpp:144
+      if (a.w_in) {  // assign_to_bags on caller workloads (balancer.cpp:18-20)
+        const double wi = a.w_in[i];
+        if (!(wi >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
+        a.w[i] = wi;
+      } else {
+        a.w[i] = gamma_weighted_workload(len, a.d_model, a.gamma);  // balancer.cpp:144
+      }
       a.seq_rank[i] = r;
       // duplicate sample_id detection inside the replica (open addressing)
       const uint64_t id = a.ids[i];
       if (id == ~0ull) {
-        if (atomicAdd(&a.sentinel[rep], 1) > 0) atomicOr(a.status, ST_DUP_ID);
+        if (atomicAdd(&a.sentinel[rep], 1) > 0 && !a.w_in) atomicOr(a.status, ST_DUP_ID);
       } else {
         uint64_t s = hash_slot(id) % (uint64_t)tsize;
         while (true) {
@@ -112,7 +119,7 @@ __global__ void __launch_bounds__(256) k_prep(PlanArgs a) {
               atomicCAS(reinterpret_cast<unsigned long long*>(tab + s), ~0ull, (unsigned long long)id);
           if (old == ~0ull) break;
           if (old == id) {
-            atomicOr(a.status, ST_DUP_ID);
+            if (!a.w_in) atomicOr(a.status, ST_DUP_ID);  // assign_to_bags allows repeats
             break;
           }
           s = (s + 1 == (uint64_t)tsize) ? 0 : s + 1;
@@ -141,7 +148,8 @@ __global__ void __launch_bounds__(1024) k_sort(PlanArgs a) {
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
       // (workload desc, sample_id asc) == ascending (~bits(w), id): w >= 0,
       // so its IEEE bits are monotone in value (balancer.cpp:37-40).
-      a.sk_hi[lo + i] = ~(uint64_t)__double_as_longlong(a.w[lo + i]);
+      const double wv = a.w[lo + i];
+      a.sk_hi[lo + i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);  // -0.0 ties +0.0
       a.sk_lo[lo + i] = a.ids[lo + i];
       a.sk_v[lo + i] = (uint32_t)i;
     }
@@ -490,6 +498,97 @@ __global__ void k_finalize(PlanArgs a) {
   }
 }
 
+// ------------------------------------------------ generic plan manifests
+// For plans that did not come from k_emit (uploaded RoutingPlans):
+// finalize_manifests (balancer.cpp:84-91) as ordered compactions by source
+// and target rank, and reverse_plan's receive order (balancer.cpp:259-285):
+// each incoming chunk's first containing segment in the origin layout, then
+// a sort by (segment, start, chunk index).
+struct GenericArgs {
+  int W;
+  const int64_t* n_chunks;
+  const uint64_t* c_id;
+  const int32_t *c_src, *c_dst;
+  const int64_t *c_start, *c_end;
+  const int64_t* seg_off;
+  const uint64_t* seg_id;
+  const int64_t *seg_first, *seg_len;
+  unsigned long long *send_count, *recv_count;
+  int64_t *send_off, *recv_off;
+  int32_t *send_idx, *recv_idx, *rev_recv_idx;
+  uint64_t *ck_hi, *ck_lo, *ck_thi, *ck_tlo;
+  uint32_t *ck_v, *ck_tv;
+  int32_t* status;
+};
+
+__global__ void k_generic_count(GenericArgs a) {
+  const int64_t n = *a.n_chunks;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&a.send_count[a.c_src[c]], 1ull);
+    atomicAdd(&a.recv_count[a.c_dst[c]], 1ull);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_generic_lists(GenericArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t sh[33];
+  __shared__ int64_t s_so, s_ro;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const int64_t n = *a.n_chunks;
+  if (tid == 0) {
+    int64_t so = 0, ro = 0;
+    for (int x = 0; x < r; ++x) {
+      so += (int64_t)a.send_count[x];
+      ro += (int64_t)a.recv_count[x];
+    }
+    s_so = so;
+    s_ro = ro;
+    a.send_off[r] = so;
+    a.recv_off[r] = ro;
+    if (r == a.W - 1) {
+      a.send_off[a.W] = so + (int64_t)a.send_count[r];
+      a.recv_off[a.W] = ro + (int64_t)a.recv_count[r];
+    }
+  }
+  __syncthreads();
+  int64_t cs = 0, cr = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += blockDim.x) {
+    const int64_t c = t0 + tid;
+    const bool fs = c < n && a.c_src[c] == r;
+    const bool fr = c < n && a.c_dst[c] == r;
+    int64_t ts, tr;
+    const int64_t es = block_excl_scan<int64_t>(fs ? 1 : 0, sh, &ts);
+    const int64_t er = block_excl_scan<int64_t>(fr ? 1 : 0, sh, &tr);
+    if (fs) a.send_idx[s_so + cs + es] = (int32_t)c;
+    if (fr) a.recv_idx[s_ro + cr + er] = (int32_t)c;
+    cs += ts;
+    cr += tr;
+  }
+  __syncthreads();
+  // reverse receive order of rank r: its outgoing chunks, keyed by the
+  // first origin segment containing them (balancer.cpp:267-277)
+  const int64_t s0 = a.seg_off[r], s1 = a.seg_off[r + 1];
+  for (int64_t i = tid; i < cs; i += blockDim.x) {
+    const int32_t c = a.send_idx[s_so + i];
+    int64_t seg = -1;
+    for (int64_t q = s0; q < s1; ++q) {
+      if (a.seg_id[q] == a.c_id[c] && a.c_start[c] >= a.seg_first[q] &&
+          a.c_end[c] <= a.seg_first[q] + a.seg_len[q]) {
+        seg = q - s0;
+        break;
+      }
+    }
+    if (seg < 0) atomicOr(a.status, 32);
+    a.ck_hi[s_so + i] = (uint64_t)(seg < 0 ? 0 : seg);
+    a.ck_lo[s_so + i] = (uint64_t)a.c_start[c];
+    a.ck_v[s_so + i] = (uint32_t)c;
+  }
+  __syncthreads();
+  block_sort(cs, a.ck_hi + s_so, a.ck_lo + s_so, a.ck_v + s_so, a.ck_thi + s_so, a.ck_tlo + s_so, a.ck_tv + s_so,
+             smem);
+  for (int64_t i = tid; i < cs; i += blockDim.x) a.rev_recv_idx[s_so + i] = (int32_t)a.ck_v[s_so + i];
+}
+
 // -------------------------------------------------------- identity kernels
 // identity_plan (balancer.cpp:227-240): chunk i = sequence i, src = dst.
 __global__ void k_identity(PlanArgs a) {
@@ -558,7 +657,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.d_model = (double)p->d_model; a.gamma = p->gamma; a.max_seqs = p->max_seqs;
   a.bag_off = p->d_bag_off; a.bag_ranks = p->d_bag_ranks; a.bag_size = p->d_bag_size;
   a.rank_bag = p->d_rank_bag; a.rank_member = p->d_rank_member;
-  a.ids = p->ids; a.lens = p->lens; a.rank_off = p->rank_off;
+  a.ids = p->ids; a.lens = p->lens; a.rank_off = p->rank_off; a.w_in = p->w_in;
   a.w = p->w; a.seq_rank = p->seq_rank; a.seq_off = p->seq_off; a.hash = p->hash;
   a.sk_hi = p->sk_hi; a.sk_lo = p->sk_lo; a.tk_hi = p->tk_hi; a.tk_lo = p->tk_lo;
   a.sk_v = p->sk_v; a.tk_v = p->tk_v;
@@ -589,6 +688,7 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->seq_bag, N); dalloc(&p->seq_G, N); dalloc(&p->seq_chunk_base, N);
   dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
   dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
+  dalloc(&p->recv_count, W);
   dalloc(&p->n_chunks, 1); dalloc(&p->n_seqs, 1);
   dalloc(&p->c_id, C); dalloc(&p->c_idx, C); dalloc(&p->c_src, C); dalloc(&p->c_dst, C);
   dalloc(&p->c_start, C); dalloc(&p->c_end, C); dalloc(&p->c_src_row, C); dalloc(&p->c_dst_row, C);
@@ -617,7 +717,10 @@ static void planner_free(sb_planner* p) {
                   p->c_dst, p->c_start, p->c_end, p->c_src_row, p->c_dst_row, p->c_seq_base,
                   p->send_off, p->recv_off, p->send_idx, p->recv_idx, p->rev_recv_idx,
                   p->origin_rows, p->target_rows, p->per_gpu, p->per_bag_occ, p->total, p->wir,
-                  p->violations, p->status, p->jobs, p->piece_off, p->n_jobs};
+                  p->violations, p->status, p->jobs, p->piece_off, p->n_jobs,
+                  p->stage_ids, p->stage_lens, p->stage_w, p->stage_off,
+                  p->seg_off, p->seg_id, p->seg_first, p->seg_len, p->recv_count, p->ck_hi, p->ck_lo,
+                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int i = 0; i < 6; ++i)
@@ -792,8 +895,106 @@ extern "C" sb_status sb_plan(sb_planner* p, const uint64_t* d_ids, const int64_t
   p->ids = d_ids;
   p->lens = d_lens;
   p->rank_off = d_rank_off;
+  p->w_in = nullptr;
   p->identity = false;
+  p->uploaded = false;
   sb::run_plan(p, (cudaStream_t)stream);
+  SB_API_END
+}
+
+// Manifests + reverse receive order for an uploaded plan (see k_generic_*).
+extern "C" sb_status sb_plan_manifests(sb_planner* p, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  if (!p->uploaded || !p->seg_off) throw Error{SB_ERR_CONFIG, "sb_plan_manifests: no uploaded plan"};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p->ck_hi) {
+    sb::dalloc(&p->ck_hi, p->max_chunks); sb::dalloc(&p->ck_lo, p->max_chunks);
+    sb::dalloc(&p->ck_thi, p->max_chunks); sb::dalloc(&p->ck_tlo, p->max_chunks);
+    sb::dalloc(&p->ck_v, p->max_chunks); sb::dalloc(&p->ck_tv, p->max_chunks);
+    SB_CUDA(cudaFuncSetAttribute(sb::k_generic_lists, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sb::kSortSmemBytes));
+  }
+  sb::GenericArgs g;
+  g.W = p->W;
+  g.n_chunks = p->n_chunks;
+  g.c_id = p->c_id; g.c_src = p->c_src; g.c_dst = p->c_dst; g.c_start = p->c_start; g.c_end = p->c_end;
+  g.seg_off = p->seg_off; g.seg_id = p->seg_id; g.seg_first = p->seg_first; g.seg_len = p->seg_len;
+  g.send_count = p->send_count; g.recv_count = p->recv_count;
+  g.send_off = p->send_off; g.recv_off = p->recv_off;
+  g.send_idx = p->send_idx; g.recv_idx = p->recv_idx; g.rev_recv_idx = p->rev_recv_idx;
+  g.ck_hi = p->ck_hi; g.ck_lo = p->ck_lo; g.ck_thi = p->ck_thi; g.ck_tlo = p->ck_tlo; g.ck_v = p->ck_v;
+  g.ck_tv = p->ck_tv;
+  g.status = p->status;
+  SB_CUDA(cudaMemsetAsync(p->send_count, 0, sizeof(unsigned long long) * p->W, s));
+  SB_CUDA(cudaMemsetAsync(p->recv_count, 0, sizeof(unsigned long long) * p->W, s));
+  SB_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int32_t), s));
+  sb::k_generic_count<<<148, 256, 0, s>>>(g);
+  SB_CHECK_LAUNCH();
+  sb::k_generic_lists<<<p->W, 1024, sb::kSortSmemBytes, s>>>(g);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(2);
+  SB_CUDA(cudaStreamSynchronize(s));
+  int32_t st = 0;
+  SB_CUDA(cudaMemcpy(&st, p->status, sizeof st, cudaMemcpyDeviceToHost));
+  if (st) throw Error{SB_ERR_INTEGRITY, "reverse_plan: a chunk does not fit any destination segment"};
+  SB_API_END
+}
+
+// assign_to_bags (balancer.cpp:15-64) on caller workloads: k_prep (workload
+// validation) -> k_sort (order + total) -> k_greedy, then the assignment in
+// sorted order is copied back.  Host arrays in and out; synchronises.
+extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t* ids, const double* workloads,
+                                       uint64_t* out_ids, double* out_w, int32_t* out_bag, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || n < 0 || (n > 0 && (!ids || !workloads || !out_ids || !out_w || !out_bag)))
+    throw Error{SB_ERR_CONFIG, "sb_assign_to_bags: bad arguments"};
+  if (p->R != 1) throw Error{SB_ERR_CONFIG, "sb_assign_to_bags: planner must describe one replica"};
+  if (n > p->max_seqs) throw Error{SB_ERR_CAPACITY, "sb_assign_to_bags: more sequences than planner capacity"};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p->stage_ids) {
+    sb::dalloc(&p->stage_ids, p->max_seqs);
+    sb::dalloc(&p->stage_lens, p->max_seqs);
+    sb::dalloc(&p->stage_w, p->max_seqs);
+    sb::dalloc(&p->stage_off, p->W + 1);
+    SB_CUDA(cudaMemset(p->stage_lens, 0, sizeof(int64_t) * p->max_seqs));
+  }
+  std::vector<int64_t> off(p->W + 1, n);
+  off[0] = 0;
+  if (n > 0) {
+    SB_CUDA(cudaMemcpyAsync(p->stage_ids, ids, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+    SB_CUDA(cudaMemcpyAsync(p->stage_w, workloads, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  }
+  SB_CUDA(cudaMemcpyAsync(p->stage_off, off.data(), sizeof(int64_t) * (p->W + 1), cudaMemcpyHostToDevice, s));
+  p->ids = p->stage_ids;
+  p->lens = p->stage_lens;
+  p->rank_off = p->stage_off;
+  p->w_in = p->stage_w;
+  p->identity = false;
+  p->uploaded = false;
+  sb::PlanArgs a = sb::make_args(p);
+  sb::plan_common_prologue(p, s);
+  sb::k_prep<<<p->W, 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  sb::k_sort<<<2 * p->R + 1, 1024, sb::kSortSmemBytes, s>>>(a);
+  SB_CHECK_LAUNCH();
+  if ((p->M + 31) / 32 <= 1) sb::k_greedy<1><<<p->R, 32, 0, s>>>(a);
+  else sb::k_greedy<2><<<p->R, 32, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(3);
+  SB_CUDA(cudaStreamSynchronize(s));
+  int32_t st = 0;
+  SB_CUDA(cudaMemcpy(&st, p->status, sizeof st, cudaMemcpyDeviceToHost));
+  p->w_in = nullptr;
+  if (st & sb::ST_NEG_LENGTH) throw Error{SB_ERR_CONFIG, "assign_to_bags: negative workload"};
+  if (st) throw Error{SB_ERR_INTEGRITY, "assign_to_bags: device status " + std::to_string(st)};
+  if (n > 0) {
+    std::vector<int32_t> idx(n);
+    SB_CUDA(cudaMemcpy(idx.data(), p->sorted_idx, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(out_w, p->sorted_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(out_bag, p->pick, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) out_ids[i] = ids[idx[i]];
+  }
   SB_API_END
 }
 
@@ -804,7 +1005,9 @@ extern "C" sb_status sb_plan_identity(sb_planner* p, const uint64_t* d_ids, cons
   p->ids = d_ids;
   p->lens = d_lens;
   p->rank_off = d_rank_off;
+  p->w_in = nullptr;
   p->identity = true;
+  p->uploaded = false;
   sb::run_identity(p, (cudaStream_t)stream);
   SB_API_END
 }
@@ -857,7 +1060,8 @@ extern "C" sb_status sb_plan_sizes(sb_planner* p, sb_stream stream, int64_t* n_c
   check_plan_status(p, (cudaStream_t)stream);
   int64_t c = 0, n = 0;
   SB_CUDA(cudaMemcpy(&c, p->n_chunks, sizeof c, cudaMemcpyDeviceToHost));
-  SB_CUDA(cudaMemcpy(&n, p->rank_off + p->W, sizeof n, cudaMemcpyDeviceToHost));
+  if (!p->uploaded && p->rank_off)  // uploaded plans carry no sequence metadata
+    SB_CUDA(cudaMemcpy(&n, p->rank_off + p->W, sizeof n, cudaMemcpyDeviceToHost));
   if (n_chunks) *n_chunks = c;
   if (n_seqs) *n_seqs = n;
   SB_API_END
