@@ -146,6 +146,11 @@ typedef struct sb_plan_host {
 } sb_plan_host;
 SB_API sb_status sb_plan_download(sb_planner* p, sb_plan_host* out, sb_stream stream);
 
+/* Planner pipeline: 0 = auto (single-CTA fused planner when the capacity is
+ * at most 2048 sequences, else the multi-kernel pipeline), 1 = force the
+ * fused planner, 2 = force the multi-kernel pipeline.  Both are bit-exact. */
+SB_API sb_status sb_planner_set_path(sb_planner* p, int path);
+
 /* Plan latency breakdown of the last sb_plan (device time, microseconds,
  * measured with events when timing is enabled; zeros otherwise). */
 SB_API sb_status sb_planner_enable_timing(sb_planner* p, int enable);

@@ -90,6 +90,7 @@ _SIGS = {
     "sb_plan_sizes": (C.c_int, [C.c_void_p] * 4),
     "sb_plan_download": (C.c_int, [C.c_void_p] * 3),
     "sb_planner_enable_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "sb_planner_set_path": (C.c_int, [C.c_void_p, C.c_int]),
     "sb_planner_timing": (C.c_int, [C.c_void_p] * 6),
     "sb_world_create": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sb_world_destroy": (C.c_int, [C.c_void_p]),

@@ -231,6 +231,10 @@ class Planner:
         self._meta = meta
         return self
 
+    def set_path(self, path: str):
+        """'auto' | 'small' (fused single-CTA planner) | 'large' (multi-kernel)."""
+        call("sb_planner_set_path", self._h, {"auto": 0, "small": 1, "large": 2}[path])
+
     def enable_timing(self, on: bool = True):
         call("sb_planner_enable_timing", self._h, int(on))
 

@@ -78,8 +78,8 @@ struct LayoutPlan {
   int U, M;
 };
 
-__global__ void k_layout(WorldArgs d, WorldArgs s, LayoutPlan lp, TensorInfo ti, int mode) {
-  const int t = threadIdx.x;
+__device__ void layout_tensor(const WorldArgs& d, const WorldArgs& s, const LayoutPlan& lp, const TensorInfo& ti,
+                              int mode, int t) {
   if (t >= d.T) return;
   int owner = -1;
   int64_t off = 0;
@@ -122,6 +122,10 @@ __global__ void k_layout(WorldArgs d, WorldArgs s, LayoutPlan lp, TensorInfo ti,
   }
 }
 
+__global__ void k_layout(WorldArgs d, WorldArgs s, LayoutPlan lp, TensorInfo ti, int mode) {
+  layout_tensor(d, s, lp, ti, mode, threadIdx.x);
+}
+
 // ----------------------------------------------------------- job builders
 struct JobArgs {
   const int64_t* n_chunks;
@@ -137,11 +141,10 @@ __device__ __forceinline__ bool is_local(const WorldArgs& w, int r) {
   return r >= w.first_local && r < w.first_local + w.n_local;
 }
 
-__global__ void k_jobs_route(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti, int reverse) {
-  const int64_t nc = *j.n_chunks;
+__device__ __forceinline__ void route_job(const JobArgs& j, const WorldArgs& s, const WorldArgs& d,
+                                          const TensorInfo& ti, int reverse, int64_t x) {
   const int T = s.T;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *j.n_jobs = nc * T;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nc * T; x += (int64_t)gridDim.x * blockDim.x) {
+  {
     const int64_t c = x / T;
     const int t = (int)(x % T);
     const int sr = reverse ? j.c_dst[c] : j.c_src[c];
@@ -160,17 +163,22 @@ __global__ void k_jobs_route(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti,
   }
 }
 
+__global__ void k_jobs_route(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti, int reverse) {
+  const int64_t n = *j.n_chunks * s.T;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *j.n_jobs = n;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+    route_job(j, s, d, ti, reverse, x);
+}
+
 // pre_attn (exchange.cpp:298-325): chunk c = (seq q, member m) held by bag
 // rank m moves, for each destination member d, its column slice d (payload)
 // or its whole rows (metadata / aux) to row seq_base(q) + start on rank d.
 // post_attn (exchange.cpp:406-431) is the transpose: destination chunk
 // c = (q, d) gathers slice m from every member m; metadata from m = 0 only.
-__global__ void k_jobs_ulysses(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti, int post) {
-  const int64_t nc = *j.n_chunks;
+__device__ __forceinline__ void ulysses_job(const JobArgs& j, const WorldArgs& s, const WorldArgs& d,
+                                            const TensorInfo& ti, int post, int64_t x) {
   const int T = s.T, G = j.max_bag;
-  const int64_t total = nc * G * T;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *j.n_jobs = total;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+  {
     const int t = (int)(x % T);
     const int64_t y = x / T;
     const int other = (int)(y % G);  // d for pre, m for post
@@ -230,6 +238,13 @@ __global__ void k_jobs_ulysses(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo t
   }
 }
 
+__global__ void k_jobs_ulysses(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti, int post) {
+  const int64_t total = *j.n_chunks * j.max_bag * s.T;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *j.n_jobs = total;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x)
+    ulysses_job(j, s, d, ti, post, x);
+}
+
 // Piece decomposition + exclusive scan (single CTA).  A job whose rows are
 // contiguous on both sides is split into kPieceBytes spans of the flat byte
 // range; otherwise into groups of kPieceBytes/width rows.
@@ -245,8 +260,7 @@ __device__ __forceinline__ int64_t job_pieces(const SbJob& j) {
   return (j.n_rows + rp - 1) / rp;
 }
 
-__global__ void __launch_bounds__(1024) k_pieces(const SbJob* jobs, const int64_t* n_jobs_p, int64_t* piece_off,
-                                                 int64_t* bytes_moved) {
+__device__ void pieces_body(const SbJob* jobs, const int64_t* n_jobs_p, int64_t* piece_off, int64_t* bytes_moved) {
   __shared__ int64_t sh[33];
   const int64_t n = *n_jobs_p;
   const int nt = blockDim.x, tid = threadIdx.x;
@@ -270,6 +284,31 @@ __global__ void __launch_bounds__(1024) k_pieces(const SbJob* jobs, const int64_
     piece_off[n] = tot;
     *bytes_moved = tb;
   }
+}
+
+__global__ void __launch_bounds__(1024) k_pieces(const SbJob* jobs, const int64_t* n_jobs_p, int64_t* piece_off,
+                                                 int64_t* bytes_moved) {
+  pieces_body(jobs, n_jobs_p, piece_off, bytes_moved);
+}
+
+// Fused exchange preparation for plans of modest size: destination layout,
+// copy jobs and the piece scan in ONE CTA (three launches become one; the
+// phases hand over through global memory inside the block).  op: 0 route,
+// 1 reverse_route, 2 pre_attn, 3 post_attn.
+__global__ void __launch_bounds__(1024) k_exchange_prep(JobArgs j, WorldArgs s, WorldArgs d, TensorInfo ti,
+                                                        LayoutPlan lp, int op, int64_t* piece_off,
+                                                        int64_t* bytes_moved) {
+  const int mode = op < 2 ? 0 : (op == 2 ? 1 : 2);
+  layout_tensor(d, s, lp, ti, mode, threadIdx.x);
+  __syncthreads();
+  const int64_t n = op < 2 ? *j.n_chunks * s.T : *j.n_chunks * j.max_bag * s.T;
+  if (threadIdx.x == 0) *j.n_jobs = n;
+  for (int64_t x = threadIdx.x; x < n; x += blockDim.x) {
+    if (op < 2) route_job(j, s, d, ti, op, x);
+    else ulysses_job(j, s, d, ti, op == 3, x);
+  }
+  __syncthreads();
+  pieces_body(j.jobs, j.n_jobs, piece_off, bytes_moved);
 }
 
 // ------------------------------------------------------------ copy kernel
@@ -346,7 +385,8 @@ __device__ void warp_copy_bytes(const SbJob& j, int64_t r0, int64_t r1, int lane
   }
 }
 
-__global__ void __launch_bounds__(kCopyThreads) k_copy(const SbJob* __restrict__ jobs,
+template <int MINB>
+__global__ void __launch_bounds__(kCopyThreads, MINB) k_copy(const SbJob* __restrict__ jobs,
                                                        const int64_t* __restrict__ piece_off,
                                                        const int64_t* __restrict__ n_jobs_p, int fence_sys) {
   const int64_t n_jobs = *n_jobs_p;
@@ -401,6 +441,137 @@ __global__ void k_rank_rows(const int64_t* lens, const int64_t* off, int64_t* ro
   int64_t tot;
   block_excl_scan<int64_t>(local, sh, &tot);
   if (threadIdx.x == 0) rows[r] = tot;
+}
+
+// ------------------------------------------------- TMA bulk copy engine
+// The same piece decomposition as k_copy, moved by the Tensor Memory
+// Accelerator instead of the LSU: one elected lane per CTA streams each
+// piece global -> shared (cp.async.bulk ... mbarrier::complete_tx) and
+// shared -> global (cp.async.bulk.global.shared::cta.bulk_group) through a
+// kTmaStages-deep ring of 32 KB stages.  Registers and issue slots stay
+// free, and a few hundred bytes of instructions keep ~200 KB per SM in
+// flight.  Used when every job is 16-byte aligned and pieces fit a stage
+// (always true for the route/Ulysses layouts here) and the destination is
+// local HBM.
+constexpr int kTmaStages = 3;
+constexpr size_t kTmaSmem = (size_t)kTmaStages * kPieceBytes;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct PieceRef {
+  const char* src;
+  char* dst;
+  int64_t rows;    // rows in this piece (flat: 1)
+  int64_t width;   // bytes per row (flat: span bytes)
+  int64_t spitch, dpitch;
+};
+
+__device__ __forceinline__ PieceRef piece_of(const SbJob& j, int64_t k) {
+  PieceRef p;
+  if (job_flat(j)) {
+    const int64_t len = j.n_rows * j.width;
+    const int64_t b = k * kPieceBytes;
+    p.src = reinterpret_cast<const char*>(j.src) + b;
+    p.dst = reinterpret_cast<char*>(j.dst) + b;
+    p.rows = 1;
+    p.width = (b + kPieceBytes < len ? kPieceBytes : len - b);
+    p.spitch = p.dpitch = 0;
+  } else {
+    const int64_t rp = job_rows_per_piece(j);
+    const int64_t r0 = k * rp, r1 = r0 + rp < j.n_rows ? r0 + rp : j.n_rows;
+    p.src = reinterpret_cast<const char*>(j.src) + r0 * j.spitch;
+    p.dst = reinterpret_cast<char*>(j.dst) + r0 * j.dpitch;
+    p.rows = r1 - r0;
+    p.width = j.width;
+    p.spitch = j.spitch;
+    p.dpitch = j.dpitch;
+  }
+  return p;
+}
+
+__global__ void __launch_bounds__(32) k_copy_tma(const SbJob* __restrict__ jobs, const int64_t* __restrict__ piece_off,
+                                                 const int64_t* __restrict__ n_jobs_p) {
+  extern __shared__ __align__(128) unsigned char stage_mem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  const int64_t n_jobs = *n_jobs_p;
+  const int64_t total = piece_off[n_jobs];
+  const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
+  if (g0 >= g1 || threadIdx.x != 0) return;  // one elected lane drives the DMA ring
+  for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  int64_t lo = 0, hi = n_jobs;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (piece_off[mid] <= g0) lo = mid;
+    else hi = mid;
+  }
+  int64_t jl = lo, js = lo;  // job cursors of the load and the store streams
+  auto load = [&](int64_t g, int s) {
+    while (piece_off[jl + 1] <= g) ++jl;
+    const PieceRef p = piece_of(jobs[jl], g - piece_off[jl]);
+    char* sm = reinterpret_cast<char*>(stage_mem) + (size_t)s * kPieceBytes;
+    mbar_expect_tx(&bars[s], (uint32_t)(p.rows * p.width));
+    for (int64_t r = 0; r < p.rows; ++r) bulk_g2s(sm + r * p.width, p.src + r * p.spitch, (uint32_t)p.width, &bars[s]);
+  };
+  auto store = [&](int64_t g, int s) {
+    while (piece_off[js + 1] <= g) ++js;
+    const PieceRef p = piece_of(jobs[js], g - piece_off[js]);
+    const char* sm = reinterpret_cast<const char*>(stage_mem) + (size_t)s * kPieceBytes;
+    for (int64_t r = 0; r < p.rows; ++r) bulk_s2g(p.dst + r * p.dpitch, sm + r * p.width, (uint32_t)p.width);
+    bulk_commit();
+  };
+  const int64_t n = g1 - g0;
+  for (int64_t k = 0; k < kTmaStages && k < n; ++k) load(g0 + k, (int)k);
+  for (int64_t k = 0; k < n; ++k) {
+    const int s = (int)(k % kTmaStages);
+    mbar_wait(&bars[s], (uint32_t)((k / kTmaStages) & 1));
+    store(g0 + k, s);
+    // refill the stage whose store was issued one step ago, once it has
+    // been read out of shared memory
+    if (k >= 1 && k - 1 + kTmaStages < n) {
+      bulk_wait_read<1>();
+      load(g0 + k - 1 + kTmaStages, (int)((k - 1) % kTmaStages));
+    }
+  }
+  bulk_wait_all();
 }
 
 static int g_num_sms = 0;
@@ -534,9 +705,35 @@ static void check_compatible(sb_planner* p, sb_world* a, sb_world* b) {
   if (a->T > 16) throw Error{SB_ERR_CONFIG, "at most 16 tensors per world"};
 }
 
-static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys) {
-  k_pieces<<<1, 1024, 0, s>>>(p->jobs, p->n_jobs, p->piece_off, p->n_jobs + 1);
-  SB_CHECK_LAUNCH();
+// Copy engines: 0 = LSU (128-bit LDG/STG, 8 loads in flight per lane),
+// 2 = LSU capped at 3 CTAs/SM worth of registers, 1 = TMA bulk.  Peer
+// (multi-process) destinations always use the LSU path.  Defaults from the
+// B200 measurements in profiles/: contiguous route spans -> LSU, strided
+// Ulysses head slices -> TMA.  SEQBAL_ROUTE_ENGINE / SEQBAL_ULYSSES_ENGINE =
+// ldg|ldg3|tma override.
+static int engine_from_env(const char* var, int dflt) {
+  const char* v = getenv(var);
+  if (!v) return dflt;
+  const std::string e(v);
+  return e == "tma" ? 1 : e == "ldg3" ? 2 : e == "ldg" ? 0 : dflt;
+}
+static int route_engine() {
+  static int e = engine_from_env("SEQBAL_ROUTE_ENGINE", 0);
+  return e;
+}
+static int ulysses_engine() {
+  static int e = engine_from_env("SEQBAL_ULYSSES_ENGINE", 1);
+  return e;
+}
+
+constexpr int64_t kFusedPrepMaxJobs = 1 << 16;  // single-CTA prep up to this many jobs
+
+static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys, bool tma_ok, int engine, bool pieces_done) {
+  if (!pieces_done) {
+    k_pieces<<<1, 1024, 0, s>>>(p->jobs, p->n_jobs, p->piece_off, p->n_jobs + 1);
+    SB_CHECK_LAUNCH();
+    count_launch(1);
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->timing) {
     if (p->copy_used + 2 > p->copy_ev.size()) {
@@ -553,10 +750,23 @@ static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys) {
     p->copy_used += 2;
     SB_CUDA(cudaEventRecord(e0, s));
   }
-  k_copy<<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+  if (!fence_sys && tma_ok && engine == 1) {
+    static bool attr = false;
+    if (!attr) {
+      SB_CUDA(cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      SB_CUDA(cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      attr = true;
+    }
+    copy_grid();
+    k_copy_tma<<<g_num_sms * 2, 32, kTmaSmem, s>>>(p->jobs, p->piece_off, p->n_jobs);
+  } else if (engine == 2) {
+    k_copy<3><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+  } else {
+    k_copy<1><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+  }
   SB_CHECK_LAUNCH();
   if (e1) SB_CUDA(cudaEventRecord(e1, s));
-  count_launch(2);
+  count_launch(1);
 }
 
 }  // namespace sb
@@ -754,13 +964,23 @@ extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_worl
   p->current_op = reverse ? 1 : 0;
   sb::LayoutPlan lp{};
   lp.rows_src = reverse ? p->origin_rows : p->target_rows;
-  sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
-  SB_CHECK_LAUNCH();
-  sb::k_jobs_route<<<std::min<int64_t>(1184, (p->max_chunks * src->T + 255) / 256), 256, 0, s>>>(
-      sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), reverse);
-  SB_CHECK_LAUNCH();
-  sb::count_launch(2);
-  sb::run_copy(p, s, dst->n_procs > 1);
+  const bool fused = p->max_chunks * src->T <= sb::kFusedPrepMaxJobs;
+  if (fused) {
+    sb::k_exchange_prep<<<1, 1024, 0, s>>>(sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), lp,
+                                           reverse ? 1 : 0, p->piece_off, p->n_jobs + 1);
+    SB_CHECK_LAUNCH();
+    sb::count_launch(1);
+  } else {
+    sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
+    SB_CHECK_LAUNCH();
+    sb::k_jobs_route<<<std::min<int64_t>(1184, (p->max_chunks * src->T + 255) / 256), 256, 0, s>>>(
+        sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), reverse);
+    SB_CHECK_LAUNCH();
+    sb::count_launch(2);
+  }
+  bool tma_ok = true;  // every row size a multiple of 16 B: all spans are TMA-legal
+  for (int64_t rb : src->row_bytes) tma_ok &= rb % 16 == 0;
+  sb::run_copy(p, s, dst->n_procs > 1, tma_ok, sb::route_engine(), fused);
   SB_API_END
 }
 
@@ -788,14 +1008,31 @@ static void ulysses(sb_planner* p, sb_world* src, sb_world* dst, cudaStream_t s,
   lp.target_rows = p->target_rows;
   lp.U = p->U;
   lp.M = p->M;
-  sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), post ? 2 : 1);
-  SB_CHECK_LAUNCH();
   const int64_t total = p->max_chunks * p->max_bag * src->T;
-  sb::k_jobs_ulysses<<<std::min<int64_t>(1184, (total + 255) / 256), 256, 0, s>>>(
-      sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), post);
-  SB_CHECK_LAUNCH();
-  sb::count_launch(2);
-  sb::run_copy(p, s, dst->n_procs > 1);
+  const bool fused = total <= sb::kFusedPrepMaxJobs;
+  if (fused) {
+    sb::k_exchange_prep<<<1, 1024, 0, s>>>(sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), lp,
+                                           post ? 3 : 2, p->piece_off, p->n_jobs + 1);
+    SB_CHECK_LAUNCH();
+    sb::count_launch(1);
+  } else {
+    sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), post ? 2 : 1);
+    SB_CHECK_LAUNCH();
+    sb::k_jobs_ulysses<<<std::min<int64_t>(1184, (total + 255) / 256), 256, 0, s>>>(
+        sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), post);
+    SB_CHECK_LAUNCH();
+    sb::count_launch(2);
+  }
+  bool tma_ok = true;  // row and head-slice sizes multiples of 16 B, slices within a stage
+  for (int t = 0; t < src->T; ++t) {
+    tma_ok &= src->row_bytes[t] % 16 == 0;
+    if (src->tensor_desc[t] == 1)
+      for (int b = 0; b < p->M; ++b) {
+        const int64_t slice = src->row_bytes[t] / p->bag_size[b];
+        tma_ok &= slice % 16 == 0 && slice <= sb::kPieceBytes;
+      }
+  }
+  sb::run_copy(p, s, dst->n_procs > 1, tma_ok, sb::ulysses_engine(), fused);
 }
 
 extern "C" sb_status sb_pre_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream) {
@@ -1194,7 +1431,7 @@ extern "C" sb_status sb_apply_moves(sb_world* src, sb_world* dst, const sb_block
   SB_CUDA(cudaMemcpyAsync(dn, &nj, sizeof nj, cudaMemcpyHostToDevice, s));
   sb::k_pieces<<<1, 1024, 0, s>>>(dj, dn, dpo, dn + 1);
   SB_CHECK_LAUNCH();
-  sb::k_copy<<<sb::copy_grid(), sb::kCopyThreads, 0, s>>>(dj, dpo, dn, 0);
+  sb::k_copy<1><<<sb::copy_grid(), sb::kCopyThreads, 0, s>>>(dj, dpo, dn, 0);
   SB_CHECK_LAUNCH();
   sb::count_launch(2);
   SB_CUDA(cudaStreamSynchronize(s));  // host job vector and staging are reused

@@ -31,6 +31,8 @@ struct sb_planner {
   bool identity = false;
   bool any_multi_bag = false;
   bool uploaded = false;  // current plan came from sb_plan_upload (no bag tables)
+  int path = 0;           // planner pipeline: 0 auto, 1 single-CTA small, 2 multi-kernel
+  size_t small_smem = 0;  // dynamic shared memory of the small path
   // origin layout of an uploaded plan (segment CSR), kept for reverse_plan
   int64_t seg_cap = 0;
   int64_t* seg_off = nullptr;  // W+1

@@ -498,6 +498,10 @@ __global__ void k_finalize(PlanArgs a) {
   }
 }
 
+}  // namespace sb
+#include "planner_small.cuh"
+namespace sb {
+
 // ------------------------------------------------ generic plan manifests
 // For plans that did not come from k_emit (uploaded RoutingPlans):
 // finalize_manifests (balancer.cpp:84-91) as ordered compactions by source
@@ -705,6 +709,15 @@ static void planner_alloc(sb_planner* p) {
   SB_CUDA(cudaMemcpy(p->d_rank_member, p->rank_member.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
   SB_CUDA(cudaFuncSetAttribute(k_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
   SB_CUDA(cudaFuncSetAttribute(k_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
+  if (p->max_seqs <= kSmallSeqs && p->W <= 1024) {
+    p->small_smem = small_layout((int)p->max_seqs, p->W, p->R * p->M, p->R).total;
+    static size_t set_to = 0;  // attribute is per function: keep the largest requested
+    if (p->small_smem > set_to) {
+      SB_CUDA(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->small_smem));
+      set_to = p->small_smem;
+    }
+  }
+  if (const char* e = getenv("SEQBAL_PLANNER")) p->path = std::string(e) == "small" ? 1 : std::string(e) == "large" ? 2 : 0;
   for (int i = 0; i < 6; ++i) SB_CUDA(cudaEventCreate(&p->ev[i]));
 }
 
@@ -735,8 +748,24 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
   SB_CUDA(cudaMemsetAsync(p->violations, 0, sizeof(int32_t), s));
 }
 
+static bool use_small_path(const sb_planner* p) {
+  if (p->path == 2) return false;
+  const bool fits = p->max_seqs <= kSmallSeqs && p->W <= 1024 && p->M <= kMaxBags;
+  return fits && (p->path == 1 || p->path == 0);
+}
+
 static void run_plan(sb_planner* p, cudaStream_t s) {
   PlanArgs a = make_args(p);
+  if (use_small_path(p)) {
+    SB_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int32_t), s));
+    if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
+    k_plan_small<<<1, 1024, p->small_smem, s>>>(a, (int)p->max_seqs);
+    SB_CHECK_LAUNCH();
+    if (p->timing)
+      for (int i = 1; i < 6; ++i) SB_CUDA(cudaEventRecord(p->ev[i], s));
+    count_launch(1);
+    return;
+  }
   plan_common_prologue(p, s);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
   k_prep<<<p->W, 256, 0, s>>>(a);
@@ -899,6 +928,15 @@ extern "C" sb_status sb_plan(sb_planner* p, const uint64_t* d_ids, const int64_t
   p->identity = false;
   p->uploaded = false;
   sb::run_plan(p, (cudaStream_t)stream);
+  SB_API_END
+}
+
+extern "C" sb_status sb_planner_set_path(sb_planner* p, int path) {
+  SB_API_BEGIN
+  if (!p || path < 0 || path > 2) throw Error{SB_ERR_CONFIG, "sb_planner_set_path: path must be 0, 1 or 2"};
+  if (path == 1 && !(p->max_seqs <= sb::kSmallSeqs && p->W <= 1024))
+    throw Error{SB_ERR_CONFIG, "sb_planner_set_path: capacity too large for the single-CTA planner"};
+  p->path = path;
   SB_API_END
 }
 

@@ -1,0 +1,483 @@
+// Single-CTA planner for small batches (up to kSmallSeqs sequences).
+//
+// The multi-kernel pipeline in planner.cu is launch-latency bound when a
+// step carries a few dozen sequences (C2: 30): six launches, each paying a
+// kernel start and a cold read of what the previous one wrote.  Here one
+// 1024-thread CTA keeps every per-sequence array in shared memory and runs
+// the same phases back to back, separated by __syncthreads:
+//   load + workload + origin offsets -> duplicate check (sort by id) ->
+//   serial FP64 totals -> sort by (workload desc, id asc) -> greedy (warp
+//   per replica) -> stable bag partition + chunk emission -> manifests,
+//   receive rows, Ulysses bases, reverse order -> WIR.
+// Results are bit-identical to the large path (tests/test_gpu_parity.py
+// runs both on the same inputs).
+#pragma once
+
+namespace sb {
+
+constexpr int kSmallSeqs = 2048;
+
+__host__ __device__ inline int small_pow2(int n) {
+  int t = 32;
+  while (t < n) t <<= 1;
+  return t;
+}
+
+struct SmallLayout {  // byte offsets into dynamic shared memory
+  size_t ids, lens, w, soff, hi, lo, v, rank, sorted, pick, G, cb, bo, rank_off, rpre, bagcnt, bagcb, bagq,
+      sendcnt, sendoff, reptot, total;
+  int T;
+};
+
+__host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int R) {
+  SmallLayout L;
+  const int T = small_pow2(cap);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += (bytes + 15) & ~size_t(15);
+    return at;
+  };
+  L.T = T;
+  L.ids = take(8ull * cap);
+  L.lens = take(8ull * cap);
+  L.w = take(8ull * cap);
+  L.soff = take(8ull * cap);
+  L.hi = take(8ull * T);
+  L.lo = take(8ull * T);
+  L.v = take(4ull * T);
+  L.rank = take(4ull * cap);
+  L.sorted = take(4ull * cap);
+  L.pick = take(4ull * cap);
+  L.G = take(4ull * cap);
+  L.cb = take(8ull * cap);
+  L.bo = take(4ull * cap);
+  L.rank_off = take(8ull * (W + 1));
+  L.rpre = take(8ull * (W + 1));
+  L.bagcnt = take(4ull * RM);
+  L.bagcb = take(8ull * RM);
+  L.bagq = take(4ull * RM);
+  L.sendcnt = take(8ull * W);
+  L.sendoff = take(8ull * (W + 1));
+  L.reptot = take(8ull * R);
+  L.total = o;
+  return L;
+}
+
+// Bitonic sort of n records already in shared memory (capacity t = pow2).
+__device__ void smem_bitonic(uint64_t* hi, uint64_t* lo, uint32_t* v, int n, int t) {
+  for (int i = n + threadIdx.x; i < t; i += blockDim.x) {
+    hi[i] = ~0ull;
+    lo[i] = ~0ull;
+    v[i] = 0xffffffffu;
+  }
+  __syncthreads();
+  for (int k = 2; k <= t; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < t / 2; i += blockDim.x) {
+        const int a = 2 * j * (i / j) + (i % j), b = a + j;
+        const bool up = (a & k) == 0;
+        if (rec_less(hi[b], lo[b], v[b], hi[a], lo[a], v[a]) == up) {
+          uint64_t x = hi[a]; hi[a] = hi[b]; hi[b] = x;
+          uint64_t y = lo[a]; lo[a] = lo[b]; lo[b] = y;
+          uint32_t z = v[a]; v[a] = v[b]; v[b] = z;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Warp-level inclusive scan helper over int64.
+__device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_incl_scan<int64_t>(x); }
+
+template <int BPL>
+__device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, const double* s_w, const int32_t* s_sorted,
+                             int32_t* s_pick, int32_t* s_bagcnt, double total_rep, int* viol_out) {
+  const int lane = threadIdx.x & 31;
+  const double target = __ddiv_rn(total_rep, (double)a.U);
+  double cap[BPL], asg[BPL], occ[BPL], rem[BPL];
+  int cnt[BPL];
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    const int j = lane + 32 * i;
+    const int size = j < a.M ? a.bag_size[j] : 0;
+    cap[i] = __dmul_rn((double)size, target);
+    asg[i] = 0.0;
+    occ[i] = occupancy(0.0, cap[i]);
+    rem[i] = __dsub_rn(cap[i], 0.0);
+    cnt[i] = 0;
+  }
+  int viol = 0;
+  for (int64_t p = 0; p < n; ++p) {
+    const double w = s_w[s_sorted[lo + p]];
+    double nasg[BPL], nocc[BPL], nrem[BPL];
+    uint64_t best_key = ~0ull;
+    uint32_t best_j = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < BPL; ++i) {
+      nasg[i] = __dadd_rn(asg[i], w);
+      nocc[i] = occupancy(nasg[i], cap[i]);
+      nrem[i] = __dsub_rn(cap[i], nasg[i]);
+      const uint32_t j = lane + 32 * i;
+      if (j < (uint32_t)a.M) {
+        const bool feasible = rem[i] >= w;
+        const uint64_t key = (feasible ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ[i]);
+        if (key < best_key) {
+          best_key = key;
+          best_j = j;
+        }
+      }
+    }
+    const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+    const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+    const uint32_t pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+    viol += (int)(m1 >> 31);
+#pragma unroll
+    for (int i = 0; i < BPL; ++i) {
+      if ((uint32_t)(lane + 32 * i) == pick) {
+        asg[i] = nasg[i];
+        occ[i] = nocc[i];
+        rem[i] = nrem[i];
+        cnt[i]++;
+      }
+    }
+    if (lane == 0) s_pick[lo + p] = (int)pick;
+  }
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < a.M) {
+      s_bagcnt[rep * a.M + j] = cnt[i];
+      a.bag_count[rep * a.M + j] = cnt[i];
+      a.per_bag_occ[rep * a.M + j] = occ[i];
+      const int g = a.bag_size[j];
+      const double per = __ddiv_rn(asg[i], (double)g);
+      for (int k = 0; k < g; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[j] + k]] = per;
+    }
+  }
+  if (lane == 0) atomicAdd(viol_out, viol);
+}
+
+__global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int64_t sh[33];
+  __shared__ int s_flag, s_viol;
+  __shared__ int warp_cnt[32][kMaxBags];
+  __shared__ int running[kMaxBags];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int W = a.W, R = a.R, M = a.M, U = a.U;
+  const SmallLayout L = small_layout(cap, W, R * M, R);
+  uint64_t* s_ids = reinterpret_cast<uint64_t*>(sm + L.ids);
+  int64_t* s_lens = reinterpret_cast<int64_t*>(sm + L.lens);
+  double* s_w = reinterpret_cast<double*>(sm + L.w);
+  int64_t* s_soff = reinterpret_cast<int64_t*>(sm + L.soff);
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(sm + L.hi);
+  uint64_t* s_lo = reinterpret_cast<uint64_t*>(sm + L.lo);
+  uint32_t* s_v = reinterpret_cast<uint32_t*>(sm + L.v);
+  int32_t* s_rank = reinterpret_cast<int32_t*>(sm + L.rank);
+  int32_t* s_sorted = reinterpret_cast<int32_t*>(sm + L.sorted);
+  int32_t* s_pick = reinterpret_cast<int32_t*>(sm + L.pick);
+  int32_t* s_G = reinterpret_cast<int32_t*>(sm + L.G);
+  int64_t* s_cb = reinterpret_cast<int64_t*>(sm + L.cb);
+  int32_t* s_bo = reinterpret_cast<int32_t*>(sm + L.bo);
+  int64_t* s_roff = reinterpret_cast<int64_t*>(sm + L.rank_off);
+  int64_t* s_rpre = reinterpret_cast<int64_t*>(sm + L.rpre);
+  int32_t* s_bagcnt = reinterpret_cast<int32_t*>(sm + L.bagcnt);
+  int64_t* s_bagcb = reinterpret_cast<int64_t*>(sm + L.bagcb);
+  int32_t* s_bagq = reinterpret_cast<int32_t*>(sm + L.bagq);
+  int64_t* s_sendcnt = reinterpret_cast<int64_t*>(sm + L.sendcnt);
+  int64_t* s_sendoff = reinterpret_cast<int64_t*>(sm + L.sendoff);
+  double* s_reptot = reinterpret_cast<double*>(sm + L.reptot);
+
+  // ---- phase 0: rank offsets, capacity
+  for (int r = tid; r <= W; r += blockDim.x) s_roff[r] = a.rank_off[r];
+  if (tid == 0) {
+    s_flag = 0;
+    s_viol = 0;
+  }
+  __syncthreads();
+  const int64_t N = s_roff[W];
+  if (N > cap) {
+    if (tid == 0) atomicOr(a.status, ST_CAPACITY);
+    return;
+  }
+  // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
+  for (int64_t i = tid; i < N; i += blockDim.x) {
+    int lo = 0, hi = W;  // rank r with roff[r] <= i < roff[r+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_roff[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    int64_t len = a.lens[i];
+    if (len < 0) {
+      atomicOr(a.status, ST_NEG_LENGTH);
+      len = 0;
+    }
+    double wv;
+    if (a.w_in) {
+      wv = a.w_in[i];
+      if (!(wv >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
+    } else {
+      wv = gamma_weighted_workload(len, a.d_model, a.gamma);
+    }
+    s_ids[i] = a.ids[i];
+    s_lens[i] = len;
+    s_w[i] = wv;
+    s_rank[i] = lo;
+    a.w[i] = wv;
+    a.seq_rank[i] = lo;
+  }
+  __syncthreads();
+  // ---- phase 2: origin packing offsets (block scan of lens in gather order)
+  {
+    const int64_t per = (N + blockDim.x - 1) / blockDim.x;
+    const int64_t b0 = tid * per, b1 = b0 + per < N ? b0 + per : N;
+    int64_t loc = 0;
+    for (int64_t i = b0; i < b1; ++i) loc += s_lens[i];
+    int64_t tot;
+    int64_t run = block_excl_scan<int64_t>(loc, sh, &tot);
+    for (int64_t i = b0; i < b1; ++i) {
+      s_soff[i] = run;
+      run += s_lens[i];
+    }
+    __syncthreads();
+    for (int r = tid; r <= W; r += blockDim.x) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : tot;
+    __syncthreads();
+    for (int64_t i = tid; i < N; i += blockDim.x) {
+      s_soff[i] -= s_rpre[s_rank[i]];
+      a.seq_off[i] = s_soff[i];
+    }
+    for (int r = tid; r < W; r += blockDim.x) {
+      a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+      s_sendcnt[r] = 0;
+    }
+    __syncthreads();
+  }
+  // ---- phase 3: duplicate sample ids inside a replica (divergence)
+  if (!a.w_in) {
+    for (int64_t i = tid; i < N; i += blockDim.x) {
+      s_hi[i] = (uint64_t)(s_rank[i] / U);
+      s_lo[i] = s_ids[i];
+      s_v[i] = (uint32_t)i;
+    }
+    __syncthreads();
+    smem_bitonic(s_hi, s_lo, s_v, (int)N, small_pow2((int)N));
+    for (int64_t i = tid + 1; i < N; i += blockDim.x)
+      if (s_hi[i] == s_hi[i - 1] && s_lo[i] == s_lo[i - 1]) s_flag = 1;
+    __syncthreads();
+    if (s_flag) {
+      if (tid == 0) atomicOr(a.status, ST_DUP_ID);
+    }
+  }
+  // ---- phase 4: serial FP64 totals (balancer.cpp:24-25, :147)
+  if (tid == 0) {
+    double s = 0.0;
+    for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_w[i]);
+    *a.total = s;
+    *a.n_seqs = N;
+  } else if (lane == 0 && warp >= 1) {
+    for (int rep = warp - 1; rep < R; rep += nw - 1) {
+      double s = 0.0;
+      for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
+      s_reptot[rep] = s;
+      a.rep_total[rep] = s;
+    }
+  }
+  __syncthreads();
+  // ---- phase 5: per replica sort by (workload desc, id asc) (balancer.cpp:37-40)
+  for (int rep = 0; rep < R; ++rep) {
+    const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      const double wv = s_w[lo + i];
+      s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
+      s_lo[i] = s_ids[lo + i];
+      s_v[i] = (uint32_t)i;
+    }
+    __syncthreads();
+    smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
+      a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
+    }
+    __syncthreads();
+  }
+  // ---- phase 6: greedy, one warp per replica (balancer.cpp:44-62)
+  for (int rep = warp; rep < R; rep += nw) {
+    const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
+    if (M <= 32) small_greedy<1>(a, rep, lo, n, s_w, s_sorted, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
+    else small_greedy<2>(a, rep, lo, n, s_w, s_sorted, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
+  }
+  __syncthreads();
+  // ---- phase 7: chunk bases of every (replica, bag)
+  if (tid == 0) {
+    int64_t cb = 0;
+    int q = 0;
+    for (int rep = 0; rep < R; ++rep) {
+      int64_t rc = 0;
+      for (int b = 0; b < M; ++b) {
+        s_bagcb[rep * M + b] = cb;
+        s_bagq[rep * M + b] = q;
+        const int64_t c = (int64_t)s_bagcnt[rep * M + b] * a.bag_size[b];
+        cb += c;
+        rc += c;
+        q += s_bagcnt[rep * M + b];
+      }
+      a.rep_chunks[rep] = rc;
+    }
+    *a.n_chunks = cb;
+    *a.violations = s_viol;
+  }
+  __syncthreads();
+  // ---- phase 8: stable bag partition + chunk emission (balancer.cpp:178-218)
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int rep = 0; rep < R; ++rep) {
+    const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
+    for (int b = tid; b < M; b += blockDim.x) running[b] = 0;
+    __syncthreads();
+    for (int64_t tile = lo; tile < hi; tile += blockDim.x) {
+      for (int e = tid; e < 32 * M; e += blockDim.x) warp_cnt[e / M][e % M] = 0;
+      __syncthreads();
+      const int64_t p = tile + tid;
+      const bool valid = p < hi;
+      const int b = valid ? s_pick[p] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int rank_in = __popc(peers & lt_mask);
+      if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
+      __syncthreads();
+      if (tid < M) {
+        int run = running[tid];
+        for (int w2 = 0; w2 < 32; ++w2) {
+          const int c = warp_cnt[w2][tid];
+          warp_cnt[w2][tid] = run;
+          run += c;
+        }
+        running[tid] = run;
+      }
+      __syncthreads();
+      if (valid) {
+        const int q = warp_cnt[warp][b] + rank_in;
+        const int s = s_sorted[p];
+        const int64_t l = s_lens[s];
+        const int g = a.bag_size[b];
+        const int64_t cb = s_bagcb[rep * M + b] + (int64_t)q * g;
+        const uint64_t id = s_ids[s];
+        const int src = s_rank[s];
+        for (int k = 0; k < g; ++k) {
+          const int64_t c = cb + k;
+          const int64_t st = chunk_start(l, g, k);
+          a.c_id[c] = id;
+          a.c_idx[c] = k;
+          a.c_start[c] = st;
+          a.c_end[c] = st + chunk_len(l, g, k);
+          a.c_src[c] = src;
+          a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
+          a.c_src_row[c] = s_soff[s] + st;
+        }
+        s_G[s] = g;
+        s_cb[s] = cb;
+        s_bo[s_bagq[rep * M + b] + q] = s;
+        a.seq_G[s] = g;
+        a.seq_chunk_base[s] = cb;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sendcnt[src]), (unsigned long long)g);
+      }
+      __syncthreads();
+    }
+  }
+  // ---- phase 9: manifest offsets (balancer.cpp:84-91)
+  if (tid == 0) {
+    int64_t so = 0, ro = 0;
+    for (int r = 0; r < W; ++r) {
+      s_sendoff[r] = so;
+      a.send_off[r] = so;
+      a.recv_off[r] = ro;
+      so += s_sendcnt[r];
+      ro += s_bagcnt[(r / U) * M + a.rank_bag[r % U]];
+    }
+    s_sendoff[W] = so;
+    a.send_off[W] = so;
+    a.recv_off[W] = ro;
+  }
+  __syncthreads();
+  // ---- phase 10: per rank lists, one warp per rank
+  for (int r = warp; r < W; r += nw) {
+    const int rep = r / U, u = r % U;
+    const int b = a.rank_bag[u], k = a.rank_member[u], g = a.bag_size[b];
+    const int nb = s_bagcnt[rep * M + b];
+    const int bq = s_bagq[rep * M + b];
+    int64_t ro = 0;
+    for (int x = 0; x < r; ++x) ro += s_bagcnt[(x / U) * M + a.rank_bag[x % U]];
+    // recv list + receive-side rows (target packing, balancer.cpp:93-101)
+    int64_t carry = 0, carry2 = 0;
+    for (int q0 = 0; q0 < nb; q0 += 32) {
+      const int q = q0 + lane;
+      const bool valid = q < nb;
+      const int s = valid ? s_bo[bq + q] : 0;
+      const int64_t l = valid ? s_lens[s] : 0;
+      const int64_t len = valid ? chunk_len(l, g, k) : 0;
+      const int64_t inc = warp_scan_incl64(len);
+      const int64_t inc2 = k == 0 ? warp_scan_incl64(l) : 0;
+      if (valid) {
+        const int64_t c = s_cb[s] + k;
+        a.c_dst_row[c] = carry + inc - len;
+        a.recv_idx[ro + q] = (int32_t)c;
+        if (k == 0) a.c_seq_base[s_cb[s]] = carry2 + inc2 - l;
+      }
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+      if (k == 0) carry2 += __shfl_sync(0xffffffffu, inc2, 31);
+    }
+    if (lane == 0) {
+      a.target_rows[r] = carry;
+      if (k == 0) a.bag_rows[rep * M + b] = carry2;
+    }
+    // reverse receive order: r's sequences in buffer order, chunks ascending
+    const int64_t s0 = s_roff[r], s1 = s_roff[r + 1];
+    int64_t c4 = 0;
+    for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool valid = i < s1;
+      const int gs = valid ? s_G[i] : 0;
+      const int64_t inc = warp_scan_incl64(gs);
+      if (valid)
+        for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[s_sendoff[r] + c4 + inc - gs + kk] = (int32_t)(s_cb[i] + kk);
+      c4 += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  __syncthreads();
+  // ---- phase 11: send lists -- r's sequences ordered by first chunk index
+  for (int64_t i = tid; i < N; i += blockDim.x) {
+    s_hi[i] = (uint64_t)s_rank[i];
+    s_lo[i] = (uint64_t)s_cb[i];
+    s_v[i] = (uint32_t)i;
+  }
+  __syncthreads();
+  smem_bitonic(s_hi, s_lo, s_v, (int)N, small_pow2((int)N));
+  for (int r = warp; r < W; r += nw) {
+    const int64_t s0 = s_roff[r], s1 = s_roff[r + 1];  // sorted by rank: same span
+    int64_t c3 = 0;
+    for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool valid = i < s1;
+      const int s = valid ? (int)s_v[i] : 0;
+      const int gs = valid ? s_G[s] : 0;
+      const int64_t inc = warp_scan_incl64(gs);
+      if (valid)
+        for (int kk = 0; kk < gs; ++kk) a.send_idx[s_sendoff[r] + c3 + inc - gs + kk] = (int32_t)(s_cb[s] + kk);
+      c3 += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
+  __syncthreads();
+  if (tid == 0) {
+    double lo = a.per_gpu[0], hi = a.per_gpu[0];
+    for (int r = 0; r < W; ++r) {
+      lo = fmin(lo, a.per_gpu[r]);
+      hi = fmax(hi, a.per_gpu[r]);
+    }
+    *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
+  }
+}
+
+}  // namespace sb

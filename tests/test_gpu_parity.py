@@ -67,6 +67,16 @@ def check_dev_world(world, ref, ranks=None):
             assert nbytes // rows == rr["width"] * 8, f"rank {r} width"
 
 
+def planner_paths_equal(a, b):
+    for k in ("c_id", "c_idx", "c_start", "c_end", "c_src", "c_dst", "send_off", "send_idx", "recv_off", "recv_idx",
+              "rev_recv_idx", "target_rows"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    for k in ("per_gpu_workload", "per_bag_occupancy"):
+        assert np.array_equal(getattr(a, k).view(np.uint64), getattr(b, k).view(np.uint64)), k
+    assert a.capacity_violations == b.capacity_violations
+    assert dbits(a.total_workload) == dbits(b.total_workload) and dbits(a.wir) == dbits(b.wir)
+
+
 def make_planner(case, meta):
     d, h, g = model_for(case)
     md = case["model"]
@@ -94,6 +104,12 @@ def test_device_plan_and_exchange_match_reference(name):
     check_plan(fwd, ref["plan"])
     check_report(report_as_oracle(hp), ref["report"])
     check_plan(reverse_as_oracle(hp, fwd), ref["reverse"], recv_ties_ok=True)
+
+    # the other planner pipeline (fused single-CTA vs multi-kernel) must agree bit for bit
+    other = make_planner(case, meta)
+    n_seqs = sum(len(x) for x in meta.ids)
+    other.set_path("large" if n_seqs <= 2048 else "auto")
+    planner_paths_equal(hp, other.plan(dm).download())
 
     # identity_plan on the same planner slots
     planner.plan_identity(dm)
@@ -159,10 +175,12 @@ def test_capacity_exceeded_is_loud():
         planner.sizes()
 
 
+@pytest.mark.parametrize("path", ["small", "large"])
 @pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2", "g8n1", "g1n2+g2n1+g4n1"])
-def test_random_plans_vs_oracle(topo):
-    rng = np.random.default_rng(hash(topo) % 2**32)
-    planner = sb.Planner(topo, 16 if "+" in topo else 8, max_seqs=4096)
+def test_random_plans_vs_oracle(topo, path):
+    rng = np.random.default_rng(sum(map(ord, topo)))
+    planner = sb.Planner(topo, 16 if "+" in topo else 8, max_seqs=2048)
+    planner.set_path(path)
     W = planner.world_size
     for trial in range(20):
         lens = [rng.integers(0, 5000, size=rng.integers(0, 40)).tolist() for _ in range(W)]
