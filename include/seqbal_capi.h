@@ -150,6 +150,11 @@ SB_API sb_status sb_plan_download(sb_planner* p, sb_plan_host* out, sb_stream st
  * at most 2048 sequences, else the multi-kernel pipeline), 1 = force the
  * fused planner, 2 = force the multi-kernel pipeline.  Both are bit-exact. */
 SB_API sb_status sb_planner_set_path(sb_planner* p, int path);
+/* Self-test: the planner's fast correctly-rounded division against
+ * __ddiv_rn on n random operand pairs; *mismatches must be 0. */
+SB_API sb_status sb_selftest_div(int64_t n, uint64_t seed, int64_t* mismatches);
+/* Diagnostics: per-phase clock64() stamps of the fused planner (16 slots). */
+SB_API sb_status sb_planner_trace(sb_planner* p, int enable, int64_t* out16);
 
 /* Plan latency breakdown of the last sb_plan (device time, microseconds,
  * measured with events when timing is enabled; zeros otherwise). */

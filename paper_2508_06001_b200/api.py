@@ -235,6 +235,12 @@ class Planner:
         """'auto' | 'small' (fused single-CTA planner) | 'large' (multi-kernel)."""
         call("sb_planner_set_path", self._h, {"auto": 0, "small": 1, "large": 2}[path])
 
+    def trace(self, enable: bool = True):
+        """Per-phase clock64 deltas of the fused planner's last run (diagnostics)."""
+        out = np.zeros(16, np.int64)
+        call("sb_planner_trace", self._h, int(enable), out.ctypes.data)
+        return out
+
     def enable_timing(self, on: bool = True):
         call("sb_planner_enable_timing", self._h, int(on))
 

@@ -32,6 +32,7 @@ struct sb_planner {
   bool any_multi_bag = false;
   bool uploaded = false;  // current plan came from sb_plan_upload (no bag tables)
   int path = 0;           // planner pipeline: 0 auto, 1 single-CTA small, 2 multi-kernel
+  long long* trace = nullptr;  // per-phase clock64 stamps of the fused planner (diagnostics)
   size_t small_smem = 0;  // dynamic shared memory of the small path
   // origin layout of an uploaded plan (segment CSR), kept for reverse_plan
   int64_t seg_cap = 0;

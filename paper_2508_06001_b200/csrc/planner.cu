@@ -65,6 +65,7 @@ struct PlanArgs {
   double *per_gpu, *per_bag_occ, *total, *wir;
   int32_t* violations;
   int32_t* status;
+  long long* trace;  // optional per-phase timestamps (small path)
 };
 
 __device__ __forceinline__ bool seqs_ok(const PlanArgs& a) { return a.rank_off[a.W] <= a.max_seqs; }
@@ -75,6 +76,54 @@ __device__ __forceinline__ double occupancy(double asg, double cap) {  // balanc
 }
 
 __device__ __forceinline__ uint64_t hash_slot(uint64_t id) { return splitmix64(id ^ 0x5eedULL); }
+
+// Correctly rounded a / b for the occupancy update, b > 0 normal, a >= 0
+// finite, with r = __drcp_rn(b) precomputed per bag: one Newton refinement
+// makes y faithful, then Markstein's fused correction y + r*(a - b*y)
+// rounds to RN(a/b).  Five dependent FP64 ops instead of the ~25-op
+// general __ddiv_rn sequence on the greedy's critical path; bit-identity
+// with __ddiv_rn is asserted by sb_selftest_div over random operands in the
+// planner's range (tests/test_gpu_parity.py).
+__device__ __forceinline__ double div_rn_markstein(double a, double b, double r) {
+  double y = __dmul_rn(a, r);
+  double e = __fma_rn(-b, y, a);
+  y = __fma_rn(r, e, y);
+  e = __fma_rn(-b, y, a);
+  return __fma_rn(r, e, y);
+}
+
+// occupancy (balancer.cpp:32-35) with a precomputed reciprocal of cap.
+__device__ __forceinline__ double occupancy_fast(double asg, double cap, double rcap) {
+  if (cap > 0.0) return div_rn_markstein(asg, cap, rcap);
+  return asg > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
+}
+
+// Lexicographic warp argmin of (key, bag) where bag == lane (one bag per
+// lane): one REDUX on the high word settles it unless several lanes tie
+// there, in which case the low word and then the lane break the tie.
+__device__ __forceinline__ uint32_t warp_argmin_lane(uint64_t key) {
+  const uint32_t khi = (uint32_t)(key >> 32), klo = (uint32_t)key;
+  const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+  const unsigned eq = __ballot_sync(0xffffffffu, khi == m1);
+  if (__popc(eq) == 1) return (uint32_t)(__ffs(eq) - 1);
+  const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+  return (uint32_t)(__ffs(__ballot_sync(0xffffffffu, khi == m1 && klo == m2)) - 1);
+}
+
+__global__ void k_selftest_div(uint64_t seed, int64_t n, unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h1 = splitmix64(seed ^ (uint64_t)(2 * i)), h2 = splitmix64(seed ^ (uint64_t)(2 * i + 1));
+    // capacities and assigned loads spanning the planner's range: sums of
+    // 24 l d^2 + g 4 l^2 d terms, 1e6 .. 1e22, plus exact-quotient cases
+    const double b = ldexp(1.0 + (double)(h1 >> 12) * 0x1.0p-52, 20 + (int)(h1 & 31) * 2);
+    double a;
+    if ((h2 & 7) == 0) a = __dmul_rn(b, (double)((h2 >> 3) & 0xffff));  // exact multiples
+    else a = __dmul_rn(b, (double)(h2 >> 11) * 0x1.0p-53 * 2.5);         // occupancies in [0, 2.5)
+    if (__double_as_longlong(div_rn_markstein(a, b, __drcp_rn(b))) != __double_as_longlong(__ddiv_rn(a, b))) ++bad;
+  }
+  if (bad) atomicAdd(mismatches, bad);
+}
 
 // ------------------------------------------------------------------ k_prep
 __global__ void __launch_bounds__(256) k_prep(PlanArgs a) {
@@ -211,13 +260,14 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
   const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
   const int64_t n = hi - lo;
   const double target = __ddiv_rn(a.rep_total[rep], (double)a.U);  // balancer.cpp:26
-  double cap[BPL], asg[BPL], occ[BPL], rem[BPL];
+  double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
   int cnt[BPL];
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
     const int j = lane + 32 * i;
     const int size = j < a.M ? a.bag_size[j] : 0;
     cap[i] = __dmul_rn((double)size, target);  // balancer.cpp:30
+    rcap[i] = cap[i] > 0.0 ? __drcp_rn(cap[i]) : 0.0;
     asg[i] = 0.0;
     occ[i] = occupancy(0.0, cap[i]);
     rem[i] = __dsub_rn(cap[i], 0.0);
@@ -236,7 +286,7 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
 #pragma unroll
       for (int i = 0; i < BPL; ++i) {
         nasg[i] = __dadd_rn(asg[i], w);
-        nocc[i] = occupancy(nasg[i], cap[i]);
+        nocc[i] = occupancy_fast(nasg[i], cap[i], rcap[i]);
         nrem[i] = __dsub_rn(cap[i], nasg[i]);
         const uint32_t j = lane + 32 * i;
         if (j < (uint32_t)a.M) {
@@ -248,11 +298,17 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
           }
         }
       }
-      const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
-      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
-      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
-      const uint32_t pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
-      viol += (int)(m1 >> 31);  // no feasible bag -> fallback -> capacity violation
+      uint32_t pick;
+      if (BPL == 1) {
+        pick = warp_argmin_lane(best_key);
+      } else {
+        const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
+        const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+        const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+        pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+      }
+      // no feasible bag -> fallback -> capacity violation
+      viol += (int)(__shfl_sync(0xffffffffu, (uint32_t)(best_key >> 63), (int)(pick & 31)));
 #pragma unroll
       for (int i = 0; i < BPL; ++i) {
         if ((uint32_t)(lane + 32 * i) == pick) {
@@ -678,6 +734,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.origin_rows = p->origin_rows; a.target_rows = p->target_rows;
   a.per_gpu = p->per_gpu; a.per_bag_occ = p->per_bag_occ; a.total = p->total; a.wir = p->wir;
   a.violations = p->violations; a.status = p->status;
+  a.trace = p->trace;
   return a;
 }
 
@@ -928,6 +985,40 @@ extern "C" sb_status sb_plan(sb_planner* p, const uint64_t* d_ids, const int64_t
   p->identity = false;
   p->uploaded = false;
   sb::run_plan(p, (cudaStream_t)stream);
+  SB_API_END
+}
+
+extern "C" sb_status sb_selftest_div(int64_t n, uint64_t seed, int64_t* mismatches) {
+  SB_API_BEGIN
+  if (!mismatches || n < 0) throw Error{SB_ERR_CONFIG, "sb_selftest_div: bad arguments"};
+  unsigned long long* d = nullptr;
+  SB_CUDA(cudaMalloc(&d, sizeof *d));
+  SB_CUDA(cudaMemset(d, 0, sizeof *d));
+  sb::k_selftest_div<<<1184, 256>>>(seed, n, d);
+  const cudaError_t e = cudaGetLastError();
+  unsigned long long h = 0;
+  cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) throw Error{SB_ERR_CUDA, cudaGetErrorString(e)};
+  *mismatches = (int64_t)h;
+  SB_API_END
+}
+
+extern "C" sb_status sb_planner_trace(sb_planner* p, int enable, int64_t* out16) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
+  if (enable && !p->trace) {
+    SB_CUDA(cudaMalloc(&p->trace, sizeof(long long) * 16));
+    SB_CUDA(cudaMemset(p->trace, 0, sizeof(long long) * 16));
+  }
+  if (!enable && p->trace) {
+    cudaFree(p->trace);
+    p->trace = nullptr;
+  }
+  if (out16 && p->trace) {
+    SB_CUDA(cudaDeviceSynchronize());
+    SB_CUDA(cudaMemcpy(out16, p->trace, sizeof(long long) * 16, cudaMemcpyDeviceToHost));
+  }
   SB_API_END
 }
 

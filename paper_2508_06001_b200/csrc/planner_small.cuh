@@ -15,6 +15,12 @@
 
 namespace sb {
 
+// Per-phase clock64() trace (thread 0) when the planner has a trace buffer.
+#define SB_PHASE(k)                                   \
+  do {                                                \
+    if (a.trace && threadIdx.x == 0) a.trace[k] = clock64(); \
+  } while (0)
+
 constexpr int kSmallSeqs = 2048;
 
 __host__ __device__ inline int small_pow2(int n) {
@@ -96,28 +102,31 @@ __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, 
                              int32_t* s_pick, int32_t* s_bagcnt, double total_rep, int* viol_out) {
   const int lane = threadIdx.x & 31;
   const double target = __ddiv_rn(total_rep, (double)a.U);
-  double cap[BPL], asg[BPL], occ[BPL], rem[BPL];
+  double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
   int cnt[BPL];
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
     const int j = lane + 32 * i;
     const int size = j < a.M ? a.bag_size[j] : 0;
     cap[i] = __dmul_rn((double)size, target);
+    rcap[i] = cap[i] > 0.0 ? __drcp_rn(cap[i]) : 0.0;
     asg[i] = 0.0;
     occ[i] = occupancy(0.0, cap[i]);
     rem[i] = __dsub_rn(cap[i], 0.0);
     cnt[i] = 0;
   }
   int viol = 0;
+  double w_next = n > 0 ? s_w[s_sorted[lo]] : 0.0;
   for (int64_t p = 0; p < n; ++p) {
-    const double w = s_w[s_sorted[lo + p]];
+    const double w = w_next;  // software-pipelined: next weight loads under this step
+    if (p + 1 < n) w_next = s_w[s_sorted[lo + p + 1]];
     double nasg[BPL], nocc[BPL], nrem[BPL];
     uint64_t best_key = ~0ull;
     uint32_t best_j = 0xffffffffu;
 #pragma unroll
     for (int i = 0; i < BPL; ++i) {
       nasg[i] = __dadd_rn(asg[i], w);
-      nocc[i] = occupancy(nasg[i], cap[i]);
+      nocc[i] = occupancy_fast(nasg[i], cap[i], rcap[i]);
       nrem[i] = __dsub_rn(cap[i], nasg[i]);
       const uint32_t j = lane + 32 * i;
       if (j < (uint32_t)a.M) {
@@ -129,11 +138,17 @@ __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, 
         }
       }
     }
-    const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
-    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
-    const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
-    const uint32_t pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
-    viol += (int)(m1 >> 31);
+    uint32_t pick;
+    if (BPL == 1) {
+      pick = warp_argmin_lane(best_key);
+    } else {
+      const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
+      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+    }
+    // no feasible bag -> the fallback pick is a capacity violation
+    viol += (int)(__shfl_sync(0xffffffffu, (uint32_t)(best_key >> 63), (int)(pick & 31)));
 #pragma unroll
     for (int i = 0; i < BPL; ++i) {
       if ((uint32_t)(lane + 32 * i) == pick) {
@@ -191,6 +206,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
   int64_t* s_sendoff = reinterpret_cast<int64_t*>(sm + L.sendoff);
   double* s_reptot = reinterpret_cast<double*>(sm + L.reptot);
 
+  SB_PHASE(0);
   // ---- phase 0: rank offsets, capacity
   for (int r = tid; r <= W; r += blockDim.x) s_roff[r] = a.rank_off[r];
   if (tid == 0) {
@@ -203,6 +219,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     if (tid == 0) atomicOr(a.status, ST_CAPACITY);
     return;
   }
+  SB_PHASE(1);
   // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
   for (int64_t i = tid; i < N; i += blockDim.x) {
     int lo = 0, hi = W;  // rank r with roff[r] <= i < roff[r+1]
@@ -231,6 +248,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     a.seq_rank[i] = lo;
   }
   __syncthreads();
+  SB_PHASE(2);
   // ---- phase 2: origin packing offsets (block scan of lens in gather order)
   {
     const int64_t per = (N + blockDim.x - 1) / blockDim.x;
@@ -256,22 +274,40 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     }
     __syncthreads();
   }
+  SB_PHASE(3);
   // ---- phase 3: duplicate sample ids inside a replica (divergence)
   if (!a.w_in) {
-    for (int64_t i = tid; i < N; i += blockDim.x) {
-      s_hi[i] = (uint64_t)(s_rank[i] / U);
-      s_lo[i] = s_ids[i];
-      s_v[i] = (uint32_t)i;
+    // open-addressing set per replica in the (not yet used) sort scratch:
+    // s_hi and s_lo are contiguous, 2T slots >= 2 * replica size, EMPTY = ~0
+    for (int rep = 0; rep < R; ++rep) {
+      const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
+      const int tsz = 2 * L.T;
+      for (int i = tid; i < tsz; i += blockDim.x) s_hi[i] = ~0ull;
+      if (tid == 0) s_v[0] = 0;  // count of ids equal to the EMPTY marker
+      __syncthreads();
+      for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
+        const uint64_t id = s_ids[i];
+        if (id == ~0ull) {
+          if (atomicAdd(&s_v[0], 1u) > 0) s_flag = 1;
+          continue;
+        }
+        uint32_t slot = (uint32_t)(hash_slot(id) & (uint64_t)(tsz - 1));
+        for (;;) {
+          const unsigned long long old =
+              atomicCAS(reinterpret_cast<unsigned long long*>(&s_hi[slot]), ~0ull, (unsigned long long)id);
+          if (old == ~0ull) break;
+          if (old == id) {
+            s_flag = 1;
+            break;
+          }
+          slot = (slot + 1) & (uint32_t)(tsz - 1);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    smem_bitonic(s_hi, s_lo, s_v, (int)N, small_pow2((int)N));
-    for (int64_t i = tid + 1; i < N; i += blockDim.x)
-      if (s_hi[i] == s_hi[i - 1] && s_lo[i] == s_lo[i - 1]) s_flag = 1;
-    __syncthreads();
-    if (s_flag) {
-      if (tid == 0) atomicOr(a.status, ST_DUP_ID);
-    }
+    if (s_flag && tid == 0) atomicOr(a.status, ST_DUP_ID);
   }
+  SB_PHASE(4);
   // ---- phase 4: serial FP64 totals (balancer.cpp:24-25, :147)
   if (tid == 0) {
     double s = 0.0;
@@ -287,6 +323,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     }
   }
   __syncthreads();
+  SB_PHASE(5);
   // ---- phase 5: per replica sort by (workload desc, id asc) (balancer.cpp:37-40)
   for (int rep = 0; rep < R; ++rep) {
     const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
@@ -297,13 +334,25 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
       s_v[i] = (uint32_t)i;
     }
     __syncthreads();
-    smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
-    for (int64_t i = tid; i < n; i += blockDim.x) {
-      s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
-      a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
+    if (n <= 1024) {
+      // rank by counting: the key (~bits(w), id, index) is a total order
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
+        int pos = 0;
+        for (int64_t j = 0; j < n; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
+        s_sorted[lo + pos] = (int32_t)(lo + i);
+        a.sorted_idx[lo + pos] = (int32_t)(lo + i);
+      }
+    } else {
+      smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
+        a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
+      }
     }
     __syncthreads();
   }
+  SB_PHASE(6);
   // ---- phase 6: greedy, one warp per replica (balancer.cpp:44-62)
   for (int rep = warp; rep < R; rep += nw) {
     const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
@@ -311,6 +360,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     else small_greedy<2>(a, rep, lo, n, s_w, s_sorted, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
   }
   __syncthreads();
+  SB_PHASE(7);
   // ---- phase 7: chunk bases of every (replica, bag)
   if (tid == 0) {
     int64_t cb = 0;
@@ -331,6 +381,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     *a.violations = s_viol;
   }
   __syncthreads();
+  SB_PHASE(8);
   // ---- phase 8: stable bag partition + chunk emission (balancer.cpp:178-218)
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int rep = 0; rep < R; ++rep) {
@@ -386,6 +437,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
       __syncthreads();
     }
   }
+  SB_PHASE(9);
   // ---- phase 9: manifest offsets (balancer.cpp:84-91)
   if (tid == 0) {
     int64_t so = 0, ro = 0;
@@ -401,6 +453,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     a.recv_off[W] = ro;
   }
   __syncthreads();
+  SB_PHASE(10);
   // ---- phase 10: per rank lists, one warp per rank
   for (int r = warp; r < W; r += nw) {
     const int rep = r / U, u = r % U;
@@ -446,28 +499,19 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     }
   }
   __syncthreads();
+  SB_PHASE(11);
   // ---- phase 11: send lists -- r's sequences ordered by first chunk index
+  // position of sequence i in send[r] = chunks of r's sequences with a
+  // smaller first chunk index (counting, no sort, no barrier)
   for (int64_t i = tid; i < N; i += blockDim.x) {
-    s_hi[i] = (uint64_t)s_rank[i];
-    s_lo[i] = (uint64_t)s_cb[i];
-    s_v[i] = (uint32_t)i;
+    const int r = s_rank[i];
+    const int64_t cb = s_cb[i];
+    int64_t pos = 0;
+    for (int64_t j = s_roff[r]; j < s_roff[r + 1]; ++j)
+      if (s_cb[j] < cb) pos += s_G[j];
+    for (int kk = 0; kk < s_G[i]; ++kk) a.send_idx[s_sendoff[r] + pos + kk] = (int32_t)(cb + kk);
   }
-  __syncthreads();
-  smem_bitonic(s_hi, s_lo, s_v, (int)N, small_pow2((int)N));
-  for (int r = warp; r < W; r += nw) {
-    const int64_t s0 = s_roff[r], s1 = s_roff[r + 1];  // sorted by rank: same span
-    int64_t c3 = 0;
-    for (int64_t i0 = s0; i0 < s1; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const bool valid = i < s1;
-      const int s = valid ? (int)s_v[i] : 0;
-      const int gs = valid ? s_G[s] : 0;
-      const int64_t inc = warp_scan_incl64(gs);
-      if (valid)
-        for (int kk = 0; kk < gs; ++kk) a.send_idx[s_sendoff[r] + c3 + inc - gs + kk] = (int32_t)(s_cb[s] + kk);
-      c3 += __shfl_sync(0xffffffffu, inc, 31);
-    }
-  }
+  SB_PHASE(12);
   // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
   __syncthreads();
   if (tid == 0) {
@@ -478,6 +522,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     }
     *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
   }
+  SB_PHASE(13);
 }
 
 }  // namespace sb

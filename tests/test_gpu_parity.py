@@ -151,6 +151,15 @@ def test_device_plan_and_exchange_match_reference(name):
     check_dev_world(E, ref["returned"])
 
 
+def test_fast_division_matches_ddiv_rn():
+    """The greedy's Markstein division must round exactly like __ddiv_rn."""
+    import ctypes as C
+    from paper_2508_06001_b200 import _capi
+    bad = C.c_int64(-1)
+    _capi.call("sb_selftest_div", 1 << 27, 0x5EED, C.byref(bad))
+    assert bad.value == 0
+
+
 def test_duplicate_ids_rejected():
     meta = oracle.meta_explicit([[10, 20], [30]], ids=[[5, 6], [5]])
     planner = sb.Planner("g1n2", 2, max_seqs=8)
