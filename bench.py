@@ -208,15 +208,28 @@ def main():
     A.fill_witness(dm)
     stream = torch.cuda.current_stream()
 
+    side = torch.cuda.Stream()
+    uly = max(planner.topology.bag_sizes) > 1
+    P = sb.Planner
+    # (op, src, dst, slot) of the step's exchanges, in order
+    ops = ([(P.ROUTE, A, B, 0), (P.PRE_ATTN, B, Cw, 2), (P.POST_ATTN, Cw, D, 3), (P.REVERSE, D, E, 1)] if uly
+           else [(P.ROUTE, A, B, 0), (P.REVERSE, B, E, 1)])
+    evs = [torch.cuda.Event() for _ in range(len(ops) + 1)]
+
     def step():
+        """plan, then every exchange prepared on a side stream (layout + jobs)
+        while the copies run back to back on the main stream."""
+        main = torch.cuda.current_stream()
         planner.plan(dm)
-        sb.route(planner, A, B)
-        if planner.topology.bag_sizes and max(planner.topology.bag_sizes) > 1:
-            sb.pre_attn(planner, B, Cw)
-            sb.post_attn(planner, Cw, D)
-            sb.reverse_route(planner, D, E)
-        else:
-            sb.reverse_route(planner, B, E)
+        evs[-1].record(main)
+        side.wait_event(evs[-1])
+        with torch.cuda.stream(side):
+            for i, (op, src, dst, slot) in enumerate(ops):
+                planner.prepare(op, src, dst, slot)
+                evs[i].record(side)
+        for i, (op, src, dst, slot) in enumerate(ops):
+            main.wait_event(evs[i])
+            planner.run(slot)
 
     for _ in range(max(3, args.warmup)):
         step()

@@ -222,6 +222,16 @@ SB_API sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_world* d
 SB_API sb_status sb_pre_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream);
 /* Inverse (post_attn, exchange.cpp:333-436).                               */
 SB_API sb_status sb_post_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream);
+/* Split form of the four calls above.  op: 0 route, 1 reverse_route,
+ * 2 pre_attn, 3 post_attn.  prepare writes the destination layout tables
+ * and the copy jobs into `slot` (0..7); run launches the copy.  Preparations
+ * depend only on the plan and on the world tables written by the previous
+ * preparation, so all of a step's preparations may run on a side stream
+ * while earlier copies are still moving data (sb_route & co. use slots
+ * 0..3 and prepare + run back to back). */
+SB_API sb_status sb_exchange_prepare(sb_planner* p, int op, sb_world* src, sb_world* dst, int slot,
+                                     sb_stream stream);
+SB_API sb_status sb_exchange_run(sb_planner* p, int slot, sb_stream stream);
 /* Synchronises and returns the world's device status (layout capacity). */
 SB_API sb_status sb_world_status(sb_world* w, sb_stream stream);
 

@@ -106,6 +106,8 @@ _SIGS = {
     "sb_route": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sb_pre_attn": (C.c_int, [C.c_void_p] * 4),
     "sb_post_attn": (C.c_int, [C.c_void_p] * 4),
+    "sb_exchange_prepare": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "sb_exchange_run": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "sb_world_status": (C.c_int, [C.c_void_p] * 2),
     "sb_world_upload": (C.c_int, [C.c_void_p] * 4),
     "sb_world_download": (C.c_int, [C.c_void_p] * 4),

@@ -231,6 +231,16 @@ class Planner:
         self._meta = meta
         return self
 
+    ROUTE, REVERSE, PRE_ATTN, POST_ATTN = 0, 1, 2, 3
+
+    def prepare(self, op: int, src: "World", dst: "World", slot: int, stream=None):
+        """Prepare an exchange (layout + copy jobs) into a slot; see sb_exchange_prepare."""
+        call("sb_exchange_prepare", self._h, op, src.handle, dst.handle, slot, _stream(stream))
+
+    def run(self, slot: int, stream=None):
+        """Launch the copy of a prepared slot."""
+        call("sb_exchange_run", self._h, slot, _stream(stream))
+
     def set_path(self, path: str):
         """'auto' | 'small' (fused single-CTA planner) | 'large' (multi-kernel)."""
         call("sb_planner_set_path", self._h, {"auto": 0, "small": 1, "large": 2}[path])

@@ -670,16 +670,32 @@ __global__ void k_checksum(WorldArgs w, unsigned long long* acc) {
   if (lane == 0 && sum) atomicAdd(acc, sum);
 }
 
+static void select_slot(sb_planner* p, int slot) {
+  if (slot < 0 || slot >= sb_planner::kSlots) throw Error{SB_ERR_CONFIG, "exchange slot out of range"};
+  p->cur_slot = slot;
+  sb_planner::Slot& sl = p->slots[slot];
+  p->jobs = sl.jobs;
+  p->piece_off = sl.piece_off;
+  p->n_jobs = sl.n_jobs;
+  p->job_cap = sl.cap;
+}
+
 void ensure_jobs(sb_planner* p, int64_t cap) {
-  if (cap <= p->job_cap) return;
-  if (p->jobs) cudaFree(p->jobs);
-  if (p->piece_off) cudaFree(p->piece_off);
-  p->jobs = nullptr;
-  p->piece_off = nullptr;
-  SB_CUDA(cudaMalloc(&p->jobs, sizeof(SbJob) * (size_t)cap));
-  SB_CUDA(cudaMalloc(&p->piece_off, sizeof(int64_t) * (size_t)(cap + 1)));
-  if (!p->n_jobs) SB_CUDA(cudaMalloc(&p->n_jobs, sizeof(int64_t) * 2));
-  p->job_cap = cap;
+  sb_planner::Slot& sl = p->slots[p->cur_slot];
+  if (cap > sl.cap) {
+    if (sl.jobs) cudaFree(sl.jobs);
+    if (sl.piece_off) cudaFree(sl.piece_off);
+    sl.jobs = nullptr;
+    sl.piece_off = nullptr;
+    SB_CUDA(cudaMalloc(&sl.jobs, sizeof(SbJob) * (size_t)cap));
+    SB_CUDA(cudaMalloc(&sl.piece_off, sizeof(int64_t) * (size_t)(cap + 1)));
+    sl.cap = cap;
+  }
+  if (!sl.n_jobs) {
+    SB_CUDA(cudaMalloc(&sl.n_jobs, sizeof(int64_t) * 2));
+    SB_CUDA(cudaMemset(sl.n_jobs, 0, sizeof(int64_t) * 2));
+  }
+  select_slot(p, p->cur_slot);
 }
 
 static JobArgs jargs(sb_planner* p) {
@@ -954,14 +970,17 @@ extern "C" sb_status sb_world_checksum(sb_world* w, uint64_t* d_acc, sb_stream s
   SB_API_END
 }
 
-extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_world* dst, sb_stream stream) {
-  SB_API_BEGIN
-  if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_route: null argument"};
+// ------------------------------------------------------ prepare / run
+// prepare: destination layout + copy jobs + piece scan into `slot`;
+// run: the copy kernel over the slot.  sb_route & co. do both back to back;
+// sb_exchange_prepare/run let a caller prepare on a side stream while an
+// earlier exchange is still copying (the preparations chain only through
+// the world tables, never through the payload).
+static void prepare_route(sb_planner* p, int slot, int reverse, sb_world* src, sb_world* dst, cudaStream_t s) {
   if (src == dst) throw Error{SB_ERR_CONFIG, "sb_route is out-of-place: src and dst must differ"};
   sb::check_compatible(p, src, dst);
-  cudaStream_t s = (cudaStream_t)stream;
+  sb::select_slot(p, slot);
   sb::ensure_jobs(p, p->max_chunks * src->T);
-  p->current_op = reverse ? 1 : 0;
   sb::LayoutPlan lp{};
   lp.rows_src = reverse ? p->origin_rows : p->target_rows;
   const bool fused = p->max_chunks * src->T <= sb::kFusedPrepMaxJobs;
@@ -980,26 +999,28 @@ extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_worl
   }
   bool tma_ok = true;  // every row size a multiple of 16 B: all spans are TMA-legal
   for (int64_t rb : src->row_bytes) tma_ok &= rb % 16 == 0;
-  sb::run_copy(p, s, dst->n_procs > 1, tma_ok, sb::route_engine(), fused);
-  SB_API_END
+  sb_planner::Slot& sl = p->slots[slot];
+  sl.prepared = true;
+  sl.pieces_done = fused;
+  sl.tma_ok = tma_ok;
+  sl.fence_sys = dst->n_procs > 1;
+  sl.engine = sb::route_engine();
+  sl.op = reverse ? 1 : 0;
 }
 
-static void ulysses(sb_planner* p, sb_world* src, sb_world* dst, cudaStream_t s, int post) {
+static void prepare_ulysses(sb_planner* p, int slot, int post, sb_world* src, sb_world* dst, cudaStream_t s) {
   if (p->identity) throw Error{SB_ERR_CONFIG, "Ulysses transforms need a balanced plan (not identity_plan)"};
   if (p->uploaded)
     throw Error{SB_ERR_CONFIG, "Ulysses transforms need a device-built plan (sb_plan); use sb_apply_moves"};
   sb::check_compatible(p, src, dst);
   if (src == dst) throw Error{SB_ERR_CONFIG, "Ulysses transforms are out-of-place: src and dst must differ"};
-  if (p->n_heads % p->max_bag != 0 || src->n_heads % p->max_bag != 0)
-    throw Error{SB_ERR_CONFIG, "pre_attn: bag of " + std::to_string(p->max_bag) +
-                                   " GPUs does not divide n_heads " + std::to_string(src->n_heads)};
   for (int b = 0; b < p->M; ++b)
     if (src->n_heads % p->bag_size[b] != 0)
       throw Error{SB_ERR_CONFIG, "pre_attn: bag of " + std::to_string(p->bag_size[b]) +
                                      " GPUs does not divide n_heads " + std::to_string(src->n_heads)};
   if (dst->max_bag < p->max_bag) throw Error{SB_ERR_CONFIG, "world max_bag smaller than the topology's bags"};
+  sb::select_slot(p, slot);
   sb::ensure_jobs(p, p->max_chunks * p->max_bag * src->T);
-  p->current_op = post ? 3 : 2;
   sb::LayoutPlan lp{};
   lp.rank_bag = p->d_rank_bag;
   lp.rank_member = p->d_rank_member;
@@ -1032,20 +1053,63 @@ static void ulysses(sb_planner* p, sb_world* src, sb_world* dst, cudaStream_t s,
         tma_ok &= slice % 16 == 0 && slice <= sb::kPieceBytes;
       }
   }
-  sb::run_copy(p, s, dst->n_procs > 1, tma_ok, sb::ulysses_engine(), fused);
+  sb_planner::Slot& sl = p->slots[slot];
+  sl.prepared = true;
+  sl.pieces_done = fused;
+  sl.tma_ok = tma_ok;
+  sl.fence_sys = dst->n_procs > 1;
+  sl.engine = sb::ulysses_engine();
+  sl.op = post ? 3 : 2;
+}
+
+static void run_slot(sb_planner* p, int slot, cudaStream_t s) {
+  sb::select_slot(p, slot);
+  sb_planner::Slot& sl = p->slots[slot];
+  if (!sl.prepared) throw Error{SB_ERR_CONFIG, "exchange slot " + std::to_string(slot) + " was not prepared"};
+  p->current_op = sl.op;
+  p->last_run_slot = slot;
+  sb::run_copy(p, s, sl.fence_sys, sl.tma_ok, sl.engine, sl.pieces_done);
+}
+
+extern "C" sb_status sb_exchange_prepare(sb_planner* p, int op, sb_world* src, sb_world* dst, int slot,
+                                         sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_exchange_prepare: null argument"};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (op == 0 || op == 1) prepare_route(p, slot, op, src, dst, s);
+  else if (op == 2 || op == 3) prepare_ulysses(p, slot, op == 3, src, dst, s);
+  else throw Error{SB_ERR_CONFIG, "sb_exchange_prepare: op must be 0..3"};
+  SB_API_END
+}
+
+extern "C" sb_status sb_exchange_run(sb_planner* p, int slot, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "sb_exchange_run: null planner"};
+  run_slot(p, slot, (cudaStream_t)stream);
+  SB_API_END
+}
+
+extern "C" sb_status sb_route(sb_planner* p, int reverse, sb_world* src, sb_world* dst, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_route: null argument"};
+  prepare_route(p, reverse ? 1 : 0, reverse ? 1 : 0, src, dst, (cudaStream_t)stream);
+  run_slot(p, reverse ? 1 : 0, (cudaStream_t)stream);
+  SB_API_END
 }
 
 extern "C" sb_status sb_pre_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream) {
   SB_API_BEGIN
   if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_pre_attn: null argument"};
-  ulysses(p, src, dst, (cudaStream_t)stream, 0);
+  prepare_ulysses(p, 2, 0, src, dst, (cudaStream_t)stream);
+  run_slot(p, 2, (cudaStream_t)stream);
   SB_API_END
 }
 
 extern "C" sb_status sb_post_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_stream stream) {
   SB_API_BEGIN
   if (!p || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_post_attn: null argument"};
-  ulysses(p, src, dst, (cudaStream_t)stream, 1);
+  prepare_ulysses(p, 3, 1, src, dst, (cudaStream_t)stream);
+  run_slot(p, 3, (cudaStream_t)stream);
   SB_API_END
 }
 
@@ -1155,7 +1219,8 @@ extern "C" sb_status sb_last_exchange_bytes(const sb_planner* p, int64_t* bytes_
   SB_API_BEGIN
   if (!p) throw Error{SB_ERR_CONFIG, "null planner"};
   int64_t b = 0;
-  if (p->n_jobs) SB_CUDA(cudaMemcpy(&b, p->n_jobs + 1, sizeof b, cudaMemcpyDeviceToHost));
+  const int64_t* nj = p->slots[p->last_run_slot].n_jobs;
+  if (nj) SB_CUDA(cudaMemcpy(&b, nj + 1, sizeof b, cudaMemcpyDeviceToHost));
   if (bytes_read) *bytes_read = b;
   if (bytes_written) *bytes_written = b;
   SB_API_END

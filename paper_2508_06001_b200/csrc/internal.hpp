@@ -95,7 +95,21 @@ struct sb_planner {
   int32_t* violations = nullptr;
   int32_t* status = nullptr;
 
-  // exchange job scratch (grown on demand)
+  // Exchange slots: a prepared exchange (destination layout written, copy
+  // jobs + piece scan in the slot's buffers) waiting to run.  Preparation can
+  // run on another stream ahead of the copy (sb_exchange_prepare/run).
+  struct Slot {
+    SbJob* jobs = nullptr;
+    int64_t* piece_off = nullptr;
+    int64_t* n_jobs = nullptr;  // [0] jobs, [1] bytes moved (one way)
+    int64_t cap = 0;
+    bool prepared = false, pieces_done = false, tma_ok = false;
+    int fence_sys = 0, engine = 0, op = 0;
+  };
+  static constexpr int kSlots = 8;
+  Slot slots[kSlots];
+  int cur_slot = 0, last_run_slot = 0;
+  // current slot's buffers (aliases of slots[cur_slot])
   SbJob* jobs = nullptr;
   int64_t* piece_off = nullptr;
   int64_t* n_jobs = nullptr;

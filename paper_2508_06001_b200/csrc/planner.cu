@@ -787,7 +787,7 @@ static void planner_free(sb_planner* p) {
                   p->c_dst, p->c_start, p->c_end, p->c_src_row, p->c_dst_row, p->c_seq_base,
                   p->send_off, p->recv_off, p->send_idx, p->recv_idx, p->rev_recv_idx,
                   p->origin_rows, p->target_rows, p->per_gpu, p->per_bag_occ, p->total, p->wir,
-                  p->violations, p->status, p->jobs, p->piece_off, p->n_jobs,
+                  p->violations, p->status,
                   p->stage_ids, p->stage_lens, p->stage_w, p->stage_off,
                   p->seg_off, p->seg_id, p->seg_first, p->seg_len, p->recv_count, p->ck_hi, p->ck_lo,
                   p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv};
@@ -796,6 +796,11 @@ static void planner_free(sb_planner* p) {
   for (int i = 0; i < 6; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (cudaEvent_t e : p->copy_ev) cudaEventDestroy(e);
+  for (auto& sl : p->slots) {
+    if (sl.jobs) cudaFree(sl.jobs);
+    if (sl.piece_off) cudaFree(sl.piece_off);
+    if (sl.n_jobs) cudaFree(sl.n_jobs);
+  }
 }
 
 static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
