@@ -504,6 +504,7 @@ int or_reverse_plan(int world_size, int64_t n_chunks, const uint64_t* c_id, cons
   for (int r = 0; r < world_size; ++r) recv_off[r + 1] += recv_off[r];
   rk_t* buf = (rk_t*)malloc(sizeof(rk_t) * (size_t)(n_chunks > 0 ? n_chunks : 1));
   int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(world_size + 1));
+  int64_t* segc = (int64_t*)calloc((size_t)(n_chunks > 0 ? n_chunks : 1), sizeof(int64_t));
   memcpy(fill, recv_off, sizeof(int64_t) * (size_t)(world_size + 1));
   for (int64_t i = 0; i < n_chunks; ++i) buf[fill[c_src[i]]++].chunk = (int32_t)i;
   for (int r = 0; r < world_size && status == 0; ++r) {
@@ -537,13 +538,16 @@ int or_reverse_plan(int world_size, int64_t n_chunks, const uint64_t* c_id, cons
       }
       buf[k].seg = found;
       buf[k].start = c_start[c];
+      segc[c] = found;
     }
     free(idx);
     if (status) break;
-    qsort(buf + recv_off[r], (size_t)(recv_off[r + 1] - recv_off[r]), sizeof(rk_t), cmp_rk);
+    /* balancer.cpp:278-283: the reference's std::sort, ties included */
     for (int64_t k = recv_off[r]; k < recv_off[r + 1]; ++k) recv_idx[k] = buf[k].chunk;
+    or_std_sort_chunks(recv_idx + recv_off[r], recv_off[r + 1] - recv_off[r], segc, c_start);
   }
   free(buf);
   free(fill);
+  free(segc);
   return status;
 }

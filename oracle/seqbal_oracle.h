@@ -11,14 +11,11 @@
  * tests/golden/make_golden.py) and against the reference tests' known-answer
  * values.
  *
- * Deliberate, documented divergences:
- *   - duplicate sample ids inside one replica are rejected (return 1); the
- *     reference silently mis-plans them (balancer.cpp:183-192 lower_bound).
- *   - reverse_plan orders receive lists by (segment, start, chunk index); the
- *     reference uses std::sort on (segment, start) (balancer.cpp:278-283),
- *     which leaves the relative order of equal keys (zero-length chunks of one
- *     sequence) unspecified.  For lists of <= 16 entries libstdc++ finishes
- *     with insertion sort, i.e. the same order as ours.
+ * Deliberate, documented divergence:
+ * duplicate sample ids inside one replica are rejected (return 1); the
+ * reference silently mis-plans them (balancer.cpp:183-192 lower_bound).
+ * reverse_plan's receive order uses libstdc++'s std::sort exactly like the
+ * reference (oracle/stdsort_ref.cpp), including the order of tied keys.
  */
 #ifndef SEQBAL_ORACLE_H
 #define SEQBAL_ORACLE_H
@@ -121,6 +118,11 @@ int or_reverse_plan(int world_size, int64_t n_chunks, const uint64_t* c_id, cons
                     const int64_t* seg_off, const uint64_t* seg_id, const int64_t* seg_first,
                     const int64_t* seg_len, int64_t* send_off, int32_t* send_idx,
                     int64_t* recv_off, int32_t* recv_idx);
+
+/* std::sort (libstdc++, oracle/stdsort_ref.cpp) of chunk indices by
+ * (seg[c], start[c]) -- the reference's receive-order sort including its
+ * tie order (balancer.cpp:278-283). */
+void or_std_sort_chunks(int32_t* v, int64_t n, const int64_t* seg, const int64_t* start);
 
 /* exchange.cpp:31-66 payload rows: fill rows x width doubles for
  * (ids[i], pos[i]) from payload_value. */

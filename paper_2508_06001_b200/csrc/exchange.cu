@@ -312,43 +312,62 @@ __global__ void __launch_bounds__(1024) k_exchange_prep(JobArgs j, WorldArgs s, 
 }
 
 // ------------------------------------------------------------ copy kernel
+// Cache-policy variants of the 128-bit streaming load/store (HINT):
+//  0: ld.global.nc.L1::no_allocate.L2::256B / st.global.L1::no_allocate
+//  1: ld.global.nc.L1::no_allocate          / st.global.L1::no_allocate
+//  2: ld.global.cs (evict-first)            / st.global.cs
+template <int HINT>
 __device__ __forceinline__ int4 ld_stream(const void* p) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if (HINT == 0)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  else if (HINT == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  else
+    asm volatile("ld.global.cs.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+template <int HINT>
 __device__ __forceinline__ void st_stream(void* p, const int4& v) {
-  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
+  if (HINT == 2)
+    asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  else
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
 }
 
 constexpr int kUnroll = 8;
 
 // Warp copies `len` contiguous bytes (16-B aligned) with kUnroll 128-bit
 // loads in flight per lane before the matching stores.
+template <int HINT>
 __device__ __forceinline__ void warp_copy_flat(const char* src, char* dst, int64_t len, int lane) {
   const int64_t step = 32 * 16 * kUnroll;
   int64_t off = (int64_t)lane * 16;
   for (; off + (kUnroll - 1) * 512 < len; off += step) {
     int4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(src + off + u * 512);
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream<HINT>(src + off + u * 512);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_stream(dst + off + u * 512, v[u]);
+    for (int u = 0; u < kUnroll; ++u) st_stream<HINT>(dst + off + u * 512, v[u]);
   }
   int4 v[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u)
-    if (off + u * 512 < len) v[u] = ld_stream(src + off + u * 512);
+    if (off + u * 512 < len) v[u] = ld_stream<HINT>(src + off + u * 512);
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u)
-    if (off + u * 512 < len) st_stream(dst + off + u * 512, v[u]);
+    if (off + u * 512 < len) st_stream<HINT>(dst + off + u * 512, v[u]);
 }
 
 // Warp copies rows [r0, r1) of a strided job: flat index over (row, vec).
+template <int HINT>
 __device__ __forceinline__ void warp_copy_rows(const SbJob& j, int64_t r0, int64_t r1, int lane) {
   const int vpr = (int)(j.width >> 4);
   const int total = (int)(r1 - r0) * vpr;
@@ -366,12 +385,12 @@ __device__ __forceinline__ void warp_copy_rows(const SbJob& j, int64_t r0, int64
       else if ((row + 1) * vpr <= f) ++row;
       rr[u] = row;
       cc[u] = f - row * vpr;
-      if (f < total) v[u] = ld_stream(src + rr[u] * j.spitch + cc[u] * 16);
+      if (f < total) v[u] = ld_stream<HINT>(src + rr[u] * j.spitch + cc[u] * 16);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int f = base + u * 32 + lane;
-      if (f < total) st_stream(dst + rr[u] * j.dpitch + cc[u] * 16, v[u]);
+      if (f < total) st_stream<HINT>(dst + rr[u] * j.dpitch + cc[u] * 16, v[u]);
     }
   }
 }
@@ -385,7 +404,7 @@ __device__ void warp_copy_bytes(const SbJob& j, int64_t r0, int64_t r1, int lane
   }
 }
 
-template <int MINB>
+template <int MINB, int HINT = 0>
 __global__ void __launch_bounds__(kCopyThreads, MINB) k_copy(const SbJob* __restrict__ jobs,
                                                        const int64_t* __restrict__ piece_off,
                                                        const int64_t* __restrict__ n_jobs_p, int fence_sys) {
@@ -414,7 +433,7 @@ __global__ void __launch_bounds__(kCopyThreads, MINB) k_copy(const SbJob* __rest
       const int64_t b = k * kPieceBytes;
       const int64_t e = b + kPieceBytes < len ? b + kPieceBytes : len;
       if (aligned) {
-        warp_copy_flat(reinterpret_cast<const char*>(j.src) + b, reinterpret_cast<char*>(j.dst) + b, e - b, lane);
+        warp_copy_flat<HINT>(reinterpret_cast<const char*>(j.src) + b, reinterpret_cast<char*>(j.dst) + b, e - b, lane);
       } else {
         const char* s = reinterpret_cast<const char*>(j.src);
         char* d = reinterpret_cast<char*>(j.dst);
@@ -423,7 +442,7 @@ __global__ void __launch_bounds__(kCopyThreads, MINB) k_copy(const SbJob* __rest
     } else {
       const int64_t rp = job_rows_per_piece(j);
       const int64_t r0 = k * rp, r1 = r0 + rp < j.n_rows ? r0 + rp : j.n_rows;
-      if (aligned) warp_copy_rows(j, r0, r1, lane);
+      if (aligned) warp_copy_rows<HINT>(j, r0, r1, lane);
       else warp_copy_bytes(j, r0, r1, lane);
     }
   }
@@ -582,7 +601,12 @@ static int copy_grid() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  return g_num_sms * 8;  // 8 CTAs x 8 warps per SM: ~64 KB+ of loads in flight per SM
+  static int per_sm = -1;  // CTAs per SM of the LSU copy grid (SEQBAL_COPY_CTAS_PER_SM)
+  if (per_sm < 0) {
+    const char* v = getenv("SEQBAL_COPY_CTAS_PER_SM");
+    per_sm = v ? std::max(1, atoi(v)) : 8;
+  }
+  return g_num_sms * per_sm;
 }
 
 // ----------------------------------------------------- witness / checksum
@@ -778,7 +802,14 @@ static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys, bool tma_ok, 
   } else if (engine == 2) {
     k_copy<3><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
   } else {
-    k_copy<1><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+    static int hint = -1;  // SEQBAL_COPY_HINT=0|1|2 (see ld_stream)
+    if (hint < 0) {
+      const char* v = getenv("SEQBAL_COPY_HINT");
+      hint = v ? atoi(v) : 0;
+    }
+    if (hint == 1) k_copy<1, 1><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+    else if (hint == 2) k_copy<1, 2><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+    else k_copy<1, 0><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
   }
   SB_CHECK_LAUNCH();
   if (e1) SB_CUDA(cudaEventRecord(e1, s));

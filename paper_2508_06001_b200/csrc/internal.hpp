@@ -88,6 +88,7 @@ struct sb_planner {
   int32_t *c_idx = nullptr, *c_src = nullptr, *c_dst = nullptr;
   int64_t *c_start = nullptr, *c_end = nullptr, *c_src_row = nullptr, *c_dst_row = nullptr;
   int64_t* c_seq_base = nullptr;  // per chunk (q,0): row base of the sequence in its bag's full layout
+  int32_t* c_seq = nullptr;       // per chunk: gather index of its sequence (reverse-order ties)
   int64_t *send_off = nullptr, *recv_off = nullptr;
   int32_t *send_idx = nullptr, *recv_idx = nullptr, *rev_recv_idx = nullptr;
   int64_t *origin_rows = nullptr, *target_rows = nullptr;

@@ -24,6 +24,7 @@
 #include "block_sort.cuh"
 #include "common.cuh"
 #include "internal.hpp"
+#include "stdsort.cuh"
 
 namespace sb {
 
@@ -59,6 +60,7 @@ struct PlanArgs {
   uint64_t* c_id;
   int32_t *c_idx, *c_src, *c_dst;
   int64_t *c_start, *c_end, *c_src_row, *c_dst_row, *c_seq_base;
+  int32_t* c_seq;
   int64_t *send_off, *recv_off;
   int32_t *send_idx, *recv_idx, *rev_recv_idx;
   int64_t *origin_rows, *target_rows;
@@ -410,6 +412,7 @@ __global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
         a.c_src[c] = src;
         a.c_dst[c] = rep * a.U + a.bag_ranks[a.bag_off[b] + k];
         a.c_src_row[c] = soff + st;
+        a.c_seq[c] = s;
       }
       a.seq_bag[s] = b;
       a.seq_G[s] = g;
@@ -418,6 +421,28 @@ __global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
     }
     __syncthreads();
   }
+}
+
+// reverse_plan's receive order for rank r (balancer.cpp:259-285) when its
+// (segment, start) keys can tie -- a sequence shorter than its bag leaves
+// several empty chunks at the same start.  Our O(C) order breaks ties by
+// chunk index; the reference's std::sort breaks them however introsort
+// happens to, so replay libstdc++'s algorithm on its input (the incoming
+// chunks in index order == send[r]) with its comparator.  Single thread;
+// lists of <= 16 entries are already identical (insertion sort is stable).
+__device__ void fix_rev_ties(const PlanArgs& a, int r, int64_t off, int64_t n) {
+  if (n <= stdsort::kThreshold) return;
+  bool tie = false;
+  for (int64_t s = a.rank_off[r]; s < a.rank_off[r + 1] && !tie; ++s)
+    tie = a.seq_G[s] > 1 && a.lens[s] < a.seq_G[s];
+  if (!tie) return;
+  for (int64_t i = 0; i < n; ++i) a.rev_recv_idx[off + i] = a.send_idx[off + i];
+  const int32_t* seq = a.c_seq;
+  const int64_t* st = a.c_start;
+  stdsort::sort(a.rev_recv_idx + off, n, [&](int32_t x, int32_t y) {
+    if (seq[x] != seq[y]) return seq[x] < seq[y];
+    return st[x] < st[y];
+  });
 }
 
 // ----------------------------------------------------------------- k_lists
@@ -531,6 +556,8 @@ __global__ void __launch_bounds__(1024) k_lists(PlanArgs a) {
     }
     c4 += tot;
   }
+  __syncthreads();  // send[r] complete: std::sort's input order
+  if (tid == 0) fix_rev_ties(a, r, s_send_off, c4);
 }
 
 // -------------------------------------------------------------- k_finalize
@@ -639,14 +666,21 @@ __global__ void __launch_bounds__(1024) k_generic_lists(GenericArgs a) {
       }
     }
     if (seg < 0) atomicOr(a.status, 32);
-    a.ck_hi[s_so + i] = (uint64_t)(seg < 0 ? 0 : seg);
-    a.ck_lo[s_so + i] = (uint64_t)a.c_start[c];
-    a.ck_v[s_so + i] = (uint32_t)c;
+    a.ck_hi[c] = (uint64_t)(seg < 0 ? 0 : seg);  // per chunk id: the comparator's segment
+    a.rev_recv_idx[s_so + i] = c;                // std::sort's input: incoming in chunk order
   }
   __syncthreads();
-  block_sort(cs, a.ck_hi + s_so, a.ck_lo + s_so, a.ck_v + s_so, a.ck_thi + s_so, a.ck_tlo + s_so, a.ck_tv + s_so,
-             smem);
-  for (int64_t i = tid; i < cs; i += blockDim.x) a.rev_recv_idx[s_so + i] = (int32_t)a.ck_v[s_so + i];
+  // balancer.cpp:278-283: the reference's std::sort on (segment, start),
+  // replayed exactly (stdsort.cuh) so tied keys land where libstdc++ puts them
+  if (tid == 0) {
+    const uint64_t* seg = a.ck_hi;
+    const int64_t* st = a.c_start;
+    stdsort::sort(a.rev_recv_idx + s_so, cs, [&](int32_t x, int32_t y) {
+      if (seg[x] != seg[y]) return seg[x] < seg[y];
+      return st[x] < st[y];
+    });
+  }
+  (void)smem;
 }
 
 // -------------------------------------------------------- identity kernels
@@ -664,6 +698,7 @@ __global__ void k_identity(PlanArgs a) {
     a.c_src[i] = r;
     a.c_dst[i] = r;
     a.c_src_row[i] = a.seq_off[i];
+    a.c_seq[i] = (int32_t)i;
     a.c_dst_row[i] = a.seq_off[i];
     a.send_idx[i] = (int32_t)i;
     a.recv_idx[i] = (int32_t)i;
@@ -729,6 +764,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.c_id = p->c_id; a.c_idx = p->c_idx; a.c_src = p->c_src; a.c_dst = p->c_dst;
   a.c_start = p->c_start; a.c_end = p->c_end; a.c_src_row = p->c_src_row; a.c_dst_row = p->c_dst_row;
   a.c_seq_base = p->c_seq_base;
+  a.c_seq = p->c_seq;
   a.send_off = p->send_off; a.recv_off = p->recv_off; a.send_idx = p->send_idx;
   a.recv_idx = p->recv_idx; a.rev_recv_idx = p->rev_recv_idx;
   a.origin_rows = p->origin_rows; a.target_rows = p->target_rows;
@@ -754,6 +790,7 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->c_id, C); dalloc(&p->c_idx, C); dalloc(&p->c_src, C); dalloc(&p->c_dst, C);
   dalloc(&p->c_start, C); dalloc(&p->c_end, C); dalloc(&p->c_src_row, C); dalloc(&p->c_dst_row, C);
   dalloc(&p->c_seq_base, C);
+  dalloc(&p->c_seq, C);
   dalloc(&p->send_off, W + 1); dalloc(&p->recv_off, W + 1);
   dalloc(&p->send_idx, C); dalloc(&p->recv_idx, C); dalloc(&p->rev_recv_idx, C);
   dalloc(&p->origin_rows, W); dalloc(&p->target_rows, W);
@@ -784,7 +821,7 @@ static void planner_free(sb_planner* p) {
                   p->sk_v, p->tk_v, p->sorted_w, p->sorted_idx, p->pick, p->seq_bag, p->seq_G,
                   p->seq_chunk_base, p->rep_total, p->sentinel, p->bag_count, p->bag_rows,
                   p->rep_chunks, p->send_count, p->n_chunks, p->n_seqs, p->c_id, p->c_idx, p->c_src,
-                  p->c_dst, p->c_start, p->c_end, p->c_src_row, p->c_dst_row, p->c_seq_base,
+                  p->c_dst, p->c_start, p->c_end, p->c_src_row, p->c_dst_row, p->c_seq_base, p->c_seq,
                   p->send_off, p->recv_off, p->send_idx, p->recv_idx, p->rev_recv_idx,
                   p->origin_rows, p->target_rows, p->per_gpu, p->per_bag_occ, p->total, p->wir,
                   p->violations, p->status,

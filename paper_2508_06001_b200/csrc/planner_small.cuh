@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
           a.c_src[c] = src;
           a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
           a.c_src_row[c] = s_soff[s] + st;
+          a.c_seq[c] = s;
         }
         s_G[s] = g;
         s_cb[s] = cb;
@@ -511,6 +512,9 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
       if (s_cb[j] < cb) pos += s_G[j];
     for (int kk = 0; kk < s_G[i]; ++kk) a.send_idx[s_sendoff[r] + pos + kk] = (int32_t)(cb + kk);
   }
+  __syncthreads();  // send lists complete: reverse-order tie replay reads them
+  for (int r = warp; r < W; r += nw)
+    if (lane == 0) fix_rev_ties(a, r, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r]);
   SB_PHASE(12);
   // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
   __syncthreads();

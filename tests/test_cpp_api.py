@@ -25,6 +25,7 @@ def build_test_binary():
     subprocess.run([gcc, "-std=c11", "-O2", "-ffp-contract=off", "-c", os.path.join(ROOT, "oracle", "seqbal_oracle.c"),
                     "-o", obj], check=True)
     cmd[cmd.index(os.path.join(ROOT, "oracle", "seqbal_oracle.c"))] = obj
+    cmd.insert(cmd.index(obj) + 1, os.path.join(ROOT, "oracle", "stdsort_ref.cpp"))
     subprocess.run(cmd, check=True)
     return BIN
 

@@ -103,7 +103,7 @@ def test_device_plan_and_exchange_match_reference(name):
     fwd = host_plan_as_oracle(hp, meta)
     check_plan(fwd, ref["plan"])
     check_report(report_as_oracle(hp), ref["report"])
-    check_plan(reverse_as_oracle(hp, fwd), ref["reverse"], recv_ties_ok=True)
+    check_plan(reverse_as_oracle(hp, fwd), ref["reverse"])  # libstdc++ tie order replayed
 
     # the other planner pipeline (fused single-CTA vs multi-kernel) must agree bit for bit
     other = make_planner(case, meta)
@@ -149,6 +149,24 @@ def test_device_plan_and_exchange_match_reference(name):
     sb.reverse_route(planner, B, E)
     E.status()
     check_dev_world(E, ref["returned"])
+
+
+@pytest.mark.parametrize("path", ["small", "large"])
+@pytest.mark.parametrize("topo", ["g8n1", "g4n2", "g2n1+g1n2+g4n1"])
+def test_reverse_ties_match_std_sort(topo, path):
+    """Sequences shorter than their bag make reverse_plan's sort keys tie; the
+    device must reproduce libstdc++ std::sort's tie order (the oracle calls
+    the real std::sort)."""
+    rng = np.random.default_rng(7 + len(topo))
+    planner = sb.Planner(topo, 8, max_seqs=2048)
+    planner.set_path(path)
+    for trial in range(10):
+        lens = [rng.integers(0, 12, size=rng.integers(3, 40)).tolist() for _ in range(8)]
+        meta = oracle.meta_explicit(lens)
+        planner.plan(device_meta(meta))
+        hp = planner.download()
+        plan, _ = oracle.plan_routing(meta, oracle.parse_topology(topo))
+        assert hp.rev_recv == oracle.reverse_plan(plan).recv, f"trial {trial}"
 
 
 def test_fast_division_matches_ddiv_rn():
