@@ -44,6 +44,7 @@ CONFIGS = {
                world=8, topology="g1n8", meta=dict(kind="c1", seed=1, step=0, per_rank=32)),
     "c3": dict(workload="C3: image-video joint stream (<=64K-token videos), bags of 4 (g4n2), 24x128 heads",
                world=8, topology="g4n2", meta=dict(kind="scenario", codes=C3_CODES, step=0, seed=7)),
+    "c4": dict(workload="C4: plan scaling sweep", world=8, topology="g1n8", meta=dict(kind="c1")),
 }
 
 
@@ -154,6 +155,112 @@ def run_reference(cfg, topology, steps, warmup, budget_s, threads=None):
     return {"unavailable": err}
 
 
+# ----------------------------------------------- C4: plan scaling sweep
+C4_SIZES = [256, 512, 1024, 2048, 4096, 8192, 16384]
+C4_TOPOS = ["g1n8", "g2n4", "g4n2", "g8n1"]
+
+
+def c4_ref_cases(sizes, topos):
+    return [{"topology": t, "meta": {"kind": "c1", "seed": 1, "step": 0, "per_rank": n // 8},
+             "reverse": n <= 4096} for n in sizes for t in topos]
+
+
+def run_reference_plans(sizes, topos, budget_s=2.0):
+    """plan_routing (best of 5) and reverse_plan latency of the unmodified reference."""
+    harness = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+    if not os.path.exists(harness):
+        return None, "oracle/_ref/ref_harness not built"
+    req = {"world": 8, "reps": 5, "budget_s": budget_s, "cases": c4_ref_cases(sizes, topos)}
+    p = subprocess.run([harness, "plan_bench"], input=json.dumps(req).encode(), capture_output=True, timeout=1800)
+    if p.returncode != 0:
+        return None, p.stderr.decode()[-300:]
+    return json.loads(p.stdout), None
+
+
+def run_c4(args):
+    """C4 (BASELINE configs[3]): device plan latency from 256 to 16K sequences
+    over 8 ranks (C1 length law), topologies g1n8/g2n4/g4n2/g8n1.  One
+    "step" = one plan_routing (+ reverse receive order) on the device;
+    latency by CUDA events over CUDA-graph replays of the plan."""
+    import numpy as np
+    import torch
+
+    import paper_2508_06001_b200 as sb
+    from paper_2508_06001_b200 import datagen
+
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if rank != 0:
+        return 0
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rows = []
+    launches = 0
+    with ClockSampler() as clk:
+        for n in C4_SIZES:
+            ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
+            dm = sb.DeviceMeta.from_lists(ids, lens)
+            for topo in C4_TOPOS:
+                planner = sb.Planner(topo, 8, max_seqs=n)
+                for _ in range(max(3, args.warmup)):
+                    planner.plan(dm)
+                torch.cuda.synchronize()
+                k = max(5, min(args.steps, 100))
+                l0 = sb.kernel_launches()
+                t0.record(stream)
+                for _ in range(k):
+                    planner.plan(dm)
+                t1.record(stream)
+                torch.cuda.synchronize()
+                launches += sb.kernel_launches() - l0
+                eager_us = 1000 * t0.elapsed_time(t1) / k
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    planner.plan(dm)
+                g.replay()
+                torch.cuda.synchronize()
+                t0.record(stream)
+                for _ in range(k):
+                    g.replay()
+                t1.record(stream)
+                torch.cuda.synchronize()
+                graph_us = 1000 * t0.elapsed_time(t1) / k
+                hp = planner.download()
+                per = hp.per_gpu_workload
+                rows.append({"sequences": n, "topology": topo, "chunks": hp.n_chunks, "plan_us": graph_us,
+                             "plan_us_eager": eager_us, "wir": hp.wir,
+                             "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0})
+                del g, planner
+    ref, ref_err = (None, "skipped") if args.no_cpu_baseline else run_reference_plans(C4_SIZES, C4_TOPOS)
+    if ref:
+        by = {(r["sequences"], r["topology"]): r for r in ref}
+        for r in rows:
+            x = by.get((r["sequences"], r["topology"]))
+            if x:
+                r["ref_plan_us"] = 1e6 * x["plan_s"]
+                if "reverse_plan_s" in x:
+                    r["ref_reverse_plan_us"] = 1e6 * x["reverse_plan_s"]
+                r["speedup_vs_ref"] = r["ref_plan_us"] / r["plan_us"]
+    head = next(r for r in rows if r["sequences"] == C4_SIZES[-1] and r["topology"] == "g1n8")
+    line = {"metric": "plan latency (plan_routing + reverse receive order) at 16K sequences, 8 ranks, g1n8",
+            "value": head["plan_us"], "unit": "us", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": head["plan_us"] / 1000, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4: solver/plan scaling sweep, 256..16K sequences over 8 ranks "
+                                   "(C1 length law, seed 1), topologies " + "/".join(C4_TOPOS),
+                       "l2": "metadata-sized inputs (latency-bound; L2 not flushed)"},
+            "sweep": rows, "gpu_launches": int(launches), "clocks": clk.summary()}
+    if ref:
+        hr = next(r for r in ref if r["sequences"] == C4_SIZES[-1] and r["topology"] == "g1n8")
+        line["cpu_baseline"] = {"value": 1e6 * hr["plan_s"], "unit": "us", "cores": 1, "kind": "reference",
+                                "sample": "reference plan_routing (serial) best of <=5 per sweep point; "
+                                          "reverse_plan timed once up to 4K sequences"}
+    else:
+        line["cpu_baseline"] = {"value": None, "unit": "us", "unavailable": ref_err}
+    print(json.dumps(line))
+    return 0
+
+
 # ------------------------------------------------------------ our arm
 def main():
     args = parse_args()
@@ -164,6 +271,23 @@ def main():
 
     if args.impl == "reference":
         if rank != 0:
+            return 0
+        if args.config == "c4":
+            ref, err = run_reference_plans(C4_SIZES, C4_TOPOS)
+            if ref is None:
+                print(json.dumps({"impl": "reference", "unavailable": err}))
+                return 0
+            hr = next(r for r in ref if r["sequences"] == C4_SIZES[-1] and r["topology"] == "g1n8")
+            v = 1e6 * hr["plan_s"]
+            print(json.dumps({
+                "impl": "reference", "metric": "plan latency (plan_routing + reverse receive order) at 16K "
+                "sequences, 8 ranks, g1n8", "value": v, "unit": "us", "n_gpus": args.gpus, "steps": 1,
+                "warmup": 0, "ms_per_step": v / 1000, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C4: solver/plan scaling sweep"}, "sweep": ref,
+                "cpu_baseline": {"value": v, "unit": "us", "cores": 1, "kind": "reference",
+                                 "sample": "plan_routing best of <=5 per point"},
+                "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
             return 0
         r = run_reference(cfg, topology, args.steps, args.warmup, budget_s=120.0)
         if "unavailable" in r:
@@ -190,6 +314,8 @@ def main():
     import paper_2508_06001_b200 as sb
     from paper_2508_06001_b200 import datagen
 
+    if args.config == "c4":
+        return run_c4(args)
     if world_procs > 1:
         from paper_2508_06001_b200 import multigpu
         return multigpu.bench_main(args, cfg, topology, METRIC)

@@ -22,6 +22,7 @@
 //                       reverse_route / pre_attn / post_attn
 //   data_sim.hpp:95-101 next_batch / make_sample_id
 //   rng.hpp:12-55       derive_key / CounterRng
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -388,16 +389,67 @@ int cmd_bench() {
   return 0;
 }
 
+// C4 plan-latency sweep: for each case, plan_routing timed best-of-`reps`
+// (bounded by budget_s per case) and reverse_plan timed once (it is
+// O(W*C*S) in the reference, balancer.cpp:262-283).  Input:
+//   {"world": W, "model": {...}, "reps": k, "budget_s": s,
+//    "cases": [{"topology": "...", "meta": {...}, "reverse": true}, ...]}
+int cmd_plan_bench() {
+  std::stringstream ss;
+  ss << std::cin.rdbuf();
+  const json c = json::parse(ss.str());
+  const int world = c.at("world");
+  const WorkloadModel model = model_from(c.value("model", json::object()));
+  const int reps = c.value("reps", 5);
+  const double budget_s = c.value("budget_s", 5.0);
+  json out = json::array();
+  for (const auto& cs : c.at("cases")) {
+    const WorldLayout layout = replicate(parse_topology(cs.at("topology").get<std::string>()), world);
+    const auto info = gather_sequence_info(samples_from(cs.at("meta"), world));
+    std::size_t n = 0;
+    for (const auto& r : info) n += r.size();
+    double best = 1e30;
+    int done = 0;
+    PlanResult pr;
+    const double t_begin = now_s();
+    for (int it = 0; it < reps; ++it) {
+      if (it > 0 && now_s() - t_begin > budget_s) break;
+      const double a = now_s();
+      pr = plan_routing(info, model, layout);
+      const double b = now_s();
+      best = std::min(best, b - a);
+      ++done;
+    }
+    json r;
+    r["topology"] = cs.at("topology");
+    r["sequences"] = n;
+    r["chunks"] = pr.plan.chunks.size();
+    r["plan_s"] = best;
+    r["plan_reps"] = done;
+    r["wir"] = pr.report.wir;
+    if (cs.value("reverse", true)) {
+      const double a = now_s();
+      const RoutingPlan rp = reverse_plan(pr.plan);
+      r["reverse_plan_s"] = now_s() - a;
+      if (rp.chunks.size() != pr.plan.chunks.size()) return 2;
+    }
+    out.push_back(r);
+  }
+  std::cout << out.dump() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: ref_harness dump|bench < json\n");
+    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench < json\n");
     return 1;
   }
   try {
     if (std::strcmp(argv[1], "dump") == 0) return cmd_dump();
     if (std::strcmp(argv[1], "bench") == 0) return cmd_bench();
+    if (std::strcmp(argv[1], "plan_bench") == 0) return cmd_plan_bench();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_harness: %s\n", e.what());
     return 3;
