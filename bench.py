@@ -396,15 +396,13 @@ def main():
     op_bytes = {}
     for name, fn in (("route", lambda: sb.route(planner, A, B)), ("pre_attn", lambda: sb.pre_attn(planner, B, Cw)),
                      ("post_attn", lambda: sb.post_attn(planner, Cw, D)),
-                     ("reverse_route", lambda: sb.reverse_route(planner, D, E))):
-        if name in ("pre_attn", "post_attn") and max(planner.topology.bag_sizes) == 1:
+                     ("reverse_route", lambda: sb.reverse_route(planner, D if uly else B, E))):
+        if name in ("pre_attn", "post_attn") and not uly:
             continue
         fn()
         torch.cuda.synchronize()
         op_bytes[name] = planner.exchange_bytes()
-    if max(planner.topology.bag_sizes) == 1:
-        sb.reverse_route(planner, B, E)
-    torch.cuda.synchronize()
+    E.status()
 
     # ---- the same step captured once into a CUDA graph and replayed: the
     # launch stream of ~30 small kernels collapses into one graph launch

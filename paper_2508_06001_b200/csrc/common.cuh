@@ -40,6 +40,7 @@ enum : int32_t {
   ST_CAPACITY = 4,      // capacity exceeded
   ST_BAG_CAP = 8,       // bag count above the compiled limit
   ST_LAYOUT = 16,       // world arena too small for the requested layout
+  ST_MISMATCH = 32,     // IntegrityError: source world layout differs from the plan (exchange.cpp:96-123)
 };
 
 // ---------------------------------------------------------- device helpers

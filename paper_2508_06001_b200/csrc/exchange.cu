@@ -70,6 +70,7 @@ static TensorInfo tinfo(sb_world* w) {
 // again (post_attn), others alias `src`.
 struct LayoutPlan {
   const int64_t* rows_src;  // mode 0: rows per rank
+  const int64_t* expect_rows;  // mode 0: rows the SOURCE must hold per rank (origin / target layout)
   const int32_t* rank_bag;  // U
   const int32_t* rank_member;
   const int32_t* bag_size;
@@ -78,9 +79,35 @@ struct LayoutPlan {
   int U, M;
 };
 
+// check_world_matches_layout (exchange.cpp:96-123) / check_bag_chunk_layout
+// (:210-251) restated on row counts: every local source rank must hold the
+// rows the plan expects for this exchange -- origin (route), target
+// (reverse_route, pre_attn) or the Ulysses full-sequence rows (post_attn on
+// multi-GPU bags).  A mismatch raises ST_MISMATCH on the destination and the
+// job builders then emit empty jobs, so a stale or foreign world is reported
+// as IntegrityError by sb_world_status instead of being read out of bounds.
+__device__ bool source_matches_plan(const WorldArgs& s, const LayoutPlan& lp, int mode) {
+  for (int r = s.first_local; r < s.first_local + s.n_local; ++r) {
+    int64_t want;
+    if (mode == 0) {
+      want = lp.expect_rows[r];
+    } else {
+      const int u = r % lp.U, rep = r / lp.U;
+      const int b = lp.rank_bag[u];
+      want = (mode == 2 && lp.bag_size[b] > 1) ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
+    }
+    if (s.rows[r] != want) return false;
+  }
+  return true;
+}
+
 __device__ void layout_tensor(const WorldArgs& d, const WorldArgs& s, const LayoutPlan& lp, const TensorInfo& ti,
                               int mode, int t) {
   if (t >= d.T) return;
+  if (t == 0) {  // the status reflects the latest exchange into d
+    if (source_matches_plan(s, lp, mode)) atomicAnd(d.status, ~ST_MISMATCH);
+    else atomicOr(d.status, ST_MISMATCH);
+  }
   int owner = -1;
   int64_t off = 0;
   for (int r = 0; r < d.W; ++r) {
@@ -155,7 +182,7 @@ __device__ __forceinline__ void route_job(const JobArgs& j, const WorldArgs& s, 
     const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
     job.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp);
     job.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp);
-    job.n_rows = is_local(s, sr) ? j.c_end[c] - j.c_start[c] : 0;
+    job.n_rows = (is_local(s, sr) && !(*d.status & ST_MISMATCH)) ? j.c_end[c] - j.c_start[c] : 0;
     job.width = ti.row_bytes[t];
     job.spitch = sp;
     job.dpitch = dp;
@@ -224,7 +251,7 @@ __device__ __forceinline__ void ulysses_job(const JobArgs& j, const WorldArgs& s
           active = other == 0;  // metadata once per destination row (exchange.cpp:424)
         }
       }
-      if (active && is_local(s, sr)) {
+      if (active && is_local(s, sr) && !(*d.status & ST_MISMATCH)) {
         const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
         job.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp + scol);
         job.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp + dcol);
@@ -961,6 +988,7 @@ extern "C" sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, 
   SB_CHECK_LAUNCH();
   sb::LayoutPlan lp{};
   lp.rows_src = w->d_rows;
+  lp.expect_rows = w->d_rows;
   sb::WorldArgs a = sb::wargs(w);
   sb::k_layout<<<1, 32, 0, s>>>(a, a, lp, sb::tinfo(w), 0);
   SB_CHECK_LAUNCH();
@@ -1014,6 +1042,7 @@ static void prepare_route(sb_planner* p, int slot, int reverse, sb_world* src, s
   sb::ensure_jobs(p, p->max_chunks * src->T);
   sb::LayoutPlan lp{};
   lp.rows_src = reverse ? p->origin_rows : p->target_rows;
+  lp.expect_rows = reverse ? p->target_rows : p->origin_rows;
   const bool fused = p->max_chunks * src->T <= sb::kFusedPrepMaxJobs;
   if (fused) {
     sb::k_exchange_prep<<<1, 1024, 0, s>>>(sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), lp,
@@ -1151,6 +1180,9 @@ extern "C" sb_status sb_world_status(sb_world* w, sb_stream stream) {
   int32_t st = 0;
   SB_CUDA(cudaMemcpy(&st, w->d_status, sizeof st, cudaMemcpyDeviceToHost));
   if (st & sb::ST_LAYOUT) throw Error{SB_ERR_CAPACITY, "world arena too small for the requested layout"};
+  if (st & sb::ST_MISMATCH)
+    throw Error{SB_ERR_INTEGRITY, "exchange source world does not match the plan's layout (rows per rank differ); "
+                                  "nothing was copied"};
   if (st) throw Error{SB_ERR_INTEGRITY, "world status " + std::to_string(st)};
   SB_API_END
 }

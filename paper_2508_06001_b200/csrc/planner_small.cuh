@@ -100,79 +100,9 @@ __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_inc
 template <int BPL>
 __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, const double* s_w, const int32_t* s_sorted,
                              int32_t* s_pick, int32_t* s_bagcnt, double total_rep, int* viol_out) {
-  const int lane = threadIdx.x & 31;
-  const double target = __ddiv_rn(total_rep, (double)a.U);
-  double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
-  int cnt[BPL];
-#pragma unroll
-  for (int i = 0; i < BPL; ++i) {
-    const int j = lane + 32 * i;
-    const int size = j < a.M ? a.bag_size[j] : 0;
-    cap[i] = __dmul_rn((double)size, target);
-    rcap[i] = cap[i] > 0.0 ? __drcp_rn(cap[i]) : 0.0;
-    asg[i] = 0.0;
-    occ[i] = occupancy(0.0, cap[i]);
-    rem[i] = __dsub_rn(cap[i], 0.0);
-    cnt[i] = 0;
-  }
-  int viol = 0;
-  double w_next = n > 0 ? s_w[s_sorted[lo]] : 0.0;
-  for (int64_t p = 0; p < n; ++p) {
-    const double w = w_next;  // software-pipelined: next weight loads under this step
-    if (p + 1 < n) w_next = s_w[s_sorted[lo + p + 1]];
-    double nasg[BPL], nocc[BPL], nrem[BPL];
-    uint64_t best_key = ~0ull;
-    uint32_t best_j = 0xffffffffu;
-#pragma unroll
-    for (int i = 0; i < BPL; ++i) {
-      nasg[i] = __dadd_rn(asg[i], w);
-      nocc[i] = occupancy_fast(nasg[i], cap[i], rcap[i]);
-      nrem[i] = __dsub_rn(cap[i], nasg[i]);
-      const uint32_t j = lane + 32 * i;
-      if (j < (uint32_t)a.M) {
-        const bool feasible = rem[i] >= w;
-        const uint64_t key = (feasible ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ[i]);
-        if (key < best_key) {
-          best_key = key;
-          best_j = j;
-        }
-      }
-    }
-    uint32_t pick;
-    if (BPL == 1) {
-      pick = warp_argmin_lane(best_key);
-    } else {
-      const uint32_t khi = (uint32_t)(best_key >> 32), klo = (uint32_t)best_key;
-      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
-      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
-      pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
-    }
-    // no feasible bag -> the fallback pick is a capacity violation
-    viol += (int)(__shfl_sync(0xffffffffu, (uint32_t)(best_key >> 63), (int)(pick & 31)));
-#pragma unroll
-    for (int i = 0; i < BPL; ++i) {
-      if ((uint32_t)(lane + 32 * i) == pick) {
-        asg[i] = nasg[i];
-        occ[i] = nocc[i];
-        rem[i] = nrem[i];
-        cnt[i]++;
-      }
-    }
-    if (lane == 0) s_pick[lo + p] = (int)pick;
-  }
-#pragma unroll
-  for (int i = 0; i < BPL; ++i) {
-    const int j = lane + 32 * i;
-    if (j < a.M) {
-      s_bagcnt[rep * a.M + j] = cnt[i];
-      a.bag_count[rep * a.M + j] = cnt[i];
-      a.per_bag_occ[rep * a.M + j] = occ[i];
-      const int g = a.bag_size[j];
-      const double per = __ddiv_rn(asg[i], (double)g);
-      for (int k = 0; k < g; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[j] + k]] = per;
-    }
-  }
-  if (lane == 0) atomicAdd(viol_out, viol);
+  const int32_t* srt = s_sorted + lo;
+  greedy_warp<BPL>(a, rep, n, total_rep, [s_w, srt](int64_t p) { return s_w[srt[p]]; }, s_pick + lo, s_bagcnt,
+                   viol_out);
 }
 
 __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {

@@ -258,3 +258,30 @@ def test_full_width_c1_roundtrip_bit_exact():
         assert rows_r == ob.rows
         assert dpl == hexd(oracle.digest(np.ascontiguousarray(ob.payload)))
         assert di == hexd(oracle.digest(ob.ids)) and dp == hexd(oracle.digest(ob.pos))
+
+
+def test_world_plan_mismatch_is_integrity_error():
+    """check_world_matches_layout (exchange.cpp:96-123): exchanging from a world
+    whose layout is not the plan's raises IntegrityError and copies nothing;
+    the next valid exchange into the same destination succeeds."""
+    meta = oracle.meta_c1(8, 4, seed=3, step=0)
+    dm = device_meta(meta)
+    planner = sb.Planner("g1n8", 8, max_seqs=32)
+    planner.plan(dm)
+    rows = int(sum(int(x.sum()) for x in meta.lens))
+    mk = lambda: sb.World(8, 24, [192], capacity_rows=rows)
+    A, B, stale, E = mk(), mk(), mk(), mk()
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    sb.reverse_route(planner, stale, E)  # stale was never routed: zero rows per rank
+    with pytest.raises(sb.IntegrityError):
+        E.status()
+    sb.route(planner, A, stale)          # route expects the origin layout: A has it
+    stale.status()
+    with pytest.raises(sb.IntegrityError):
+        sb.route(planner, stale, B)      # stale now holds the target layout, not the origin
+        B.status()
+    sb.reverse_route(planner, stale, E)
+    E.status()
+    for r in range(8):
+        assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r))

@@ -1,0 +1,42 @@
+"""Per-phase planner latency across the C4 sweep (diagnostics, needs a GPU).
+
+Large path: CUDA events between the planner kernels (sb_planner_timing).
+Small path: clock64 stamps per phase of the fused single-CTA planner.
+
+    python tools/plan_profile.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2508_06001_b200 as sb  # noqa: E402
+from paper_2508_06001_b200 import datagen  # noqa: E402
+
+SMALL = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
+         "rank_lists", "send", "wir"]
+for n in [256, 2048, 4096, 16384]:
+    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
+    dm = sb.DeviceMeta.from_lists(ids, lens)
+    for topo in ["g1n8", "g8n1"]:
+        for path in (["small", "large"] if n <= 2048 else ["large"]):
+            p = sb.Planner(topo, 8, max_seqs=n)
+            p.set_path(path)
+            if path == "small":
+                p.trace(True)
+                for _ in range(5):
+                    p.plan(dm)
+                torch.cuda.synchronize()
+                t = p.trace(True)
+                d = np.diff(t[:14])
+                print(f"n={n} {topo} small: total {int(t[13]-t[0])} cyc;",
+                      " ".join(f"{a}={int(c)}" for a, c in zip(SMALL, d)))
+            else:
+                p.enable_timing(True)
+                for _ in range(5):
+                    p.plan(dm)
+                torch.cuda.synchronize()
+                tm = p.timing()
+                print(f"n={n} {topo} large:", " ".join(f"{k}={v:.1f}" for k, v in tm.items()))
