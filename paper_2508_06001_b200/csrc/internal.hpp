@@ -75,6 +75,8 @@ struct sb_planner {
   int32_t* bag_count = nullptr;      // R*M
   int64_t* bag_rows = nullptr;       // R*M
   int64_t* rep_chunks = nullptr;     // R
+  int64_t* rep_cbase = nullptr;      // R+1
+  int32_t* bag_seq = nullptr;        // max_seqs
   unsigned long long* send_count = nullptr;  // W
   unsigned long long* recv_count = nullptr;  // W (generic manifests)
   // chunk-sized sort scratch for the generic reverse order (lazy)
@@ -122,6 +124,10 @@ struct sb_planner {
   std::vector<int> copy_op;
   size_t copy_used = 0;
   int current_op = 0;
+
+  // side stream for work that overlaps the main planner chain (serial totals)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 
   // timing
   bool timing = false;

@@ -2,24 +2,30 @@
 // identity_plan (:227-240) and the receive order of reverse_plan (:242-287),
 // reproduced bit-exactly on the GPU.
 //
-// Pipeline (one stream, no host synchronisation, graph-capturable):
-//   k_prep      W CTAs     workloads (FP64, reference operation order), per
-//                          rank row offsets (block scan), duplicate-id hash
-//   k_sort      2R+1 CTAs  per replica sort by (workload desc, id asc);
-//                          serial per-replica and global FP64 totals
-//   k_greedy    R warps    the multi-knapsack greedy: lane = bag, warp
-//                          argmin via REDUX, speculative division
-//   k_emit      R CTAs     stable bag partition (match_any + scan) and
-//                          chunk emission in the reference's chunk order
-//   k_lists     W CTAs     send/recv manifests, receive-side row offsets,
-//                          reverse receive order, Ulysses sequence bases
-//   k_finalize  1 CTA      WIR, chunk count
+// Pipeline (no host synchronisation, graph-capturable):
+//   k_prep        W CTAs       workloads (FP64, reference operation order), per
+//                              rank row offsets (block scan), duplicate-id hash
+//   k_totals      R+1 CTAs     serial per-replica / global FP64 totals (side
+//                              stream, overlaps the sort)
+//   k_sort_tiles  tiles        2048-record bitonic tiles in shared memory
+//   k_merge_pass  x log2(n/2048)  co-rank merges, one record per thread
+//   k_sort_finish              greedy order (workload desc, id asc)
+//   k_greedy      R warps      the multi-knapsack greedy: lane = bag, warp
+//                              argmin via REDUX, speculative next-step keys
+//   k_emit        R CTAs       stable bag partition (match_any + scan)
+//   k_emit_chunks chunk grid   chunk emission in the reference's chunk order
+//   k_lists       W CTAs       send/recv manifests, receive-side row offsets,
+//                              reverse receive order, Ulysses sequence bases
+//   k_finalize    1 CTA        WIR, chunk count
+// Batches of <= 2048 sequences take the fused single-CTA planner instead
+// (planner_small.cuh).
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstring>
 #include <limits>
 #include <new>
+#include <utility>
 
 #include "block_sort.cuh"
 #include "common.cuh"
@@ -55,6 +61,8 @@ struct PlanArgs {
   int32_t* bag_count;
   int64_t* bag_rows;
   int64_t* rep_chunks;
+  int64_t* rep_cbase;  // R+1: first chunk of each replica
+  int32_t* bag_seq;    // N: sequences grouped by (replica, bag), q ascending
   unsigned long long* send_count;
   int64_t *n_chunks, *n_seqs;
   uint64_t* c_id;
@@ -170,63 +178,178 @@ __global__ void __launch_bounds__(256) k_prep(PlanArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ k_sort
-__global__ void __launch_bounds__(1024) k_sort(PlanArgs a) {
+// ------------------------------------------------------------------ sort
+// Per replica sort by (workload desc, sample_id asc) (balancer.cpp:37-40) as
+// ascending (~bits(w), id, local index): w >= 0, so its IEEE bits are
+// monotone in value; the index makes the order total, so the result does not
+// depend on sort stability.  Multi-CTA: k_sort_tiles sorts 2048-record tiles
+// in shared memory (one CTA per tile of every replica), then log2(n/2048)
+// k_merge_pass launches merge run pairs by co-rank (each record's output
+// slot = its rank in its own run + its rank in the partner run, one binary
+// search per record, all CTAs busy); k_sort_finish emits the greedy order.
+
+// Replica of gathered position g (replicas are contiguous in gather order).
+__device__ __forceinline__ int replica_of(const PlanArgs& a, int64_t g) {
+  int lo = 0, hi = a.R;  // rank_off[lo*U] <= g < rank_off[hi*U]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.rank_off[mid * a.U] <= g) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(1024) k_sort_tiles(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (!seqs_ok(a)) return;
+  int b = blockIdx.x, rep = -1;
+  int64_t lo = 0, n = 0;
+  for (int r = 0; r < a.R; ++r) {
+    const int64_t rl = a.rank_off[r * a.U], rn = a.rank_off[r * a.U + a.U] - rl;
+    const int tiles = (int)((rn + kSortTile - 1) / kSortTile);
+    if (b < tiles) {
+      rep = r;
+      lo = rl;
+      n = rn;
+      break;
+    }
+    b -= tiles;
+  }
+  if (rep < 0) return;
+  const int64_t t0 = (int64_t)b * kSortTile;
+  const int cnt = (int)(n - t0 < kSortTile ? n - t0 : kSortTile);
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* s_lo = s_hi + kSortTile;
+  uint32_t* s_v = reinterpret_cast<uint32_t*>(s_lo + kSortTile);
+  int tile = 64;
+  while (tile < cnt) tile <<= 1;
+  for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+    if (i < cnt) {
+      const double wv = a.w[lo + t0 + i];
+      s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);  // -0.0 ties +0.0
+      s_lo[i] = a.ids[lo + t0 + i];
+      s_v[i] = (uint32_t)(t0 + i);
+    } else {
+      s_hi[i] = ~0ull;
+      s_lo[i] = ~0ull;
+      s_v[i] = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= tile; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < tile / 2; i += blockDim.x) {
+        const int l = 2 * j * (i / j) + (i % j), h = l + j;
+        const bool up = (l & k) == 0;
+        const uint64_t lh = s_hi[l], ll = s_lo[l], hh = s_hi[h], hl = s_lo[h];
+        const uint32_t lv = s_v[l], hv = s_v[h];
+        if (rec_less(hh, hl, hv, lh, ll, lv) == up) {
+          s_hi[l] = hh; s_lo[l] = hl; s_v[l] = hv;
+          s_hi[h] = lh; s_lo[h] = ll; s_v[h] = lv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    a.sk_hi[lo + t0 + i] = s_hi[i];
+    a.sk_lo[lo + t0 + i] = s_lo[i];
+    a.sk_v[lo + t0 + i] = s_v[i];
+  }
+}
+
+// One merge level: runs of `width` records (replica-relative) pairwise.
+__global__ void __launch_bounds__(256) k_merge_pass(PlanArgs a, int64_t width, const uint64_t* __restrict__ shi,
+                                                    const uint64_t* __restrict__ slo, const uint32_t* __restrict__ sv,
+                                                    uint64_t* dhi, uint64_t* dlo, uint32_t* dv) {
+  if (!seqs_ok(a)) return;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.rank_off[a.W]) return;
+  const int rep = replica_of(a, g);
+  const int64_t lo = a.rank_off[rep * a.U], n = a.rank_off[rep * a.U + a.U] - lo;
+  const int64_t d = g - lo, run = d / width, base = run * width, pbase = (run ^ 1) * width;
+  const uint64_t kh = shi[g], kl = slo[g];
+  const uint32_t kv = sv[g];
+  int64_t plen = n - pbase;
+  plen = plen < 0 ? 0 : (plen > width ? width : plen);
+  int64_t c = 0;  // partner records ordered before this one
+  if (plen > 0) {
+    int64_t l = 0, h = plen;
+    const int64_t p0 = lo + pbase;
+    while (l < h) {
+      const int64_t m = (l + h) >> 1;
+      if (rec_less(shi[p0 + m], slo[p0 + m], sv[p0 + m], kh, kl, kv)) l = m + 1;
+      else h = m;
+    }
+    c = l;
+  }
+  const int64_t out = lo + (base < pbase ? base : pbase) + (d - base) + c;
+  dhi[out] = kh;
+  dlo[out] = kl;
+  dv[out] = kv;
+}
+
+__global__ void k_sort_finish(PlanArgs a, const uint32_t* __restrict__ sv) {
+  if (!seqs_ok(a)) return;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.rank_off[a.W]) return;
+  const int64_t lo = a.rank_off[replica_of(a, g) * a.U];
+  const int64_t s = lo + sv[g];
+  a.sorted_idx[g] = (int32_t)s;
+  a.sorted_w[g] = a.w[s];
+}
+
+// Serial FP64 totals (dependent chains): per replica in gather order
+// (balancer.cpp:24-25) and BalanceReport::total_workload over every replica
+// (balancer.cpp:147).  One CTA per sum: all threads stage 2048-workload
+// chunks into shared memory (double-buffered) while thread 0 runs the add
+// chain over the previous chunk, so the chain never waits on global loads.
+// Runs on the planner's side stream, concurrently with the sort.
+constexpr int kTotalsChunk = 2048;
+
+__global__ void __launch_bounds__(256) k_totals(PlanArgs a) {
+  __shared__ double buf[2][kTotalsChunk];
+  if (!seqs_ok(a)) return;
   const int b = blockIdx.x;
+  int64_t lo, hi;
   if (b < a.R) {
-    const int64_t lo = a.rank_off[b * a.U], hi = a.rank_off[b * a.U + a.U];
-    const int64_t n = hi - lo;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      // (workload desc, sample_id asc) == ascending (~bits(w), id): w >= 0,
-      // so its IEEE bits are monotone in value (balancer.cpp:37-40).
-      const double wv = a.w[lo + i];
-      a.sk_hi[lo + i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);  // -0.0 ties +0.0
-      a.sk_lo[lo + i] = a.ids[lo + i];
-      a.sk_v[lo + i] = (uint32_t)i;
+    lo = a.rank_off[b * a.U];
+    hi = a.rank_off[b * a.U + a.U];
+  } else {
+    lo = 0;
+    hi = a.rank_off[a.W];
+  }
+  const int64_t n = hi - lo;
+  const int chunks = (int)((n + kTotalsChunk - 1) / kTotalsChunk);
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < kTotalsChunk && i < n; i += blockDim.x) buf[0][i] = a.w[lo + i];
+  __syncthreads();
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t nb = (int64_t)(c + 1) * kTotalsChunk;
+    for (int64_t i = threadIdx.x; i < kTotalsChunk && nb + i < n; i += blockDim.x)
+      buf[(c + 1) & 1][i] = a.w[lo + nb + i];
+    if (threadIdx.x == 0) {
+      const double* x = buf[c & 1];
+      const int cnt = (int)(n - (int64_t)c * kTotalsChunk < kTotalsChunk ? n - (int64_t)c * kTotalsChunk
+                                                                          : kTotalsChunk);
+      int i = 0;
+      for (; i + 8 <= cnt; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = x[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
+      }
+      for (; i < cnt; ++i) s = __dadd_rn(s, x[i]);
     }
     __syncthreads();
-    block_sort(n, a.sk_hi + lo, a.sk_lo + lo, a.sk_v + lo, a.tk_hi + lo, a.tk_lo + lo, a.tk_v + lo, smem);
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const int64_t s = lo + a.sk_v[lo + i];
-      a.sorted_idx[lo + i] = (int32_t)s;
-      a.sorted_w[lo + i] = a.w[s];
-    }
-  } else if (b < 2 * a.R) {
-    // per-replica total in gather order (balancer.cpp:24-25): a dependent
-    // FP64 chain, so one lane; loads are issued ahead of the adds.
-    if (threadIdx.x != 0) return;
-    const int rep = b - a.R;
-    const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
-    double s = 0.0;
-    int64_t i = lo;
-    for (; i + 8 <= hi; i += 8) {
-      double v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = a.w[i + k];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
-    }
-    for (; i < hi; ++i) s = __dadd_rn(s, a.w[i]);
-    a.rep_total[rep] = s;
+  }
+  if (threadIdx.x != 0) return;
+  if (b < a.R) {
+    a.rep_total[b] = s;
   } else {
-    // BalanceReport::total_workload: one running sum over every replica in
-    // gather order (balancer.cpp:147).
-    if (threadIdx.x != 0) return;
-    const int64_t n = a.rank_off[a.W];
-    double s = 0.0;
-    int64_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-      double v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = a.w[i + k];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
-    }
-    for (; i < n; ++i) s = __dadd_rn(s, a.w[i]);
     *a.total = s;
-    *a.n_seqs = n;
+    *a.n_seqs = hi;
   }
 }
 
@@ -259,14 +382,17 @@ __device__ __forceinline__ uint64_t greedy_key(bool feasible, double occ) {
   return (feasible ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ);
 }
 
-template <int BPL, class GetW>
+constexpr int kGreedyChunk = 1024;  // `hook(p0)` runs before every chunk of this many steps
+
+template <int BPL, class GetW, class Hook>
 __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t n, double total_rep, GetW getw,
-                                            int32_t* pick_out, int32_t* bagcnt_out, int* viol_out) {
+                                            Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out) {
   const int lane = threadIdx.x & 31;
   const double target = __ddiv_rn(total_rep, (double)a.U);  // balancer.cpp:26
   double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
   uint64_t key[BPL];
   int cnt[BPL];
+  hook(0);
   double w_a = n > 0 ? getw(0) : 0.0, w_b = n > 1 ? getw(1) : 0.0, w_c = n > 2 ? getw(2) : 0.0;
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
@@ -281,11 +407,15 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     cnt[i] = 0;
   }
   int viol = 0;
-  for (int64_t p = 0; p < n; ++p) {
+  const int nn = (int)n;  // <= max_seqs < 2^31: 32-bit loop arithmetic
+  for (int p0 = 0; p0 < nn; p0 += kGreedyChunk) {
+  if (p0 > 0) hook(p0);
+  const int p1 = nn - p0 < kGreedyChunk ? nn : p0 + kGreedyChunk;
+  for (int p = p0; p < p1; ++p) {
     const double w = w_a, wn = w_b;  // w_p and w_{p+1} (0 past the end: unused)
     w_a = w_b;
     w_b = w_c;
-    w_c = (p + 3 < n) ? getw(p + 3) : 0.0;  // prefetch under this step
+    w_c = getw(p + 3 < nn ? p + 3 : nn - 1);  // prefetch under this step (clamped: no branch)
     double nasg[BPL], nocc[BPL], nrem[BPL];
     uint64_t kwin[BPL], knot[BPL];
     uint64_t best = ~0ull;
@@ -319,6 +449,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     }
     if (lane == 0) pick_out[p] = (int)pick;
   }
+  }
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
     const int j = lane + 32 * i;
@@ -334,15 +465,30 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
   if (lane == 0) atomicAdd(viol_out, viol);
 }
 
-// Large path: one warp per replica over the globally sorted workloads.
+// Large path: one warp per replica.  The sorted workloads stream through a
+// two-chunk shared-memory ring: at the start of chunk k the warp loads chunk
+// k+1 (coalesced, latency hidden under 1024 greedy steps), so the chain's
+// three-step-ahead prefetch always hits shared memory.
 template <int BPL>
 __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
+  __shared__ double ring[2][kGreedyChunk];
   if (!seqs_ok(a)) return;
-  const int rep = blockIdx.x;
+  const int rep = blockIdx.x, lane = threadIdx.x;
   const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  const int n = (int)(hi - lo);
   const double* sw = a.sorted_w + lo;
-  greedy_warp<BPL>(a, rep, hi - lo, a.rep_total[rep], [sw](int64_t p) { return sw[p]; }, a.pick + lo, nullptr,
-                   a.violations);
+  auto load = [&](int c) {
+    const int b = c * kGreedyChunk;
+    for (int i = lane; i < kGreedyChunk && b + i < n; i += 32) ring[c & 1][i] = sw[b + i];
+  };
+  auto hook = [&](int p0) {
+    if (p0 == 0) load(0);
+    load(p0 / kGreedyChunk + 1);
+    __syncwarp();
+  };
+  greedy_warp<BPL>(a, rep, n, a.rep_total[rep],
+                   [&](int p) { return ring[(p / kGreedyChunk) & 1][p % kGreedyChunk]; }, hook, a.pick + lo,
+                   nullptr, a.violations);
 }
 
 // ------------------------------------------------------------------ k_emit
@@ -363,22 +509,33 @@ __device__ void replica_bases(const PlanArgs& a, int rep, int64_t* rep_base, int
   }
 }
 
+// Phase A (one CTA per replica): q = rank of each sequence among its bag's
+// sequences in greedy order (a stable bag partition, match_any + per-warp
+// counts), per-sequence fields, and the inverse map bag_seq[(bag, q)] = s
+// that lets phase B emit chunks in parallel.
 __global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
   __shared__ int warp_cnt[32][kMaxBags];
   __shared__ int running[kMaxBags];
   __shared__ int64_t bag_base[kMaxBags];
+  __shared__ int64_t seq_base[kMaxBags];
   __shared__ int64_t rep_base;
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
   if (tid == 0) {
     replica_bases(a, rep, &rep_base, bag_base);
-    int64_t c = 0;
-    for (int b = 0; b < a.M; ++b) c += (int64_t)a.bag_count[rep * a.M + b] * a.bag_size[b];
+    int64_t c = 0, sq = lo;
+    for (int b = 0; b < a.M; ++b) {
+      seq_base[b] = sq;
+      sq += a.bag_count[rep * a.M + b];
+      c += (int64_t)a.bag_count[rep * a.M + b] * a.bag_size[b];
+    }
     a.rep_chunks[rep] = c;
+    a.rep_cbase[rep] = rep_base;
+    if (rep == a.R - 1) a.rep_cbase[a.R] = rep_base + c;
   }
   if (tid < a.M) running[tid] = 0;
   __syncthreads();
-  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int64_t tile = lo; tile < hi; tile += blockDim.x) {
     for (int e = tid; e < 32 * a.M; e += blockDim.x) warp_cnt[e / a.M][e % a.M] = 0;
@@ -403,31 +560,57 @@ __global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
     if (valid) {
       const int q = warp_cnt[warp][b] + rank_in;
       const int s = a.sorted_idx[p];
-      const int64_t l = a.lens[s] < 0 ? 0 : a.lens[s];
       const int g = a.bag_size[b];
-      const int64_t cb = rep_base + bag_base[b] + (int64_t)q * g;
-      const uint64_t id = a.ids[s];
-      const int src = a.seq_rank[s];
-      const int64_t soff = a.seq_off[s];
-      for (int k = 0; k < g; ++k) {
-        const int64_t c = cb + k;
-        const int64_t st = chunk_start(l, g, k);
-        a.c_id[c] = id;
-        a.c_idx[c] = k;
-        a.c_start[c] = st;
-        a.c_end[c] = st + chunk_len(l, g, k);
-        a.c_src[c] = src;
-        a.c_dst[c] = rep * a.U + a.bag_ranks[a.bag_off[b] + k];
-        a.c_src_row[c] = soff + st;
-        a.c_seq[c] = s;
-      }
+      a.bag_seq[seq_base[b] + q] = s;
       a.seq_bag[s] = b;
       a.seq_G[s] = g;
-      a.seq_chunk_base[s] = cb;
-      atomicAdd(&a.send_count[src], (unsigned long long)g);
+      a.seq_chunk_base[s] = rep_base + bag_base[b] + (int64_t)q * g;
+      atomicAdd(&a.send_count[a.seq_rank[s]], (unsigned long long)g);
     }
     __syncthreads();
   }
+}
+
+// Phase B (grid over chunk capacity): chunk c = (replica, bag b, q, k) ->
+// sequence bag_seq[(b, q)]; every field written coalesced across threads
+// (balancer.cpp:178-218 chunk emission).
+__global__ void __launch_bounds__(256) k_emit_chunks(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.rep_cbase[a.R]) return;
+  int rep = 0;
+  {
+    int l = 0, h = a.R;  // rep_cbase[l] <= c < rep_cbase[h]
+    while (h - l > 1) {
+      const int m = (l + h) >> 1;
+      if (a.rep_cbase[m] <= c) l = m;
+      else h = m;
+    }
+    rep = l;
+  }
+  int64_t rel = c - a.rep_cbase[rep], sq = a.rank_off[rep * a.U];
+  int b = 0;
+  for (;; ++b) {
+    const int64_t nb = a.bag_count[rep * a.M + b];
+    const int64_t span = nb * a.bag_size[b];
+    if (rel < span || b == a.M - 1) break;
+    rel -= span;
+    sq += nb;
+  }
+  const int g = a.bag_size[b];
+  const int64_t q = rel / g;
+  const int k = (int)(rel - q * g);
+  const int s = a.bag_seq[sq + q];
+  const int64_t l = a.lens[s] < 0 ? 0 : a.lens[s];
+  const int64_t st = chunk_start(l, g, k);
+  a.c_id[c] = a.ids[s];
+  a.c_idx[c] = k;
+  a.c_start[c] = st;
+  a.c_end[c] = st + chunk_len(l, g, k);
+  a.c_src[c] = a.seq_rank[s];
+  a.c_dst[c] = rep * a.U + a.bag_ranks[a.bag_off[b] + k];
+  a.c_src_row[c] = a.seq_off[s] + st;
+  a.c_seq[c] = s;
 }
 
 // reverse_plan's receive order for rank r (balancer.cpp:259-285) when its
@@ -439,10 +622,6 @@ __global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
 // lists of <= 16 entries are already identical (insertion sort is stable).
 __device__ void fix_rev_ties(const PlanArgs& a, int r, int64_t off, int64_t n) {
   if (n <= stdsort::kThreshold) return;
-  bool tie = false;
-  for (int64_t s = a.rank_off[r]; s < a.rank_off[r + 1] && !tie; ++s)
-    tie = a.seq_G[s] > 1 && a.lens[s] < a.seq_G[s];
-  if (!tie) return;
   for (int64_t i = 0; i < n; ++i) a.rev_recv_idx[off + i] = a.send_idx[off + i];
   const int32_t* seq = a.c_seq;
   const int64_t* st = a.c_start;
@@ -465,7 +644,6 @@ __device__ void fix_rev_ties(const PlanArgs& a, int r, int64_t off, int64_t n) {
 //   c_seq_base   = row base of each sequence in its bag's full-sequence
 //                  layout (pre_attn shells, exchange.cpp:291-295).
 __global__ void __launch_bounds__(1024) k_lists(PlanArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t sh[33];
   __shared__ int64_t s_recv_off, s_send_off, s_rep_base;
   __shared__ int64_t s_bag_base[kMaxBags];
@@ -525,36 +703,37 @@ __global__ void __launch_bounds__(1024) k_lists(PlanArgs a) {
     }
     if (tid == 0) a.bag_rows[rep * a.M + b] = c2;
   }
-  // send list: rank r's sequences ordered by first chunk index
+  // send list: rank r's sequences ordered by first chunk index.  Chunk order
+  // is (replica, bag, q, k), i.e. the order of bag_seq over r's replica, so
+  // this is a stable filter of bag_seq by source rank, each sequence
+  // expanded to its G chunks.
   const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
   const int64_t n = hi - lo;
-  for (int64_t i = tid; i < n; i += blockDim.x) {
-    a.sk_hi[lo + i] = (uint64_t)a.seq_chunk_base[lo + i];
-    a.sk_lo[lo + i] = 0;
-    a.sk_v[lo + i] = (uint32_t)i;
-  }
-  __syncthreads();
-  block_sort(n, a.sk_hi + lo, a.sk_lo + lo, a.sk_v + lo, a.tk_hi + lo, a.tk_lo + lo, a.tk_v + lo, smem);
-  int64_t c3 = 0;
-  for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int64_t i = i0 + tid;
-    const bool valid = i < n;
-    const int64_t s = valid ? lo + a.sk_v[lo + i] : 0;
-    const int gs = valid ? a.seq_G[s] : 0;
-    int64_t tot;
-    const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
-    if (valid) {
-      const int64_t cb = a.seq_chunk_base[s];
-      for (int kk = 0; kk < gs; ++kk) a.send_idx[s_send_off + c3 + ex + kk] = (int32_t)(cb + kk);
+  {
+    const int64_t rlo = a.rank_off[rep * a.U], rhi = a.rank_off[rep * a.U + a.U];
+    int64_t c3 = 0;
+    for (int64_t i0 = rlo; i0 < rhi; i0 += blockDim.x) {
+      const int64_t i = i0 + tid;
+      const int s = i < rhi ? a.bag_seq[i] : 0;
+      const bool mine = i < rhi && a.seq_rank[s] == r;
+      const int gs = mine ? a.seq_G[s] : 0;
+      int64_t tot;
+      const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
+      if (mine) {
+        const int64_t cb = a.seq_chunk_base[s];
+        for (int kk = 0; kk < gs; ++kk) a.send_idx[s_send_off + c3 + ex + kk] = (int32_t)(cb + kk);
+      }
+      c3 += tot;
     }
-    c3 += tot;
   }
   // reverse receive order: sequences in buffer order, chunks ascending
   int64_t c4 = 0;
+  int tie = 0;  // a sequence shorter than its bag: empty chunks with equal (segment, start)
   for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
     const int64_t i = i0 + tid;
     const bool valid = i < n;
     const int gs = valid ? a.seq_G[lo + i] : 0;
+    tie |= (gs > 1 && a.lens[lo + i] < gs) ? 1 : 0;
     int64_t tot;
     const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
     if (valid) {
@@ -563,8 +742,8 @@ __global__ void __launch_bounds__(1024) k_lists(PlanArgs a) {
     }
     c4 += tot;
   }
-  __syncthreads();  // send[r] complete: std::sort's input order
-  if (tid == 0) fix_rev_ties(a, r, s_send_off, c4);
+  tie = __syncthreads_or(tie);  // also: send[r] complete (std::sort's input order)
+  if (tid == 0 && tie) fix_rev_ties(a, r, s_send_off, c4);
 }
 
 // -------------------------------------------------------------- k_finalize
@@ -767,6 +946,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.seq_bag = p->seq_bag; a.seq_G = p->seq_G; a.seq_chunk_base = p->seq_chunk_base;
   a.rep_total = p->rep_total; a.sentinel = p->sentinel; a.bag_count = p->bag_count;
   a.bag_rows = p->bag_rows; a.rep_chunks = p->rep_chunks; a.send_count = p->send_count;
+  a.rep_cbase = p->rep_cbase; a.bag_seq = p->bag_seq;
   a.n_chunks = p->n_chunks; a.n_seqs = p->n_seqs;
   a.c_id = p->c_id; a.c_idx = p->c_idx; a.c_src = p->c_src; a.c_dst = p->c_dst;
   a.c_start = p->c_start; a.c_end = p->c_end; a.c_src_row = p->c_src_row; a.c_dst_row = p->c_dst_row;
@@ -792,6 +972,7 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->seq_bag, N); dalloc(&p->seq_G, N); dalloc(&p->seq_chunk_base, N);
   dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
   dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
+  dalloc(&p->rep_cbase, R + 1); dalloc(&p->bag_seq, N);
   dalloc(&p->recv_count, W);
   dalloc(&p->n_chunks, 1); dalloc(&p->n_seqs, 1);
   dalloc(&p->c_id, C); dalloc(&p->c_idx, C); dalloc(&p->c_src, C); dalloc(&p->c_dst, C);
@@ -808,8 +989,7 @@ static void planner_alloc(sb_planner* p) {
   SB_CUDA(cudaMemcpy(p->d_bag_size, p->bag_size.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
   SB_CUDA(cudaMemcpy(p->d_rank_bag, p->rank_bag.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
   SB_CUDA(cudaMemcpy(p->d_rank_member, p->rank_member.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
-  SB_CUDA(cudaFuncSetAttribute(k_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
-  SB_CUDA(cudaFuncSetAttribute(k_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
+  SB_CUDA(cudaFuncSetAttribute(k_sort_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
   if (p->max_seqs <= kSmallSeqs && p->W <= 1024) {
     p->small_smem = small_layout((int)p->max_seqs, p->W, p->R * p->M, p->R).total;
     static size_t set_to = 0;  // attribute is per function: keep the largest requested
@@ -820,6 +1000,9 @@ static void planner_alloc(sb_planner* p) {
   }
   if (const char* e = getenv("SEQBAL_PLANNER")) p->path = std::string(e) == "small" ? 1 : std::string(e) == "large" ? 2 : 0;
   for (int i = 0; i < 6; ++i) SB_CUDA(cudaEventCreate(&p->ev[i]));
+  SB_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  SB_CUDA(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming));
+  SB_CUDA(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming));
 }
 
 static void planner_free(sb_planner* p) {
@@ -834,11 +1017,14 @@ static void planner_free(sb_planner* p) {
                   p->violations, p->status,
                   p->stage_ids, p->stage_lens, p->stage_w, p->stage_off,
                   p->seg_off, p->seg_id, p->seg_first, p->seg_len, p->recv_count, p->ck_hi, p->ck_lo,
-                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv};
+                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv, p->rep_cbase, p->bag_seq};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int i = 0; i < 6; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  if (p->fork_ev) cudaEventDestroy(p->fork_ev);
+  if (p->join_ev) cudaEventDestroy(p->join_ev);
+  if (p->side) cudaStreamDestroy(p->side);
   for (cudaEvent_t e : p->copy_ev) cudaEventDestroy(e);
   for (auto& sl : p->slots) {
     if (sl.jobs) cudaFree(sl.jobs);
@@ -860,12 +1046,44 @@ static bool use_small_path(const sb_planner* p) {
   return fits && (p->path == 1 || p->path == 0);
 }
 
+static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool order) {
+  // serial totals on the side stream, overlapping the sort
+  SB_CUDA(cudaEventRecord(p->fork_ev, s));
+  SB_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
+  k_totals<<<p->R + 1, 256, 0, p->side>>>(a);
+  SB_CHECK_LAUNCH();
+  SB_CUDA(cudaEventRecord(p->join_ev, p->side));
+  int launches = 1;
+  if (order) {
+    const int64_t N = p->max_seqs;
+    const int tiles = (int)((N + kSortTile - 1) / kSortTile) + p->R;
+    k_sort_tiles<<<tiles, 1024, kSortSmemBytes, s>>>(a);
+    SB_CHECK_LAUNCH();
+    uint64_t *shi = p->sk_hi, *slo = p->sk_lo, *dhi = p->tk_hi, *dlo = p->tk_lo;
+    uint32_t *sv = p->sk_v, *dv = p->tk_v;
+    const int blocks = (int)((N + 255) / 256);
+    for (int64_t width = kSortTile; width < N; width <<= 1) {
+      k_merge_pass<<<blocks, 256, 0, s>>>(a, width, shi, slo, sv, dhi, dlo, dv);
+      SB_CHECK_LAUNCH();
+      std::swap(shi, dhi);
+      std::swap(slo, dlo);
+      std::swap(sv, dv);
+      ++launches;
+    }
+    k_sort_finish<<<blocks, 256, 0, s>>>(a, sv);
+    SB_CHECK_LAUNCH();
+    launches += 2;
+  }
+  SB_CUDA(cudaStreamWaitEvent(s, p->join_ev, 0));
+  count_launch(launches);
+}
+
 static void run_plan(sb_planner* p, cudaStream_t s) {
   PlanArgs a = make_args(p);
   if (use_small_path(p)) {
     SB_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int32_t), s));
     if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
-    k_plan_small<<<1, 1024, p->small_smem, s>>>(a, (int)p->max_seqs);
+    k_plan_small<<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
     SB_CHECK_LAUNCH();
     if (p->timing)
       for (int i = 1; i < 6; ++i) SB_CUDA(cudaEventRecord(p->ev[i], s));
@@ -877,8 +1095,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   k_prep<<<p->W, 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[1], s));
-  k_sort<<<2 * p->R + 1, 1024, kSortSmemBytes, s>>>(a);
-  SB_CHECK_LAUNCH();
+  launch_sort(p, a, s, true);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[2], s));
   const int bpl = (p->M + 31) / 32;
   if (bpl <= 1) k_greedy<1><<<p->R, 32, 0, s>>>(a);
@@ -887,8 +1104,10 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[3], s));
   k_emit<<<p->R, 1024, 0, s>>>(a);
   SB_CHECK_LAUNCH();
+  k_emit_chunks<<<(int)((p->max_chunks + 255) / 256), 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[4], s));
-  k_lists<<<p->W, 1024, kSortSmemBytes, s>>>(a);
+  k_lists<<<p->W, 1024, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
@@ -901,8 +1120,7 @@ static void run_identity(sb_planner* p, cudaStream_t s) {
   plan_common_prologue(p, s);
   k_prep<<<p->W, 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
-  k_sort<<<2 * p->R + 1, 1024, kSortSmemBytes, s>>>(a);  // totals (sorted order unused)
-  SB_CHECK_LAUNCH();
+  launch_sort(p, a, s, false);  // totals only (sorted order unused)
   k_identity<<<148, 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   k_identity_report<<<(p->W + 127) / 128, 128, 0, s>>>(a);
@@ -1154,12 +1372,11 @@ extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t*
   sb::plan_common_prologue(p, s);
   sb::k_prep<<<p->W, 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
-  sb::k_sort<<<2 * p->R + 1, 1024, sb::kSortSmemBytes, s>>>(a);
-  SB_CHECK_LAUNCH();
+  sb::launch_sort(p, a, s, true);
   if ((p->M + 31) / 32 <= 1) sb::k_greedy<1><<<p->R, 32, 0, s>>>(a);
   else sb::k_greedy<2><<<p->R, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
-  sb::count_launch(3);
+  sb::count_launch(2);
   SB_CUDA(cudaStreamSynchronize(s));
   int32_t st = 0;
   SB_CUDA(cudaMemcpy(&st, p->status, sizeof st, cudaMemcpyDeviceToHost));

@@ -22,6 +22,7 @@ namespace sb {
   } while (0)
 
 constexpr int kSmallSeqs = 2048;
+constexpr int kSmallThreads = 512;  // 128 registers per thread: the greedy keeps its speculation in registers
 
 __host__ __device__ inline int small_pow2(int n) {
   int t = 32;
@@ -31,7 +32,7 @@ __host__ __device__ inline int small_pow2(int n) {
 
 struct SmallLayout {  // byte offsets into dynamic shared memory
   size_t ids, lens, w, soff, hi, lo, v, rank, sorted, pick, G, cb, bo, rank_off, rpre, bagcnt, bagcb, bagq,
-      sendcnt, sendoff, reptot, total;
+      sendcnt, sendoff, reptot, tie, total;
   int T;
 };
 
@@ -65,6 +66,7 @@ __host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int 
   L.bagq = take(4ull * RM);
   L.sendcnt = take(8ull * W);
   L.sendoff = take(8ull * (W + 1));
+  L.tie = take(4ull * W);
   L.reptot = take(8ull * R);
   L.total = o;
   return L;
@@ -100,12 +102,11 @@ __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_inc
 template <int BPL>
 __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, const double* s_w, const int32_t* s_sorted,
                              int32_t* s_pick, int32_t* s_bagcnt, double total_rep, int* viol_out) {
-  const int32_t* srt = s_sorted + lo;
-  greedy_warp<BPL>(a, rep, n, total_rep, [s_w, srt](int64_t p) { return s_w[srt[p]]; }, s_pick + lo, s_bagcnt,
-                   viol_out);
+  const double* ws = s_w + lo;  // workloads already gathered into greedy order
+  greedy_warp<BPL>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo, s_bagcnt, viol_out);
 }
 
-__global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
+__global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int64_t sh[33];
   __shared__ int s_flag, s_viol;
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
   int32_t* s_bagq = reinterpret_cast<int32_t*>(sm + L.bagq);
   int64_t* s_sendcnt = reinterpret_cast<int64_t*>(sm + L.sendcnt);
   int64_t* s_sendoff = reinterpret_cast<int64_t*>(sm + L.sendoff);
+  int32_t* s_tie = reinterpret_cast<int32_t*>(sm + L.tie);
   double* s_reptot = reinterpret_cast<double*>(sm + L.reptot);
 
   SB_PHASE(0);
@@ -269,7 +271,9 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
       for (int64_t i = tid; i < n; i += blockDim.x) {
         const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
         int pos = 0;
-        for (int64_t j = 0; j < n; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
+        const int nj = (int)n;
+#pragma unroll 8
+        for (int j = 0; j < nj; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
         s_sorted[lo + pos] = (int32_t)(lo + i);
         a.sorted_idx[lo + pos] = (int32_t)(lo + i);
       }
@@ -283,11 +287,15 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     __syncthreads();
   }
   SB_PHASE(6);
-  // ---- phase 6: greedy, one warp per replica (balancer.cpp:44-62)
+  // ---- phase 6: greedy, one warp per replica (balancer.cpp:44-62), over the
+  // workloads gathered into greedy order (the sort scratch is free now)
+  double* s_wsorted = reinterpret_cast<double*>(s_hi);
+  for (int64_t i = tid; i < N; i += blockDim.x) s_wsorted[i] = s_w[s_sorted[i]];
+  __syncthreads();
   for (int rep = warp; rep < R; rep += nw) {
     const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
-    if (M <= 32) small_greedy<1>(a, rep, lo, n, s_w, s_sorted, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
-    else small_greedy<2>(a, rep, lo, n, s_w, s_sorted, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
+    if (M <= 32) small_greedy<1>(a, rep, lo, n, s_wsorted, nullptr, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
+    else small_greedy<2>(a, rep, lo, n, s_wsorted, nullptr, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
   }
   __syncthreads();
   SB_PHASE(7);
@@ -419,15 +427,19 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
     // reverse receive order: r's sequences in buffer order, chunks ascending
     const int64_t s0 = s_roff[r], s1 = s_roff[r + 1];
     int64_t c4 = 0;
+    bool tie = false;  // a sequence shorter than its bag: equal (segment, start) keys
     for (int64_t i0 = s0; i0 < s1; i0 += 32) {
       const int64_t i = i0 + lane;
       const bool valid = i < s1;
       const int gs = valid ? s_G[i] : 0;
+      tie |= gs > 1 && s_lens[i] < gs;
       const int64_t inc = warp_scan_incl64(gs);
       if (valid)
         for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[s_sendoff[r] + c4 + inc - gs + kk] = (int32_t)(s_cb[i] + kk);
       c4 += __shfl_sync(0xffffffffu, inc, 31);
     }
+    tie = __any_sync(0xffffffffu, tie);
+    if (lane == 0) s_tie[r] = tie ? 1 : 0;
   }
   __syncthreads();
   SB_PHASE(11);
@@ -444,7 +456,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(PlanArgs a, int cap) {
   }
   __syncthreads();  // send lists complete: reverse-order tie replay reads them
   for (int r = warp; r < W; r += nw)
-    if (lane == 0) fix_rev_ties(a, r, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r]);
+    if (lane == 0 && s_tie[r]) fix_rev_ties(a, r, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r]);
   SB_PHASE(12);
   // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
   __syncthreads();

@@ -17,10 +17,17 @@ from paper_2508_06001_b200 import datagen  # noqa: E402
 
 SMALL = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
          "rank_lists", "send", "wir"]
-for n in [256, 2048, 4096, 16384]:
-    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
+C2 = ["g2b8i256f1s0", "g2b4i512f1s0", "g2b2i768f1s0", "g2b1i1024f1s0"]
+for n in ["c2", 256, 2048, 4096, 16384]:
+    if n == "c2":
+        ids, lens = datagen.metadata("scenario", 8, codes=C2, step=0, seed=7)
+        n = sum(len(x) for x in ids)
+        topos = ["g1n4+g2n2"]
+    else:
+        ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
+        topos = ["g1n8", "g8n1"]
     dm = sb.DeviceMeta.from_lists(ids, lens)
-    for topo in ["g1n8", "g8n1"]:
+    for topo in topos:
         for path in (["small", "large"] if n <= 2048 else ["large"]):
             p = sb.Planner(topo, 8, max_seqs=n)
             p.set_path(path)
