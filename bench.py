@@ -45,6 +45,7 @@ CONFIGS = {
     "c3": dict(workload="C3: image-video joint stream (<=64K-token videos), bags of 4 (g4n2), 24x128 heads",
                world=8, topology="g4n2", meta=dict(kind="scenario", codes=C3_CODES, step=0, seed=7)),
     "c4": dict(workload="C4: plan scaling sweep", world=8, topology="g1n8", meta=dict(kind="c1")),
+    "c5": dict(workload="C5: 1000-step dynamic stream", world=8, topology="g1n2+g2n1+g4n1", meta=dict(kind="c1")),
 }
 
 
@@ -261,6 +262,121 @@ def run_c4(args):
     return 0
 
 
+# ------------------------------------------- C5: 1000-step dynamic stream
+C5_STEPS = 1000
+
+
+def run_reference_stream(steps, budget_s, threads=None):
+    """The reference on the C5 schedule: plan_routing every step, full data
+    path (route + Ulysses + reverse, Exec::Parallel) every 50th step."""
+    from paper_2508_06001_b200.scenarios import C5_SCENARIOS, C5_SEED, C5_TOPOLOGY, C5_WORLD
+    harness = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+    if not os.path.exists(harness):
+        return None, "oracle/_ref/ref_harness not built"
+    env = dict(os.environ)
+    env["OMP_NUM_THREADS"] = str(threads or os.cpu_count() or 1)
+    req = {"world": C5_WORLD, "topology": C5_TOPOLOGY, "scenarios": [{"codes": c} for c in C5_SCENARIOS],
+           "seed": C5_SEED, "steps": steps, "full_every": 50, "payload_width": PAYLOAD_BYTES // 8,
+           "budget_s": budget_s}
+    p = subprocess.run([harness, "stream"], input=json.dumps(req).encode(), capture_output=True, env=env,
+                       timeout=1800)
+    if p.returncode != 0:
+        return None, p.stderr.decode()[-300:]
+    return json.loads(p.stdout), None
+
+
+def run_c5(args):
+    """C5 (BASELINE configs[4]): 1000-step dynamic stream.  Step s draws every
+    rank's batch on the device from scenario s mod 3 (low-res / mixed /
+    joint image+video, 8-GPU sharding group), then origin layout + witness
+    payload, plan, route, Ulysses pre/post (bags of 2 and 4), reverse_route.
+    Timed without the inline checks (one captured step replayed 1000 times);
+    a second pass runs all 1000 steps with simulate_step's checks on."""
+    import numpy as np
+    import torch
+
+    import paper_2508_06001_b200 as sb
+    from paper_2508_06001_b200.scenarios import C5_SCENARIOS, C5_SEED, C5_TOPOLOGY, C5_WORLD
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    steps = C5_STEPS
+    sch = sb.Schedule([sb.Scenario(c) for c in C5_SCENARIOS], C5_WORLD, C5_SEED)
+    planner = sb.Planner(C5_TOPOLOGY, C5_WORLD, max_seqs=sch.max_seqs)
+    drv = sb.Driver(planner, sch, n_heads=24, payload_row_bytes=PAYLOAD_BYTES, verify=False, record_cap=steps)
+    stream = torch.cuda.current_stream()
+    drv.set_step(0)
+    for _ in range(max(3, args.warmup)):
+        drv.step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        drv.step()
+    drv.set_step(0)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = sb.kernel_launches()
+    with ClockSampler() as clk:
+        ev0.record(stream)
+        for _ in range(steps):
+            g.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = sb.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    recs = drv.records()
+    prog = drv.progress()
+    assert prog["steps_run"] == steps and prog["next_step"] == steps
+    tokens = np.array([r["tokens"] for r in recs], np.float64)
+    wir = np.array([r["wir"] for r in recs])
+    mm = np.array([r["max_over_mean"] for r in recs])
+    by_scen = {}
+    for r in recs:
+        by_scen.setdefault(r["scenario"], []).append(r["max_over_mean"])
+    del g, drv
+    # verification pass: all steps with simulate_step's inline checks
+    vdrv = sb.Driver(planner, sch, n_heads=24, payload_row_bytes=PAYLOAD_BYTES, verify=True, record_cap=steps)
+    vdrv.set_step(0)
+    t0 = time.time()
+    vdrv.run(steps)
+    vprog = vdrv.progress()
+    verify_s = time.time() - t0
+    vrecs = vdrv.records()
+    same_plans = all(a["wir"] == b["wir"] and a["chunks"] == b["chunks"] for a, b in zip(recs, vrecs))
+    line = {
+        "metric": "sustained round-trip tokens/s over a 1000-step dynamic stream; workload imbalance",
+        "value": float(tokens.sum() / (ms * 1e-3)), "unit": "tokens/s", "n_gpus": 1, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (device-generated)",
+        "config": {"workload": "C5: 1000-step dynamic stream, step s from scenario s mod 3 of " +
+                               json.dumps(C5_SCENARIOS) + f" (seed {C5_SEED}), world {C5_WORLD}, topology "
+                               f"{C5_TOPOLOGY}, hidden 3072 bf16 rows + 16 B metadata",
+                   "step": "device generate + origin layout + witness fill + plan + route + pre_attn + post_attn "
+                           "+ reverse_route (one CUDA graph, device step counter)",
+                   "l2": "inputs larger than L2 (worlds of 0.4-0.7 GB)"},
+        "tokens_per_step": {"mean": float(tokens.mean()), "min": int(tokens.min()), "max": int(tokens.max())},
+        "wir": {"mean": float(wir.mean()), "max": float(wir.max())},
+        "max_over_mean": {"mean": float(mm.mean()), "max": float(mm.max()),
+                          "per_scenario_mean": {str(k): float(np.mean(v)) for k, v in sorted(by_scen.items())}},
+        "verify": {"steps": vprog["steps_run"], "failed_checks": vprog["failed"], "plans_identical": same_plans,
+                   "checks": "route + pre_attn conserve content_checksum; post_attn(pre_attn(x)) == x; perturbed "
+                             "payload returns home bitwise (simulator.cpp:106-159)", "wall_s": verify_s},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        ref, err = run_reference_stream(steps, budget_s=args.cpu_budget_s)
+        if ref:
+            line["cpu_baseline"] = {"value": ref["roundtrip_tokens_per_s"], "unit": "tokens/s",
+                                    "cores": ref["threads"], "kind": "reference",
+                                    "sample": f"{ref['steps']} steps planned ({1e6 * ref['plan_s_per_step']:.0f} "
+                                              f"us/plan), full round trip on {ref['full_steps']} sampled steps "
+                                              "(every 50th, budget-bounded), Exec::Parallel"}
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "unavailable": err}
+    print(json.dumps(line))
+    return 0
+
+
 # ------------------------------------------------------------ our arm
 def main():
     args = parse_args()
@@ -289,6 +405,22 @@ def main():
                                  "sample": "plan_routing best of <=5 per point"},
                 "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
             return 0
+        if args.config == "c5":
+            ref, err = run_reference_stream(C5_STEPS, budget_s=120.0)
+            if ref is None:
+                print(json.dumps({"impl": "reference", "unavailable": err}))
+                return 0
+            v = ref["roundtrip_tokens_per_s"]
+            print(json.dumps({
+                "impl": "reference", "metric": "sustained round-trip tokens/s over a 1000-step dynamic stream; "
+                "workload imbalance", "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": ref["steps"],
+                "warmup": 0, "ms_per_step": 1000 * ref["roundtrip_s_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": "C5: 1000-step dynamic stream"},
+                "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": ref["threads"], "kind": "reference",
+                                 "sample": f"{ref['full_steps']} full round trips sampled every 50th step"},
+                "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+            return 0
         r = run_reference(cfg, topology, args.steps, args.warmup, budget_s=120.0)
         if "unavailable" in r:
             print(json.dumps({"impl": "reference", "unavailable": r["unavailable"]}))
@@ -316,6 +448,8 @@ def main():
 
     if args.config == "c4":
         return run_c4(args)
+    if args.config == "c5":
+        return run_c5(args)
     if world_procs > 1:
         from paper_2508_06001_b200 import multigpu
         return multigpu.bench_main(args, cfg, topology, METRIC)

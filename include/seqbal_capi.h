@@ -210,6 +210,11 @@ SB_API sb_status sb_world_perturb(sb_world* w, sb_stream stream);
  * tensor 1, accumulated into *d_acc (device uint64, caller zeroes it). */
 SB_API sb_status sb_world_checksum(sb_world* w, uint64_t* d_acc, sb_stream stream);
 
+/* worlds_bitwise_equal (exchange.cpp:459-480) on the hosted ranks: adds the
+ * number of differing 16-byte words (+1 per rank/tensor whose shape differs)
+ * to *d_count (device uint64, caller zeroes it); 0 == bitwise equal. */
+SB_API sb_status sb_world_compare(sb_world* a, sb_world* b, uint64_t* d_count, sb_stream stream);
+
 /* ------------------------------------------------------------ exchange -- */
 /* route (exchange.cpp:127-194): every chunk of the current plan moves to its
  * target rank, packed in receive order; out-of-place from `src` to `dst`.
@@ -250,6 +255,82 @@ SB_API sb_status sb_world_write_rank(sb_world* w, int tensor, int rank, const vo
                                      sb_stream stream);
 /* Current per-rank rows/pitch as host arrays (synchronises). */
 SB_API sb_status sb_world_shape(sb_world* w, int tensor, int64_t* rows, int64_t* pitch, sb_stream stream);
+
+/* ------------------------------------- upstream generator (data_sim) -- */
+/* A sharding-group scenario: g{G}b{B}i{R}f{F}s{S} data streams
+ * (parse_data_code, data_sim.cpp:39-76 -- same grammar, ParseError messages
+ * and byte offsets), a scenario file (parse_scenario, :95-129) or a preset
+ * (:152-170).  group_size 0 = the sum of the streams' GPU counts. */
+typedef struct sb_scenario sb_scenario;
+SB_API sb_status sb_scenario_create(const char* const* codes, int n_codes, int group_size, sb_scenario** out);
+SB_API sb_status sb_scenario_parse(const char* text, sb_scenario** out);
+SB_API sb_status sb_scenario_preset(const char* name, sb_scenario** out);
+SB_API sb_status sb_scenario_destroy(sb_scenario* sc);
+/* specs5 (optional): n_streams x {gpus, batch, resolution, frames, smooth}. */
+SB_API sb_status sb_scenario_info(const sb_scenario* sc, int* group_size, int* n_streams, int32_t* specs5);
+
+/* K scenarios on the device for a world of `world` ranks: step s draws
+ * every rank's batch from scenario s mod K with next_batch
+ * (data_sim.cpp:225-248) -- ids make_sample_id(step, rank, i), lengths
+ * text U[0,392] + visual_tokens(stream, aspect multiplier) -- bit-exactly.
+ * bounds: the largest sequence count / total rows any step can produce. */
+typedef struct sb_schedule sb_schedule;
+SB_API sb_status sb_schedule_create(const sb_scenario* const* scenarios, int K, int world, uint64_t seed,
+                                    sb_schedule** out);
+SB_API sb_status sb_schedule_destroy(sb_schedule* s);
+SB_API sb_status sb_schedule_bounds(const sb_schedule* s, int64_t* max_seqs, int64_t* max_rows);
+/* Writes the gathered metadata of step (step + (d_step ? *d_step : 0)):
+ * ids/lens in gather order and rank_off[world + 1].  One kernel. */
+SB_API sb_status sb_schedule_generate(const sb_schedule* s, int64_t step, const int64_t* d_step, uint64_t* d_ids,
+                                      int64_t* d_lens, int64_t* d_rank_off, sb_stream stream);
+
+/* ---------------------------------------------- step driver (simulator) -- */
+/* simulate_step (simulator.cpp:45-178) on the device path: generate the
+ * step's batches -> origin layout + witness payload -> plan_routing ->
+ * route -> pre_attn/post_attn (multi-GPU bags) -> reverse_route.  With
+ * verify, the reference's inline checks run on the device: content
+ * checksum conserved by route and pre_attn, post_attn(pre_attn(x)) == x
+ * bitwise, and a perturbed payload (block_perturbation) returns home
+ * bitwise.  The step index lives in device memory and advances per step,
+ * so sb_driver_step is graph-capturable; records land in a device ring of
+ * record_cap entries indexed by step. */
+enum {
+  SB_CHECK_ROUTE_CONSERVED = 1,
+  SB_CHECK_PRE_CONSERVED = 2,
+  SB_CHECK_POST_INVERTS_PRE = 4,
+  SB_CHECK_REVERSE_RESTORES = 8,
+  SB_CHECK_ALL = 15
+};
+typedef struct sb_step_record {
+  int64_t step;
+  int64_t tokens;
+  int64_t sequences;
+  int64_t chunks;
+  double wir;             /* BalanceReport::wir (metrics.cpp:20-31)            */
+  double max_over_mean;   /* max(per_gpu_workload) / mean                       */
+  double total_workload;  /* BalanceReport::total_workload                      */
+  uint64_t checksum;      /* content_checksum of the step's input (verify)      */
+  int32_t scenario;       /* s mod K                                            */
+  int32_t capacity_violations;
+  int32_t checks;         /* SB_CHECK_* bits that held (verify)                 */
+  int32_t verified;
+} sb_step_record;
+typedef struct sb_driver sb_driver;
+SB_API sb_status sb_driver_create(sb_planner* p, const sb_schedule* s, int n_heads, int64_t payload_row_bytes,
+                                  int verify, int64_t record_cap, sb_driver** out);
+SB_API sb_status sb_driver_destroy(sb_driver* d);
+SB_API sb_status sb_driver_set_step(sb_driver* d, int64_t step, sb_stream stream);  /* synchronises */
+SB_API sb_status sb_driver_step(sb_driver* d, sb_stream stream);
+SB_API sb_status sb_driver_run(sb_driver* d, int64_t n_steps, sb_stream stream);
+/* next step index, steps run since set_step, steps whose checks failed (synchronises). */
+SB_API sb_status sb_driver_progress(sb_driver* d, int64_t* next_step, int64_t* steps_run, int64_t* failed,
+                                    sb_stream stream);
+SB_API sb_status sb_driver_records(sb_driver* d, sb_step_record* host, int64_t capacity, int64_t* n_out,
+                                   sb_stream stream);
+/* which: 0 origin (A), 1 routed (B), 2 Ulysses (C), 3 post_attn (D), 4 returned (E). */
+SB_API sb_status sb_driver_world(const sb_driver* d, int which, sb_world** out);
+SB_API sb_status sb_driver_meta(const sb_driver* d, const uint64_t** ids, const int64_t** lens,
+                                const int64_t** rank_off);
 
 /* ------------------------------------- host-buffer drop-in entry points -- */
 /* assign_to_bags (balancer.hpp:30-31, balancer.cpp:15-64) on caller

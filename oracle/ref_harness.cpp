@@ -439,17 +439,177 @@ int cmd_plan_bench() {
   return 0;
 }
 
+// Scenario (sharding-group) config from JSON: {"codes": [...], "group_size": G}
+// (group_size defaults to the sum of the streams' GPU counts), {"preset":
+// name} or {"text": scenario-file text} (data_sim.cpp:95-165).
+ShardingGroupConfig scenario_from(const json& j) {
+  if (j.contains("preset")) return scenario_preset(j.at("preset").get<std::string>());
+  if (j.contains("text")) {
+    std::istringstream in(j.at("text").get<std::string>());
+    return parse_scenario(in);
+  }
+  ShardingGroupConfig cfg;
+  int sum = 0;
+  for (const auto& c : j.at("codes")) {
+    cfg.streams.push_back(parse_data_code(c.get<std::string>()));
+    sum += cfg.streams.back().gpus;
+  }
+  cfg.group_size = j.value("group_size", sum);
+  cfg.validate();
+  return cfg;
+}
+
+// Upstream generator goldens: next_batch per rank for several steps, and the
+// parser's verdict (ParseError offset / ConfigError) on data codes.
+int cmd_batches() {
+  std::stringstream ss;
+  ss << std::cin.rdbuf();
+  const json c = json::parse(ss.str());
+  json out;
+  out["cases"] = json::array();
+  for (const auto& cs : c.value("cases", json::array())) {
+    const ShardingGroupConfig cfg = scenario_from(cs);
+    const int world = cs.at("world");
+    const std::uint64_t seed = cs.at("seed");
+    json jc;
+    jc["group_size"] = cfg.group_size;
+    jc["streams"] = json::array();
+    for (const auto& st : cfg.streams) jc["streams"].push_back(format_data_code(st));
+    jc["steps"] = json::array();
+    for (const auto& stv : cs.at("steps")) {
+      const std::int64_t step = stv.get<std::int64_t>();
+      json js;
+      js["step"] = step;
+      js["ranks"] = json::array();
+      for (int r = 0; r < world; ++r) {
+        json jr = json::array();
+        for (const SampleMeta& m : next_batch(cfg, r, step, seed)) jr.push_back({m.sample_id, m.text_len, m.visual_len});
+        js["ranks"].push_back(jr);
+      }
+      jc["steps"].push_back(js);
+    }
+    out["cases"].push_back(jc);
+  }
+  out["parse"] = json::array();
+  for (const auto& code : c.value("parse", json::array())) {
+    json jp;
+    jp["code"] = code;
+    try {
+      jp["format"] = format_data_code(parse_data_code(code.get<std::string>()));
+    } catch (const ParseError& e) {
+      jp["error"] = "ParseError";
+      jp["offset"] = e.offset();
+      jp["what"] = e.what();
+    }
+    out["parse"].push_back(jp);
+  }
+  std::cout << out.dump() << "\n";
+  return 0;
+}
+
+// C5 dynamic stream on the reference: step s draws every rank's batch from
+// scenario s mod K (next_batch, seed), plans it (plan_routing, timed each
+// step) and, every `full_every` steps while the budget lasts, runs the full
+// data path (make_world untimed; route + pre/post_attn per multi-GPU bag +
+// reverse_route timed, Exec::Parallel).  Emits per-step WIR / max-over-mean
+// bits (golden for the device driver) and the timings (CPU baseline).
+int cmd_stream() {
+  std::stringstream ss;
+  ss << std::cin.rdbuf();
+  const json c = json::parse(ss.str());
+  const int world = c.at("world");
+  const WorkloadModel model = model_from(c.value("model", json::object()));
+  const WorldLayout layout = replicate(parse_topology(c.at("topology").get<std::string>()), world);
+  std::vector<ShardingGroupConfig> scen;
+  for (const auto& j : c.at("scenarios")) scen.push_back(scenario_from(j));
+  const std::uint64_t seed = c.at("seed");
+  const std::int64_t first = c.value("first_step", 0);
+  const std::int64_t steps = c.at("steps");
+  const int full_every = c.value("full_every", 50);
+  const int width = c.value("payload_width", 768);
+  const double budget_s = c.value("budget_s", 1e30);
+  const Exec exec = Exec::Parallel;
+  json per = json::array();
+  double t_plan = 0, t_full = 0;
+  std::int64_t full_tokens = 0, full_steps = 0, tokens_all = 0;
+  const double t_begin = now_s();
+  std::int64_t done = 0;
+  for (std::int64_t s = first; s < first + steps; ++s) {
+    if (s > first && now_s() - t_begin > budget_s) break;
+    const ShardingGroupConfig& cfg = scen[static_cast<std::size_t>(s % static_cast<std::int64_t>(scen.size()))];
+    std::vector<std::vector<SampleMeta>> batches(world);
+    for (int r = 0; r < world; ++r) batches[r] = next_batch(cfg, r, s, seed);
+    const auto info = gather_sequence_info(batches);
+    std::int64_t tokens = 0, nseq = 0;
+    for (const auto& r : info)
+      for (const auto& q : r) {
+        tokens += q.length;
+        ++nseq;
+      }
+    const double a = now_s();
+    const PlanResult pr = plan_routing(info, model, layout);
+    t_plan += now_s() - a;
+    tokens_all += tokens;
+    double mx = 0, sum = 0;
+    for (double v : pr.report.per_gpu_workload) {
+      mx = std::max(mx, v);
+      sum += v;
+    }
+    json js;
+    js["step"] = s;
+    js["tokens"] = tokens;
+    js["sequences"] = nseq;
+    js["chunks"] = pr.plan.chunks.size();
+    js["wir"] = dbits(pr.report.wir);
+    js["total_workload"] = dbits(pr.report.total_workload);
+    js["violations"] = pr.report.capacity_violations;
+    js["max_over_mean"] = sum > 0 ? mx / (sum / static_cast<double>(world)) : 1.0;
+    per.push_back(js);
+    if (full_every > 0 && (s - first) % full_every == 0 && now_s() - t_begin <= budget_s) {
+      const World w0 = make_world(batches, width, model.shape.n_heads);
+      const double b = now_s();
+      World routed = route(w0, pr.plan, exec);
+      for (int rep = 0; rep < layout.num_replicas(); ++rep)
+        for (const auto& ub : layout.unit.bags) {
+          if (ub.size() < 2) continue;
+          const ComputeBag bag = global_bag(layout, rep, ub.bag_id);
+          pre_attn(routed, bag, exec);
+          post_attn(routed, bag, exec);
+        }
+      World back = reverse_route(routed, pr.plan, exec);
+      t_full += now_s() - b;
+      full_tokens += tokens;
+      ++full_steps;
+      if (back.ranks.size() != w0.ranks.size()) return 2;
+    }
+    ++done;
+  }
+  json out;
+  out["steps"] = done;
+  out["per_step"] = per;
+  out["plan_s_per_step"] = done ? t_plan / static_cast<double>(done) : 0.0;
+  out["tokens_per_step"] = done ? static_cast<double>(tokens_all) / static_cast<double>(done) : 0.0;
+  out["full_steps"] = full_steps;
+  out["roundtrip_tokens_per_s"] = t_full > 0 ? static_cast<double>(full_tokens) / t_full : 0.0;
+  out["roundtrip_s_per_step"] = full_steps ? t_full / static_cast<double>(full_steps) : 0.0;
+  out["threads"] = omp_get_max_threads();
+  std::cout << out.dump() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench < json\n");
+    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench|batches|stream < json\n");
     return 1;
   }
   try {
     if (std::strcmp(argv[1], "dump") == 0) return cmd_dump();
     if (std::strcmp(argv[1], "bench") == 0) return cmd_bench();
     if (std::strcmp(argv[1], "plan_bench") == 0) return cmd_plan_bench();
+    if (std::strcmp(argv[1], "batches") == 0) return cmd_batches();
+    if (std::strcmp(argv[1], "stream") == 0) return cmd_stream();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_harness: %s\n", e.what());
     return 3;

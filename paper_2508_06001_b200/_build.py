@@ -23,7 +23,7 @@ INCLUDE = os.path.join(ROOT, "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-CUDA_SOURCES = ["planner.cu", "exchange.cu", "peer.cu"]
+CUDA_SOURCES = ["planner.cu", "exchange.cu", "peer.cu", "stream.cu"]
 HOST_SOURCES = ["host/seqbal_api.cpp"]
 
 

@@ -132,7 +132,37 @@ _SIGS = {
     "sb_barrier_buffer": (C.c_int, [C.c_void_p] * 3),
     "sb_barrier_set_peers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "sb_barrier_wait": (C.c_int, [C.c_void_p] * 2),
+    "sb_world_compare": (C.c_int, [C.c_void_p] * 4),
+    "sb_scenario_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "sb_scenario_parse": (C.c_int, [C.c_char_p, C.c_void_p]),
+    "sb_scenario_preset": (C.c_int, [C.c_char_p, C.c_void_p]),
+    "sb_scenario_destroy": (C.c_int, [C.c_void_p]),
+    "sb_scenario_info": (C.c_int, [C.c_void_p] * 4),
+    "sb_schedule_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p]),
+    "sb_schedule_destroy": (C.c_int, [C.c_void_p]),
+    "sb_schedule_bounds": (C.c_int, [C.c_void_p] * 3),
+    "sb_schedule_generate": (C.c_int, [C.c_void_p, C.c_int64] + [C.c_void_p] * 5),
+    "sb_driver_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_int64, C.c_void_p]),
+    "sb_driver_destroy": (C.c_int, [C.c_void_p]),
+    "sb_driver_set_step": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "sb_driver_step": (C.c_int, [C.c_void_p] * 2),
+    "sb_driver_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "sb_driver_progress": (C.c_int, [C.c_void_p] * 5),
+    "sb_driver_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "sb_driver_world": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "sb_driver_meta": (C.c_int, [C.c_void_p] * 4),
 }
+
+
+class StepRecord(C.Structure):
+    """sb_step_record (include/seqbal_capi.h)."""
+    _fields_ = [("step", C.c_int64), ("tokens", C.c_int64), ("sequences", C.c_int64), ("chunks", C.c_int64),
+                ("wir", C.c_double), ("max_over_mean", C.c_double), ("total_workload", C.c_double),
+                ("checksum", C.c_uint64), ("scenario", C.c_int32), ("capacity_violations", C.c_int32),
+                ("checks", C.c_int32), ("verified", C.c_int32)]
+
+
+SB_CHECK_ALL = 15
 
 
 def exported_symbols() -> list[str]:

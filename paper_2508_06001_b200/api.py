@@ -17,7 +17,7 @@ from . import _capi
 from ._capi import ConfigError, ParseError, call
 
 __all__ = ["Topology", "parse_topology", "Model", "Planner", "World", "DeviceMeta", "HostPlan",
-           "route", "reverse_route", "pre_attn", "post_attn", "kernel_launches"]
+           "route", "reverse_route", "pre_attn", "post_attn", "kernel_launches", "Scenario", "Schedule", "Driver"]
 
 
 def _torch():
@@ -126,6 +126,28 @@ class DeviceMeta:
         self.rank_off = torch.as_tensor(np.asarray(rank_off, np.int64), device=dev)
         self.world = len(rank_off) - 1
         self.n = int(rank_off[-1])
+
+    @classmethod
+    def empty(cls, capacity: int, world: int, device=None):
+        """Device buffers for up to `capacity` sequences over `world` ranks
+        (filled by Schedule.generate)."""
+        return cls(np.zeros(0, np.uint64), np.zeros(0, np.int64), np.zeros(world + 1, np.int64), device)._grow(
+            capacity)
+
+    def _grow(self, capacity):
+        torch = _torch()
+        n = max(capacity, 1)
+        self.ids = torch.zeros(n, dtype=torch.int64, device=self.ids.device)
+        self.lens = torch.zeros(n, dtype=torch.int64, device=self.lens.device)
+        return self
+
+    def to_lists(self):
+        """(ids, lens) per rank, host numpy (synchronises)."""
+        off = self.rank_off.cpu().numpy()
+        ids = self.ids.cpu().numpy().view(np.uint64)
+        lens = self.lens.cpu().numpy()
+        return ([ids[off[r]:off[r + 1]].copy() for r in range(len(off) - 1)],
+                [lens[off[r]:off[r + 1]].copy() for r in range(len(off) - 1)])
 
     @classmethod
     def from_lists(cls, ids_per_rank, lens_per_rank, device=None):
@@ -327,7 +349,7 @@ class World:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and getattr(self, "_owned", True):
             _capi.load().sb_world_destroy(h)
             self._h = None
 
@@ -362,6 +384,14 @@ class World:
 
     def status(self, stream=None):
         call("sb_world_status", self._h, _stream(stream))
+
+    def compare(self, other: "World", stream=None) -> int:
+        """worlds_bitwise_equal (exchange.cpp:459-480): number of differing
+        16-byte words (0 == bitwise equal)."""
+        torch = _torch()
+        acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+        call("sb_world_compare", self._h, other.handle, C.c_void_p(acc.data_ptr()), _stream(stream))
+        return int(acc.item())
 
     def shape(self, t: int = 0, stream=None):
         W = self.world_size
@@ -413,3 +443,125 @@ def post_attn(planner: Planner, src: World, dst: World, stream=None):
     """post_attn (exchange.cpp:333-436) for every multi-GPU bag at once."""
     call("sb_post_attn", planner.handle, src.handle, dst.handle, _stream(stream))
     return dst
+
+
+# -------------------------------------------------- upstream generator
+class Scenario:
+    """ShardingGroupConfig (data_sim.hpp:46-51): data codes, a scenario file's
+    text (parse_scenario) or a preset name.  Parsing is host-side and raises
+    the reference's ParseError / ConfigError with its messages."""
+
+    def __init__(self, codes=None, group_size: int = 0, text: str | None = None, preset: str | None = None):
+        h = C.c_void_p()
+        if preset is not None:
+            call("sb_scenario_preset", preset.encode(), C.byref(h))
+        elif text is not None:
+            call("sb_scenario_parse", text.encode(), C.byref(h))
+        else:
+            enc = [c.encode() for c in (codes or [])]
+            arr = (C.c_char_p * max(1, len(enc)))(*enc)
+            call("sb_scenario_create", arr, len(enc), int(group_size), C.byref(h))
+        self._h = h
+        g, n = C.c_int(), C.c_int()
+        call("sb_scenario_info", h, C.byref(g), C.byref(n), None)
+        spec = np.zeros(5 * max(1, n.value), np.int32)
+        call("sb_scenario_info", h, None, None, spec.ctypes.data)
+        self.group_size = g.value
+        self.streams = [tuple(int(x) for x in spec[5 * i:5 * i + 5]) for i in range(n.value)]
+
+    def codes(self):
+        return [f"g{g}b{b}i{r}f{f}s{s}" for g, b, r, f, s in self.streams]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _capi.load().sb_scenario_destroy(h)
+            self._h = None
+
+
+class Schedule:
+    """K scenarios on the device: step s draws every rank's batch from
+    scenario s mod K (next_batch, data_sim.cpp:225-248) with one kernel."""
+
+    def __init__(self, scenarios, world: int, seed: int):
+        _torch()
+        self.scenarios = [x if isinstance(x, Scenario) else Scenario(x) for x in scenarios]
+        arr = (C.c_void_p * len(self.scenarios))(*[x._h.value for x in self.scenarios])
+        h = C.c_void_p()
+        call("sb_schedule_create", arr, len(self.scenarios), int(world), C.c_uint64(seed), C.byref(h))
+        self._h = h
+        self.world = world
+        self.seed = seed
+        ms, mr = C.c_int64(), C.c_int64()
+        call("sb_schedule_bounds", h, C.byref(ms), C.byref(mr))
+        self.max_seqs, self.max_rows = ms.value, mr.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _capi.load().sb_schedule_destroy(h)
+            self._h = None
+
+    def generate(self, step: int, meta: DeviceMeta | None = None, stream=None) -> DeviceMeta:
+        meta = meta or DeviceMeta.empty(self.max_seqs, self.world)
+        ids, lens, off = meta.ptrs()
+        call("sb_schedule_generate", self._h, int(step), None, ids, lens, off, _stream(stream))
+        meta.n = None  # device-resident; see rank_off
+        return meta
+
+
+class Driver:
+    """simulate_step (simulator.cpp:45-178) on the device path; one step =
+    generate -> origin layout + witness -> plan -> route -> Ulysses pre/post
+    -> reverse_route, with the reference's inline checks when verify."""
+
+    def __init__(self, planner: Planner, schedule: Schedule, n_heads: int = 24, payload_row_bytes: int = 6144,
+                 verify: bool = True, record_cap: int = 1024):
+        h = C.c_void_p()
+        call("sb_driver_create", planner.handle, schedule._h, int(n_heads), int(payload_row_bytes), int(verify),
+             int(record_cap), C.byref(h))
+        self._h = h
+        self.planner, self.schedule = planner, schedule
+        self.record_cap = record_cap
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _capi.load().sb_driver_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_step(self, step: int, stream=None):
+        call("sb_driver_set_step", self._h, int(step), _stream(stream))
+
+    def step(self, stream=None):
+        call("sb_driver_step", self._h, _stream(stream))
+
+    def run(self, n: int, stream=None):
+        call("sb_driver_run", self._h, int(n), _stream(stream))
+
+    def progress(self, stream=None):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        call("sb_driver_progress", self._h, C.byref(a), C.byref(b), C.byref(c), _stream(stream))
+        return {"next_step": a.value, "steps_run": b.value, "failed": c.value}
+
+    def records(self, stream=None):
+        buf = (_capi.StepRecord * self.record_cap)()
+        n = C.c_int64()
+        call("sb_driver_records", self._h, buf, self.record_cap, C.byref(n), _stream(stream))
+        return [{f: getattr(r, f) for f, _ in _capi.StepRecord._fields_} for r in buf]
+
+    def world(self, which: int) -> "World":
+        h = C.c_void_p()
+        call("sb_driver_world", self._h, int(which), C.byref(h))
+        w = World.__new__(World)  # borrowed handle: the driver owns and frees it
+        w._h = h
+        w._owned = False
+        w._keep = self
+        w.world_size = w.n_local = self.schedule.world
+        w.first_local = 0
+        w.T = 2
+        return w

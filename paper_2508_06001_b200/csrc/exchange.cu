@@ -721,6 +721,41 @@ __global__ void k_checksum(WorldArgs w, unsigned long long* acc) {
   if (lane == 0 && sum) atomicAdd(acc, sum);
 }
 
+// worlds_bitwise_equal (exchange.cpp:459-480) on hosted ranks: per rank the
+// row counts must match, then every byte of every tensor (16-B words).
+// Adds the number of differing words (+1 per rank whose rows differ) to
+// *count; 0 means bitwise equal.
+__global__ void k_world_compare(WorldArgs a, WorldArgs b, TensorInfo ti, unsigned long long* count) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long bad = 0;
+  for (int lr = 0; lr < a.n_local; ++lr) {
+    const int r = a.first_local + lr;
+    const int64_t rows = a.rows[r];
+    if (rows != b.rows[r]) {
+      if (tid == 0) ++bad;
+      continue;
+    }
+    for (int t = 0; t < a.T; ++t) {
+      const int64_t ap = a.pitch[t * a.W + r], bp = b.pitch[t * b.W + r];
+      if (ap != bp) {
+        if (tid == 0) ++bad;
+        continue;
+      }
+      const int64_t words = rows * ap / 16;  // row bytes are multiples of 16 on the compared layouts
+      const int4* x = reinterpret_cast<const int4*>(a.base[t * a.W + r]);
+      const int4* y = reinterpret_cast<const int4*>(b.base[t * b.W + r]);
+      for (int64_t i = tid; i < words; i += nthreads) {
+        const int4 u = x[i], v = y[i];
+        bad += (u.x != v.x) | (u.y != v.y) | (u.z != v.z) | (u.w != v.w);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+
 static void select_slot(sb_planner* p, int slot) {
   if (slot < 0 || slot >= sb_planner::kSlots) throw Error{SB_ERR_CONFIG, "exchange slot out of range"};
   p->cur_slot = slot;
@@ -1014,6 +1049,20 @@ extern "C" sb_status sb_world_perturb(sb_world* w, sb_stream stream) {
   SB_API_BEGIN
   if (!w) throw Error{SB_ERR_CONFIG, "null world"};
   sb::k_perturb<<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w));
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_compare(sb_world* a, sb_world* b, uint64_t* d_count, sb_stream stream) {
+  SB_API_BEGIN
+  if (!a || !b || !d_count) throw Error{SB_ERR_CONFIG, "sb_world_compare: null argument"};
+  if (a->W != b->W || a->T != b->T || a->n_local != b->n_local || a->first_local != b->first_local)
+    throw Error{SB_ERR_CONFIG, "sb_world_compare: worlds of different shape"};
+  for (int t = 0; t < a->T; ++t)
+    if (a->row_bytes[t] % 16 != 0) throw Error{SB_ERR_CONFIG, "sb_world_compare: row bytes must be multiples of 16"};
+  sb::k_world_compare<<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(
+      sb::wargs(a), sb::wargs(b), sb::tinfo(a), reinterpret_cast<unsigned long long*>(d_count));
   SB_CHECK_LAUNCH();
   sb::count_launch();
   SB_API_END
