@@ -309,20 +309,22 @@ def run_c5(args):
     drv.set_step(0)
     for _ in range(max(3, args.warmup)):
         drv.step()
+    l0 = sb.kernel_launches()
+    drv.step()
+    launches_per_step = sb.kernel_launches() - l0  # graph replays run exactly these kernels
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         drv.step()
     drv.set_step(0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = sb.kernel_launches()
     with ClockSampler() as clk:
         ev0.record(stream)
         for _ in range(steps):
             g.replay()
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = sb.kernel_launches() - launches0
+    launches = launches_per_step * steps
     ms = ev0.elapsed_time(ev1)
     recs = drv.records()
     prog = drv.progress()
@@ -361,7 +363,7 @@ def run_c5(args):
         "verify": {"steps": vprog["steps_run"], "failed_checks": vprog["failed"], "plans_identical": same_plans,
                    "checks": "route + pre_attn conserve content_checksum; post_attn(pre_attn(x)) == x; perturbed "
                              "payload returns home bitwise (simulator.cpp:106-159)", "wall_s": verify_s},
-        "gpu_launches": int(launches), "clocks": clk.summary(),
+        "gpu_launches": int(launches), "gpu_launches_per_step": int(launches_per_step), "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
         ref, err = run_reference_stream(steps, budget_s=args.cpu_budget_s)

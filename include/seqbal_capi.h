@@ -256,6 +256,26 @@ SB_API sb_status sb_world_write_rank(sb_world* w, int tensor, int rank, const vo
 /* Current per-rank rows/pitch as host arrays (synchronises). */
 SB_API sb_status sb_world_shape(sb_world* w, int tensor, int64_t* rows, int64_t* pitch, sb_stream stream);
 
+/* ------------------------------------------- uniform (T5) balancer -- */
+/* balance_uniform_items / reverse_uniform_plan (balancer.hpp:122-144,
+ * balancer.cpp:411-462) for identical-cost items: post-counts differ by at
+ * most 1, moves minimal, +1 slots to the largest counts (ties toward the
+ * lower rank), surpluses paired with deficits in rank order.  The plan is
+ * computed on the device from device counts[world]; sb_uniform_route moves
+ * the items (rows_per_item rows each, every tensor of the world) with the
+ * route copy engines: a surplus rank keeps its first final_count items and
+ * sends the rest in move order; a deficit rank appends received items in
+ * move order.  reverse != 0 sends every relocated item home. */
+typedef struct sb_uniform sb_uniform;
+SB_API sb_status sb_uniform_create(int world, sb_uniform** out);
+SB_API sb_status sb_uniform_destroy(sb_uniform* u);
+SB_API sb_status sb_uniform_plan(sb_uniform* u, const int64_t* d_counts, sb_stream stream);
+/* Synchronises; moves3 = n_moves x {src_rank, dst_rank, count} (<= 2*world). */
+SB_API sb_status sb_uniform_download(sb_uniform* u, int64_t* final_counts, int64_t* moves3, int64_t* n_moves,
+                                     int64_t* total_moved, sb_stream stream);
+SB_API sb_status sb_uniform_route(sb_uniform* u, int reverse, int64_t rows_per_item, sb_world* src, sb_world* dst,
+                                  sb_stream stream);
+
 /* ------------------------------------- upstream generator (data_sim) -- */
 /* A sharding-group scenario: g{G}b{B}i{R}f{F}s{S} data streams
  * (parse_data_code, data_sim.cpp:39-76 -- same grammar, ParseError messages

@@ -691,3 +691,56 @@ def ref_run(cmd: str, case: dict, timeout: float = 600) -> dict:
     if p.returncode != 0:
         raise RuntimeError(f"ref_harness {cmd} failed: {p.stderr.decode()[-500:]}")
     return json.loads(p.stdout)
+
+
+# ------------------------------------------------ uniform (T5) balancer
+def balance_uniform_items(counts):
+    """balance_uniform_items (balancer.cpp:411-448): final counts differ by at
+    most one, the +1 slots go to the largest counts (std::stable_sort by
+    count desc, ties toward the lower rank), surpluses paired with deficits
+    in rank order.  Returns (final_counts, moves[(src, dst, count)], total)."""
+    n = len(counts)
+    if n == 0:
+        return [], [], 0
+    if any(c < 0 for c in counts):
+        raise ValueError("balance_uniform_items: negative count")
+    total = sum(counts)
+    base, rem = divmod(total, n)
+    order = sorted(range(n), key=lambda r: -counts[r])  # Python's sort is stable
+    final = [base] * n
+    for i in range(rem):
+        final[order[i]] += 1
+    surplus = [[r, counts[r] - final[r]] for r in range(n) if counts[r] > final[r]]
+    deficit = [[r, final[r] - counts[r]] for r in range(n) if counts[r] < final[r]]
+    moves, moved, si, di = [], 0, 0, 0
+    while si < len(surplus) and di < len(deficit):
+        m = min(surplus[si][1], deficit[di][1])
+        moves.append((surplus[si][0], deficit[di][0], m))
+        moved += m
+        surplus[si][1] -= m
+        deficit[di][1] -= m
+        if surplus[si][1] == 0:
+            si += 1
+        if deficit[di][1] == 0:
+            di += 1
+    return final, moves, moved
+
+
+def reverse_uniform_plan(moves):
+    """reverse_uniform_plan (balancer.cpp:450-460): every move reversed, same order."""
+    return [(d, s, c) for s, d, c in moves]
+
+
+def uniform_item_layout(counts, final, moves):
+    """Item placement realised by sb_uniform_route (our documented layout;
+    the reference defines counts and moves only): rank r keeps its first
+    min(count, final) items; a surplus rank's trailing items leave in move
+    order; a deficit rank appends received items in move order.  Returns,
+    per destination rank, the (origin rank, origin item index) list."""
+    out = [[(r, i) for i in range(min(counts[r], final[r]))] for r in range(len(counts))]
+    sent = [0] * len(counts)
+    for s, d, c in moves:
+        for k in range(c):
+            out[d].append((s, final[s] + sent[s] + k))
+        sent[s] += c
+    return out

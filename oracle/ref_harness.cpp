@@ -597,11 +597,40 @@ int cmd_stream() {
   return 0;
 }
 
+// balance_uniform_items / reverse_uniform_plan goldens: {"counts": [[...], ...]}
+int cmd_uniform() {
+  std::stringstream ss;
+  ss << std::cin.rdbuf();
+  const json c = json::parse(ss.str());
+  json out = json::array();
+  for (const auto& cv : c.at("counts")) {
+    const std::vector<std::int64_t> counts = cv.get<std::vector<std::int64_t>>();
+    json r;
+    r["counts"] = counts;
+    try {
+      const UniformPlan p = balance_uniform_items(counts);
+      r["final_counts"] = p.final_counts;
+      r["total_moved"] = p.total_moved;
+      r["moves"] = json::array();
+      for (const UniformMove& m : p.moves) r["moves"].push_back({m.src_rank, m.dst_rank, m.count});
+      const UniformPlan q = reverse_uniform_plan(p, counts);
+      r["reverse_moves"] = json::array();
+      for (const UniformMove& m : q.moves) r["reverse_moves"].push_back({m.src_rank, m.dst_rank, m.count});
+      r["reverse_final_counts"] = q.final_counts;
+    } catch (const ConfigError& e) {
+      r["error"] = std::string("ConfigError: ") + e.what();
+    }
+    out.push_back(r);
+  }
+  std::cout << out.dump() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench|batches|stream < json\n");
+    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench|batches|stream|uniform < json\n");
     return 1;
   }
   try {
@@ -610,6 +639,7 @@ int main(int argc, char** argv) {
     if (std::strcmp(argv[1], "plan_bench") == 0) return cmd_plan_bench();
     if (std::strcmp(argv[1], "batches") == 0) return cmd_batches();
     if (std::strcmp(argv[1], "stream") == 0) return cmd_stream();
+    if (std::strcmp(argv[1], "uniform") == 0) return cmd_uniform();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_harness: %s\n", e.what());
     return 3;

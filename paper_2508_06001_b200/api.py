@@ -17,7 +17,8 @@ from . import _capi
 from ._capi import ConfigError, ParseError, call
 
 __all__ = ["Topology", "parse_topology", "Model", "Planner", "World", "DeviceMeta", "HostPlan",
-           "route", "reverse_route", "pre_attn", "post_attn", "kernel_launches", "Scenario", "Schedule", "Driver"]
+           "route", "reverse_route", "pre_attn", "post_attn", "kernel_launches", "Scenario", "Schedule", "Driver",
+           "UniformBalancer"]
 
 
 def _torch():
@@ -565,3 +566,44 @@ class Driver:
         w.first_local = 0
         w.T = 2
         return w
+
+
+# ------------------------------------------------ uniform (T5) balancer
+class UniformBalancer:
+    """balance_uniform_items / reverse_uniform_plan (balancer.cpp:411-462) on
+    the device, plus the item exchange (see sb_uniform_route)."""
+
+    def __init__(self, world: int):
+        _torch()
+        h = C.c_void_p()
+        call("sb_uniform_create", int(world), C.byref(h))
+        self._h = h
+        self.world = world
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _capi.load().sb_uniform_destroy(h)
+            self._h = None
+
+    def plan(self, counts, stream=None):
+        """counts: device int64 tensor [world] (or host sequence)."""
+        torch = _torch()
+        if not isinstance(counts, torch.Tensor):
+            counts = torch.as_tensor(np.asarray(counts, np.int64), device="cuda")
+        self._counts = counts
+        call("sb_uniform_plan", self._h, C.c_void_p(counts.data_ptr()), _stream(stream))
+        return self
+
+    def download(self, stream=None):
+        fin = np.zeros(self.world, np.int64)
+        mv = np.zeros(3 * 2 * self.world, np.int64)
+        n, tot = C.c_int64(), C.c_int64()
+        call("sb_uniform_download", self._h, fin.ctypes.data, mv.ctypes.data, C.byref(n), C.byref(tot),
+             _stream(stream))
+        moves = [tuple(int(x) for x in mv[3 * i:3 * i + 3]) for i in range(n.value)]
+        return {"final_counts": fin.tolist(), "moves": moves, "total_moved": tot.value}
+
+    def route(self, src: World, dst: World, rows_per_item: int = 1, reverse: bool = False, stream=None):
+        call("sb_uniform_route", self._h, int(reverse), int(rows_per_item), src.handle, dst.handle, _stream(stream))
+        return dst

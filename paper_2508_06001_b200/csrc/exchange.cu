@@ -830,6 +830,9 @@ static int ulysses_engine() {
 
 constexpr int64_t kFusedPrepMaxJobs = 1 << 16;  // single-CTA prep up to this many jobs
 
+static void launch_copy(SbJob* jobs, int64_t* piece_off, int64_t* n_jobs, cudaStream_t s, int fence_sys,
+                        bool tma_ok, int engine);
+
 static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys, bool tma_ok, int engine, bool pieces_done) {
   if (!pieces_done) {
     k_pieces<<<1, 1024, 0, s>>>(p->jobs, p->n_jobs, p->piece_off, p->n_jobs + 1);
@@ -852,6 +855,13 @@ static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys, bool tma_ok, 
     p->copy_used += 2;
     SB_CUDA(cudaEventRecord(e0, s));
   }
+  launch_copy(p->jobs, p->piece_off, p->n_jobs, s, fence_sys, tma_ok, engine);
+  if (e1) SB_CUDA(cudaEventRecord(e1, s));
+}
+
+// The copy engines over a prepared job list (pieces already scanned).
+static void launch_copy(SbJob* jobs, int64_t* piece_off, int64_t* n_jobs, cudaStream_t s, int fence_sys,
+                        bool tma_ok, int engine) {
   if (!fence_sys && tma_ok && engine == 1) {
     static bool attr = false;
     if (!attr) {
@@ -860,21 +870,20 @@ static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys, bool tma_ok, 
       attr = true;
     }
     copy_grid();
-    k_copy_tma<<<g_num_sms * 2, 32, kTmaSmem, s>>>(p->jobs, p->piece_off, p->n_jobs);
+    k_copy_tma<<<g_num_sms * 2, 32, kTmaSmem, s>>>(jobs, piece_off, n_jobs);
   } else if (engine == 2) {
-    k_copy<3><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+    k_copy<3><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
   } else {
     static int hint = -1;  // SEQBAL_COPY_HINT=0|1|2 (see ld_stream)
     if (hint < 0) {
       const char* v = getenv("SEQBAL_COPY_HINT");
       hint = v ? atoi(v) : 0;
     }
-    if (hint == 1) k_copy<1, 1><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
-    else if (hint == 2) k_copy<1, 2><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
-    else k_copy<1, 0><<<copy_grid(), kCopyThreads, 0, s>>>(p->jobs, p->piece_off, p->n_jobs, fence_sys);
+    if (hint == 1) k_copy<1, 1><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
+    else if (hint == 2) k_copy<1, 2><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
+    else k_copy<1, 0><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
   }
   SB_CHECK_LAUNCH();
-  if (e1) SB_CUDA(cudaEventRecord(e1, s));
   count_launch(1);
 }
 
@@ -1612,5 +1621,269 @@ extern "C" sb_status sb_apply_moves(sb_world* src, sb_world* dst, const sb_block
   SB_CHECK_LAUNCH();
   sb::count_launch(2);
   SB_CUDA(cudaStreamSynchronize(s));  // host job vector and staging are reused
+  SB_API_END
+}
+
+// =============================================== uniform (T5) balancer
+// balance_uniform_items / reverse_uniform_plan (balancer.cpp:411-462): the
+// appendix's balancer for identical-cost items (T5 text strings).  Plan on
+// the device (one CTA), then the items move with the same copy engines as
+// route.  The reference defines counts and moves only; the item layout the
+// exchange realises (documented in DESIGN.md): a surplus rank keeps its
+// first final_count items and sends the rest, in order, along its moves in
+// move order; a deficit rank appends what it receives after its own items in
+// move order.  The reverse exchange is the exact inverse.
+struct sb_uniform {
+  int W = 0;
+  int64_t* counts = nullptr;  // W   (copy of the planned counts)
+  int64_t* final_ = nullptr;  // W
+  int64_t* mv = nullptr;      // 5 * 2W: src, dst, count, src item offset, dst item offset
+  int64_t* hdr = nullptr;     // [0] moves, [1] total moved, [2] status
+  int64_t* rows = nullptr;    // 2W: destination / expected source rows of the current exchange
+  SbJob* jobs = nullptr;
+  int64_t* piece_off = nullptr;
+  int64_t* n_jobs = nullptr;  // [0] jobs, [1] bytes
+  int64_t job_cap = 0;
+};
+
+namespace sb {
+
+__global__ void __launch_bounds__(1024) k_uniform_plan(const int64_t* __restrict__ counts_in, int W, int64_t* counts,
+                                                       int64_t* fin, int64_t* mv, int64_t* hdr) {
+  __shared__ int64_t sh[33];
+  __shared__ int64_t s_base, s_rem;
+  int64_t local = 0;
+  int neg = 0;
+  for (int r = threadIdx.x; r < W; r += blockDim.x) {
+    const int64_t c = counts_in[r];
+    counts[r] = c;
+    neg |= c < 0;
+    local += c;
+  }
+  int64_t total;
+  block_excl_scan<int64_t>(local, sh, &total);
+  neg = __syncthreads_or(neg);
+  if (threadIdx.x == 0) {
+    s_base = total / W;
+    s_rem = total % W;
+    hdr[2] = neg;  // ConfigError: balance_uniform_items: negative count
+  }
+  __syncthreads();
+  // +1 slots to the largest counts, ties toward the lower rank
+  // (std::stable_sort by count desc): rank r's position in that order
+  for (int r = threadIdx.x; r < W; r += blockDim.x) {
+    const int64_t c = counts[r];
+    int pos = 0;
+    for (int q = 0; q < W; ++q) pos += (counts[q] > c) || (counts[q] == c && q < r);
+    fin[r] = s_base + (pos < s_rem ? 1 : 0);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  // pair surpluses with deficits in rank order (two cursors)
+  int si = 0, di = 0, n = 0;
+  int64_t moved_total = 0, s_left = 0, d_left = 0, s_sent = 0, d_got = 0;
+  auto next_s = [&](int from) {
+    for (int r = from; r < W; ++r)
+      if (counts[r] - fin[r] > 0) return r;
+    return W;
+  };
+  auto next_d = [&](int from) {
+    for (int r = from; r < W; ++r)
+      if (counts[r] - fin[r] < 0) return r;
+    return W;
+  };
+  si = next_s(0);
+  di = next_d(0);
+  if (si < W) s_left = counts[si] - fin[si];
+  if (di < W) d_left = fin[di] - counts[di];
+  while (si < W && di < W) {
+    const int64_t m = s_left < d_left ? s_left : d_left;
+    mv[5 * n + 0] = si;
+    mv[5 * n + 1] = di;
+    mv[5 * n + 2] = m;
+    mv[5 * n + 3] = fin[si] + s_sent;   // first item leaving si
+    mv[5 * n + 4] = counts[di] + d_got;  // first free slot on di
+    ++n;
+    moved_total += m;
+    s_left -= m;
+    d_left -= m;
+    s_sent += m;
+    d_got += m;
+    if (s_left == 0) {
+      si = next_s(si + 1);
+      s_sent = 0;
+      if (si < W) s_left = counts[si] - fin[si];
+    }
+    if (d_left == 0) {
+      di = next_d(di + 1);
+      d_got = 0;
+      if (di < W) d_left = fin[di] - counts[di];
+    }
+  }
+  hdr[0] = n;
+  hdr[1] = moved_total;
+}
+
+// Destination rows (items x rows_per_item) of the exchange and the rows the
+// source must hold.
+__global__ void k_uniform_rows(const int64_t* counts, const int64_t* fin, int W, int64_t rpi, int reverse,
+                               int64_t* rows) {
+  for (int r = threadIdx.x; r < W; r += blockDim.x) {
+    rows[r] = (reverse ? counts[r] : fin[r]) * rpi;   // destination
+    rows[W + r] = (reverse ? fin[r] : counts[r]) * rpi;  // expected source
+  }
+}
+
+__global__ void k_uniform_jobs(const int64_t* counts, const int64_t* fin, const int64_t* mv, const int64_t* hdr,
+                               int W, int64_t rpi, int reverse, WorldArgs s, WorldArgs d, TensorInfo ti, SbJob* jobs,
+                               int64_t* n_jobs) {
+  const int T = s.T;
+  const int64_t total = (int64_t)3 * W * T;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_jobs = total;
+  const bool bad = (*d.status & ST_MISMATCH) != 0;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x % T);
+    const int64_t e = x / T;
+    SbJob j;
+    j.src = j.dst = 0;
+    j.n_rows = 0;
+    j.width = ti.row_bytes[t];
+    int sr = 0, dr = 0;
+    int64_t srow = 0, drow = 0, n = 0;
+    if (e < W) {  // items that stay: the first min(count, final) of the rank
+      sr = dr = (int)e;
+      const int64_t keep = counts[e] < fin[e] ? counts[e] : fin[e];
+      n = keep * rpi;
+    } else if (e - W < hdr[0]) {
+      const int64_t* m = mv + 5 * (e - W);
+      if (!reverse) {
+        sr = (int)m[0];
+        dr = (int)m[1];
+        srow = m[3] * rpi;
+        drow = m[4] * rpi;
+      } else {
+        sr = (int)m[1];
+        dr = (int)m[0];
+        srow = m[4] * rpi;
+        drow = m[3] * rpi;
+      }
+      n = m[2] * rpi;
+    }
+    if (n > 0 && !bad && is_local(s, sr)) {
+      const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
+      j.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp);
+      j.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp);
+      j.n_rows = n;
+      j.spitch = sp;
+      j.dpitch = dp;
+    } else {
+      j.spitch = j.dpitch = j.width;
+    }
+    jobs[x] = j;
+  }
+}
+
+}  // namespace sb
+
+extern "C" sb_status sb_uniform_create(int world, sb_uniform** out) {
+  SB_API_BEGIN
+  if (!out || world < 1) throw Error{SB_ERR_CONFIG, "sb_uniform_create: world must be >= 1"};
+  *out = nullptr;
+  sb_uniform* u = new sb_uniform();
+  u->W = world;
+  try {
+    SB_CUDA(cudaMalloc(&u->counts, sizeof(int64_t) * world));
+    SB_CUDA(cudaMalloc(&u->final_, sizeof(int64_t) * world));
+    SB_CUDA(cudaMalloc(&u->mv, sizeof(int64_t) * 5 * 2 * world));
+    SB_CUDA(cudaMalloc(&u->hdr, sizeof(int64_t) * 3));
+    SB_CUDA(cudaMemset(u->hdr, 0, sizeof(int64_t) * 3));
+    SB_CUDA(cudaMalloc(&u->rows, sizeof(int64_t) * 2 * world));
+    SB_CUDA(cudaMalloc(&u->n_jobs, sizeof(int64_t) * 2));
+  } catch (...) {
+    sb_uniform_destroy(u);
+    throw;
+  }
+  *out = u;
+  SB_API_END
+}
+
+extern "C" sb_status sb_uniform_destroy(sb_uniform* u) {
+  if (!u) return SB_OK;
+  void* ptrs[] = {u->counts, u->final_, u->mv, u->hdr, u->rows, u->jobs, u->piece_off, u->n_jobs};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete u;
+  return SB_OK;
+}
+
+extern "C" sb_status sb_uniform_plan(sb_uniform* u, const int64_t* d_counts, sb_stream stream) {
+  SB_API_BEGIN
+  if (!u || !d_counts) throw Error{SB_ERR_CONFIG, "sb_uniform_plan: null argument"};
+  sb::k_uniform_plan<<<1, 1024, 0, (cudaStream_t)stream>>>(d_counts, u->W, u->counts, u->final_, u->mv, u->hdr);
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
+  SB_API_END
+}
+
+extern "C" sb_status sb_uniform_download(sb_uniform* u, int64_t* final_counts, int64_t* moves3, int64_t* n_moves,
+                                         int64_t* total_moved, sb_stream stream) {
+  SB_API_BEGIN
+  if (!u) throw Error{SB_ERR_CONFIG, "null uniform plan"};
+  cudaStream_t s = (cudaStream_t)stream;
+  SB_CUDA(cudaStreamSynchronize(s));
+  int64_t hdr[3];
+  SB_CUDA(cudaMemcpy(hdr, u->hdr, sizeof hdr, cudaMemcpyDeviceToHost));
+  if (hdr[2]) throw Error{SB_ERR_CONFIG, "balance_uniform_items: negative count"};
+  if (final_counts) SB_CUDA(cudaMemcpy(final_counts, u->final_, sizeof(int64_t) * u->W, cudaMemcpyDeviceToHost));
+  if (moves3 && hdr[0] > 0) {
+    std::vector<int64_t> mv((size_t)(5 * hdr[0]));
+    SB_CUDA(cudaMemcpy(mv.data(), u->mv, sizeof(int64_t) * mv.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < hdr[0]; ++i)
+      for (int k = 0; k < 3; ++k) moves3[3 * i + k] = mv[(size_t)(5 * i + k)];
+  }
+  if (n_moves) *n_moves = hdr[0];
+  if (total_moved) *total_moved = hdr[1];
+  SB_API_END
+}
+
+// Moves the items of the current uniform plan: forward (reverse == 0) from
+// the counts layout to the balanced one, or back (reverse_uniform_plan).
+// Every rank's tensor rows are items x rows_per_item.
+extern "C" sb_status sb_uniform_route(sb_uniform* u, int reverse, int64_t rows_per_item, sb_world* src, sb_world* dst,
+                                      sb_stream stream) {
+  SB_API_BEGIN
+  if (!u || !src || !dst) throw Error{SB_ERR_CONFIG, "sb_uniform_route: null argument"};
+  if (src == dst) throw Error{SB_ERR_CONFIG, "sb_uniform_route is out-of-place: src and dst must differ"};
+  if (rows_per_item < 1) throw Error{SB_ERR_CONFIG, "rows_per_item must be >= 1"};
+  if (src->W != u->W || dst->W != u->W || src->T != dst->T)
+    throw Error{SB_ERR_CONFIG, "sb_uniform_route: world shape differs from the plan"};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t cap = (int64_t)3 * u->W * src->T;
+  if (cap > u->job_cap) {
+    if (u->jobs) cudaFree(u->jobs);
+    if (u->piece_off) cudaFree(u->piece_off);
+    u->jobs = nullptr;
+    u->piece_off = nullptr;
+    SB_CUDA(cudaMalloc(&u->jobs, sizeof(SbJob) * (size_t)cap));
+    SB_CUDA(cudaMalloc(&u->piece_off, sizeof(int64_t) * (size_t)(cap + 1)));
+    u->job_cap = cap;
+  }
+  sb::k_uniform_rows<<<1, 256, 0, s>>>(u->counts, u->final_, u->W, rows_per_item, reverse ? 1 : 0, u->rows);
+  SB_CHECK_LAUNCH();
+  sb::LayoutPlan lp{};
+  lp.rows_src = u->rows;
+  lp.expect_rows = u->rows + u->W;
+  sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
+  SB_CHECK_LAUNCH();
+  sb::k_uniform_jobs<<<std::max<int64_t>(1, std::min<int64_t>(148, (cap + 255) / 256)), 256, 0, s>>>(
+      u->counts, u->final_, u->mv, u->hdr, u->W, rows_per_item, reverse ? 1 : 0, sb::wargs(src), sb::wargs(dst),
+      sb::tinfo(src), u->jobs, u->n_jobs);
+  SB_CHECK_LAUNCH();
+  sb::k_pieces<<<1, 1024, 0, s>>>(u->jobs, u->n_jobs, u->piece_off, u->n_jobs + 1);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(4);
+  bool tma_ok = true;
+  for (int64_t rb : src->row_bytes) tma_ok &= rb % 16 == 0;
+  sb::launch_copy(u->jobs, u->piece_off, u->n_jobs, s, dst->n_procs > 1, tma_ok, sb::route_engine());
   SB_API_END
 }

@@ -4,6 +4,8 @@ UNMODIFIED reference (oracle/_ref/ref_harness, built by oracle/Makefile).
   tests/golden/batches.json -- next_batch (data_sim.cpp:225-248) per rank for
       several scenarios / seeds / steps, and parse_data_code verdicts
       (data_sim.cpp:39-76) incl. ParseError offsets;
+  tests/golden/uniform.json -- balance_uniform_items / reverse_uniform_plan
+      (balancer.cpp:411-462) on hand and random count vectors;
   tests/golden/stream.json  -- the C5 1000-step schedule's first steps planned
       by plan_routing: per-step tokens, sequences, chunks, WIR and total
       workload bits, capacity violations.
@@ -59,7 +61,16 @@ def main():
     stream["inputs"] = {"world": C5_WORLD, "topology": C5_TOPOLOGY, "scenarios": C5_SCENARIOS, "seed": C5_SEED}
     with open(os.path.join(HERE, "stream.json"), "w") as f:
         json.dump(stream, f, separators=(",", ":"))
-    print("wrote batches.json and stream.json")
+    import random
+    rng = random.Random(2508)
+    counts = [[4, 0], [3, 3, 3], [5, 0, 0], [0], [0, 0, 0, 0], [7], [1, 0, 0, 0, 0, 0, 0, 9], [2, -1]]
+    for _ in range(60):
+        w = rng.choice([2, 3, 4, 8, 16, 64])
+        counts.append([rng.choice([0, rng.randint(0, 5), rng.randint(0, 200)]) for _ in range(w)])
+    uni = harness("uniform", {"counts": counts})
+    with open(os.path.join(HERE, "uniform.json"), "w") as f:
+        json.dump(uni, f, separators=(",", ":"))
+    print("wrote batches.json, stream.json and uniform.json")
 
 
 if __name__ == "__main__":
