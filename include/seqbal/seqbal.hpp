@@ -178,6 +178,12 @@ PlanResult plan_routing(const std::vector<std::vector<SequenceInfo>>& per_rank_s
 RoutingPlan identity_plan(const std::vector<std::vector<SequenceInfo>>& per_rank_seqs);
 RoutingPlan reverse_plan(const RoutingPlan& plan);
 
+// Plan wire format (balancer.hpp:105-109, balancer.cpp:289-352): byte-identical
+// to the reference's nlohmann::json output; plan_from_json rebuilds the
+// manifests and target layout from chunks + origins.
+std::string plan_to_json(const RoutingPlan& plan, const BalanceReport& report);
+PlanResult plan_from_json(const std::string& text);
+
 // ---------------------------------------------------------------- metrics
 double workload_imbalance_ratio(const std::vector<double>& per_gpu_workloads);  // metrics.hpp:29
 

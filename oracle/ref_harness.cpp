@@ -626,11 +626,61 @@ int cmd_uniform() {
   return 0;
 }
 
+// nlohmann::json's text for doubles given as IEEE bit patterns (hex).
+int cmd_dtoa() {
+  std::stringstream ss;
+  ss << std::cin.rdbuf();
+  const json c = json::parse(ss.str());
+  json out = json::array();
+  for (const auto& h : c.at("bits")) {
+    const std::uint64_t b = std::stoull(h.get<std::string>(), nullptr, 16);
+    double d;
+    std::memcpy(&d, &b, 8);
+    out.push_back(json(d).dump());
+  }
+  std::cout << out.dump() << "\n";
+  return 0;
+}
+
+// The CLI's `plan` subcommand (tools/main.cpp:200-230) on in-memory inputs:
+// sequential ids, ModelShape{d_model, n_heads, d_model / n_heads, 1}.
+int cmd_cli_plan() {
+  std::stringstream ss;
+  ss << std::cin.rdbuf();
+  const json c = json::parse(ss.str());
+  json out = json::array();
+  for (const auto& cs : c.at("cases")) {
+    json r;
+    try {
+      std::vector<std::vector<SequenceInfo>> per_rank;
+      std::uint64_t id = 0;
+      for (const auto& rank_lens : cs.at("lens")) {
+        std::vector<SequenceInfo> seqs;
+        for (const auto& l : rank_lens) seqs.push_back({id++, l.get<std::int64_t>()});
+        per_rank.push_back(std::move(seqs));
+      }
+      const int d_model = cs.value("d_model", 3072), n_heads = cs.value("n_heads", 24);
+      WorkloadModel model;
+      model.shape = ModelShape{d_model, n_heads, d_model / n_heads, 1};
+      model.gamma = cs.value("gamma", kGammaH100);
+      const Topology topology = parse_topology(cs.at("topology").get<std::string>());
+      const WorldLayout layout = replicate(topology, static_cast<int>(per_rank.size()));
+      const PlanResult result = plan_routing(per_rank, model, layout);
+      r["json"] = plan_to_json(result.plan, result.report);
+    } catch (const std::exception& e) {
+      r["error"] = e.what();
+    }
+    out.push_back(r);
+  }
+  std::cout << out.dump() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench|batches|stream|uniform < json\n");
+    std::fprintf(stderr, "usage: ref_harness dump|bench|plan_bench|batches|stream|uniform|dtoa|cli_plan < json\n");
     return 1;
   }
   try {
@@ -640,6 +690,8 @@ int main(int argc, char** argv) {
     if (std::strcmp(argv[1], "batches") == 0) return cmd_batches();
     if (std::strcmp(argv[1], "stream") == 0) return cmd_stream();
     if (std::strcmp(argv[1], "uniform") == 0) return cmd_uniform();
+    if (std::strcmp(argv[1], "dtoa") == 0) return cmd_dtoa();
+    if (std::strcmp(argv[1], "cli_plan") == 0) return cmd_cli_plan();
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_harness: %s\n", e.what());
     return 3;

@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CUDA_SOURCES = ["planner.cu", "exchange.cu", "peer.cu", "stream.cu"]
-HOST_SOURCES = ["host/seqbal_api.cpp"]
+HOST_SOURCES = ["host/seqbal_api.cpp", "host/plan_json.cpp"]
 
 
 def _nvcc() -> str:
@@ -47,7 +47,7 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 def _deps(sources):
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
-    hdrs += [os.path.join(INCLUDE, "seqbal_capi.h")]
+    hdrs += [os.path.join(INCLUDE, "seqbal_capi.h"), os.path.join(CSRC, "host", "pow10_table.inc")]
     seqbal_inc = os.path.join(INCLUDE, "seqbal")
     if os.path.isdir(seqbal_inc):
         hdrs += [os.path.join(seqbal_inc, f) for f in os.listdir(seqbal_inc)]
@@ -77,12 +77,22 @@ def build(verbose: bool = False, force: bool = False) -> dict:
     if host_srcs:
         host_so = os.path.join(LIB, "libseqbal.so")
         if force or _stale(host_so, _deps(host_srcs) + [cuda_so]):
-            cmd = [_cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, *host_srcs, "-o", host_so,
+            cmd = [_cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, "-I", os.path.join(CSRC, "host"),
+                   *host_srcs, "-o", host_so,
                    "-L", LIB, "-lseqbal_cuda", "-Wl,-rpath,$ORIGIN"]
             if verbose:
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)
         out["host"] = host_so
+        cli_src = os.path.join(CSRC, "host", "seqbal_cli.cpp")
+        cli = os.path.join(LIB, "seqbal")
+        if force or _stale(cli, [cli_src, host_so] + _deps([])):
+            cmd = [_cxx(), "-std=c++20", "-O2", "-I", INCLUDE, cli_src, "-o", cli, "-L", LIB, "-lseqbal",
+                   "-lseqbal_cuda", "-Wl,-rpath,$ORIGIN"]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
+        out["cli"] = cli
     return out
 
 
