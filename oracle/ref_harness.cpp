@@ -656,11 +656,16 @@ int cmd_cli_plan() {
       std::uint64_t id = 0;
       for (const auto& rank_lens : cs.at("lens")) {
         std::vector<SequenceInfo> seqs;
-        for (const auto& l : rank_lens) seqs.push_back({id++, l.get<std::int64_t>()});
+        for (const auto& l : rank_lens) {
+          const std::int64_t len = l.get<std::int64_t>();
+          if (len < 0) throw ConfigError("sequence lengths must be >= 0");  // main.cpp:212
+          seqs.push_back({id++, len});
+        }
         per_rank.push_back(std::move(seqs));
       }
       const int d_model = cs.value("d_model", 3072), n_heads = cs.value("n_heads", 24);
       WorkloadModel model;
+      if (d_model % n_heads != 0) throw ConfigError("d_model must be divisible by n_heads");  // main.cpp:220
       model.shape = ModelShape{d_model, n_heads, d_model / n_heads, 1};
       model.gamma = cs.value("gamma", kGammaH100);
       const Topology topology = parse_topology(cs.at("topology").get<std::string>());
