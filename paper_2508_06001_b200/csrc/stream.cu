@@ -420,6 +420,10 @@ struct sb_driver {
   uint64_t* d_acc = nullptr;      // [0..2] checksums, [3..4] compare counts
   sb_step_record* d_rec = nullptr;
   int64_t rec_cap = 0;
+  // plan + exchange preparations run on a side stream under the witness
+  // fill and the earlier copies; ev[0] fork, ev[1..4] slot prepared
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[5] = {};
 };
 
 namespace sb {
@@ -525,6 +529,8 @@ extern "C" sb_status sb_driver_create(sb_planner* p, const sb_schedule* s, int n
     SB_CUDA(cudaMalloc(&d->d_acc, sizeof(uint64_t) * 5));
     SB_CUDA(cudaMalloc(&d->d_rec, sizeof(sb_step_record) * (size_t)d->rec_cap));
     SB_CUDA(cudaMemset(d->d_rec, 0, sizeof(sb_step_record) * (size_t)d->rec_cap));
+    SB_CUDA(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
+    for (auto& e : d->ev) SB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   } catch (...) {
     sb_driver_destroy(d);
     throw;
@@ -540,6 +546,9 @@ extern "C" sb_status sb_driver_destroy(sb_driver* d) {
   void* ptrs[] = {d->ids, d->lens, d->rank_off, d->d_step, d->d_scen, d->d_acc, d->d_rec};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  for (auto& e : d->ev)
+    if (e) cudaEventDestroy(e);
+  if (d->side) cudaStreamDestroy(d->side);
   delete d;
   return SB_OK;
 }
@@ -555,40 +564,64 @@ extern "C" sb_status sb_driver_set_step(sb_driver* d, int64_t step, sb_stream st
 
 // One step (simulate_step, simulator.cpp:45-178, on the device path).
 // Stream-ordered, no host synchronisation: capturable into a CUDA graph
-// whose replays advance the device step counter.
+// whose replays advance the device step counter.  Schedule:
+//   main: generate -> origin layout -> witness fill -> [checks] -> route copy
+//         -> pre copy -> post copy -> reverse copy -> record
+//   side: plan -> record plan -> prepare route / pre / post / reverse
+// (preparations touch only the plan and world tables, never payload, so the
+// plan and every layout + job build run under the witness fill and the
+// earlier copies; each copy waits for its own preparation).
 extern "C" sb_status sb_driver_step(sb_driver* d, sb_stream stream) {
   SB_API_BEGIN
   if (!d) throw Error{SB_ERR_CONFIG, "null driver"};
   cudaStream_t s = (cudaStream_t)stream;
+  sb_stream side = (sb_stream)d->side;
   sb_world *A = d->w[0], *B = d->w[1], *C = d->w[2], *D = d->w[3], *E = d->w[4];
   sb::k_generate<<<d->s->world, 256, 0, s>>>(gen_args(d->s), 0, d->d_step, d->ids, d->lens, d->rank_off, d->d_scen);
   SB_CHECK_LAUNCH();
   sb::count_launch();
   sb::ck(sb_world_layout_origin(A, d->lens, d->rank_off, stream));
-  sb::ck(sb_world_fill_witness(A, d->ids, d->lens, d->rank_off, stream));
-  sb::ck(sb_plan(d->p, d->ids, d->lens, d->rank_off, stream));
-  sb::k_record<<<1, 1024, 0, s>>>(d->d_rec, d->rec_cap, d->d_step, d->d_scen, d->lens, d->rank_off, d->p->W,
-                                  d->p->n_chunks, d->p->per_gpu, d->p->wir, d->p->total, d->p->violations);
+  SB_CUDA(cudaEventRecord(d->ev[0], s));
+  SB_CUDA(cudaStreamWaitEvent(d->side, d->ev[0], 0));
+  // side: plan, record, preparations
+  sb::ck(sb_plan(d->p, d->ids, d->lens, d->rank_off, side));
+  sb::k_record<<<1, 1024, 0, d->side>>>(d->d_rec, d->rec_cap, d->d_step, d->d_scen, d->lens, d->rank_off, d->p->W,
+                                        d->p->n_chunks, d->p->per_gpu, d->p->wir, d->p->total, d->p->violations);
   SB_CHECK_LAUNCH();
   sb::count_launch();
+  sb_world* back_src = d->uly ? D : B;
+  sb::ck(sb_exchange_prepare(d->p, 0, A, B, 0, side));
+  SB_CUDA(cudaEventRecord(d->ev[1], d->side));
+  if (d->uly) {
+    sb::ck(sb_exchange_prepare(d->p, 2, B, C, 2, side));
+    SB_CUDA(cudaEventRecord(d->ev[2], d->side));
+    sb::ck(sb_exchange_prepare(d->p, 3, C, D, 3, side));
+    SB_CUDA(cudaEventRecord(d->ev[3], d->side));
+  }
+  sb::ck(sb_exchange_prepare(d->p, 1, back_src, E, 1, side));
+  SB_CUDA(cudaEventRecord(d->ev[4], d->side));
+  // main: input synthesis, then the copies as their preparations land
+  sb::ck(sb_world_fill_witness(A, d->ids, d->lens, d->rank_off, stream));
   if (d->verify) {
     SB_CUDA(cudaMemsetAsync(d->d_acc, 0, sizeof(uint64_t) * 5, s));
     sb::ck(sb_world_checksum(A, d->d_acc + 0, stream));
   }
-  sb::ck(sb_route(d->p, 0, A, B, stream));
+  SB_CUDA(cudaStreamWaitEvent(s, d->ev[1], 0));
+  sb::ck(sb_exchange_run(d->p, 0, stream));
   if (d->verify) sb::ck(sb_world_checksum(B, d->d_acc + 1, stream));
-  sb_world* back_src = B;
   if (d->uly) {
-    sb::ck(sb_pre_attn(d->p, B, C, stream));
+    SB_CUDA(cudaStreamWaitEvent(s, d->ev[2], 0));
+    sb::ck(sb_exchange_run(d->p, 2, stream));
     if (d->verify) sb::ck(sb_world_checksum(C, d->d_acc + 2, stream));
-    sb::ck(sb_post_attn(d->p, C, D, stream));
+    SB_CUDA(cudaStreamWaitEvent(s, d->ev[3], 0));
+    sb::ck(sb_exchange_run(d->p, 3, stream));
     if (d->verify) sb::ck(sb_world_compare(D, B, d->d_acc + 3, stream));
-    back_src = D;
   }
   // simulated transformer output: every row shifts by block_perturbation
   // (simulator.cpp:128-136); the reverse route must carry it home
   if (d->verify) sb::ck(sb_world_perturb(back_src, stream));
-  sb::ck(sb_route(d->p, 1, back_src, E, stream));
+  SB_CUDA(cudaStreamWaitEvent(s, d->ev[4], 0));  // also joins the side stream (record, plan)
+  sb::ck(sb_exchange_run(d->p, 1, stream));
   if (d->verify) {
     sb::ck(sb_world_perturb(A, stream));  // expected: the original world, perturbed
     sb::ck(sb_world_compare(E, A, d->d_acc + 4, stream));

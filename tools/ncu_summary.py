@@ -23,8 +23,8 @@ tot = sum(sum(v) for v in agg.values())
 share = [{"kernel": k, "launches": len(v), "total_us": round(sum(v), 2), "avg_us": round(sum(v) / len(v), 2),
           "min_us": round(min(v), 2), "share": round(sum(v) / tot, 4)}
          for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(io.StringIO(raw)))
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout if rep != "-" else ""
+rr = list(csv.reader(io.StringIO(raw))) or [[], []]
 H, U = rr[0], rr[1]
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
