@@ -454,7 +454,7 @@ def main():
         return run_c5(args)
     if world_procs > 1:
         from paper_2508_06001_b200 import multigpu
-        return multigpu.bench_main(args, cfg, topology, METRIC)
+        return multigpu.bench_main(args, cfg, topology, METRIC, clock_sampler=lambda dev: ClockSampler(dev))
 
     torch.cuda.set_device(0)
     W = cfg["world"]

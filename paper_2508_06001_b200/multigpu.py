@@ -219,7 +219,28 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, A, B, Cw, D, E,
     return meta
 
 
-def bench_main(args, cfg, topology, metric):
+def _a2a_roofline(busiest: int, route_us: float, same_device: bool) -> dict:
+    """Busiest-GPU all-to-all bandwidth of the route phase against NVLink 5
+    (900 GB/s per direction).  When the processes share one GPU (functional
+    runs on a one-GPU box) the 'peer' stores are local HBM traffic, so the
+    bound is the measured HBM copy peak instead."""
+    achieved = busiest / (route_us * 1e-6) / 1e9 if route_us > 0 else None
+    if same_device:
+        peak = 6550.4
+        try:
+            with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")) as f:
+                peak = float(json.load(f).get("hbm_gbs", peak))
+        except OSError:
+            pass
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": None,
+                "note": "all processes on one GPU: peer stores are local HBM traffic"}
+    return {"bound": "nvlink", "achieved": achieved, "peak": 900.0, "unit": "GB/s",
+            "frac": achieved / 900.0 if achieved else None, "traffic": None}
+
+
+def bench_main(args, cfg, topology, metric, clock_sampler=None):
     """bench.py --gpus N under torchrun: N processes, one GPU each."""
     import torch
     import torch.distributed as dist
@@ -268,16 +289,56 @@ def bench_main(args, cfg, topology, metric):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     group.barrier()
     torch.cuda.synchronize()
+    clk = clock_sampler(torch.cuda.current_device()) if clock_sampler else None
+    if clk:
+        clk.__enter__()
     ev0.record(stream)
     for _ in range(args.steps):
         step(group, gather, planner, A, B, Cw, D, E, ulysses)
     ev1.record(stream)
     torch.cuda.synchronize()
+    if clk:
+        clk.__exit__(None, None, None)
     launches = _capi.load().sb_kernel_launches() - n0
     ms = group.max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     nr, us_r = planner.copy_timing(0)
     route_us = group.max_over_ranks(us_r / max(1, nr))
     planner.enable_timing(False)
+
+    # e2e through the public API with host buffers: every step uploads this
+    # process's ranks (metadata + payload image) from pinned memory, re-lays
+    # out the origin world, runs the step and downloads the restored ranks.
+    mb, pb = A.arena(0)[1], A.arena(1)[1]
+    rows_local = int(sum(int(x.sum()) for x in all_lens[first:first + n_local]))
+    h_meta = torch.empty(rows_local * meta_b, dtype=torch.uint8).pin_memory()
+    h_pay = torch.empty(rows_local * payload, dtype=torch.uint8).pin_memory()
+    o_meta, o_pay = torch.empty_like(h_meta).pin_memory(), torch.empty_like(h_pay).pin_memory()
+    A.download([h_meta.data_ptr(), h_pay.data_ptr()], [h_meta.numel(), h_pay.numel()])
+    torch.cuda.synchronize()
+    del mb, pb
+
+    def e2e_step():
+        gather.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
+        A.upload([h_meta.data_ptr(), h_pay.data_ptr()], [h_meta.numel(), h_pay.numel()])
+        m = step(group, gather, planner, A, B, Cw, D, E, ulysses)
+        E.download([o_meta.data_ptr(), o_pay.data_ptr()], [o_meta.numel(), o_pay.numel()])
+        return m
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_ok = bool(torch.equal(o_pay, h_pay) and torch.equal(o_meta, h_meta))
+    k = max(3, min(args.steps, 20))
+    group.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(k):
+        e2e_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = group.max_over_ranks(ev0.elapsed_time(ev1)) / k
+    n_meta_local = int(sum(len(x) for x in all_ids[first:first + n_local]))
+    h2d = group.sum_u64(h_meta.numel() + h_pay.numel() + 16 * n_meta_local + 8 * (n_local + 1))
+    d2h = group.sum_u64(o_meta.numel() + o_pay.numel())
     per = hp.per_gpu_workload
     line = {
         "metric": metric, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": group.size,
@@ -290,11 +351,11 @@ def bench_main(args, cfg, topology, metric):
         "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
         "a2a_gbs": busiest / (route_us * 1e-6) / 1e9 if route_us > 0 else None,
         "a2a_busiest_bytes": busiest, "route_copy_us": route_us,
-        "roofline": {"bound": "nvlink", "achieved": busiest / (route_us * 1e-6) / 1e9 if route_us > 0 else None,
-                     "peak": 900.0, "unit": "GB/s",
-                     "frac": (busiest / (route_us * 1e-6) / 1e9 / 900.0) if route_us > 0 else None,
-                     "traffic": None},
+        "roofline": _a2a_roofline(busiest, route_us, group.same_device),
         "gpu_launches": int(launches), "checksum_conserved": bool(cs),
+        "clocks": clk.summary() if clk else None,
+        "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "round_trip_bit_exact": e2e_ok},
     }
     if group.rank == 0:
         print(json.dumps(line))
