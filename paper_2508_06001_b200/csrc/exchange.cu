@@ -823,9 +823,16 @@ static int route_engine() {
   static int e = engine_from_env("SEQBAL_ROUTE_ENGINE", 0);
   return e;
 }
-static int ulysses_engine() {
-  static int e = engine_from_env("SEQBAL_ULYSSES_ENGINE", 1);
-  return e;
+// Ulysses copies move head slices of row_bytes / G bytes.  Measured on B200
+// (profiles/r01b): the TMA bulk ring wins for wide slices (C2, G = 2,
+// 3072 B: 45 vs 59 us) and loses for narrow ones (C3, G = 8, 768 B: 341 vs
+// 237 us -- one issuing thread per CTA cannot keep enough small bulk copies
+// in flight); at G = 4 (1536 B) they tie.  Default: TMA when every payload
+// slice is >= 2 KB, else the LSU engine.  SEQBAL_ULYSSES_ENGINE overrides.
+static int ulysses_engine(int64_t min_slice_bytes) {
+  static int e = engine_from_env("SEQBAL_ULYSSES_ENGINE", -1);
+  if (e >= 0) return e;
+  return min_slice_bytes >= 2048 ? 1 : 0;
 }
 
 constexpr int64_t kFusedPrepMaxJobs = 1 << 16;  // single-CTA prep up to this many jobs
@@ -1163,12 +1170,14 @@ static void prepare_ulysses(sb_planner* p, int slot, int post, sb_world* src, sb
     sb::count_launch(2);
   }
   bool tma_ok = true;  // row and head-slice sizes multiples of 16 B, slices within a stage
+  int64_t min_slice = INT64_MAX;
   for (int t = 0; t < src->T; ++t) {
     tma_ok &= src->row_bytes[t] % 16 == 0;
     if (src->tensor_desc[t] == 1)
       for (int b = 0; b < p->M; ++b) {
         const int64_t slice = src->row_bytes[t] / p->bag_size[b];
         tma_ok &= slice % 16 == 0 && slice <= sb::kPieceBytes;
+        if (p->bag_size[b] > 1) min_slice = std::min(min_slice, slice);
       }
   }
   sb_planner::Slot& sl = p->slots[slot];
@@ -1176,7 +1185,7 @@ static void prepare_ulysses(sb_planner* p, int slot, int post, sb_world* src, sb
   sl.pieces_done = fused;
   sl.tma_ok = tma_ok;
   sl.fence_sys = dst->n_procs > 1;
-  sl.engine = sb::ulysses_engine();
+  sl.engine = sb::ulysses_engine(min_slice);
   sl.op = post ? 3 : 2;
 }
 
