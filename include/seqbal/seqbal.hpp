@@ -19,6 +19,7 @@
 #pragma once
 
 #include <cstdint>
+#include <iosfwd>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -188,6 +189,42 @@ PlanResult plan_from_json(const std::string& text);
 double workload_imbalance_ratio(const std::vector<double>& per_gpu_workloads);  // metrics.hpp:29
 
 // --------------------------------------------------------------- data sim
+// data_sim.hpp:11-102.  Grammar and presets parse on the host with the
+// reference's messages; next_batch runs the device generator
+// (sb_schedule_generate) and downloads the rank's samples.
+inline constexpr int kSpatialStride = 16;
+inline constexpr int kTemporalNum = 5;
+inline constexpr int kTemporalDen = 17;
+inline constexpr int kMaxTextTokens = 392;
+inline constexpr double kAspectMultMin = 0.96;
+inline constexpr double kAspectMultMax = 1.04;
+
+struct StreamSpec {
+  int gpus = 1;
+  int batch_per_gpu = 1;
+  int resolution = 256;
+  int frames = 1;
+  bool smooth = false;
+  bool operator==(const StreamSpec&) const = default;
+};
+
+StreamSpec parse_data_code(std::string_view code);  // throws ParseError
+std::string format_data_code(const StreamSpec& spec);
+
+struct ShardingGroupConfig {
+  std::vector<StreamSpec> streams;
+  int group_size = 0;
+  void validate() const;  // throws ConfigError
+};
+
+ShardingGroupConfig parse_scenario(std::istream& in);
+ShardingGroupConfig parse_scenario_file(const std::string& path);
+ShardingGroupConfig preset_lowres_image();
+ShardingGroupConfig preset_mixed_image();
+ShardingGroupConfig preset_joint_image_video();
+ShardingGroupConfig scenario_preset(std::string_view name);
+std::vector<std::string> scenario_preset_names();
+
 struct SampleMeta {  // data_sim.hpp:61-68 (the record make_world consumes)
   std::uint64_t sample_id = 0;
   std::int64_t text_len = 0;
@@ -195,6 +232,33 @@ struct SampleMeta {  // data_sim.hpp:61-68 (the record make_world consumes)
   int origin_rank = 0;
   std::int64_t total_len() const { return text_len + visual_len; }
 };
+
+std::int64_t latent_frames(const StreamSpec& spec);
+std::int64_t visual_tokens(const StreamSpec& spec, double aspect_multiplier);
+int stream_of_rank(const ShardingGroupConfig& config, int group_rank);
+double aspect_multiplier(std::uint64_t seed, std::int64_t step, int stream_index);
+std::vector<SampleMeta> next_batch(const ShardingGroupConfig& config, int rank, std::int64_t step,
+                                   std::uint64_t seed);
+SampleMeta dummy_sample(int rank, std::int64_t step);
+std::uint64_t make_sample_id(std::int64_t step, int rank, int index);
+
+// ---------------------------------------------------- uniform (T5) balancer
+// balancer.hpp:122-144; planned on the device (sb_uniform_plan).
+struct UniformMove {
+  int src_rank = 0;
+  int dst_rank = 0;
+  std::int64_t count = 0;
+  bool operator==(const UniformMove&) const = default;
+};
+
+struct UniformPlan {
+  std::vector<std::int64_t> final_counts;
+  std::vector<UniformMove> moves;
+  std::int64_t total_moved = 0;
+};
+
+UniformPlan balance_uniform_items(const std::vector<std::int64_t>& counts);
+UniformPlan reverse_uniform_plan(const UniformPlan& plan, const std::vector<std::int64_t>& original_counts);
 
 // --------------------------------------------------------------- exchange
 // exchange.hpp:14-114.

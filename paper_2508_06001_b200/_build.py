@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CUDA_SOURCES = ["planner.cu", "exchange.cu", "peer.cu", "stream.cu"]
-HOST_SOURCES = ["host/seqbal_api.cpp", "host/plan_json.cpp"]
+HOST_SOURCES = ["host/seqbal_api.cpp", "host/plan_json.cpp", "host/seqbal_ext.cpp"]
 
 
 def _nvcc() -> str:

@@ -3,11 +3,14 @@
 // (balancer_test.cpp, exchange_test.cpp), plus direct comparisons with the
 // C oracle (oracle/seqbal_oracle.c, test infrastructure) on random inputs.
 // Built by tests/test_cpp_api.py; needs a CUDA device.
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
 #include <map>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -365,12 +368,164 @@ static void test_block_moves() {
   CHECK(a.ranks[0].sample_ids[50] == world.ranks[1].sample_ids[0]);
 }
 
+// data_sim_test.cpp:15-166 on the device generator (next_batch) and the
+// host grammar.
+static void test_data_sim() {
+  CHECK((parse_data_code("g32b32i256f1s0") == StreamSpec{32, 32, 256, 1, false}));
+  CHECK((parse_data_code("g8b2i256f85s1") == StreamSpec{8, 2, 256, 85, true}));
+  CHECK((parse_data_code("g1b1i16f1s0") == StreamSpec{1, 1, 16, 1, false}));
+  for (const auto& name : scenario_preset_names()) {
+    const ShardingGroupConfig config = scenario_preset(name);
+    CHECK(config.group_size == 32);
+    for (const StreamSpec& s : config.streams) CHECK(parse_data_code(format_data_code(s)) == s);
+  }
+  const std::pair<const char*, std::size_t> bad[] = {{"", 0}, {"b32g32i256f1s0", 0}, {"g32b32i256f1", 12},
+                                                     {"g32b32i256f1s2", 13}, {"g32b32i255f1s0", 7},
+                                                     {"g0b32i256f1s0", 1}, {"g32b32i256f1s0x", 14},
+                                                     {"g32b0i256f1s0", 4}, {"g32b32i256f0s0", 11}};
+  for (const auto& [text, off] : bad) {
+    bool thrown = false;
+    try {
+      parse_data_code(text);
+    } catch (const ParseError& e) {
+      thrown = true;
+      CHECK(e.offset() == off);
+    }
+    CHECK(thrown);
+  }
+  CHECK(visual_tokens(StreamSpec{1, 1, 256, 1, false}, 1.0) == 256);
+  CHECK(visual_tokens(StreamSpec{1, 1, 512, 85, true}, 1.0) == 25600);
+  CHECK(latent_frames(StreamSpec{1, 1, 512, 85, true}) == 25);
+  CHECK(latent_frames(StreamSpec{1, 1, 512, 17, true}) == 5);
+  CHECK(visual_tokens(StreamSpec{1, 1, 256, 4, false}, 1.0) == 1024);
+  CHECK(visual_tokens(StreamSpec{1, 1, 16, 1, true}, 1.0) == 1);
+  CHECK(visual_tokens(StreamSpec{1, 1, 256, 1, false}, 0.96) == 246);
+  CHECK(visual_tokens(StreamSpec{1, 1, 256, 1, false}, 1.04) == 266);
+  const ShardingGroupConfig mixed = preset_mixed_image();
+  CHECK(stream_of_rank(mixed, 0) == 0 && stream_of_rank(mixed, 15) == 0 && stream_of_rank(mixed, 16) == 1);
+  CHECK(stream_of_rank(mixed, 19) == 1 && stream_of_rank(mixed, 20) == 2 && stream_of_rank(mixed, 24) == 3);
+  CHECK(stream_of_rank(mixed, 31) == 3);
+  CHECK_THROWS(stream_of_rank(mixed, 32), ConfigError);
+  ShardingGroupConfig wrong;
+  wrong.group_size = 8;
+  wrong.streams.push_back(parse_data_code("g4b1i256f1s0"));
+  CHECK_THROWS(wrong.validate(), ConfigError);
+  // next_batch: deterministic, rank/step/seed sensitive, stream-shaped
+  const auto a = next_batch(mixed, 5, 3, 42), b = next_batch(mixed, 5, 3, 42);
+  CHECK(a.size() == b.size());
+  bool same = a.size() == b.size(), diff = false;
+  const auto r6 = next_batch(mixed, 6, 3, 42), s4 = next_batch(mixed, 5, 4, 42), z = next_batch(mixed, 5, 3, 43);
+  for (size_t i = 0; i < a.size() && same; ++i) {
+    same &= a[i].sample_id == b[i].sample_id && a[i].text_len == b[i].text_len && a[i].visual_len == b[i].visual_len;
+    diff |= a[i].text_len != r6[i].text_len || a[i].text_len != s4[i].text_len || a[i].text_len != z[i].text_len;
+  }
+  CHECK(same && diff);
+  const auto r17 = next_batch(mixed, 17, 0, 7);
+  CHECK(r17.size() == 5);
+  for (const SampleMeta& sm : r17) CHECK(sm.origin_rank == 17 && sm.text_len >= 0 && sm.text_len <= kMaxTextTokens);
+  for (int rank : {0, 3, 16, 20, 24}) {
+    const int si = stream_of_rank(mixed, rank);
+    const double mult = aspect_multiplier(7, 11, si);
+    for (const SampleMeta& sm : next_batch(mixed, rank, 11, 7))
+      CHECK(sm.visual_len == visual_tokens(mixed.streams[si], mult));
+  }
+  const ShardingGroupConfig lowres = preset_lowres_image();
+  for (int step = 0; step < 40; ++step) {
+    const auto batch = next_batch(lowres, 0, step, 1234);
+    CHECK(batch.size() == 32);
+    for (const SampleMeta& sm : batch) CHECK(sm.visual_len >= 246 && sm.visual_len <= 266);
+  }
+  const auto r33 = next_batch(mixed, 33, 0, 7);
+  CHECK(r33.size() == 4 && r33.front().origin_rank == 33);
+  std::istringstream sc("# x\ngroup_size 4\ng2b1i512f1s0\n\ng2b4i256f1s1 # y\n");
+  const ShardingGroupConfig parsed = parse_scenario(sc);
+  CHECK(parsed.group_size == 4 && parsed.streams.size() == 2 && parsed.streams[1].smooth);
+  std::istringstream nohdr("g2b1i512f1s0\n");
+  CHECK_THROWS(parse_scenario(nohdr), ParseError);
+  const SampleMeta d = dummy_sample(3, 9);
+  CHECK(d.sample_id == make_sample_id(9, 3, 0) && d.visual_len == 1 && d.text_len == 0);
+}
+
+// balancer_test.cpp:298-370 on the device uniform balancer.
+static std::int64_t min_moves_oracle(const std::vector<std::int64_t>& counts) {
+  const int n = static_cast<int>(counts.size());
+  std::int64_t total = 0;
+  for (auto c : counts) total += c;
+  const std::int64_t base = total / n;
+  const int rem = static_cast<int>(total % n);
+  std::int64_t best = INT64_MAX;
+  for (int mask = 0; mask < (1 << n); ++mask) {
+    if (__builtin_popcount(mask) != rem) continue;
+    std::int64_t moved = 0;
+    for (int r = 0; r < n; ++r) moved += std::max<std::int64_t>(0, counts[r] - (base + ((mask >> r) & 1)));
+    best = std::min(best, moved);
+  }
+  return best;
+}
+
+static void test_uniform() {
+  const UniformPlan p = balance_uniform_items({4, 0});
+  CHECK((p.final_counts == std::vector<std::int64_t>{2, 2}) && p.total_moved == 2);
+  const UniformPlan q = balance_uniform_items({3, 3, 3});
+  CHECK((q.final_counts == std::vector<std::int64_t>{3, 3, 3}) && q.total_moved == 0 && q.moves.empty());
+  const UniformPlan r = balance_uniform_items({5, 0, 0});
+  CHECK((r.final_counts == std::vector<std::int64_t>{2, 2, 1}) && r.total_moved == 3);
+  CHECK_THROWS(balance_uniform_items({1, -1}), ConfigError);
+  uint64_t state = 55;
+  for (int trial = 0; trial < 300; ++trial) {
+    auto next = [&](int lo, int hi) {
+      state = state * 6364136223846793005ULL + 1442695040888963407ULL;
+      return lo + static_cast<int>((state >> 33) % static_cast<uint64_t>(hi - lo + 1));
+    };
+    const int n = next(1, 8);
+    std::vector<std::int64_t> counts(n);
+    for (auto& c : counts) c = next(0, 12);
+    const UniformPlan u = balance_uniform_items(counts);
+    std::int64_t total = 0, ftotal = 0, lo = INT64_MAX, hi = INT64_MIN;
+    for (int k = 0; k < n; ++k) {
+      total += counts[k];
+      ftotal += u.final_counts[k];
+      lo = std::min(lo, u.final_counts[k]);
+      hi = std::max(hi, u.final_counts[k]);
+    }
+    CHECK(total == ftotal && hi - lo <= 1);
+    CHECK(u.total_moved == min_moves_oracle(counts));
+    std::vector<std::int64_t> sim = counts;
+    for (const UniformMove& m : u.moves) {
+      sim[m.src_rank] -= m.count;
+      sim[m.dst_rank] += m.count;
+    }
+    CHECK(sim == u.final_counts);
+    for (const UniformMove& m : reverse_uniform_plan(u, counts).moves) {
+      sim[m.src_rank] -= m.count;
+      sim[m.dst_rank] += m.count;
+    }
+    CHECK(sim == counts);
+  }
+}
+
+// balancer.cpp:289-352 wire format through the drop-in API: a device plan
+// serialises and re-reads to an equal plan.
+static void test_plan_json() {
+  std::vector<std::vector<SequenceInfo>> seqs = {{{1, 900}, {2, 30}, {3, 0}}, {{4, 64}}, {{5, 4096}, {6, 7}}, {}};
+  WorkloadModel m;
+  const PlanResult pr = plan_routing(seqs, m, replicate(parse_topology("g1n2+g2n1"), 4));
+  const std::string js = plan_to_json(pr.plan, pr.report);
+  const PlanResult back = plan_from_json(js);
+  CHECK(back.plan == pr.plan);
+  CHECK(plan_to_json(back.plan, back.report) == js);
+  CHECK(js.rfind("{\"chunks\":[{\"chunk_index\":0,", 0) == 0);
+  CHECK_THROWS(plan_from_json("{\"world_size\":2,\"chunks\":[],\"origins\":[[]]}"), ConfigError);
+  CHECK_THROWS(plan_from_json("{\"world_size\":"), ParseError);
+}
+
 int main() {
   const std::pair<const char*, std::function<void()>> tests[] = {
       {"assign_to_bags", test_assign},        {"plan_routing", test_plan_routing},
       {"reverse_plan", test_reverse_plan},    {"route", test_route_split_and_mismatch},
       {"round_trips", test_round_trips},      {"ulysses", test_ulysses},
-      {"block_moves", test_block_moves}};
+      {"block_moves", test_block_moves},      {"data_sim", test_data_sim},
+      {"uniform", test_uniform},              {"plan_json", test_plan_json}};
   for (const auto& [name, fn] : tests) {
     const int before = g_fail;
     try {
