@@ -285,3 +285,39 @@ def test_world_plan_mismatch_is_integrity_error():
     E.status()
     for r in range(8):
         assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r))
+
+
+@pytest.mark.parametrize("path", ["small", "large"])
+@pytest.mark.parametrize("world,topo", [(64, "g2n4"), (256, "g4n2+g8n1"), (96, "g1n4+g2n2+g4n1")])
+def test_many_replicas_vs_oracle(world, topo, path):
+    """Large worlds: many replicas planned independently (balancer.cpp:136-219),
+    ragged ranks including empty ones and zero-length sequences."""
+    rng = np.random.default_rng(world)
+    lens = [rng.integers(0, 3000, size=rng.integers(0, 6)).tolist() for _ in range(world)]
+    meta = oracle.meta_explicit(lens)
+    planner = sb.Planner(topo, world, max_seqs=max(1, sum(len(x) for x in lens)))
+    planner.set_path(path)
+    planner.plan(device_meta(meta))
+    hp = planner.download()
+    plan, rep = oracle.plan_routing(meta, oracle.parse_topology(topo))
+    got = host_plan_as_oracle(hp, meta)
+    assert got.chunk_rows() == plan.chunk_rows()
+    assert got.send == plan.send and got.recv == plan.recv
+    assert [dbits(x) for x in hp.per_gpu_workload] == [dbits(x) for x in rep.per_gpu_workload]
+    assert [dbits(x) for x in hp.per_bag_occupancy] == [dbits(x) for x in rep.per_bag_occupancy]
+    assert dbits(hp.wir) == dbits(rep.wir) and dbits(hp.total_workload) == dbits(rep.total_workload)
+    assert hp.rev_recv == oracle.reverse_plan(plan).recv
+    # and the data path on the same plan
+    rows = int(sum(sum(x) for x in lens))
+    mk = lambda: sb.World(world, 24, [192], capacity_rows=max(1, rows), max_bag=planner.max_bag)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    dm = device_meta(meta)
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    sb.route(planner, A, B)
+    sb.pre_attn(planner, B, Cw)
+    sb.post_attn(planner, Cw, D)
+    sb.reverse_route(planner, D, E)
+    E.status()
+    assert E.compare(A) == 0 and D.compare(B) == 0
+    assert Cw.checksum() == A.checksum()
