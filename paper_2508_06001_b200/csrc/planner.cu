@@ -384,7 +384,10 @@ __device__ __forceinline__ uint64_t greedy_key(bool feasible, double occ) {
 
 constexpr int kGreedyChunk = 1024;  // `hook(p0)` runs before every chunk of this many steps
 
-template <int BPL, class GetW, class Hook>
+// CHUNK > 0: `hook(p0)` runs before every CHUNK steps (the large path's
+// shared-memory ring); CHUNK == 0: one flat loop (the nested form costs the
+// fused planner ~45 cycles per sequence in code generation).
+template <int BPL, int CHUNK, class GetW, class Hook>
 __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t n, double total_rep, GetW getw,
                                             Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out) {
   const int lane = threadIdx.x & 31;
@@ -408,10 +411,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
   }
   int viol = 0;
   const int nn = (int)n;  // <= max_seqs < 2^31: 32-bit loop arithmetic
-  for (int p0 = 0; p0 < nn; p0 += kGreedyChunk) {
-  if (p0 > 0) hook(p0);
-  const int p1 = nn - p0 < kGreedyChunk ? nn : p0 + kGreedyChunk;
-  for (int p = p0; p < p1; ++p) {
+  auto step = [&](int p) {
     const double w = w_a, wn = w_b;  // w_p and w_{p+1} (0 past the end: unused)
     w_a = w_b;
     w_b = w_c;
@@ -448,7 +448,15 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
       cnt[i] += won ? 1 : 0;
     }
     if (lane == 0) pick_out[p] = (int)pick;
-  }
+  };
+  if constexpr (CHUNK == 0) {
+    for (int p = 0; p < nn; ++p) step(p);
+  } else {
+    for (int p0 = 0; p0 < nn; p0 += CHUNK) {
+      if (p0 > 0) hook(p0);
+      const int p1 = nn - p0 < CHUNK ? nn : p0 + CHUNK;
+      for (int p = p0; p < p1; ++p) step(p);
+    }
   }
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
@@ -486,7 +494,7 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
     load(p0 / kGreedyChunk + 1);
     __syncwarp();
   };
-  greedy_warp<BPL>(a, rep, n, a.rep_total[rep],
+  greedy_warp<BPL, kGreedyChunk>(a, rep, n, a.rep_total[rep],
                    [&](int p) { return ring[(p / kGreedyChunk) & 1][p % kGreedyChunk]; }, hook, a.pick + lo,
                    nullptr, a.violations);
 }
@@ -1040,10 +1048,17 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
   SB_CUDA(cudaMemsetAsync(p->violations, 0, sizeof(int32_t), s));
 }
 
+// Path choice.  The fused single-CTA planner wins while launches dominate
+// (256 sequences: 38 vs 88 us); its chunk phases are one CTA, so with many
+// chunks the multi-kernel path wins (2048 sequences, bags of 8 = 16 K
+// chunks: 363 vs 286 us; tools/plan_profile.py, profiles/r01b).
+constexpr int64_t kSmallChunks = 8192;
+
 static bool use_small_path(const sb_planner* p) {
   if (p->path == 2) return false;
   const bool fits = p->max_seqs <= kSmallSeqs && p->W <= 1024 && p->M <= kMaxBags;
-  return fits && (p->path == 1 || p->path == 0);
+  if (p->path == 1) return fits;
+  return fits && p->max_chunks <= kSmallChunks;
 }
 
 static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool order) {

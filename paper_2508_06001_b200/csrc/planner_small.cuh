@@ -103,7 +103,8 @@ template <int BPL>
 __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, const double* s_w, const int32_t* s_sorted,
                              int32_t* s_pick, int32_t* s_bagcnt, double total_rep, int* viol_out) {
   const double* ws = s_w + lo;  // workloads already gathered into greedy order
-  greedy_warp<BPL>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo, s_bagcnt, viol_out);
+  greedy_warp<BPL, 0>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo, s_bagcnt,
+                      viol_out);
 }
 
 __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int cap) {
@@ -267,15 +268,29 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
     }
     __syncthreads();
     if (n <= 1024) {
-      // rank by counting: the key (~bits(w), id, index) is a total order
-      for (int64_t i = tid; i < n; i += blockDim.x) {
-        const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
+      // rank by counting: the key (~bits(w), id, index) is a total order.
+      // k = blockDim/n lanes (power of two <= 32) share one record's count,
+      // each over a slice of the candidates (broadcast smem reads), then a
+      // shuffle reduction inside the k-lane group.
+      const int nn = (int)n;
+      int k = 1;
+      while (k < 32 && 2 * k * nn <= (int)blockDim.x) k <<= 1;
+      const int per = (nn + k - 1) / k;
+      for (int base = 0; base < nn * k; base += blockDim.x) {
+        const int x = base + tid;
+        const int i = x / k, part = x % k;
         int pos = 0;
-        const int nj = (int)n;
+        if (i < nn) {
+          const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
+          const int j0 = part * per, j1 = j0 + per < nn ? j0 + per : nn;
 #pragma unroll 8
-        for (int j = 0; j < nj; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
-        s_sorted[lo + pos] = (int32_t)(lo + i);
-        a.sorted_idx[lo + pos] = (int32_t)(lo + i);
+          for (int j = j0; j < j1; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
+        }
+        for (int o = k >> 1; o > 0; o >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, o);
+        if (i < nn && part == 0) {
+          s_sorted[lo + pos] = (int32_t)(lo + i);
+          a.sorted_idx[lo + pos] = (int32_t)(lo + i);
+        }
       }
     } else {
       smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
