@@ -477,6 +477,25 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
 // two-chunk shared-memory ring: at the start of chunk k the warp loads chunk
 // k+1 (coalesced, latency hidden under 1024 greedy steps), so the chain's
 // three-step-ahead prefetch always hits shared memory.
+// Replicas of up to kGreedyStage sequences are staged whole into dynamic
+// shared memory first (k_greedy_staged: flat loop, 137 vs 158 cycles per
+// sequence); larger ones stream through the ring.
+constexpr int kGreedyStage = 24576;  // 192 KB of workloads
+
+template <int BPL>
+__global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
+  extern __shared__ __align__(16) double stage[];
+  if (!seqs_ok(a)) return;
+  const int rep = blockIdx.x, lane = threadIdx.x;
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  const int n = (int)(hi - lo);
+  const double* sw = a.sorted_w + lo;
+  for (int i = lane; i < n; i += 32) stage[i] = sw[i];
+  __syncwarp();
+  greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
+                      nullptr, a.violations);
+}
+
 template <int BPL>
 __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
   __shared__ double ring[2][kGreedyChunk];
@@ -1093,6 +1112,27 @@ static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool o
   count_launch(launches);
 }
 
+// k_greedy_staged when every replica fits the staging buffer (the planner's
+// sequence capacity bounds every replica), else the ring-fed k_greedy.
+static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
+  const bool wide = (p->M + 31) / 32 > 1;
+  if (p->max_seqs <= kGreedyStage) {
+    const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
+    static int set_to[2] = {0, 0};
+    if (smem > set_to[wide]) {
+      if (wide) SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      else SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      set_to[wide] = smem;
+    }
+    if (wide) k_greedy_staged<2><<<p->R, 32, smem, s>>>(a);
+    else k_greedy_staged<1><<<p->R, 32, smem, s>>>(a);
+  } else {
+    if (wide) k_greedy<2><<<p->R, 32, 0, s>>>(a);
+    else k_greedy<1><<<p->R, 32, 0, s>>>(a);
+  }
+  SB_CHECK_LAUNCH();
+}
+
 static void run_plan(sb_planner* p, cudaStream_t s) {
   PlanArgs a = make_args(p);
   if (use_small_path(p)) {
@@ -1112,10 +1152,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[1], s));
   launch_sort(p, a, s, true);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[2], s));
-  const int bpl = (p->M + 31) / 32;
-  if (bpl <= 1) k_greedy<1><<<p->R, 32, 0, s>>>(a);
-  else k_greedy<2><<<p->R, 32, 0, s>>>(a);
-  SB_CHECK_LAUNCH();
+  launch_greedy(p, a, s);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[3], s));
   k_emit<<<p->R, 1024, 0, s>>>(a);
   SB_CHECK_LAUNCH();
@@ -1388,9 +1425,7 @@ extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t*
   sb::k_prep<<<p->W, 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   sb::launch_sort(p, a, s, true);
-  if ((p->M + 31) / 32 <= 1) sb::k_greedy<1><<<p->R, 32, 0, s>>>(a);
-  else sb::k_greedy<2><<<p->R, 32, 0, s>>>(a);
-  SB_CHECK_LAUNCH();
+  sb::launch_greedy(p, a, s);
   sb::count_launch(2);
   SB_CUDA(cudaStreamSynchronize(s));
   int32_t st = 0;
