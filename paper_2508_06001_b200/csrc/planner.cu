@@ -3,10 +3,12 @@
 // reproduced bit-exactly on the GPU.
 //
 // Pipeline (no host synchronisation, graph-capturable):
-//   k_prep        W CTAs       workloads (FP64, reference operation order), per
-//                              rank row offsets (block scan), duplicate-id hash
-//   k_totals      R+1 CTAs     serial per-replica / global FP64 totals (side
-//                              stream, overlaps the sort)
+//   k_totals      R+1 CTAs     serial per-replica / global FP64 totals, forked
+//                              onto a side stream at the start (workloads
+//                              recomputed from lengths), joined before the greedy
+//   k_prep_seq    seq grid     workloads (FP64, reference operation order), owner
+//                              rank, duplicate-id hash
+//   k_prep_rows   W CTAs       per-rank origin row offsets (block scan)
 //   k_sort_tiles  tiles        2048-record bitonic tiles in shared memory
 //   k_merge_pass  x log2(n/2048)  co-rank merges, one record per thread
 //   k_sort_finish              greedy order (workload desc, id asc)
@@ -117,56 +119,69 @@ __global__ void k_selftest_div(uint64_t seed, int64_t n, unsigned long long* mis
   if (bad) atomicAdd(mismatches, bad);
 }
 
-// ------------------------------------------------------------------ k_prep
-__global__ void __launch_bounds__(256) k_prep(PlanArgs a) {
-  __shared__ int64_t sh[33];
-  const int r = blockIdx.x;
+// ------------------------------------------------------------------ prep
+// Per sequence (grid over the capacity, one thread per gathered sequence):
+// workload (balancer.cpp:144; or the caller's for assign_to_bags), owning
+// rank, length check (workload_model.cpp:66) and the duplicate-id check
+// inside the replica (open addressing in global memory).
+__device__ __forceinline__ double seq_workload(const PlanArgs& a, int64_t i) {
+  if (a.w_in) return a.w_in[i];
+  const int64_t len = a.lens[i];
+  return gamma_weighted_workload(len < 0 ? 0 : len, a.d_model, a.gamma);
+}
+
+__global__ void __launch_bounds__(256) k_prep_seq(PlanArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (!seqs_ok(a)) {
-    if (r == 0 && threadIdx.x == 0) atomicOr(a.status, ST_CAPACITY);
+    if (i == 0) atomicOr(a.status, ST_CAPACITY);
     return;
   }
-  const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
-  const int rep = r / a.U;
+  if (i >= a.rank_off[a.W]) return;
+  int lo = 0, hi = a.W;  // rank r with rank_off[r] <= i < rank_off[r+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.rank_off[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  const int r = lo, rep = r / a.U;
+  if (a.lens[i] < 0) atomicOr(a.status, ST_NEG_LENGTH);
+  const double wi = seq_workload(a, i);
+  if (a.w_in && !(wi >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);  // balancer.cpp:18-20
+  a.w[i] = wi;
+  a.seq_rank[i] = r;
   const int64_t rlo = a.rank_off[rep * a.U], rhi = a.rank_off[rep * a.U + a.U];
   const int64_t tsize = 2 * (rhi - rlo);
   uint64_t* tab = a.hash + 2 * rlo;
+  const uint64_t id = a.ids[i];
+  if (id == ~0ull) {
+    if (atomicAdd(&a.sentinel[rep], 1) > 0 && !a.w_in) atomicOr(a.status, ST_DUP_ID);
+    return;
+  }
+  uint64_t slot = hash_slot(id) % (uint64_t)tsize;
+  while (true) {
+    const unsigned long long old =
+        atomicCAS(reinterpret_cast<unsigned long long*>(tab + slot), ~0ull, (unsigned long long)id);
+    if (old == ~0ull) break;
+    if (old == id) {
+      if (!a.w_in) atomicOr(a.status, ST_DUP_ID);  // assign_to_bags allows repeats
+      break;
+    }
+    slot = (slot + 1 == (uint64_t)tsize) ? 0 : slot + 1;
+  }
+}
+
+// Per rank: origin packing offsets (block scan of the lengths in buffer order).
+__global__ void __launch_bounds__(256) k_prep_rows(PlanArgs a) {
+  __shared__ int64_t sh[33];
+  const int r = blockIdx.x;
+  if (!seqs_ok(a)) return;
+  const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
   int64_t carry = 0;
   for (int64_t base = lo; base < hi; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < hi;
-    int64_t len = 0;
-    if (valid) {
-      len = a.lens[i];
-      if (len < 0) {
-        atomicOr(a.status, ST_NEG_LENGTH);
-        len = 0;
-      }
-      if (a.w_in) {  // assign_to_bags on caller workloads (balancer.cpp:18-20)
-        const double wi = a.w_in[i];
-        if (!(wi >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
-        a.w[i] = wi;
-      } else {
-        a.w[i] = gamma_weighted_workload(len, a.d_model, a.gamma);  // balancer.cpp:144
-      }
-      a.seq_rank[i] = r;
-      // duplicate sample_id detection inside the replica (open addressing)
-      const uint64_t id = a.ids[i];
-      if (id == ~0ull) {
-        if (atomicAdd(&a.sentinel[rep], 1) > 0 && !a.w_in) atomicOr(a.status, ST_DUP_ID);
-      } else {
-        uint64_t s = hash_slot(id) % (uint64_t)tsize;
-        while (true) {
-          const unsigned long long old =
-              atomicCAS(reinterpret_cast<unsigned long long*>(tab + s), ~0ull, (unsigned long long)id);
-          if (old == ~0ull) break;
-          if (old == id) {
-            if (!a.w_in) atomicOr(a.status, ST_DUP_ID);  // assign_to_bags allows repeats
-            break;
-          }
-          s = (s + 1 == (uint64_t)tsize) ? 0 : s + 1;
-        }
-      }
-    }
+    int64_t len = valid ? a.lens[i] : 0;
+    len = len < 0 ? 0 : len;
     int64_t tot;
     const int64_t ex = block_excl_scan<int64_t>(len, sh, &tot);
     if (valid) a.seq_off[i] = carry + ex;
@@ -322,23 +337,37 @@ __global__ void __launch_bounds__(256) k_totals(PlanArgs a) {
   const int64_t n = hi - lo;
   const int chunks = (int)((n + kTotalsChunk - 1) / kTotalsChunk);
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < kTotalsChunk && i < n; i += blockDim.x) buf[0][i] = a.w[lo + i];
+  // workloads recomputed from the lengths (bit-identical to k_prep_seq's),
+  // so the chain starts with the plan instead of after the per-sequence pass
+  for (int64_t i = threadIdx.x; i < kTotalsChunk && i < n; i += blockDim.x) buf[0][i] = seq_workload(a, lo + i);
   __syncthreads();
   for (int c = 0; c < chunks; ++c) {
     const int64_t nb = (int64_t)(c + 1) * kTotalsChunk;
     for (int64_t i = threadIdx.x; i < kTotalsChunk && nb + i < n; i += blockDim.x)
-      buf[(c + 1) & 1][i] = a.w[lo + nb + i];
+      buf[(c + 1) & 1][i] = seq_workload(a, lo + nb + i);
     if (threadIdx.x == 0) {
       const double* x = buf[c & 1];
       const int cnt = (int)(n - (int64_t)c * kTotalsChunk < kTotalsChunk ? n - (int64_t)c * kTotalsChunk
                                                                           : kTotalsChunk);
+      // software-pipelined: the next 8 loads are in flight under this 8-add chain
       int i = 0;
-      for (; i + 8 <= cnt; i += 8) {
-        double v[8];
+      double v[8], u[8];
+      if (cnt >= 8) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = x[i + k];
+        for (int k = 0; k < 8; ++k) v[k] = x[k];
+      }
+      for (; i + 16 <= cnt; i += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) u[k] = x[i + 8 + k];
 #pragma unroll
         for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = u[k];
+      }
+      if (i + 8 <= cnt) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
+        i += 8;
       }
       for (; i < cnt; ++i) s = __dadd_rn(s, x[i]);
     }
@@ -1080,14 +1109,28 @@ static bool use_small_path(const sb_planner* p) {
   return fits && p->max_chunks <= kSmallChunks;
 }
 
-static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool order) {
-  // serial totals on the side stream, overlapping the sort
+// The serial FP64 totals fork onto the planner's side stream as soon as the
+// metadata is there (they recompute workloads from lengths) and join before
+// the greedy: the chain overlaps the per-sequence pass and the sort.
+static void launch_totals(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
   SB_CUDA(cudaEventRecord(p->fork_ev, s));
   SB_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
   k_totals<<<p->R + 1, 256, 0, p->side>>>(a);
   SB_CHECK_LAUNCH();
   SB_CUDA(cudaEventRecord(p->join_ev, p->side));
-  int launches = 1;
+  count_launch(1);
+}
+
+static void launch_prep(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
+  k_prep_seq<<<(int)((p->max_seqs + 255) / 256), 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_prep_rows<<<p->W, 256, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  count_launch(2);
+}
+
+static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool order) {
+  int launches = 0;
   if (order) {
     const int64_t N = p->max_seqs;
     const int tiles = (int)((N + kSortTile - 1) / kSortTile) + p->R;
@@ -1108,7 +1151,7 @@ static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool o
     SB_CHECK_LAUNCH();
     launches += 2;
   }
-  SB_CUDA(cudaStreamWaitEvent(s, p->join_ev, 0));
+  SB_CUDA(cudaStreamWaitEvent(s, p->join_ev, 0));  // totals joined
   count_launch(launches);
 }
 
@@ -1147,8 +1190,8 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   }
   plan_common_prologue(p, s);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
-  k_prep<<<p->W, 256, 0, s>>>(a);
-  SB_CHECK_LAUNCH();
+  launch_totals(p, a, s);
+  launch_prep(p, a, s);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[1], s));
   launch_sort(p, a, s, true);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[2], s));
@@ -1164,22 +1207,22 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
-  count_launch(6);
+  count_launch(4);
 }
 
 static void run_identity(sb_planner* p, cudaStream_t s) {
   PlanArgs a = make_args(p);
   plan_common_prologue(p, s);
-  k_prep<<<p->W, 256, 0, s>>>(a);
-  SB_CHECK_LAUNCH();
-  launch_sort(p, a, s, false);  // totals only (sorted order unused)
+  launch_totals(p, a, s);
+  launch_prep(p, a, s);
+  launch_sort(p, a, s, false);  // join the totals only (sorted order unused)
   k_identity<<<148, 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   k_identity_report<<<(p->W + 127) / 128, 128, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   k_identity_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
-  count_launch(5);
+  count_launch(3);
 }
 
 }  // namespace sb
@@ -1389,7 +1432,7 @@ extern "C" sb_status sb_plan_manifests(sb_planner* p, sb_stream stream) {
   SB_API_END
 }
 
-// assign_to_bags (balancer.cpp:15-64) on caller workloads: k_prep (workload
+// assign_to_bags (balancer.cpp:15-64) on caller workloads: k_prep_seq (workload
 // validation) -> k_sort (order + total) -> k_greedy, then the assignment in
 // sorted order is copied back.  Host arrays in and out; synchronises.
 extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t* ids, const double* workloads,
@@ -1422,8 +1465,8 @@ extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t*
   p->uploaded = false;
   sb::PlanArgs a = sb::make_args(p);
   sb::plan_common_prologue(p, s);
-  sb::k_prep<<<p->W, 256, 0, s>>>(a);
-  SB_CHECK_LAUNCH();
+  sb::launch_totals(p, a, s);
+  sb::launch_prep(p, a, s);
   sb::launch_sort(p, a, s, true);
   sb::launch_greedy(p, a, s);
   sb::count_launch(2);
