@@ -34,15 +34,16 @@ C2_CODES = ["g2b8i256f1s0", "g2b4i512f1s0", "g2b2i768f1s0", "g2b1i1024f1s0"]
 C3_CODES = ["g1b1i1024f51s1", "g1b1i512f85s1", "g2b2i512f1s0", "g2b4i256f1s0", "g2b1i1024f1s0"]
 PAYLOAD_BYTES = 6144  # 3072 x bf16 per token row (== 768 doubles in the reference)
 META_BYTES = 16       # {sample_id u64, position i64} per row (exchange.hpp:28-29)
+ROPE_BYTES = 16       # RoPE ids per token: (t, h, w) int32 + pad -- a whole-row aux tensor
 
 CONFIGS = {
     "c2": dict(workload="C2: FLUX-like mixed-resolution stream (data_sim g2b8i256f1s0,g2b4i512f1s0,"
                         "g2b2i768f1s0,g2b1i1024f1s0; T5 text U[0,392]), 8 ranks, bags of 1 and 2 "
-                        "(g1n4+g2n2), hidden 3072 bf16 rows + 16 B position metadata",
+                        "(g1n4+g2n2), hidden 3072 bf16 rows + 16 B position metadata + 16 B RoPE ids",
                world=8, topology="g1n4+g2n2", meta=dict(kind="scenario", codes=C2_CODES, step=0, seed=7)),
-    "c1": dict(workload="C1: 8 ranks x 32 seqs, text U[64,512] + image U[256,4096], g1n8, hidden 3072 bf16",
+    "c1": dict(workload="C1: 8 ranks x 32 seqs, text U[64,512] + image U[256,4096], g1n8, hidden 3072 bf16 + RoPE ids",
                world=8, topology="g1n8", meta=dict(kind="c1", seed=1, step=0, per_rank=32)),
-    "c3": dict(workload="C3: image-video joint stream (<=64K-token videos), bags of 4 (g4n2), 24x128 heads",
+    "c3": dict(workload="C3: image-video joint stream (<=64K-token videos), bags of 4 (g4n2), 24x128 heads + RoPE ids",
                world=8, topology="g4n2", meta=dict(kind="scenario", codes=C3_CODES, step=0, seed=7)),
     "c4": dict(workload="C4: plan scaling sweep", world=8, topology="g1n8", meta=dict(kind="c1")),
     "c5": dict(workload="C5: 1000-step dynamic stream", world=8, topology="g1n2+g2n1+g4n1", meta=dict(kind="c1")),
@@ -69,6 +70,20 @@ def load_peaks():
             d = json.load(f)
         return float(d.get("hbm_gbs", 6650.0)), "measured"
     return 6650.0, "fallback"
+
+
+def fill_rope(world, W):
+    """RoPE ids of every origin row: (t, h, w) int32 + pad derived from the
+    row's position (a 64-wide latent grid; text rows share the grid)."""
+    import numpy as np
+    for r in range(W):
+        meta = world.read_rank(0, r).view(np.int64).reshape(-1, 2)
+        pos = meta[:, 1]
+        rope = np.zeros((len(pos), 4), np.int32)
+        rope[:, 0] = (pos // 4096).astype(np.int32)
+        rope[:, 1] = ((pos // 64) % 64).astype(np.int32)
+        rope[:, 2] = (pos % 64).astype(np.int32)
+        world.write_rank(2, r, rope)
 
 
 # ------------------------------------------------------------------ clocks
@@ -464,10 +479,11 @@ def main():
     dm = sb.DeviceMeta.from_lists(ids, lens)
     planner = sb.Planner(topology, W, max_seqs=max(n_seqs, 1))
     G = planner.max_bag
-    mk = lambda: sb.World(W, 24, [PAYLOAD_BYTES], capacity_rows=tokens, max_bag=G)
+    mk = lambda: sb.World(W, 24, [PAYLOAD_BYTES], capacity_rows=tokens, aux_row_bytes=[ROPE_BYTES], max_bag=G)
     A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
     A.layout_origin(dm)
     A.fill_witness(dm)
+    fill_rope(A, W)
     stream = torch.cuda.current_stream()
 
     side = torch.cuda.Stream()
@@ -499,7 +515,7 @@ def main():
     E.status()
     # correctness of what we time: E == A byte for byte
     for r in range(W):
-        assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r)), "round trip not bit-exact"
+        assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), "round trip not bit-exact"
     hp = planner.download()
     per = hp.per_gpu_workload
     max_mean = float(per.max() / per.mean()) if per.mean() > 0 else 1.0
@@ -560,7 +576,8 @@ def main():
         graph_ms = ev0.elapsed_time(ev1) / args.steps
         E.status()
         for r in range(W):
-            assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r)), "graph round trip not bit-exact"
+            assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), \
+                "graph round trip not bit-exact"
         graph_ok = True
         if graph_ms < ms_per_step:
             ms_per_step = graph_ms
@@ -631,7 +648,8 @@ def main():
         pipe_ms = ev0.elapsed_time(ev1) / (2 * pairs)
         E.status()
         for r in range(W):
-            assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r)), "pipelined round trip not bit-exact"
+            assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), \
+                "pipelined round trip not bit-exact"
     except Exception as e:
         pipe_err = f"{type(e).__name__}: {e}"
     ms_per_step_serial = ms_per_step
@@ -666,7 +684,7 @@ def main():
     except Exception:
         pass
 
-    row_bytes = PAYLOAD_BYTES + META_BYTES
+    row_bytes = PAYLOAD_BYTES + META_BYTES + ROPE_BYTES
     route_bytes = 2 * tokens * row_bytes  # every row read once and written once (out-of-place)
     hbm_peak, peak_kind = load_peaks()
     route_kernel_us = us_route / max(1, n_route)
@@ -682,11 +700,10 @@ def main():
             traffic = pj.get("route_copy_dram_bytes")
 
     # ---- e2e through the C-ABI with pinned host buffers
-    host_meta = torch.empty(tokens * META_BYTES, dtype=torch.uint8, pin_memory=True)
-    host_pay = torch.empty(tokens * PAYLOAD_BYTES, dtype=torch.uint8, pin_memory=True)
-    out_meta = torch.empty_like(host_meta).pin_memory()  # empty_like drops pinning
-    out_pay = torch.empty_like(host_pay).pin_memory()
-    A.download([host_meta.data_ptr(), host_pay.data_ptr()], [host_meta.numel(), host_pay.numel()])
+    sizes = [tokens * META_BYTES, tokens * PAYLOAD_BYTES, tokens * ROPE_BYTES]
+    host_in = [torch.empty(n, dtype=torch.uint8).pin_memory() for n in sizes]
+    ptrs_in = [h.data_ptr() for h in host_in]
+    A.download(ptrs_in, sizes)
     torch.cuda.synchronize()
     flat_ids = np.concatenate(ids).view(np.int64)
     flat_lens = np.concatenate(lens)
@@ -695,14 +712,14 @@ def main():
     h_ids = torch.from_numpy(flat_ids.copy()).pin_memory()
     h_lens = torch.from_numpy(flat_lens.copy()).pin_memory()
     h_off = torch.from_numpy(off).pin_memory()
-    h2d = host_meta.numel() + host_pay.numel() + 8 * (len(flat_ids) * 2 + W + 1)
-    d2h = out_meta.numel() + out_pay.numel()
+    h2d = sum(sizes) + 8 * (len(flat_ids) * 2 + W + 1)
+    d2h = sum(sizes)
     # Two in-flight steps: step k's H2D (copy stream) and step k-1's D2H
     # (second copy stream) run on the two DMA engines while the device
     # computes; every step still copies its own inputs in and result out.
     A2s, Es = [mk(), mk()], [E, mk()]
     metas = [sb.DeviceMeta.from_lists(ids, lens), sb.DeviceMeta.from_lists(ids, lens)]
-    outs = [(out_meta, out_pay), (torch.empty_like(host_meta).pin_memory(), torch.empty_like(host_pay).pin_memory())]
+    outs = [[torch.empty(n, dtype=torch.uint8).pin_memory() for n in sizes] for _ in range(2)]
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
@@ -719,7 +736,7 @@ def main():
             m.ids.copy_(h_ids, non_blocking=True)
             m.lens.copy_(h_lens, non_blocking=True)
             m.rank_off.copy_(h_off, non_blocking=True)
-            A2.upload([host_meta.data_ptr(), host_pay.data_ptr()], [host_meta.numel(), host_pay.numel()])
+            A2.upload(ptrs_in, sizes)
             ev_in[i].record(h2d_s)
         stream.wait_event(ev_in[i])
         stream.wait_event(ev_out[i])  # step k-2's result has left Ei
@@ -736,23 +753,23 @@ def main():
         ev_comp[i].record(stream)
         with torch.cuda.stream(d2h_s):
             d2h_s.wait_event(ev_comp[i])
-            Ei.download([outs[i][0].data_ptr(), outs[i][1].data_ptr()], [host_meta.numel(), host_pay.numel()])
+            Ei.download([o.data_ptr() for o in outs[i]], sizes)
             ev_out[i].record(d2h_s)
 
     for k in range(4):
         e2e_step(k)
     torch.cuda.synchronize()
-    for oi, (om, op_) in enumerate(outs):
-        if not (torch.equal(op_, host_pay) and torch.equal(om, host_meta)):
+    for oi, out in enumerate(outs):
+        same = [torch.equal(o, h) for o, h in zip(out, host_in)]
+        if not all(same):
             diag = []
             for w, nm in ((B, "B"), (Cw, "C"), (D, "D"), (Es[oi], "E")):
                 try:
                     w.status()
                 except Exception as ex:
                     diag.append(f"{nm}: {ex}")
-            bad = (op_ != host_pay).nonzero()
-            raise AssertionError(f"e2e round trip not bit-exact (out {oi}; meta equal {torch.equal(om, host_meta)}; "
-                                 f"payload bytes differing {bad.numel()} first {bad[:1].tolist()}; status {diag})")
+            raise AssertionError(f"e2e round trip not bit-exact (out {oi}; meta/payload/rope equal {same}; "
+                                 f"status {diag})")
     e2e_steps = max(4, min(args.steps, 50))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()

@@ -263,23 +263,28 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     planner = Planner(topology, W, max_seqs=max(1, W * cap))
     G = planner.max_bag
     ulysses = G > 1
-    payload, meta_b = 6144, 16
-    mk = lambda: make_world(group, W, 24, [payload], capacity_rows=tokens, max_bag=G)
+    payload, meta_b, rope_b = 6144, 16, 16
+    mk = lambda: make_world(group, W, 24, [payload], capacity_rows=tokens, max_bag=G, aux_row_bytes=(rope_b,))
     A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
     meta = gather.gather()
     gather.status()
     A.layout_origin(meta)
     A.fill_witness(meta)
+    for r in range(first, first + n_local):  # RoPE ids (t, h, w) from positions
+        pos = A.read_rank(0, r).view(np.int64).reshape(-1, 2)[:, 1]
+        rope = np.zeros((len(pos), 4), np.int32)
+        rope[:, 0], rope[:, 1], rope[:, 2] = pos // 4096, (pos // 64) % 64, pos % 64
+        A.write_rank(2, r, rope)
     group.barrier()
     for _ in range(max(3, args.warmup)):
         step(group, gather, planner, A, B, Cw, D, E, ulysses)
     torch.cuda.synchronize()
     E.status()
     for r in range(first, first + n_local):
-        assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r)), "round trip not bit-exact"
+        assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), "round trip not bit-exact"
     cs = group.sum_u64(B.checksum()) == group.sum_u64(A.checksum())
     hp = planner.download()
-    sent, recv = exchange_bytes(hp.c_src, hp.c_dst, hp.c_start, hp.c_end, W, group.size, payload + meta_b)
+    sent, recv = exchange_bytes(hp.c_src, hp.c_dst, hp.c_start, hp.c_end, W, group.size, payload + meta_b + rope_b)
     busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
 
     stream = torch.cuda.current_stream()
@@ -308,25 +313,23 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     # e2e through the public API with host buffers: every step uploads this
     # process's ranks (metadata + payload image) from pinned memory, re-lays
     # out the origin world, runs the step and downloads the restored ranks.
-    mb, pb = A.arena(0)[1], A.arena(1)[1]
     rows_local = int(sum(int(x.sum()) for x in all_lens[first:first + n_local]))
-    h_meta = torch.empty(rows_local * meta_b, dtype=torch.uint8).pin_memory()
-    h_pay = torch.empty(rows_local * payload, dtype=torch.uint8).pin_memory()
-    o_meta, o_pay = torch.empty_like(h_meta).pin_memory(), torch.empty_like(h_pay).pin_memory()
-    A.download([h_meta.data_ptr(), h_pay.data_ptr()], [h_meta.numel(), h_pay.numel()])
+    sizes = [rows_local * meta_b, rows_local * payload, rows_local * rope_b]
+    h_in = [torch.empty(n, dtype=torch.uint8).pin_memory() for n in sizes]
+    h_out = [torch.empty(n, dtype=torch.uint8).pin_memory() for n in sizes]
+    A.download([h.data_ptr() for h in h_in], sizes)
     torch.cuda.synchronize()
-    del mb, pb
 
     def e2e_step():
         gather.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
-        A.upload([h_meta.data_ptr(), h_pay.data_ptr()], [h_meta.numel(), h_pay.numel()])
+        A.upload([h.data_ptr() for h in h_in], sizes)
         m = step(group, gather, planner, A, B, Cw, D, E, ulysses)
-        E.download([o_meta.data_ptr(), o_pay.data_ptr()], [o_meta.numel(), o_pay.numel()])
+        E.download([h.data_ptr() for h in h_out], sizes)
         return m
 
     e2e_step()
     torch.cuda.synchronize()
-    e2e_ok = bool(torch.equal(o_pay, h_pay) and torch.equal(o_meta, h_meta))
+    e2e_ok = all(bool(torch.equal(o, h)) for o, h in zip(h_out, h_in))
     k = max(3, min(args.steps, 20))
     group.barrier()
     torch.cuda.synchronize()
@@ -337,15 +340,15 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     torch.cuda.synchronize()
     e2e_ms = group.max_over_ranks(ev0.elapsed_time(ev1)) / k
     n_meta_local = int(sum(len(x) for x in all_ids[first:first + n_local]))
-    h2d = group.sum_u64(h_meta.numel() + h_pay.numel() + 16 * n_meta_local + 8 * (n_local + 1))
-    d2h = group.sum_u64(o_meta.numel() + o_pay.numel())
+    h2d = group.sum_u64(sum(sizes) + 16 * n_meta_local + 8 * (n_local + 1))
+    d2h = group.sum_u64(sum(sizes))
     per = hp.per_gpu_workload
     line = {
         "metric": metric, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": group.size,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": W,
-                   "tokens_per_step": tokens, "sequences": n_seqs, "row_bytes": payload + meta_b,
+                   "tokens_per_step": tokens, "sequences": n_seqs, "row_bytes": payload + meta_b + rope_b,
                    "parallelism": f"{W} ranks over {group.size} GPUs (peer-store all-to-all)",
                    "barrier": group.mode},
         "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
