@@ -103,3 +103,24 @@ def test_missing_library_is_loud(tmp_path):
             _capi.load(str(tmp_path / "nope.so"))
     finally:
         _capi._lib = saved
+
+
+def test_generator_driver_uniform_config_errors_without_gpu():
+    """Argument validation of the §8(f) entry points runs before any CUDA
+    call, with the reference's messages (simulator.cpp:15-21)."""
+    L = _capi.load()
+    codes = (C.c_char_p * 1)(b"g2b4i256f1s0")
+    sc = C.c_void_p()
+    assert L.sb_scenario_create(codes, 1, 0, C.byref(sc)) == _capi.SB_OK
+    arr = (C.c_void_p * 1)(sc.value)
+    sch = C.c_void_p()
+    st = L.sb_schedule_create(arr, 1, 3, 7, C.byref(sch))  # world 3 not a multiple of group 2
+    assert st == _capi.SB_ERR_CONFIG
+    assert b"is not a multiple of the data sharding group 2" in L.sb_last_error()
+    assert L.sb_schedule_create(arr, 0, 2, 7, C.byref(sch)) == _capi.SB_ERR_CONFIG
+    L.sb_scenario_destroy(sc)
+    d = C.c_void_p()
+    assert L.sb_driver_create(None, None, 24, 6144, 1, 8, C.byref(d)) == _capi.SB_ERR_CONFIG
+    u = C.c_void_p()
+    assert L.sb_uniform_create(0, C.byref(u)) == _capi.SB_ERR_CONFIG
+    assert L.sb_uniform_route(None, 0, 1, None, None, None) == _capi.SB_ERR_CONFIG
