@@ -374,6 +374,10 @@ class World:
     def fill_witness(self, meta: DeviceMeta, stream=None):
         call("sb_world_fill_witness", self._h, *meta.ptrs(), _stream(stream))
 
+    def fill_meta(self, meta: DeviceMeta, stream=None):
+        """Row metadata only (sb_world_fill_meta); payload untouched."""
+        call("sb_world_fill_meta", self._h, *meta.ptrs(), _stream(stream))
+
     def perturb(self, stream=None):
         call("sb_world_perturb", self._h, _stream(stream))
 

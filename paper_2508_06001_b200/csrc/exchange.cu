@@ -677,6 +677,39 @@ __global__ void k_witness(WorldArgs w, TensorInfo ti, const uint64_t* ids, const
   }
 }
 
+// Row metadata {sample_id, position} of the origin layout: one CTA per hosted
+// rank scans the rank's lengths in shared memory, then each warp writes
+// whole sequences (coalesced 16-B stores, no per-row search).
+__global__ void __launch_bounds__(1024) k_fill_meta(WorldArgs w, const uint64_t* ids, const int64_t* rank_off,
+                                                    const int64_t* lens) {
+  __shared__ int64_t sh[33];
+  __shared__ int64_t s_off[1024];
+  const int r = w.first_local + blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t s0 = rank_off[r], s1 = rank_off[r + 1];
+  int64_t carry = 0;
+  for (int64_t b = s0; b < s1; b += blockDim.x) {
+    const int64_t s = b + threadIdx.x;
+    const int64_t l = s < s1 ? (lens[s] > 0 ? lens[s] : 0) : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan<int64_t>(l, sh, &tot);
+    s_off[threadIdx.x] = carry + ex;
+    __syncthreads();
+    for (int64_t q = b + warp; q < s1 && q < b + blockDim.x; q += nw) {
+      const int64_t first = s_off[q - b];
+      const int64_t l2 = lens[q] > 0 ? lens[q] : 0;
+      const uint64_t id = ids[q];
+      for (int64_t pos = lane; pos < l2; pos += 32) {
+        uint64_t* m = reinterpret_cast<uint64_t*>(w.base[r] + (first + pos) * w.pitch[r]);
+        m[0] = id;
+        m[1] = (uint64_t)pos;
+      }
+    }
+    carry += tot;
+    __syncthreads();
+  }
+}
+
 // simulator.cpp:128-136 on hosted full-width ranks.
 __global__ void k_perturb(WorldArgs w, TensorInfo ti) {
   const int lane = threadIdx.x & 31;
@@ -1066,8 +1099,7 @@ extern "C" sb_status sb_world_fill_meta(sb_world* w, const uint64_t* d_ids, cons
                                         const int64_t* d_rank_off, sb_stream stream) {
   SB_API_BEGIN
   if (!w || !d_ids || !d_lens || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_world_fill_meta: null argument"};
-  sb::k_witness<false><<<sb::copy_grid(), 256, 0, (cudaStream_t)stream>>>(sb::wargs(w), sb::tinfo(w), d_ids,
-                                                                          d_rank_off, d_lens);
+  sb::k_fill_meta<<<w->n_local, 1024, 0, (cudaStream_t)stream>>>(sb::wargs(w), d_ids, d_rank_off, d_lens);
   SB_CHECK_LAUNCH();
   sb::count_launch();
   SB_API_END

@@ -133,3 +133,18 @@ def test_world_compare_detects_differences():
     assert a.compare(b) > 0
     a.perturb()
     assert a.compare(b) == 0
+
+
+def test_fill_meta_equals_witness_metadata():
+    """sb_world_fill_meta writes exactly the witness' row metadata."""
+    for codes in C5_SCENARIOS:
+        sch = sb.Schedule([sb.Scenario(codes)], C5_WORLD, C5_SEED)
+        meta = sch.generate(4)
+        mk = lambda: sb.World(C5_WORLD, 24, [192], capacity_rows=sch.max_rows)
+        a, b = mk(), mk()
+        for w in (a, b):
+            w.layout_origin(meta)
+        a.fill_witness(meta)
+        b.fill_meta(meta)
+        for r in range(C5_WORLD):
+            assert np.array_equal(a.read_rank(0, r), b.read_rank(0, r)), r
