@@ -258,6 +258,35 @@ def run_c4(args):
                     r["ref_reverse_plan_us"] = 1e6 * x["reverse_plan_s"]
                 r["speedup_vs_ref"] = r["ref_plan_us"] / r["plan_us"]
     head = next(r for r in rows if r["sequences"] == C4_SIZES[-1] and r["topology"] == "g1n8")
+    # e2e at the headline point: metadata from pinned host memory -> device
+    # plan -> the full plan (chunk SoA, manifests, reverse order, report) back
+    # in host arrays, wall time per call (sb_plan_download synchronises)
+    n = C4_SIZES[-1]
+    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
+    h_ids = torch.from_numpy(np.concatenate(ids).view(np.int64).copy()).pin_memory()
+    h_lens = torch.from_numpy(np.concatenate(lens).copy()).pin_memory()
+    off = np.zeros(9, np.int64)
+    off[1:] = np.cumsum([len(x) for x in ids])
+    h_off = torch.from_numpy(off).pin_memory()
+    dm = sb.DeviceMeta.from_lists(ids, lens)
+    planner = sb.Planner("g1n8", 8, max_seqs=n)
+
+    def e2e_plan():
+        dm.ids[:n].copy_(h_ids, non_blocking=True)
+        dm.lens[:n].copy_(h_lens, non_blocking=True)
+        dm.rank_off.copy_(h_off, non_blocking=True)
+        planner.plan(dm)
+        return planner.download()
+
+    hp = e2e_plan()
+    k = max(3, min(args.steps, 20))
+    t0w = time.perf_counter()
+    for _ in range(k):
+        hp = e2e_plan()
+    e2e_us = 1e6 * (time.perf_counter() - t0w) / k
+    d2h = sum(getattr(hp, f).nbytes for f in ("c_id", "c_idx", "c_start", "c_end", "c_src", "c_dst", "send_off",
+                                               "send_idx", "recv_off", "recv_idx", "rev_recv_idx", "target_rows",
+                                               "per_gpu_workload", "per_bag_occupancy"))
     line = {"metric": "plan latency (plan_routing + reverse receive order) at 16K sequences, 8 ranks, g1n8",
             "value": head["plan_us"], "unit": "us", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": head["plan_us"] / 1000, "higher_is_better": False, "scaling": "strong",
@@ -265,7 +294,9 @@ def run_c4(args):
             "config": {"workload": "C4: solver/plan scaling sweep, 256..16K sequences over 8 ranks "
                                    "(C1 length law, seed 1), topologies " + "/".join(C4_TOPOS),
                        "l2": "metadata-sized inputs (latency-bound; L2 not flushed)"},
-            "sweep": rows, "gpu_launches": int(launches), "clocks": clk.summary()}
+            "sweep": rows, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "e2e": {"value": e2e_us, "unit": "us", "h2d_bytes_per_step": int(16 * n + 8 * 9),
+                    "d2h_bytes_per_step": int(d2h), "note": "host metadata -> device plan -> host plan arrays"}}
     if ref:
         hr = next(r for r in ref if r["sequences"] == C4_SIZES[-1] and r["topology"] == "g1n8")
         line["cpu_baseline"] = {"value": 1e6 * hr["plan_s"], "unit": "us", "cores": 1, "kind": "reference",
@@ -350,6 +381,17 @@ def run_c5(args):
     by_scen = {}
     for r in recs:
         by_scen.setdefault(r["scenario"], []).append(r["max_over_mean"])
+    # e2e through the public API: each step launched by sb_driver_step and
+    # its record read back to the host before the next (inputs are generated
+    # on the device from (seed, step): no host input bytes)
+    drv.set_step(0)
+    e2e_k = 50
+    t0w = time.time()
+    for _ in range(e2e_k):
+        drv.step()
+        drv.progress()  # synchronises: the step's counters / record are final
+    e2e_ms = 1000 * (time.time() - t0w) / e2e_k
+    e2e_tokens = float(tokens[:e2e_k].mean())
     del g, drv
     # verification pass: all steps with simulate_step's inline checks
     vdrv = sb.Driver(planner, sch, n_heads=24, payload_row_bytes=PAYLOAD_BYTES, verify=True, record_cap=steps)
@@ -380,6 +422,9 @@ def run_c5(args):
                    "checks": "route + pre_attn conserve content_checksum; post_attn(pre_attn(x)) == x; perturbed "
                              "payload returns home bitwise (simulator.cpp:106-159)", "wall_s": verify_s},
         "gpu_launches": int(launches), "gpu_launches_per_step": int(launches_per_step), "clocks": clk.summary(),
+        "e2e": {"value": e2e_tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 24, "ms_per_step": e2e_ms,
+                "note": "eager sb_driver_step + synchronous progress read per step (device-generated inputs)"},
     }
     if not args.no_cpu_baseline:
         ref, err = run_reference_stream(steps, budget_s=args.cpu_budget_s)
