@@ -1777,24 +1777,27 @@ __global__ void __launch_bounds__(1024) k_uniform_plan(const int64_t* __restrict
   hdr[1] = moved_total;
 }
 
-// Destination rows (items x rows_per_item) of the exchange and the rows the
-// source must hold.
-__global__ void k_uniform_rows(const int64_t* counts, const int64_t* fin, int W, int64_t rpi, int reverse,
-                               int64_t* rows) {
+// One CTA prepares a uniform exchange: destination rows, the destination
+// layout (with the source-layout check), the item jobs and the piece scan.
+__global__ void __launch_bounds__(1024) k_uniform_prep(const int64_t* counts, const int64_t* fin, const int64_t* mv,
+                                                       const int64_t* hdr, int W, int64_t rpi, int reverse,
+                                                       WorldArgs s, WorldArgs d, TensorInfo ti, int64_t* rows,
+                                                       SbJob* jobs, int64_t* n_jobs, int64_t* piece_off) {
   for (int r = threadIdx.x; r < W; r += blockDim.x) {
-    rows[r] = (reverse ? counts[r] : fin[r]) * rpi;   // destination
+    rows[r] = (reverse ? counts[r] : fin[r]) * rpi;      // destination
     rows[W + r] = (reverse ? fin[r] : counts[r]) * rpi;  // expected source
   }
-}
-
-__global__ void k_uniform_jobs(const int64_t* counts, const int64_t* fin, const int64_t* mv, const int64_t* hdr,
-                               int W, int64_t rpi, int reverse, WorldArgs s, WorldArgs d, TensorInfo ti, SbJob* jobs,
-                               int64_t* n_jobs) {
+  __syncthreads();
+  LayoutPlan lp{};
+  lp.rows_src = rows;
+  lp.expect_rows = rows + W;
+  layout_tensor(d, s, lp, ti, 0, threadIdx.x);
+  __syncthreads();
   const int T = s.T;
   const int64_t total = (int64_t)3 * W * T;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *n_jobs = total;
+  if (threadIdx.x == 0) *n_jobs = total;
   const bool bad = (*d.status & ST_MISMATCH) != 0;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t x = threadIdx.x; x < total; x += blockDim.x) {
     const int t = (int)(x % T);
     const int64_t e = x / T;
     SbJob j;
@@ -1834,6 +1837,8 @@ __global__ void k_uniform_jobs(const int64_t* counts, const int64_t* fin, const 
     }
     jobs[x] = j;
   }
+  __syncthreads();
+  pieces_body(jobs, n_jobs, piece_off, n_jobs + 1);
 }
 
 }  // namespace sb
@@ -1921,20 +1926,11 @@ extern "C" sb_status sb_uniform_route(sb_uniform* u, int reverse, int64_t rows_p
     SB_CUDA(cudaMalloc(&u->piece_off, sizeof(int64_t) * (size_t)(cap + 1)));
     u->job_cap = cap;
   }
-  sb::k_uniform_rows<<<1, 256, 0, s>>>(u->counts, u->final_, u->W, rows_per_item, reverse ? 1 : 0, u->rows);
+  sb::k_uniform_prep<<<1, 1024, 0, s>>>(u->counts, u->final_, u->mv, u->hdr, u->W, rows_per_item, reverse ? 1 : 0,
+                                        sb::wargs(src), sb::wargs(dst), sb::tinfo(src), u->rows, u->jobs, u->n_jobs,
+                                        u->piece_off);
   SB_CHECK_LAUNCH();
-  sb::LayoutPlan lp{};
-  lp.rows_src = u->rows;
-  lp.expect_rows = u->rows + u->W;
-  sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
-  SB_CHECK_LAUNCH();
-  sb::k_uniform_jobs<<<std::max<int64_t>(1, std::min<int64_t>(148, (cap + 255) / 256)), 256, 0, s>>>(
-      u->counts, u->final_, u->mv, u->hdr, u->W, rows_per_item, reverse ? 1 : 0, sb::wargs(src), sb::wargs(dst),
-      sb::tinfo(src), u->jobs, u->n_jobs);
-  SB_CHECK_LAUNCH();
-  sb::k_pieces<<<1, 1024, 0, s>>>(u->jobs, u->n_jobs, u->piece_off, u->n_jobs + 1);
-  SB_CHECK_LAUNCH();
-  sb::count_launch(4);
+  sb::count_launch(1);
   bool tma_ok = true;
   for (int64_t rb : src->row_bytes) tma_ok &= rb % 16 == 0;
   sb::launch_copy(u->jobs, u->piece_off, u->n_jobs, s, dst->n_procs > 1, tma_ok, sb::route_engine());
