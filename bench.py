@@ -735,6 +735,21 @@ def main():
     row_bytes = PAYLOAD_BYTES + META_BYTES + ROPE_BYTES
     route_bytes = 2 * tokens * row_bytes  # every row read once and written once (out-of-place)
     hbm_peak, peak_kind = load_peaks()
+    # context: a plain contiguous device copy of the same bytes (torch copy_,
+    # best of 5) -- the practical peak at this transfer size
+    _src = torch.empty(route_bytes // 2, dtype=torch.uint8, device="cuda")
+    _dst = torch.empty_like(_src)
+    _dst.copy_(_src)
+    torch.cuda.synchronize()
+    size_ms = 1e9
+    for _ in range(5):
+        t0.record(stream)
+        _dst.copy_(_src)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        size_ms = min(size_ms, t0.elapsed_time(t1))
+    size_matched_gbs = route_bytes / (size_ms * 1e-3) / 1e9
+    del _src, _dst
     route_kernel_us = us_route / max(1, n_route)
     achieved = route_bytes / (route_kernel_us * 1e-6) / 1e9
     # Ulysses: rows of multi-GPU bags; metadata replicated to every member
@@ -907,7 +922,9 @@ def main():
                       "pre_attn_copy": us_pre / max(1, n_pre), "post_attn_copy": us_post / max(1, n_post)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_copy (route)", "algorithmic_bytes_per_launch": route_bytes},
+                     "kernel": "k_copy (route)", "algorithmic_bytes_per_launch": route_bytes,
+                     "size_matched_copy_gbs": size_matched_gbs,
+                     "frac_of_size_matched_copy": achieved / size_matched_gbs},
         "a2a_gbs": None,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -1,5 +1,7 @@
-for h in 0 1 2; do for c in 2 4 8; do
-  SEQBAL_COPY_HINT=$h SEQBAL_COPY_CTAS_PER_SM=$c timeout 200 python bench.py --no-cpu-baseline --steps 100 > gpurun_out/sw_${h}_${c}.log 2>&1
+#!/bin/bash
+# Route copy engine knobs on C2 (phases_us per exchange); run under gpurun.
+for h in 0 2; do for c in 4 8 16; do
+  SEQBAL_COPY_HINT=$h SEQBAL_COPY_CTAS_PER_SM=$c timeout 200 python bench.py --no-cpu-baseline --steps 100 > gpurun_out/sw_${h}_${c}.log 2>/dev/null
   python - <<PY
 import json
 d=json.loads(open("gpurun_out/sw_${h}_${c}.log").read().strip().splitlines()[-1])
