@@ -345,6 +345,13 @@ SB_API sb_status sb_driver_create(sb_planner* p, const sb_schedule* s, int n_hea
                                   int verify, int64_t record_cap, sb_driver** out);
 SB_API sb_status sb_driver_destroy(sb_driver* d);
 SB_API sb_status sb_driver_set_step(sb_driver* d, int64_t step, sb_stream stream);  /* synchronises */
+/* Plan-ahead schedule (on != 0): the driver keeps a second slot (a clone of
+ * the planner + five worlds + metadata) and, while step s's copies run,
+ * generates, plans and prepares step s+1 on a side stream; results are
+ * identical to the serial schedule.  Step s+1 is prepared before step s
+ * returns, so a captured graph must hold an even number of steps.
+ * Synchronises; prepares the step the device counter names. */
+SB_API sb_status sb_driver_set_pipeline(sb_driver* d, int on, sb_stream stream);
 SB_API sb_status sb_driver_step(sb_driver* d, sb_stream stream);
 SB_API sb_status sb_driver_run(sb_driver* d, int64_t n_steps, sb_stream stream);
 /* next step index, steps run since set_step, steps whose checks failed (synchronises). */
@@ -352,7 +359,8 @@ SB_API sb_status sb_driver_progress(sb_driver* d, int64_t* next_step, int64_t* s
                                     sb_stream stream);
 SB_API sb_status sb_driver_records(sb_driver* d, sb_step_record* host, int64_t capacity, int64_t* n_out,
                                    sb_stream stream);
-/* which: 0 origin (A), 1 routed (B), 2 Ulysses (C), 3 post_attn (D), 4 returned (E). */
+/* Worlds / metadata of the most recently issued step.
+ * which: 0 origin (A), 1 routed (B), 2 Ulysses (C), 3 post_attn (D), 4 returned (E). */
 SB_API sb_status sb_driver_world(const sb_driver* d, int which, sb_world** out);
 SB_API sb_status sb_driver_meta(const sb_driver* d, const uint64_t** ids, const int64_t** lens,
                                 const int64_t** rank_off);

@@ -151,6 +151,7 @@ _SIGS = {
     "sb_driver_progress": (C.c_int, [C.c_void_p] * 5),
     "sb_driver_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "sb_driver_world": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "sb_driver_set_pipeline": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "sb_driver_meta": (C.c_int, [C.c_void_p] * 4),
     "sb_uniform_create": (C.c_int, [C.c_int, C.c_void_p]),
     "sb_uniform_destroy": (C.c_int, [C.c_void_p]),

@@ -542,6 +542,11 @@ class Driver:
     def set_step(self, step: int, stream=None):
         call("sb_driver_set_step", self._h, int(step), _stream(stream))
 
+    def set_pipeline(self, on: bool = True, stream=None):
+        """Plan-ahead schedule: step s+1 is generated, planned and prepared
+        on a side stream under step s's copies (graphs: even step counts)."""
+        call("sb_driver_set_pipeline", self._h, int(bool(on)), _stream(stream))
+
     def step(self, stream=None):
         call("sb_driver_step", self._h, _stream(stream))
 

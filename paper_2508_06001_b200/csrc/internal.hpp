@@ -154,4 +154,7 @@ struct sb_world {
 
 namespace sb {
 void ensure_jobs(sb_planner* p, int64_t cap);
+// A second planner with p's topology, model and capacity (fresh device
+// scratch; the plan-ahead driver alternates two of them).
+sb_planner* planner_clone(const sb_planner* p);
 }

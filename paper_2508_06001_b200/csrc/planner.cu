@@ -1327,6 +1327,29 @@ extern "C" sb_status sb_planner_create(const sb_planner_desc* d, sb_planner** ou
   SB_API_END
 }
 
+namespace sb {
+sb_planner* planner_clone(const sb_planner* p) {
+  sb_planner_desc d{};
+  d.world_size = p->W;
+  d.unit_size = p->U;
+  d.n_bags = p->M;
+  d.bag_offsets = p->bag_off.data();
+  d.bag_ranks = p->bag_ranks.data();
+  d.d_model = p->d_model;
+  d.n_heads = p->n_heads;
+  d.d_head = p->d_head;
+  d.n_blocks = p->n_blocks;
+  d.gamma = p->gamma;
+  d.k = p->k;
+  d.max_seqs = p->max_seqs;
+  sb_planner* q = nullptr;
+  const sb_status st = sb_planner_create(&d, &q);
+  if (st != SB_OK) throw Error{st, sb_last_error()};
+  q->path = p->path;
+  return q;
+}
+}  // namespace sb
+
 extern "C" sb_status sb_planner_destroy(sb_planner* p) {
   SB_API_BEGIN
   if (p) {

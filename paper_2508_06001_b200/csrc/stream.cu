@@ -407,21 +407,36 @@ extern "C" sb_status sb_schedule_generate(const sb_schedule* s, int64_t step, co
 }
 
 // ---------------------------------------------------------------- driver
-struct sb_driver {
+// One step's device state: its gathered metadata, planner and the five
+// worlds of simulate_step (A origin, B routed, C Ulysses, D post, E returned).
+struct DriverSlot {
   sb_planner* p = nullptr;
-  sb_schedule* s = nullptr;
-  int verify = 0, uly = 0;
-  sb_world* w[5] = {};  // A origin, B routed, C Ulysses, D post, E returned
+  bool own_p = false;
+  sb_world* w[5] = {};
   uint64_t* ids = nullptr;
   int64_t* lens = nullptr;
   int64_t* rank_off = nullptr;
-  int64_t* d_step = nullptr;      // [0] next step; [1] steps run; [2] failed checks
-  int32_t* d_scen = nullptr;
-  uint64_t* d_acc = nullptr;      // [0..2] checksums, [3..4] compare counts
+  int32_t* scen = nullptr;
+  sb_step_record* stage = nullptr;  // the step's record until its copies (and checks) are done
+};
+
+struct sb_driver {
+  sb_schedule* s = nullptr;
+  int verify = 0, uly = 0;
+  int n_heads = 0;
+  int64_t row_bytes = 0;
+  // slot 0 plans with the caller's planner; slot 1 (plan-ahead only) with a clone
+  DriverSlot slot[2];
+  int cur = 0;    // slot of the next step
+  int last = 0;   // slot of the most recently issued step
+  bool pipeline = false, primed = false;
+  int64_t* d_step = nullptr;  // [0] next step; [1] steps run; [2] failed checks; [3] next step to generate
+  uint64_t* d_acc = nullptr;  // [0..2] checksums, [3..4] compare counts
   sb_step_record* d_rec = nullptr;
   int64_t rec_cap = 0;
-  // plan + exchange preparations run on a side stream under the witness
-  // fill and the earlier copies; ev[0] fork, ev[1..4] slot prepared
+  // plan + exchange preparations run on a side stream: under the witness
+  // fill and the earlier copies (serial schedule), or a whole step ahead
+  // (plan-ahead); ev[0] fork, ev[1..4] slot prepared
   cudaStream_t side = nullptr;
   cudaEvent_t ev[5] = {};
 };
@@ -429,10 +444,11 @@ struct sb_driver {
 namespace sb {
 
 // Step record from the device plan + the meta (balancer.hpp:78-89 report,
-// the reference harness's max/mean), and the inline check bits.
-__global__ void k_record(sb_step_record* rec, int64_t cap, const int64_t* d_step, const int32_t* scen,
-                         const int64_t* lens, const int64_t* rank_off, int W, const int64_t* n_chunks,
-                         const double* per_gpu, const double* wir, const double* total, const int32_t* viol) {
+// the reference harness's max/mean).  The step index is the generator's
+// counter, which this kernel advances.
+__global__ void k_record(sb_step_record* stage, int64_t* d_gen, const int32_t* scen, const int64_t* lens,
+                         const int64_t* rank_off, int W, const int64_t* n_chunks, const double* per_gpu,
+                         const double* wir, const double* total, const int32_t* viol) {
   __shared__ int64_t part[32];
   const int64_t n = rank_off[W];
   int64_t t = 0;
@@ -443,8 +459,8 @@ __global__ void k_record(sb_step_record* rec, int64_t cap, const int64_t* d_step
   if (threadIdx.x != 0) return;
   int64_t tokens = 0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tokens += part[w];
-  const int64_t step = d_step[0];
-  sb_step_record& r = rec[step % cap];
+  const int64_t step = *d_gen;
+  sb_step_record& r = *stage;
   r.step = step;
   r.tokens = tokens;
   r.sequences = n;
@@ -462,13 +478,14 @@ __global__ void k_record(sb_step_record* rec, int64_t cap, const int64_t* d_step
   r.capacity_violations = *viol;
   r.checks = 0;
   r.verified = 0;
+  *d_gen = step + 1;
 }
 
-__global__ void k_record_checks(sb_step_record* rec, int64_t cap, int64_t* d_step, const uint64_t* acc, int uly,
-                                int verify) {
+// Closes a step: its record (plus the inline check bits) enters the ring.
+__global__ void k_record_checks(sb_step_record* rec, int64_t cap, int64_t* d_step, const sb_step_record* stage,
+                                const uint64_t* acc, int uly, int verify) {
   if (threadIdx.x != 0) return;
-  const int64_t step = d_step[0];
-  sb_step_record& r = rec[step % cap];
+  sb_step_record r = *stage;
   if (verify) {
     int c = 0;
     c |= acc[1] == acc[0] ? SB_CHECK_ROUTE_CONSERVED : 0;
@@ -480,12 +497,125 @@ __global__ void k_record_checks(sb_step_record* rec, int64_t cap, int64_t* d_ste
     r.checksum = acc[0];
     if (c != SB_CHECK_ALL) d_step[2] += 1;
   }
-  d_step[0] = step + 1;
+  rec[r.step % cap] = r;
+  d_step[0] = r.step + 1;
   d_step[1] += 1;
 }
 
 static void ck(sb_status st) {
   if (st != SB_OK) throw Error{st, sb_last_error()};
+}
+
+static void slot_alloc(sb_driver* d, DriverSlot& x, sb_planner* p, bool own) {
+  x.p = p;
+  x.own_p = own;
+  const int64_t rb[1] = {d->row_bytes};
+  sb_world_desc wd{};
+  wd.world_size = p->W;
+  wd.n_local = p->W;
+  wd.first_local = 0;
+  wd.n_heads = d->n_heads;
+  wd.n_payload = 1;
+  wd.n_aux = 0;
+  wd.row_bytes = rb;
+  wd.capacity_rows = d->s->max_rows;
+  wd.max_bag = p->max_bag;
+  for (auto& w : x.w) ck(sb_world_create(&wd, &w));
+  SB_CUDA(cudaMalloc(&x.ids, sizeof(uint64_t) * (size_t)std::max<int64_t>(1, d->s->max_seqs)));
+  SB_CUDA(cudaMalloc(&x.lens, sizeof(int64_t) * (size_t)std::max<int64_t>(1, d->s->max_seqs)));
+  SB_CUDA(cudaMalloc(&x.rank_off, sizeof(int64_t) * (size_t)(p->W + 1)));
+  SB_CUDA(cudaMalloc(&x.scen, sizeof(int32_t)));
+  SB_CUDA(cudaMalloc(&x.stage, sizeof(sb_step_record)));
+  SB_CUDA(cudaMemset(x.stage, 0, sizeof(sb_step_record)));
+}
+
+static void slot_free(DriverSlot& x) {
+  for (auto& w : x.w)
+    if (w) sb_world_destroy(w);
+  void* ptrs[] = {x.ids, x.lens, x.rank_off, x.scen, x.stage};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (x.own_p && x.p) sb_planner_destroy(x.p);
+  x = DriverSlot{};
+}
+
+static void launch_generate(sb_driver* d, DriverSlot& x, cudaStream_t st) {
+  k_generate<<<d->s->world, 256, 0, st>>>(gen_args(d->s), 0, d->d_step + 3, x.ids, x.lens, x.rank_off, x.scen);
+  SB_CHECK_LAUNCH();
+  count_launch();
+}
+
+static void launch_record(sb_driver* d, DriverSlot& x, cudaStream_t st) {
+  k_record<<<1, 1024, 0, st>>>(x.stage, d->d_step + 3, x.scen, x.lens, x.rank_off, x.p->W, x.p->n_chunks,
+                               x.p->per_gpu, x.p->wir, x.p->total, x.p->violations);
+  SB_CHECK_LAUNCH();
+  count_launch();
+}
+
+static void fill_origin(sb_driver* d, DriverSlot& x, sb_stream st) {
+  // With verification the origin payload is the reference witness (the
+  // checks need it); timed steps write the row metadata only -- the payload
+  // stands for hidden states produced upstream, as the reference's CPU
+  // timing excludes make_world.
+  if (d->verify) ck(sb_world_fill_witness(x.w[0], x.ids, x.lens, x.rank_off, st));
+  else ck(sb_world_fill_meta(x.w[0], x.ids, x.lens, x.rank_off, st));
+}
+
+// Everything of a step that precedes its data movement -- generate, origin
+// layout + rows, plan, record, the four exchange preparations -- on one
+// stream (the plan-ahead schedule runs it a step early on the side stream).
+static void prepare_step(sb_driver* d, DriverSlot& x, cudaStream_t st) {
+  const sb_stream sst = (sb_stream)st;
+  sb_world *A = x.w[0], *B = x.w[1], *C = x.w[2], *D = x.w[3], *E = x.w[4];
+  launch_generate(d, x, st);
+  ck(sb_world_layout_origin(A, x.lens, x.rank_off, sst));
+  fill_origin(d, x, sst);
+  ck(sb_plan(x.p, x.ids, x.lens, x.rank_off, sst));
+  ck(sb_exchange_prepare(x.p, 0, A, B, 0, sst));
+  if (d->uly) {
+    ck(sb_exchange_prepare(x.p, 2, B, C, 2, sst));
+    ck(sb_exchange_prepare(x.p, 3, C, D, 3, sst));
+  }
+  ck(sb_exchange_prepare(x.p, 1, d->uly ? D : B, E, 1, sst));
+  launch_record(d, x, st);
+}
+
+// The data movement of a prepared step, with simulate_step's checks under
+// verify.  `wait` (serial schedule): slot k's copy first waits for ev[k].
+static void move_step(sb_driver* d, DriverSlot& x, cudaStream_t s, bool wait) {
+  const sb_stream st = (sb_stream)s;
+  sb_world *A = x.w[0], *B = x.w[1], *C = x.w[2], *D = x.w[3], *E = x.w[4];
+  sb_world* back_src = d->uly ? D : B;
+  if (d->verify) {
+    SB_CUDA(cudaMemsetAsync(d->d_acc, 0, sizeof(uint64_t) * 5, s));
+    ck(sb_world_checksum(A, d->d_acc + 0, st));
+  }
+  if (wait) SB_CUDA(cudaStreamWaitEvent(s, d->ev[1], 0));
+  ck(sb_exchange_run(x.p, 0, st));
+  if (d->verify) ck(sb_world_checksum(B, d->d_acc + 1, st));
+  if (d->uly) {
+    if (wait) SB_CUDA(cudaStreamWaitEvent(s, d->ev[2], 0));
+    ck(sb_exchange_run(x.p, 2, st));
+    if (d->verify) ck(sb_world_checksum(C, d->d_acc + 2, st));
+    if (wait) SB_CUDA(cudaStreamWaitEvent(s, d->ev[3], 0));
+    ck(sb_exchange_run(x.p, 3, st));
+    if (d->verify) ck(sb_world_compare(D, B, d->d_acc + 3, st));
+  }
+  // simulated transformer output: every row shifts by block_perturbation
+  // (simulator.cpp:128-136); the reverse route must carry it home
+  if (d->verify) ck(sb_world_perturb(back_src, st));
+  if (wait) SB_CUDA(cudaStreamWaitEvent(s, d->ev[4], 0));  // also joins the side stream (record, plan)
+  ck(sb_exchange_run(x.p, 1, st));
+  if (d->verify) {
+    ck(sb_world_perturb(A, st));  // expected: the original world, perturbed
+    ck(sb_world_compare(E, A, d->d_acc + 4, st));
+  }
+}
+
+static void close_step(sb_driver* d, DriverSlot& x, cudaStream_t s) {
+  k_record_checks<<<1, 32, 0, s>>>(d->d_rec, d->rec_cap, d->d_step, x.stage, d->d_acc, d->uly, d->verify);
+  SB_CHECK_LAUNCH();
+  count_launch();
 }
 
 }  // namespace sb
@@ -502,30 +632,16 @@ extern "C" sb_status sb_driver_create(sb_planner* p, const sb_schedule* s, int n
   if (payload_row_bytes <= 0 || payload_row_bytes % 16 != 0 || payload_row_bytes % 8 != 0)
     throw Error{SB_ERR_CONFIG, "payload row bytes must be a positive multiple of 16"};
   sb_driver* d = new sb_driver();
-  d->p = p;
   d->s = const_cast<sb_schedule*>(s);
   d->verify = verify ? 1 : 0;
   d->uly = p->any_multi_bag ? 1 : 0;
+  d->n_heads = n_heads;
+  d->row_bytes = payload_row_bytes;
   d->rec_cap = record_cap > 0 ? record_cap : 1;
   try {
-    const int64_t rb[1] = {payload_row_bytes};
-    sb_world_desc wd{};
-    wd.world_size = p->W;
-    wd.n_local = p->W;
-    wd.first_local = 0;
-    wd.n_heads = n_heads;
-    wd.n_payload = 1;
-    wd.n_aux = 0;
-    wd.row_bytes = rb;
-    wd.capacity_rows = s->max_rows;
-    wd.max_bag = p->max_bag;
-    for (auto& w : d->w) sb::ck(sb_world_create(&wd, &w));
-    SB_CUDA(cudaMalloc(&d->ids, sizeof(uint64_t) * (size_t)std::max<int64_t>(1, s->max_seqs)));
-    SB_CUDA(cudaMalloc(&d->lens, sizeof(int64_t) * (size_t)std::max<int64_t>(1, s->max_seqs)));
-    SB_CUDA(cudaMalloc(&d->rank_off, sizeof(int64_t) * (size_t)(p->W + 1)));
-    SB_CUDA(cudaMalloc(&d->d_step, sizeof(int64_t) * 3));
-    SB_CUDA(cudaMemset(d->d_step, 0, sizeof(int64_t) * 3));
-    SB_CUDA(cudaMalloc(&d->d_scen, sizeof(int32_t)));
+    sb::slot_alloc(d, d->slot[0], p, false);
+    SB_CUDA(cudaMalloc(&d->d_step, sizeof(int64_t) * 4));
+    SB_CUDA(cudaMemset(d->d_step, 0, sizeof(int64_t) * 4));
     SB_CUDA(cudaMalloc(&d->d_acc, sizeof(uint64_t) * 5));
     SB_CUDA(cudaMalloc(&d->d_rec, sizeof(sb_step_record) * (size_t)d->rec_cap));
     SB_CUDA(cudaMemset(d->d_rec, 0, sizeof(sb_step_record) * (size_t)d->rec_cap));
@@ -541,9 +657,8 @@ extern "C" sb_status sb_driver_create(sb_planner* p, const sb_schedule* s, int n
 
 extern "C" sb_status sb_driver_destroy(sb_driver* d) {
   if (!d) return SB_OK;
-  for (auto& w : d->w)
-    if (w) sb_world_destroy(w);
-  void* ptrs[] = {d->ids, d->lens, d->rank_off, d->d_step, d->d_scen, d->d_acc, d->d_rec};
+  for (auto& x : d->slot) sb::slot_free(x);
+  void* ptrs[] = {d->d_step, d->d_acc, d->d_rec};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& e : d->ev)
@@ -556,84 +671,112 @@ extern "C" sb_status sb_driver_destroy(sb_driver* d) {
 extern "C" sb_status sb_driver_set_step(sb_driver* d, int64_t step, sb_stream stream) {
   SB_API_BEGIN
   if (!d || step < 0) throw Error{SB_ERR_CONFIG, "sb_driver_set_step: bad argument"};
-  const int64_t v[3] = {step, 0, 0};
-  SB_CUDA(cudaMemcpyAsync(d->d_step, v, sizeof v, cudaMemcpyHostToDevice, (cudaStream_t)stream));
-  SB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t v[4] = {step, 0, 0, step};
+  SB_CUDA(cudaMemcpyAsync(d->d_step, v, sizeof v, cudaMemcpyHostToDevice, s));
+  d->primed = false;
+  if (d->pipeline) {  // plan-ahead: the first step is prepared now
+    sb::prepare_step(d, d->slot[d->cur], s);
+    d->primed = true;
+  }
+  SB_CUDA(cudaStreamSynchronize(s));
+  SB_API_END
+}
+
+extern "C" sb_status sb_driver_set_pipeline(sb_driver* d, int on, sb_stream stream) {
+  SB_API_BEGIN
+  if (!d) throw Error{SB_ERR_CONFIG, "null driver"};
+  cudaStream_t s = (cudaStream_t)stream;
+  SB_CUDA(cudaStreamSynchronize(s));
+  if (on && !d->slot[1].p) {
+    sb_planner* q = sb::planner_clone(d->slot[0].p);
+    try {
+      sb::slot_alloc(d, d->slot[1], q, true);
+    } catch (...) {
+      if (!d->slot[1].p) sb_planner_destroy(q);
+      sb::slot_free(d->slot[1]);
+      throw;
+    }
+  }
+  d->pipeline = on != 0;
+  d->cur = 0;
+  d->last = 0;
+  d->primed = false;
+  // resume at the step the device counter names (a prepared-ahead step is dropped)
+  SB_CUDA(cudaMemcpyAsync(d->d_step + 3, d->d_step, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  if (d->pipeline) {
+    sb::prepare_step(d, d->slot[0], s);
+    d->primed = true;
+  }
+  SB_CUDA(cudaStreamSynchronize(s));
   SB_API_END
 }
 
 // One step (simulate_step, simulator.cpp:45-178, on the device path).
 // Stream-ordered, no host synchronisation: capturable into a CUDA graph
-// whose replays advance the device step counter.  Schedule:
-//   main: generate -> origin layout -> witness fill -> [checks] -> route copy
-//         -> pre copy -> post copy -> reverse copy -> record
-//   side: plan -> record plan -> prepare route / pre / post / reverse
+// whose replays advance the device step counter.
+// Serial schedule:
+//   main: generate -> origin layout -> origin fill -> route copy -> pre copy
+//         -> post copy -> reverse copy -> close
+//   side: plan -> prepare route / pre / post / reverse -> record
 // (preparations touch only the plan and world tables, never payload, so the
-// plan and every layout + job build run under the witness fill and the
-// earlier copies; each copy waits for its own preparation).
+// plan and every layout + job build run under the fill and the earlier
+// copies; each copy waits for its own preparation).
+// Plan-ahead schedule (sb_driver_set_pipeline): two slots alternate; while
+// step s's copies run on the main stream, the side stream generates, lays
+// out, fills, plans and prepares step s+1 in the other slot, joining before
+// step s closes.  A graph must therefore hold an even number of steps.
 extern "C" sb_status sb_driver_step(sb_driver* d, sb_stream stream) {
   SB_API_BEGIN
   if (!d) throw Error{SB_ERR_CONFIG, "null driver"};
   cudaStream_t s = (cudaStream_t)stream;
   sb_stream side = (sb_stream)d->side;
-  sb_world *A = d->w[0], *B = d->w[1], *C = d->w[2], *D = d->w[3], *E = d->w[4];
-  sb::k_generate<<<d->s->world, 256, 0, s>>>(gen_args(d->s), 0, d->d_step, d->ids, d->lens, d->rank_off, d->d_scen);
-  SB_CHECK_LAUNCH();
-  sb::count_launch();
-  sb::ck(sb_world_layout_origin(A, d->lens, d->rank_off, stream));
+  if (d->pipeline) {
+    DriverSlot& x = d->slot[d->cur];
+    DriverSlot& y = d->slot[d->cur ^ 1];
+    if (!d->primed) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      SB_CUDA(cudaStreamIsCapturing(s, &cs));
+      if (cs != cudaStreamCaptureStatusNone)
+        throw Error{SB_ERR_CONFIG, "plan-ahead driver: run set_step or one eager step before graph capture"};
+      sb::prepare_step(d, x, s);
+      d->primed = true;
+    }
+    SB_CUDA(cudaEventRecord(d->ev[0], s));
+    SB_CUDA(cudaStreamWaitEvent(d->side, d->ev[0], 0));
+    sb::prepare_step(d, y, d->side);
+    SB_CUDA(cudaEventRecord(d->ev[1], d->side));
+    sb::move_step(d, x, s, false);
+    SB_CUDA(cudaStreamWaitEvent(s, d->ev[1], 0));
+    sb::close_step(d, x, s);
+    d->last = d->cur;
+    d->cur ^= 1;
+    return SB_OK;
+  }
+  DriverSlot& x = d->slot[0];
+  sb_world *A = x.w[0], *B = x.w[1], *C = x.w[2], *D = x.w[3], *E = x.w[4];
+  sb::launch_generate(d, x, s);
+  sb::ck(sb_world_layout_origin(A, x.lens, x.rank_off, stream));
   SB_CUDA(cudaEventRecord(d->ev[0], s));
   SB_CUDA(cudaStreamWaitEvent(d->side, d->ev[0], 0));
-  // side: plan, record, preparations
-  sb::ck(sb_plan(d->p, d->ids, d->lens, d->rank_off, side));
-  sb::k_record<<<1, 1024, 0, d->side>>>(d->d_rec, d->rec_cap, d->d_step, d->d_scen, d->lens, d->rank_off, d->p->W,
-                                        d->p->n_chunks, d->p->per_gpu, d->p->wir, d->p->total, d->p->violations);
-  SB_CHECK_LAUNCH();
-  sb::count_launch();
-  sb_world* back_src = d->uly ? D : B;
-  sb::ck(sb_exchange_prepare(d->p, 0, A, B, 0, side));
+  // side: plan, preparations, record
+  sb::ck(sb_plan(x.p, x.ids, x.lens, x.rank_off, side));
+  sb::ck(sb_exchange_prepare(x.p, 0, A, B, 0, side));
   SB_CUDA(cudaEventRecord(d->ev[1], d->side));
   if (d->uly) {
-    sb::ck(sb_exchange_prepare(d->p, 2, B, C, 2, side));
+    sb::ck(sb_exchange_prepare(x.p, 2, B, C, 2, side));
     SB_CUDA(cudaEventRecord(d->ev[2], d->side));
-    sb::ck(sb_exchange_prepare(d->p, 3, C, D, 3, side));
+    sb::ck(sb_exchange_prepare(x.p, 3, C, D, 3, side));
     SB_CUDA(cudaEventRecord(d->ev[3], d->side));
   }
-  sb::ck(sb_exchange_prepare(d->p, 1, back_src, E, 1, side));
+  sb::ck(sb_exchange_prepare(x.p, 1, d->uly ? D : B, E, 1, side));
+  sb::launch_record(d, x, d->side);
   SB_CUDA(cudaEventRecord(d->ev[4], d->side));
-  // main: input synthesis, then the copies as their preparations land.  With
-  // verification the origin payload is the reference witness (the checks
-  // need it); timed steps write the row metadata only -- the payload stands
-  // for hidden states produced upstream, as the reference's CPU timing
-  // excludes make_world.
-  if (d->verify) sb::ck(sb_world_fill_witness(A, d->ids, d->lens, d->rank_off, stream));
-  else sb::ck(sb_world_fill_meta(A, d->ids, d->lens, d->rank_off, stream));
-  if (d->verify) {
-    SB_CUDA(cudaMemsetAsync(d->d_acc, 0, sizeof(uint64_t) * 5, s));
-    sb::ck(sb_world_checksum(A, d->d_acc + 0, stream));
-  }
-  SB_CUDA(cudaStreamWaitEvent(s, d->ev[1], 0));
-  sb::ck(sb_exchange_run(d->p, 0, stream));
-  if (d->verify) sb::ck(sb_world_checksum(B, d->d_acc + 1, stream));
-  if (d->uly) {
-    SB_CUDA(cudaStreamWaitEvent(s, d->ev[2], 0));
-    sb::ck(sb_exchange_run(d->p, 2, stream));
-    if (d->verify) sb::ck(sb_world_checksum(C, d->d_acc + 2, stream));
-    SB_CUDA(cudaStreamWaitEvent(s, d->ev[3], 0));
-    sb::ck(sb_exchange_run(d->p, 3, stream));
-    if (d->verify) sb::ck(sb_world_compare(D, B, d->d_acc + 3, stream));
-  }
-  // simulated transformer output: every row shifts by block_perturbation
-  // (simulator.cpp:128-136); the reverse route must carry it home
-  if (d->verify) sb::ck(sb_world_perturb(back_src, stream));
-  SB_CUDA(cudaStreamWaitEvent(s, d->ev[4], 0));  // also joins the side stream (record, plan)
-  sb::ck(sb_exchange_run(d->p, 1, stream));
-  if (d->verify) {
-    sb::ck(sb_world_perturb(A, stream));  // expected: the original world, perturbed
-    sb::ck(sb_world_compare(E, A, d->d_acc + 4, stream));
-  }
-  sb::k_record_checks<<<1, 32, 0, s>>>(d->d_rec, d->rec_cap, d->d_step, d->d_acc, d->uly, d->verify);
-  SB_CHECK_LAUNCH();
-  sb::count_launch();
+  // main: input synthesis, then the copies as their preparations land
+  sb::fill_origin(d, x, stream);
+  sb::move_step(d, x, s, true);
+  sb::close_step(d, x, s);
+  d->last = 0;
   SB_API_END
 }
 
@@ -677,7 +820,7 @@ extern "C" sb_status sb_driver_records(sb_driver* d, sb_step_record* host, int64
 extern "C" sb_status sb_driver_world(const sb_driver* d, int which, sb_world** out) {
   SB_API_BEGIN
   if (!d || !out || which < 0 || which > 4) throw Error{SB_ERR_CONFIG, "sb_driver_world: bad argument"};
-  *out = d->w[which];
+  *out = d->slot[d->last].w[which];
   SB_API_END
 }
 
@@ -685,8 +828,9 @@ extern "C" sb_status sb_driver_meta(const sb_driver* d, const uint64_t** ids, co
                                     const int64_t** rank_off) {
   SB_API_BEGIN
   if (!d) throw Error{SB_ERR_CONFIG, "null driver"};
-  if (ids) *ids = d->ids;
-  if (lens) *lens = d->lens;
-  if (rank_off) *rank_off = d->rank_off;
+  const DriverSlot& x = d->slot[d->last];
+  if (ids) *ids = x.ids;
+  if (lens) *lens = x.lens;
+  if (rank_off) *rank_off = x.rank_off;
   SB_API_END
 }

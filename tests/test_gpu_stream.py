@@ -118,6 +118,53 @@ def test_driver_step_graph_replay_advances():
         assert recs[s]["checks"] == 15
 
 
+def test_driver_plan_ahead_matches_serial():
+    """The plan-ahead schedule (step s+1 prepared under step s's copies, two
+    alternating slots) gives the serial schedule's records, checks and
+    worlds; an even-length graph of it replays with the counter advancing."""
+    import torch
+    n = 12
+    sch, planner, ser = _c5_driver(width=192, cap=32)
+    ser.set_step(0)
+    ser.run(n)
+    ser_recs = ser.records()
+    ser_sum = ser.world(4).checksum()
+    _, planner2, pip = _c5_driver(width=192, cap=32)
+    pip.set_pipeline(True)
+    pip.set_step(0)
+    pip.run(n)
+    prog = pip.progress()
+    assert prog == {"next_step": n, "steps_run": n, "failed": 0}
+    pip_recs = pip.records()
+    for s in range(n):
+        a, b = ser_recs[s], pip_recs[s]
+        assert a == b, s
+        assert a["verified"] == 1 and a["checks"] == 15
+    assert pip.world(4).checksum() == ser_sum
+    # graph of two steps, replayed: steps n .. n+5
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pip.step()
+        pip.step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    prog = pip.progress()
+    assert prog["next_step"] == n + 6 and prog["failed"] == 0
+    recs = {r["step"]: r for r in pip.records() if r["verified"]}
+    for s in range(n, n + 6):
+        gold = next((x for x in STREAM["per_step"] if x["step"] == s), None)
+        assert recs[s]["checks"] == 15
+        if gold:
+            assert f"{dbits(recs[s]['wir']):016x}" == gold["wir"]
+    # back to the serial schedule at the device counter
+    pip.set_pipeline(False)
+    pip.step()
+    assert pip.progress()["next_step"] == n + 7
+    r = {x["step"]: x for x in pip.records()}[n + 6]
+    assert r["checks"] == 15
+
+
 def test_world_compare_detects_differences():
     """The check primitive the driver relies on: equal worlds compare 0,
     a perturbed copy does not, and perturbing both restores equality."""
