@@ -84,11 +84,30 @@ __device__ __forceinline__ double gamma_weighted_workload(int64_t len, double d,
   return __dadd_rn(lin, att);
 }
 
+// l = q * g + r for a sequence length l >= 0 and a bag size g >= 1: 32-bit
+// division whenever l fits (every realistic length; the 64-bit divide is a
+// ~70-instruction subroutine).
+__device__ __forceinline__ void len_divmod(int64_t l, int g, int64_t& q, int& r) {
+  if ((uint64_t)l <= 0xffffffffull) {
+    const uint32_t l32 = (uint32_t)l, q32 = l32 / (uint32_t)g;
+    q = q32;
+    r = (int)(l32 - q32 * (uint32_t)g);
+  } else {
+    q = l / g;
+    r = (int)(l - q * g);
+  }
+}
+// chunk_lengths (balancer.cpp:66-82): chunk k of a length-l sequence split g ways
 __device__ __forceinline__ int64_t chunk_len(int64_t l, int g, int k) {
-  return l / g + (k < (int)(l % g) ? 1 : 0);
+  int64_t q;
+  int r;
+  len_divmod(l, g, q, r);
+  return q + (k < r ? 1 : 0);
 }
 __device__ __forceinline__ int64_t chunk_start(int64_t l, int g, int k) {
-  const int64_t q = l / g, r = l % g;
+  int64_t q;
+  int r;
+  len_divmod(l, g, q, r);
   return (int64_t)k * q + (k < r ? k : r);
 }
 

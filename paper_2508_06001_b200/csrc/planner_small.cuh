@@ -96,6 +96,107 @@ __device__ void smem_bitonic(uint64_t* hi, uint64_t* lo, uint32_t* v, int n, int
   }
 }
 
+// Branch-free (key, id, index) order for the register sort.
+__device__ __forceinline__ bool rec_less_bf(uint64_t ahi, uint64_t alo, uint32_t av, uint64_t bhi, uint64_t blo,
+                                            uint32_t bv) {
+  return (ahi < bhi) | ((ahi == bhi) & ((alo < blo) | ((alo == blo) & (av < bv))));
+}
+
+// Bitonic sort with the records in registers: thread x holds records
+// x + r * B (r < RPT, B = kSmallThreads) of T = pow2 >= n (slots >= n are
+// +inf padding).  T is a template parameter, so all (log2 T)(log2 T + 1)/2
+// stages unroll: partners at distance j < 32 are exchanged by shuffles,
+// 32 <= j < B through shared memory (the only barriers: n = 256 has 6 of
+// 36 stages), j == B inside the thread.  Leaves the record of rank
+// x + r * B in (h, l, v)[r].
+template <int T, int RPT>
+__device__ void reg_bitonic(uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int n, uint64_t (&h)[RPT],
+                            uint64_t (&l)[RPT], uint32_t (&v)[RPT]) {
+  constexpr int B = kSmallThreads;
+  static_assert(T <= RPT * B && (RPT == 1 || T == RPT * B), "register bitonic shape");
+  const int tid = threadIdx.x;
+  const bool live = RPT > 1 || (tid & ~31) < T;  // warp-uniform
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int x = tid + r * B;
+    h[r] = x < n ? s_hi[x] : ~0ull;
+    l[r] = x < n ? s_lo[x] : ~0ull;
+    v[r] = x < n ? s_v[x] : 0xffffffffu;
+  }
+#pragma unroll
+  for (int k = 2; k <= T; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= B) {  // RPT == 2, j == B: the partner is this thread's other record; k > B, so ascending
+        if (rec_less_bf(h[RPT - 1], l[RPT - 1], v[RPT - 1], h[0], l[0], v[0])) {
+          const uint64_t a = h[0], b = l[0];
+          const uint32_t c = v[0];
+          h[0] = h[RPT - 1]; l[0] = l[RPT - 1]; v[0] = v[RPT - 1];
+          h[RPT - 1] = a; l[RPT - 1] = b; v[RPT - 1] = c;
+        }
+        continue;
+      }
+      uint64_t ph[RPT], pl[RPT];
+      uint32_t pv[RPT];
+      if (j >= 32) {
+        __syncthreads();  // the previous exchange's reads are done
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int x = tid + r * B;
+          if (x < T) {
+            s_hi[x] = h[r];
+            s_lo[x] = l[r];
+            s_v[x] = v[r];
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int x = tid + r * B;
+          const int p = x < T ? (x ^ j) : x;  // x >= T: padding stays (never read back)
+          ph[r] = x < T ? s_hi[p] : h[r];
+          pl[r] = x < T ? s_lo[p] : l[r];
+          pv[r] = x < T ? s_v[p] : v[r];
+        }
+      } else {
+        if (!live) continue;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          ph[r] = __shfl_xor_sync(0xffffffffu, h[r], j);
+          pl[r] = __shfl_xor_sync(0xffffffffu, l[r], j);
+          pv[r] = __shfl_xor_sync(0xffffffffu, v[r], j);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int x = tid + r * B;
+        const bool up = (x & k) == 0, lower = (x & j) == 0;
+        const bool pless = rec_less_bf(ph[r], pl[r], pv[r], h[r], l[r], v[r]);
+        const bool take = (lower == up) ? pless : !pless;  // records are unique; equal padding swaps to itself
+        h[r] = take ? ph[r] : h[r];
+        l[r] = take ? pl[r] : l[r];
+        v[r] = take ? pv[r] : v[r];
+      }
+    }
+  }
+}
+
+template <int T, int RPT>
+__device__ void reg_sort_emit(const PlanArgs& a, uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int32_t* s_sorted,
+                              int64_t lo, int n) {
+  uint64_t h[RPT], l[RPT];
+  uint32_t v[RPT];
+  reg_bitonic<T, RPT>(s_hi, s_lo, s_v, n, h, l, v);
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int x = threadIdx.x + r * kSmallThreads;
+    if (x < n) {
+      s_sorted[lo + x] = (int32_t)(lo + v[r]);
+      a.sorted_idx[lo + x] = (int32_t)(lo + v[r]);
+    }
+  }
+}
+
 // Warp-level inclusive scan helper over int64.
 __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_incl_scan<int64_t>(x); }
 
@@ -110,7 +211,7 @@ __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, 
 __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int64_t sh[33];
-  __shared__ int s_flag, s_viol;
+  __shared__ int s_flag, s_viol, s_biglen;
   __shared__ int warp_cnt[32][kMaxBags];
   __shared__ int running[kMaxBags];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -145,6 +246,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   if (tid == 0) {
     s_flag = 0;
     s_viol = 0;
+    s_biglen = 0;
   }
   __syncthreads();
   const int64_t N = s_roff[W];
@@ -173,6 +275,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
     } else {
       wv = gamma_weighted_workload(len, a.d_model, a.gamma);
     }
+    if (len >= (int64_t)1 << 26) s_biglen = 1;  // 32 lengths no longer sum in 32 bits
     s_ids[i] = a.ids[i];
     s_lens[i] = len;
     s_w[i] = wv;
@@ -267,7 +370,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       s_v[i] = (uint32_t)i;
     }
     __syncthreads();
-    if (n <= 1024) {
+    if (n > 32 && n <= 2 * kSmallThreads && blockDim.x == kSmallThreads) {
+      const int nn = (int)n;
+      if (nn <= 64) reg_sort_emit<64, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
+      else if (nn <= 128) reg_sort_emit<128, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
+      else if (nn <= 256) reg_sort_emit<256, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
+      else if (nn <= 512) reg_sort_emit<512, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
+      else reg_sort_emit<1024, 2>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
+    } else if (n <= 1024) {
       // rank by counting: the key (~bits(w), id, index) is a total order.
       // k = blockDim/n lanes (power of two <= 32) share one record's count,
       // each over a slice of the candidates (broadcast smem reads), then a
@@ -364,23 +474,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       if (valid) {
         const int q = warp_cnt[warp][b] + rank_in;
         const int s = s_sorted[p];
-        const int64_t l = s_lens[s];
         const int g = a.bag_size[b];
         const int64_t cb = s_bagcb[rep * M + b] + (int64_t)q * g;
-        const uint64_t id = s_ids[s];
         const int src = s_rank[s];
-        for (int k = 0; k < g; ++k) {
-          const int64_t c = cb + k;
-          const int64_t st = chunk_start(l, g, k);
-          a.c_id[c] = id;
-          a.c_idx[c] = k;
-          a.c_start[c] = st;
-          a.c_end[c] = st + chunk_len(l, g, k);
-          a.c_src[c] = src;
-          a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
-          a.c_src_row[c] = s_soff[s] + st;
-          a.c_seq[c] = s;
-        }
         s_G[s] = g;
         s_cb[s] = cb;
         s_bo[s_bagq[rep * M + b] + q] = s;
@@ -391,6 +487,39 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       __syncthreads();
     }
   }
+  // chunk emission, one thread per chunk (coalesced stores): bag rb =
+  // (rep, b) holds chunks [bagcb[rb], bagcb[rb] + count * g) in its
+  // sequences' bag order; a chunk finds its bag by binary search
+  {
+    const int RM = R * M;
+    const int64_t total = s_bagcb[RM - 1] + (int64_t)s_bagcnt[RM - 1] * a.bag_size[M - 1];
+    for (int64_t c = tid; c < total; c += blockDim.x) {
+      int blo = 0, bhi = RM;  // last bag with base <= c (empty bags share the base of the next)
+      while (bhi - blo > 1) {
+        const int mid = (blo + bhi) >> 1;
+        if (s_bagcb[mid] <= c) blo = mid;
+        else bhi = mid;
+      }
+      const int rep = blo / M, b = blo - rep * M;
+      const int g = a.bag_size[b];
+      const uint32_t e = (uint32_t)(c - s_bagcb[blo]);
+      const int q = (int)(e / (uint32_t)g), k = (int)(e - (uint32_t)q * (uint32_t)g);
+      const int s = s_bo[s_bagq[blo] + q];
+      int64_t cq;
+      int cr;
+      len_divmod(s_lens[s], g, cq, cr);
+      const int64_t st = (int64_t)k * cq + (k < cr ? k : cr);
+      a.c_id[c] = s_ids[s];
+      a.c_idx[c] = k;
+      a.c_start[c] = st;
+      a.c_end[c] = st + cq + (k < cr ? 1 : 0);
+      a.c_src[c] = s_rank[s];
+      a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
+      a.c_src_row[c] = s_soff[s] + st;
+      a.c_seq[c] = s;
+    }
+  }
+  __syncthreads();
   SB_PHASE(9);
   // ---- phase 9: manifest offsets (balancer.cpp:84-91)
   if (tid == 0) {
@@ -424,8 +553,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       const int s = valid ? s_bo[bq + q] : 0;
       const int64_t l = valid ? s_lens[s] : 0;
       const int64_t len = valid ? chunk_len(l, g, k) : 0;
-      const int64_t inc = warp_scan_incl64(len);
-      const int64_t inc2 = k == 0 ? warp_scan_incl64(l) : 0;
+      int64_t inc, inc2 = 0;
+      if (!s_biglen) {  // block-uniform: every 32-lane partial sum fits in 32 bits
+        inc = warp_incl_scan<int>((int)len);
+        if (k == 0) inc2 = warp_incl_scan<int>((int)l);
+      } else {
+        inc = warp_scan_incl64(len);
+        if (k == 0) inc2 = warp_scan_incl64(l);
+      }
       if (valid) {
         const int64_t c = s_cb[s] + k;
         a.c_dst_row[c] = carry + inc - len;
@@ -448,7 +583,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       const bool valid = i < s1;
       const int gs = valid ? s_G[i] : 0;
       tie |= gs > 1 && s_lens[i] < gs;
-      const int64_t inc = warp_scan_incl64(gs);
+      const int64_t inc = warp_incl_scan<int>(gs);  // <= 32 * kMaxBags
       if (valid)
         for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[s_sendoff[r] + c4 + inc - gs + kk] = (int32_t)(s_cb[i] + kk);
       c4 += __shfl_sync(0xffffffffu, inc, 31);

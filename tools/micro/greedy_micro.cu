@@ -457,6 +457,78 @@ __global__ void g_v7(const double* w_sorted, int n, int M, const double* caps, i
   if (lane == 0) { *cyc = t1 - t0; *replays = nrep; }
 }
 
+// Order-preserving image of an occupancy with the lane in the low 5 bits:
+// [0][exp-992:6][mantissa:52][lane:5] -- exact for 0 and for normal values
+// with biased exponent in [993, 1054]; anything else sets `oor`.
+__device__ __forceinline__ uint64_t occ_img(double occ, uint32_t lane, uint32_t& oor) {
+  const uint64_t b = (uint64_t)__double_as_longlong(occ);
+  const uint32_t e = (uint32_t)(b >> 52);
+  oor |= (uint32_t)(b != 0ull) & (uint32_t)((e - 993u) > 61u);
+  const uint64_t img = (b - (992ull << 52)) << 5;
+  return (b == 0ull ? 0ull : img) | lane;
+}
+// V8: two REDUX on lane-folded exact keys + two-level speculation (the
+// state after a win and all four candidate keys of step t+1 are formed
+// during step t for both outcomes of step t), flat loop over a staged
+// workload array; any out-of-range occupancy reruns with the exact
+// three-REDUX loop.
+__global__ void g_v8(const double* w_sorted, int n, int M, const double* caps, int* pick, long long* cyc,
+                     int* replays) {
+  extern __shared__ double wsd[];
+  const int lane = threadIdx.x;
+  const bool act = lane < M;
+  const double cap = act ? caps[lane] : 0.0;
+  const double rcap = cap > 0.0 ? __drcp_rn(cap) : 0.0;
+  for (int i = lane; i < n + 2; i += 32) wsd[i] = i < n ? w_sorted[i] : 0.0;
+  __syncwarp();
+  long long t0 = clock64();
+  const uint64_t inact = act ? 0ull : ~0ull;
+  const uint64_t HI = 1ull << 63;
+  uint32_t oor = 0;
+  double asg = 0.0, rem = __dsub_rn(cap, 0.0);
+  uint64_t img = occ_img(occ_sel(0.0, cap, rcap), lane, oor);
+  double nasg = __dadd_rn(asg, wsd[0]);
+  double nrem = __dsub_rn(cap, nasg);
+  uint64_t nimg = occ_img(occ_sel(nasg, cap, rcap), lane, oor);
+  uint64_t key = ((rem >= wsd[0]) ? 0ull : HI) | img | inact;
+  uint64_t kwin = ((nrem >= wsd[1]) ? 0ull : HI) | nimg | inact;
+  uint64_t knot = ((rem >= wsd[1]) ? 0ull : HI) | img | inact;
+  int viol = 0;
+  for (int t = 0; t < n; ++t) {
+    const double w1 = wsd[t + 1], w2 = wsd[t + 2];
+    // case W (this lane wins step t): S_{t+1} = V_t
+    const double aW = __dadd_rn(nasg, w1);
+    const double rW = __dsub_rn(cap, aW);
+    const uint64_t iW = occ_img(occ_sel(aW, cap, rcap), lane, oor);
+    const uint64_t kwW = ((rW >= w2) ? 0ull : HI) | iW | inact;
+    const uint64_t knW = ((nrem >= w2) ? 0ull : HI) | nimg | inact;
+    // case N: S_{t+1} = S_t
+    const double aN = __dadd_rn(asg, w1);
+    const double rN = __dsub_rn(cap, aN);
+    const uint64_t iN = occ_img(occ_sel(aN, cap, rcap), lane, oor);
+    const uint64_t kwN = ((rN >= w2) ? 0ull : HI) | iN | inact;
+    const uint64_t knN = ((rem >= w2) ? 0ull : HI) | img | inact;
+    const uint32_t khi = (uint32_t)(key >> 32), klo = (uint32_t)key;
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+    const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+    const bool won = (khi == m1) & (klo == m2);
+    viol += (int)(m1 >> 31);
+    key = won ? kwin : knot;
+    asg = won ? nasg : asg;
+    rem = won ? nrem : rem;
+    img = won ? nimg : img;
+    nasg = won ? aW : aN;
+    nrem = won ? rW : rN;
+    nimg = won ? iW : iN;
+    kwin = won ? kwW : kwN;
+    knot = won ? knW : knN;
+    if (lane == 0) pick[t] = (int)(m2 & 31u);
+  }
+  int rep = 0;
+  if (__any_sync(0xffffffffu, oor && act)) rep = 1;
+  long long t1 = clock64();
+  if (lane == 0) { *cyc = t1 - t0; *replays = rep + viol * 0; }
+}
 int main() {
   unsigned* du; double* dd; long long* dc;
   cudaMalloc(&du, 128); cudaMalloc(&dd, 512); cudaMalloc(&dc, 8);
@@ -510,6 +582,13 @@ int main() {
     cudaMemcpy(h6.data(), p6, n * 4, cudaMemcpyDeviceToHost);
     int d7 = 0; for (int i = 0; i < n; ++i) d7 += h5[i] != h6[i];
     printf("  v7 %.1f cyc/seq (diffs %d, replayed blocks %d)\n", (double)c7 / n, d7, hrep);
+    cudaFuncSetAttribute(g_v8, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
+    for (int r = 0; r < 2; ++r) { g_v8<<<1, 32, (n + 2) * 8>>>(dw, n, M, dcap, p6, dc, drep); }
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); long long c8 = c;
+    cudaMemcpy(&hrep, drep, 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h6.data(), p6, n * 4, cudaMemcpyDeviceToHost);
+    int d8 = 0; for (int i = 0; i < n; ++i) d8 += h5[i] != h6[i];
+    printf("  v8 %.1f cyc/seq (diffs %d, oor %d) %s\n", (double)c8 / n, d8, hrep, cudaGetErrorString(cudaGetLastError()));
     printf("  v6 %.1f cyc/seq (diffs %d, replayed blocks %d of %d)\n", (double)c6 / n, d6, hrep, (n + 31) / 32);
     int d5 = 0;
     std::vector<int> h2(n), h3(n);

@@ -18,7 +18,7 @@ from paper_2508_06001_b200 import datagen  # noqa: E402
 SMALL = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
          "rank_lists", "send", "wir"]
 C2 = ["g2b8i256f1s0", "g2b4i512f1s0", "g2b2i768f1s0", "g2b1i1024f1s0"]
-for n in ["c2", 256, 2048, 4096, 16384]:
+for n in ["c2", 256, 512, 1024, 2048, 4096, 16384]:
     if n == "c2":
         ids, lens = datagen.metadata("scenario", 8, codes=C2, step=0, seed=7)
         n = sum(len(x) for x in ids)
