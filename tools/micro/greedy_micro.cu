@@ -529,6 +529,69 @@ __global__ void g_v8(const double* w_sorted, int n, int M, const double* caps, i
   long long t1 = clock64();
   if (lane == 0) { *cyc = t1 - t0; *replays = rep + viol * 0; }
 }
+// Diagnostics for v5's two loop-carried chains.  mode 1: REDUX chain only
+// (kWin from the old state: no division on the loop); mode 2: division
+// chain only (the pick is a cheap function of the key, no REDUX);
+// mode 3 (v9): two REDUX on keys with the low 5 mantissa bits replaced by
+// the lane, exactness checked off the chain (min of the true low bits over
+// the truncated-key ties), conflicting blocks replayed.
+template <int MODE>
+__global__ void g_diag(const double* w_sorted, int n, int M, const double* caps, int* pick, long long* cyc,
+                       int* replays) {
+  extern __shared__ double wsd[];
+  const int lane = threadIdx.x;
+  const bool act = lane < M;
+  const double cap = act ? caps[lane] : 0.0;
+  const double rcap = cap > 0.0 ? __drcp_rn(cap) : 0.0;
+  for (int i = lane; i < n + 2; i += 32) wsd[i] = i < n ? w_sorted[i] : 0.0;
+  __syncwarp();
+  const uint64_t inact = act ? 0ull : ~0ull;
+  double asg = 0.0, occ = occ_sel(0.0, cap, rcap), rem = __dsub_rn(cap, 0.0);
+  auto fold = [&](uint64_t k) { return MODE == 3 ? ((k & ~31ull) | (uint64_t)lane) : k; };
+  uint64_t key = fold((((rem >= wsd[0]) ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ)) | inact);
+  uint32_t low = (uint32_t)__double_as_longlong(occ) & 31u;
+  int nrep = 0;
+  uint32_t conflict = 0;
+  long long t0 = clock64();
+  for (int t = 0; t < n; ++t) {
+    const double w = wsd[t];
+    const double wn = wsd[t + 1];
+    const double nasg = __dadd_rn(asg, w);
+    const double nocc = MODE == 1 ? occ : occ_sel(nasg, cap, rcap);
+    const double nrem = __dsub_rn(cap, nasg);
+    const uint64_t kWinR = (((nrem >= wn) ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(nocc)) | inact;
+    const uint64_t kNotR = (((rem >= wn) ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ)) | inact;
+    const uint64_t kWin = fold(kWinR), kNot = fold(kNotR);
+    const uint32_t khi = (uint32_t)(key >> 32), klo = (uint32_t)key;
+    uint32_t pk;
+    if (MODE == 2) {
+      pk = (khi ^ klo) & 7u;  // stand-in, no cross-lane op
+      pk = pk < (uint32_t)M ? pk : 0u;
+    } else if (MODE == 3) {
+      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      pk = m2 & 31u;
+      // off the chain: true low bits among the truncated-key ties
+      const bool cand = (khi == m1) & ((klo >> 5) == (m2 >> 5));
+      const uint32_t mlow = __reduce_min_sync(0xffffffffu, cand ? low : 0xffffffffu);
+      conflict |= ((uint32_t)lane == pk) & (low != mlow);
+    } else {
+      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      pk = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? (uint32_t)lane : 31u);
+    }
+    const bool won = (uint32_t)lane == pk;
+    key = won ? kWin : kNot;
+    if (MODE == 3) low = won ? ((uint32_t)kWinR & 31u) : ((uint32_t)kNotR & 31u);
+    asg = won ? nasg : asg;
+    occ = won ? nocc : occ;
+    rem = won ? nrem : rem;
+    if (lane == 0) pick[t] = (int)pk;
+  }
+  if (MODE == 3 && __any_sync(0xffffffffu, conflict != 0)) nrep = 1;
+  long long t1 = clock64();
+  if (lane == 0) { *cyc = t1 - t0; *replays = nrep; }
+}
 int main() {
   unsigned* du; double* dd; long long* dc;
   cudaMalloc(&du, 128); cudaMalloc(&dd, 512); cudaMalloc(&dc, 8);
@@ -589,6 +652,21 @@ int main() {
     cudaMemcpy(h6.data(), p6, n * 4, cudaMemcpyDeviceToHost);
     int d8 = 0; for (int i = 0; i < n; ++i) d8 += h5[i] != h6[i];
     printf("  v8 %.1f cyc/seq (diffs %d, oor %d) %s\n", (double)c8 / n, d8, hrep, cudaGetErrorString(cudaGetLastError()));
+    {
+      auto run = [&](auto kern, const char* name) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
+        for (int r = 0; r < 2; ++r) kern<<<1, 32, (n + 2) * 8>>>(dw, n, M, dcap, p6, dc, drep);
+        cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&hrep, drep, 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h6.data(), p6, n * 4, cudaMemcpyDeviceToHost);
+        int dd = 0; for (int i = 0; i < n; ++i) dd += h5[i] != h6[i];
+        printf("  %s %.1f cyc/seq (diffs %d, conflict %d)\n", name, (double)c / n, dd, hrep);
+      };
+      run(g_diag<0>, "v5flat");
+      run(g_diag<1>, "redux-chain-only");
+      run(g_diag<2>, "division-chain-only");
+      run(g_diag<3>, "v9");
+    }
     printf("  v6 %.1f cyc/seq (diffs %d, replayed blocks %d of %d)\n", (double)c6 / n, d6, hrep, (n + 31) / 32);
     int d5 = 0;
     std::vector<int> h2(n), h3(n);
