@@ -547,7 +547,18 @@ __global__ void g_diag(const double* w_sorted, int n, int M, const double* caps,
   __syncwarp();
   const uint64_t inact = act ? 0ull : ~0ull;
   double asg = 0.0, occ = occ_sel(0.0, cap, rcap), rem = __dsub_rn(cap, 0.0);
-  auto fold = [&](uint64_t k) { return MODE == 3 ? ((k & ~31ull) | (uint64_t)lane) : k; };
+  uint32_t oorf = 0;
+  auto fold = [&](uint64_t k) -> uint64_t {
+    if (MODE == 3) return (k & ~31ull) | (uint64_t)lane;
+    if (MODE == 4) {  // exact lane-folded key (v7's layout), out-of-range occupancies flagged
+      const uint64_t b = k & ~(1ull << 63);
+      const uint32_t e = (uint32_t)(b >> 52);
+      oorf |= (uint32_t)(b != 0ull) & (uint32_t)((e - 993u) > 61u);
+      const uint64_t img = (b == 0ull) ? 0ull : ((b - (992ull << 52)) << 5);
+      return (k & (1ull << 63)) | img | (uint64_t)lane;
+    }
+    return k;
+  };
   uint64_t key = fold((((rem >= wsd[0]) ? 0ull : (1ull << 63)) | (uint64_t)__double_as_longlong(occ)) | inact);
   uint32_t low = (uint32_t)__double_as_longlong(occ) & 31u;
   int nrep = 0;
@@ -567,6 +578,10 @@ __global__ void g_diag(const double* w_sorted, int n, int M, const double* caps,
     if (MODE == 2) {
       pk = (khi ^ klo) & 7u;  // stand-in, no cross-lane op
       pk = pk < (uint32_t)M ? pk : 0u;
+    } else if (MODE == 4) {
+      const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      pk = m2 & 31u;
     } else if (MODE == 3) {
       const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
       const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
@@ -589,6 +604,7 @@ __global__ void g_diag(const double* w_sorted, int n, int M, const double* caps,
     if (lane == 0) pick[t] = (int)pk;
   }
   if (MODE == 3 && __any_sync(0xffffffffu, conflict != 0)) nrep = 1;
+  if (MODE == 4 && __any_sync(0xffffffffu, oorf != 0 && act)) nrep = 1;
   long long t1 = clock64();
   if (lane == 0) { *cyc = t1 - t0; *replays = nrep; }
 }
@@ -666,6 +682,7 @@ int main() {
       run(g_diag<1>, "redux-chain-only");
       run(g_diag<2>, "division-chain-only");
       run(g_diag<3>, "v9");
+      run(g_diag<4>, "v10");
     }
     printf("  v6 %.1f cyc/seq (diffs %d, replayed blocks %d of %d)\n", (double)c6 / n, d6, hrep, (n + 31) / 32);
     int d5 = 0;
