@@ -604,9 +604,19 @@ def main():
     n_post, us_post = planner.copy_timing(3)
     planner.plan(dm)
     torch.cuda.synchronize()
-    plan_breakdown = planner.timing()
+    plan_breakdown = {"path": "multi-kernel", "us": planner.timing()}
     planner.enable_timing(False)
     planner.copy_timing_reset()
+    planner.trace(True)  # fused single-CTA planner: per-phase SM cycles (zeros when the multi-kernel path ran)
+    planner.plan(dm)
+    torch.cuda.synchronize()
+    tr = planner.trace(True)
+    planner.trace(False)
+    if tr[13] > tr[0] > 0:
+        names = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
+                 "rank_lists", "send", "wir"]
+        plan_breakdown = {"path": "fused single-CTA", "total_cycles": int(tr[13] - tr[0]),
+                          "cycles": {k: int(v) for k, v in zip(names, np.diff(tr[:14]))}}
     # algorithmic bytes of each exchange (read == written), from the device
     op_bytes = {}
     for name, fn in (("route", lambda: sb.route(planner, A, B)), ("pre_attn", lambda: sb.pre_attn(planner, B, Cw)),
@@ -959,7 +969,7 @@ def main():
         else:
             line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"],
                                     "kind": "reference",
-                                    "sample": f"{r['steps']} full C2 steps (~{args.cpu_budget_s:.0f} s budget), "
+                                    "sample": f"{r['steps']} full {args.config.upper()} steps (~{args.cpu_budget_s:.0f} s budget), "
                                               "reference plan_routing+route+pre/post_attn+reverse_route, "
                                               "Exec::Parallel, 768 doubles/row"}
     print(json.dumps(line))
