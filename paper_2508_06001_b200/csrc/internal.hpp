@@ -77,6 +77,9 @@ struct sb_planner {
   int64_t* rep_chunks = nullptr;     // R
   int64_t* rep_cbase = nullptr;      // R+1
   int32_t* bag_seq = nullptr;        // max_seqs
+  int32_t* tile_cnt = nullptr;       // R * ceil(max_seqs / 1024) * M: emission tile bag counts
+  int64_t* bag_cbase = nullptr;      // R*M: first chunk of (replica, bag) within the replica
+  int64_t* bag_sbase = nullptr;      // R*M: first bag_seq slot of (replica, bag)
   unsigned long long* send_count = nullptr;  // W
   unsigned long long* recv_count = nullptr;  // W (generic manifests)
   // chunk-sized sort scratch for the generic reverse order (lazy)

@@ -65,6 +65,8 @@ struct PlanArgs {
   int64_t* rep_chunks;
   int64_t* rep_cbase;  // R+1: first chunk of each replica
   int32_t* bag_seq;    // N: sequences grouped by (replica, bag), q ascending
+  int32_t* tile_cnt;   // R * ceil(N / kEmitTile) * M: picks per (replica, tile, bag)
+  int64_t *bag_cbase, *bag_sbase;  // R*M
   unsigned long long* send_count;
   int64_t *n_chunks, *n_seqs;
   uint64_t* c_id;
@@ -565,66 +567,88 @@ __device__ void replica_bases(const PlanArgs& a, int rep, int64_t* rep_base, int
   }
 }
 
-// Phase A (one CTA per replica): q = rank of each sequence among its bag's
-// sequences in greedy order (a stable bag partition, match_any + per-warp
-// counts), per-sequence fields, and the inverse map bag_seq[(bag, q)] = s
-// that lets phase B emit chunks in parallel.
-__global__ void __launch_bounds__(1024) k_emit(PlanArgs a) {
-  __shared__ int warp_cnt[32][kMaxBags];
-  __shared__ int running[kMaxBags];
-  __shared__ int64_t bag_base[kMaxBags];
-  __shared__ int64_t seq_base[kMaxBags];
-  __shared__ int64_t rep_base;
+// Phase A1 (grid: tiles of kEmitTile greedy positions x replicas): per-tile
+// bag counts of the picks.
+constexpr int kEmitTile = 1024;
+
+__global__ void __launch_bounds__(kEmitTile) k_emit_count(PlanArgs a) {
+  __shared__ int cnt[kMaxBags];
   if (!seqs_ok(a)) return;
-  const int rep = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rep = blockIdx.y, tile = blockIdx.x;
   const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
-  if (tid == 0) {
-    replica_bases(a, rep, &rep_base, bag_base);
+  if (tile == 0 && threadIdx.x == 0) {  // the replica's (bag -> first chunk, first bag_seq slot) bases
     int64_t c = 0, sq = lo;
     for (int b = 0; b < a.M; ++b) {
-      seq_base[b] = sq;
-      sq += a.bag_count[rep * a.M + b];
-      c += (int64_t)a.bag_count[rep * a.M + b] * a.bag_size[b];
+      const int64_t nb = a.bag_count[rep * a.M + b];
+      a.bag_cbase[rep * a.M + b] = c;
+      a.bag_sbase[rep * a.M + b] = sq;
+      c += nb * a.bag_size[b];
+      sq += nb;
     }
     a.rep_chunks[rep] = c;
-    a.rep_cbase[rep] = rep_base;
-    if (rep == a.R - 1) a.rep_cbase[a.R] = rep_base + c;
   }
-  if (tid < a.M) running[tid] = 0;
+  const int64_t p0 = lo + (int64_t)tile * kEmitTile;
+  if (p0 >= hi) return;
+  if (threadIdx.x < a.M) cnt[threadIdx.x] = 0;
   __syncthreads();
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int64_t tile = lo; tile < hi; tile += blockDim.x) {
-    for (int e = tid; e < 32 * a.M; e += blockDim.x) warp_cnt[e / a.M][e % a.M] = 0;
-    __syncthreads();
-    const int64_t p = tile + tid;
-    const bool valid = p < hi;
-    const int b = valid ? a.pick[p] : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
-    const int rank_in = __popc(peers & lt_mask);
-    if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
-    __syncthreads();
-    if (tid < a.M) {
-      int run = running[tid];
-      for (int w = 0; w < 32; ++w) {
-        const int c = warp_cnt[w][tid];
-        warp_cnt[w][tid] = run;
-        run += c;
-      }
-      running[tid] = run;
+  const int64_t p = p0 + threadIdx.x;
+  if (p < hi) atomicAdd(&cnt[a.pick[p]], 1);
+  __syncthreads();
+  if (threadIdx.x < a.M) a.tile_cnt[((int64_t)rep * gridDim.x + tile) * a.M + threadIdx.x] = cnt[threadIdx.x];
+}
+
+// Phase A2 (same grid): q = rank of each pick among its bag's picks in
+// greedy order -- a stable bag partition (balancer.cpp:178-218): earlier
+// tiles' counts + match_any / per-warp counts inside the tile; then the
+// per-sequence fields and the inverse map bag_seq[(bag, q)] = s that lets
+// phase B emit chunks in parallel.
+__global__ void __launch_bounds__(kEmitTile) k_emit(PlanArgs a) {
+  __shared__ int warp_cnt[kEmitTile / 32][kMaxBags];
+  __shared__ int64_t rep_base;
+  if (!seqs_ok(a)) return;
+  const int rep = blockIdx.y, tile = blockIdx.x;
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  if (threadIdx.x == 0) {  // chunks of earlier replicas (rep_chunks from k_emit_count)
+    int64_t acc = 0;
+    for (int r = 0; r < rep; ++r) acc += a.rep_chunks[r];
+    rep_base = acc;
+    if (tile == 0) {  // also for empty replicas
+      a.rep_cbase[rep] = acc;
+      if (rep == a.R - 1) a.rep_cbase[a.R] = acc + a.rep_chunks[rep];
     }
-    __syncthreads();
-    if (valid) {
-      const int q = warp_cnt[warp][b] + rank_in;
-      const int s = a.sorted_idx[p];
-      const int g = a.bag_size[b];
-      a.bag_seq[seq_base[b] + q] = s;
-      a.seq_bag[s] = b;
-      a.seq_G[s] = g;
-      a.seq_chunk_base[s] = rep_base + bag_base[b] + (int64_t)q * g;
-      atomicAdd(&a.send_count[a.seq_rank[s]], (unsigned long long)g);
-    }
-    __syncthreads();
   }
+  const int64_t p0 = lo + (int64_t)tile * kEmitTile;
+  if (p0 >= hi) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t p = p0 + tid;
+  const bool valid = p < hi;
+  const int b = valid ? a.pick[p] : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, b);
+  const int rank_in = __popc(peers & ((1u << lane) - 1u));
+  for (int e = tid; e < (kEmitTile / 32) * a.M; e += blockDim.x) warp_cnt[e / a.M][e % a.M] = 0;
+  __syncthreads();
+  if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
+  __syncthreads();
+  if (tid < a.M) {  // exclusive prefix over earlier tiles, then over this tile's warps
+    int run = 0;
+    const int* tc = a.tile_cnt + (int64_t)rep * gridDim.x * a.M + tid;
+    for (int t = 0; t < tile; ++t) run += tc[(int64_t)t * a.M];
+    for (int w = 0; w < kEmitTile / 32; ++w) {
+      const int c = warp_cnt[w][tid];
+      warp_cnt[w][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (!valid) return;
+  const int q = warp_cnt[warp][b] + rank_in;
+  const int s = a.sorted_idx[p];
+  const int g = a.bag_size[b];
+  a.bag_seq[a.bag_sbase[rep * a.M + b] + q] = s;
+  a.seq_bag[s] = b;
+  a.seq_G[s] = g;
+  a.seq_chunk_base[s] = rep_base + a.bag_cbase[rep * a.M + b] + (int64_t)q * g;
+  atomicAdd(&a.send_count[a.seq_rank[s]], (unsigned long long)g);
 }
 
 // Phase B (grid over chunk capacity): chunk c = (replica, bag b, q, k) ->
@@ -1003,6 +1027,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.rep_total = p->rep_total; a.sentinel = p->sentinel; a.bag_count = p->bag_count;
   a.bag_rows = p->bag_rows; a.rep_chunks = p->rep_chunks; a.send_count = p->send_count;
   a.rep_cbase = p->rep_cbase; a.bag_seq = p->bag_seq;
+  a.tile_cnt = p->tile_cnt; a.bag_cbase = p->bag_cbase; a.bag_sbase = p->bag_sbase;
   a.n_chunks = p->n_chunks; a.n_seqs = p->n_seqs;
   a.c_id = p->c_id; a.c_idx = p->c_idx; a.c_src = p->c_src; a.c_dst = p->c_dst;
   a.c_start = p->c_start; a.c_end = p->c_end; a.c_src_row = p->c_src_row; a.c_dst_row = p->c_dst_row;
@@ -1029,6 +1054,7 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
   dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
   dalloc(&p->rep_cbase, R + 1); dalloc(&p->bag_seq, N);
+  dalloc(&p->tile_cnt, R * ((N + 1023) / 1024) * M); dalloc(&p->bag_cbase, R * M); dalloc(&p->bag_sbase, R * M);
   dalloc(&p->recv_count, W);
   dalloc(&p->n_chunks, 1); dalloc(&p->n_seqs, 1);
   dalloc(&p->c_id, C); dalloc(&p->c_idx, C); dalloc(&p->c_src, C); dalloc(&p->c_dst, C);
@@ -1073,7 +1099,8 @@ static void planner_free(sb_planner* p) {
                   p->violations, p->status,
                   p->stage_ids, p->stage_lens, p->stage_w, p->stage_off,
                   p->seg_off, p->seg_id, p->seg_first, p->seg_len, p->recv_count, p->ck_hi, p->ck_lo,
-                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv, p->rep_cbase, p->bag_seq};
+                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv, p->rep_cbase, p->bag_seq, p->tile_cnt,
+                  p->bag_cbase, p->bag_sbase};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int i = 0; i < 6; ++i)
@@ -1197,7 +1224,10 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[2], s));
   launch_greedy(p, a, s);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[3], s));
-  k_emit<<<p->R, 1024, 0, s>>>(a);
+  const dim3 eg((unsigned)((p->max_seqs + kEmitTile - 1) / kEmitTile), (unsigned)p->R);
+  k_emit_count<<<eg, kEmitTile, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_emit<<<eg, kEmitTile, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   k_emit_chunks<<<(int)((p->max_chunks + 255) / 256), 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
@@ -1207,7 +1237,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
-  count_launch(4);
+  count_launch(6);  // greedy, emit count, emit, emit chunks, lists, finalize
 }
 
 static void run_identity(sb_planner* p, cudaStream_t s) {
