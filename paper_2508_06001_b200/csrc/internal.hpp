@@ -78,6 +78,8 @@ struct sb_planner {
   int64_t* rep_cbase = nullptr;      // R+1
   int32_t* bag_seq = nullptr;        // max_seqs
   int32_t* tile_cnt = nullptr;       // R * ceil(max_seqs / 1024) * M: emission tile bag counts
+  int64_t* list_sum = nullptr;       // W * ceil(max_seqs / 1024) * 4: manifest tile sums
+  int32_t* list_tie = nullptr;       // W: reverse-order tie flags
   int64_t* bag_cbase = nullptr;      // R*M: first chunk of (replica, bag) within the replica
   int64_t* bag_sbase = nullptr;      // R*M: first bag_seq slot of (replica, bag)
   unsigned long long* send_count = nullptr;  // W

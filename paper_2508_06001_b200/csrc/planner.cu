@@ -66,6 +66,8 @@ struct PlanArgs {
   int64_t* rep_cbase;  // R+1: first chunk of each replica
   int32_t* bag_seq;    // N: sequences grouped by (replica, bag), q ascending
   int32_t* tile_cnt;   // R * ceil(N / kEmitTile) * M: picks per (replica, tile, bag)
+  int64_t* list_sum;   // W * ceil(N / kListTile) * 4: per-tile sums of k_lists' four domains
+  int32_t* list_tie;   // W: reverse order of rank r needs the std::sort replay
   int64_t *bag_cbase, *bag_sbase;  // R*M
   unsigned long long* send_count;
   int64_t *n_chunks, *n_seqs;
@@ -554,18 +556,6 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
 // (a stable partition of the greedy order by bag); chunk k of (b, q) is
 // global chunk rep_base + bag_base[b] + q*G_b + k and targets the bag's k-th
 // rank.
-__device__ void replica_bases(const PlanArgs& a, int rep, int64_t* rep_base, int64_t* bag_base) {
-  // rep_base = chunks of earlier replicas; bag_base[b] within this replica.
-  int64_t rb = 0;
-  for (int r = 0; r < rep; ++r)
-    for (int b = 0; b < a.M; ++b) rb += (int64_t)a.bag_count[r * a.M + b] * a.bag_size[b];
-  *rep_base = rb;
-  int64_t acc = 0;
-  for (int b = 0; b < a.M; ++b) {
-    bag_base[b] = acc;
-    acc += (int64_t)a.bag_count[rep * a.M + b] * a.bag_size[b];
-  }
-}
 
 // Phase A1 (grid: tiles of kEmitTile greedy positions x replicas): per-tile
 // bag counts of the picks.
@@ -712,119 +702,160 @@ __device__ void fix_rev_ties(const PlanArgs& a, int r, int64_t off, int64_t n) {
 }
 
 // ----------------------------------------------------------------- k_lists
-// One CTA per global rank r.  Builds
+// Per global rank r (grid: tiles of kListTile elements x ranks), four
+// scans over r's domains:
 //   recv[r]      = chunks (q, k) of r's bag member slot k, q ascending
 //                  (finalize_manifests, balancer.cpp:84-91), plus the
 //                  receive-side row offsets (target packing, :93-101);
+//   c_seq_base   = row base of each sequence in its bag's full-sequence
+//                  layout (member 0 only; pre_attn shells, exchange.cpp:291-295);
 //   send[r]      = chunks with source r in chunk order: r's sequences sorted
-//                  by their first chunk index, each expanded to G chunks;
+//                  by their first chunk index, each expanded to G chunks --
+//                  a stable filter of bag_seq (chunk order is (replica, bag,
+//                  q, k)) by source rank;
 //   rev_recv[r]  = reverse_plan's receive order (:259-285): r's sequences in
 //                  buffer order, chunks by start (chunk index breaks the
-//                  zero-length ties);
-//   c_seq_base   = row base of each sequence in its bag's full-sequence
-//                  layout (pre_attn shells, exchange.cpp:291-295).
-__global__ void __launch_bounds__(1024) k_lists(PlanArgs a) {
-  __shared__ int64_t sh[33];
-  __shared__ int64_t s_recv_off, s_send_off, s_rep_base;
-  __shared__ int64_t s_bag_base[kMaxBags];
+//                  zero-length ties; libstdc++'s order replayed by k_finalize).
+// k_lists_count sums each tile of each domain (and the rank offsets),
+// k_lists adds the earlier tiles' sums to an in-tile block scan.
+constexpr int kListTile = 1024;
+
+struct ListDomains {
+  int rep, b, k, g, n_b;
+  int64_t cb0, rlo, rhi, lo, hi;
+};
+
+__device__ __forceinline__ ListDomains list_domains(const PlanArgs& a, int r) {
+  ListDomains d;
+  d.rep = r / a.U;
+  const int u = r % a.U;
+  d.b = a.rank_bag[u];
+  d.k = a.rank_member[u];
+  d.g = a.bag_size[d.b];
+  d.n_b = a.bag_count[d.rep * a.M + d.b];
+  d.cb0 = a.rep_cbase[d.rep] + a.bag_cbase[d.rep * a.M + d.b];
+  d.rlo = a.rank_off[d.rep * a.U];
+  d.rhi = a.rank_off[d.rep * a.U + a.U];
+  d.lo = a.rank_off[r];
+  d.hi = a.rank_off[r + 1];
+  return d;
+}
+
+// The four per-element values of domain position o (0 when out of range).
+__device__ __forceinline__ void list_values(const PlanArgs& a, const ListDomains& d, int r, int64_t o, int64_t v[4]) {
+  v[0] = v[1] = v[2] = v[3] = 0;
+  if (o < d.n_b) {
+    const int64_t c = d.cb0 + o * d.g + d.k;
+    v[0] = a.c_end[c] - a.c_start[c];
+    if (d.k == 0) v[1] = a.c_end[c + d.g - 1];  // the last chunk ends at the sequence length
+  }
+  if (d.rlo + o < d.rhi) {
+    const int s = a.bag_seq[d.rlo + o];
+    v[2] = a.seq_rank[s] == r ? a.seq_G[s] : 0;
+  }
+  if (d.lo + o < d.hi) v[3] = a.seq_G[d.lo + o];
+}
+
+__global__ void __launch_bounds__(kListTile) k_lists_count(PlanArgs a) {
+  __shared__ int64_t part[kListTile / 32][4];
   if (!seqs_ok(a)) return;
-  const int r = blockIdx.x, tid = threadIdx.x;
-  const int rep = r / a.U, u = r % a.U;
-  const int b = a.rank_bag[u], k = a.rank_member[u];
-  const int g = a.bag_size[b];
-  const int n_b = a.bag_count[rep * a.M + b];
-  if (tid == 0) {
-    replica_bases(a, rep, &s_rep_base, s_bag_base);
+  const int r = blockIdx.y, t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const ListDomains d = list_domains(a, r);
+  if (t == 0 && tid == 0) {  // manifest offsets (balancer.cpp:84-91)
     int64_t ro = 0, so = 0;
     for (int x = 0; x < r; ++x) {
-      const int xr = x / a.U, xu = x % a.U;
-      ro += a.bag_count[xr * a.M + a.rank_bag[xu]];
+      ro += a.bag_count[(x / a.U) * a.M + a.rank_bag[x % a.U]];
       so += (int64_t)a.send_count[x];
     }
-    s_recv_off = ro;
-    s_send_off = so;
     a.recv_off[r] = ro;
     a.send_off[r] = so;
     if (r == a.W - 1) {
-      a.recv_off[a.W] = ro + n_b;
+      a.recv_off[a.W] = ro + d.n_b;
       a.send_off[a.W] = so + (int64_t)a.send_count[r];
     }
+    a.list_tie[r] = 0;
+  }
+  const int64_t o0 = (int64_t)t * kListTile;
+  if (o0 >= d.n_b && d.rlo + o0 >= d.rhi && d.lo + o0 >= d.hi) return;
+  int64_t v[4];
+  list_values(a, d, r, o0 + tid, v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int64_t x = v[j];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) part[warp][j] = x;
   }
   __syncthreads();
-  const int64_t cb0 = s_rep_base + s_bag_base[b];
-  // recv list and target row offsets
-  int64_t carry = 0;
-  for (int64_t q0 = 0; q0 < n_b; q0 += blockDim.x) {
-    const int64_t q = q0 + tid;
-    const bool valid = q < n_b;
-    const int64_t c = cb0 + q * g + k;
-    const int64_t len = valid ? a.c_end[c] - a.c_start[c] : 0;
-    int64_t tot;
-    const int64_t ex = block_excl_scan<int64_t>(len, sh, &tot);
-    if (valid) {
-      a.c_dst_row[c] = carry + ex;
-      a.recv_idx[s_recv_off + q] = (int32_t)c;
-    }
-    carry += tot;
+  if (tid < 4) {
+    int64_t x = 0;
+    for (int w = 0; w < kListTile / 32; ++w) x += part[w][tid];
+    a.list_sum[((int64_t)r * gridDim.x + t) * 4 + tid] = x;
   }
-  if (tid == 0) a.target_rows[r] = carry;
-  // Ulysses: per-sequence base rows in the bag's full layout (member 0 only)
-  if (k == 0) {
-    int64_t c2 = 0;
-    for (int64_t q0 = 0; q0 < n_b; q0 += blockDim.x) {
-      const int64_t q = q0 + tid;
-      const bool valid = q < n_b;
-      const int64_t c = cb0 + q * g;
-      const int64_t full = valid ? a.c_end[c + g - 1] : 0;  // last chunk ends at l
-      int64_t tot;
-      const int64_t ex = block_excl_scan<int64_t>(full, sh, &tot);
-      if (valid) a.c_seq_base[c] = c2 + ex;
-      c2 += tot;
-    }
-    if (tid == 0) a.bag_rows[rep * a.M + b] = c2;
-  }
-  // send list: rank r's sequences ordered by first chunk index.  Chunk order
-  // is (replica, bag, q, k), i.e. the order of bag_seq over r's replica, so
-  // this is a stable filter of bag_seq by source rank, each sequence
-  // expanded to its G chunks.
-  const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
-  const int64_t n = hi - lo;
-  {
-    const int64_t rlo = a.rank_off[rep * a.U], rhi = a.rank_off[rep * a.U + a.U];
-    int64_t c3 = 0;
-    for (int64_t i0 = rlo; i0 < rhi; i0 += blockDim.x) {
-      const int64_t i = i0 + tid;
-      const int s = i < rhi ? a.bag_seq[i] : 0;
-      const bool mine = i < rhi && a.seq_rank[s] == r;
-      const int gs = mine ? a.seq_G[s] : 0;
-      int64_t tot;
-      const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
-      if (mine) {
-        const int64_t cb = a.seq_chunk_base[s];
-        for (int kk = 0; kk < gs; ++kk) a.send_idx[s_send_off + c3 + ex + kk] = (int32_t)(cb + kk);
-      }
-      c3 += tot;
-    }
-  }
-  // reverse receive order: sequences in buffer order, chunks ascending
-  int64_t c4 = 0;
-  int tie = 0;  // a sequence shorter than its bag: empty chunks with equal (segment, start)
-  for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int64_t i = i0 + tid;
-    const bool valid = i < n;
-    const int gs = valid ? a.seq_G[lo + i] : 0;
-    tie |= (gs > 1 && a.lens[lo + i] < gs) ? 1 : 0;
-    int64_t tot;
-    const int64_t ex = block_excl_scan<int64_t>((int64_t)gs, sh, &tot);
-    if (valid) {
-      const int64_t cb = a.seq_chunk_base[lo + i];
-      for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[s_send_off + c4 + ex + kk] = (int32_t)(cb + kk);
-    }
-    c4 += tot;
-  }
-  tie = __syncthreads_or(tie);  // also: send[r] complete (std::sort's input order)
-  if (tid == 0 && tie) fix_rev_ties(a, r, s_send_off, c4);
 }
+
+__global__ void __launch_bounds__(kListTile) k_lists(PlanArgs a) {
+  __shared__ int64_t sh[33];
+  __shared__ int64_t base[4];
+  if (!seqs_ok(a)) return;
+  const int r = blockIdx.y, t = blockIdx.x, tid = threadIdx.x;
+  const int T = gridDim.x;
+  const ListDomains d = list_domains(a, r);
+  const int64_t* ts = a.list_sum + (int64_t)r * T * 4;
+  if (t == 0 && tid == 32) {  // totals: target rows of r, full rows of its bag
+    int64_t tr = 0, br = 0;
+    for (int x = 0; x < T; ++x) {
+      tr += ts[x * 4 + 0];
+      br += ts[x * 4 + 1];
+    }
+    a.target_rows[r] = tr;
+    if (d.k == 0) a.bag_rows[d.rep * a.M + d.b] = br;
+  }
+  const int64_t o0 = (int64_t)t * kListTile;
+  if (o0 >= d.n_b && d.rlo + o0 >= d.rhi && d.lo + o0 >= d.hi) return;
+  if (tid < 4) {
+    int64_t x = 0;
+    for (int y = 0; y < t; ++y) x += ts[y * 4 + tid];
+    base[tid] = x;
+  }
+  const int64_t recv_off = a.recv_off[r], send_off = a.send_off[r];
+  const int64_t o = o0 + tid;
+  int64_t v[4];
+  list_values(a, d, r, o, v);
+  int64_t tot;
+  __syncthreads();  // base
+  if (o0 < d.n_b) {  // recv list + target rows
+    const int64_t ex = block_excl_scan<int64_t>(v[0], sh, &tot);
+    if (o < d.n_b) {
+      const int64_t c = d.cb0 + o * d.g + d.k;
+      a.c_dst_row[c] = base[0] + ex;
+      a.recv_idx[recv_off + o] = (int32_t)c;
+    }
+    if (d.k == 0) {  // Ulysses: per-sequence base rows in the bag's full layout
+      const int64_t ex1 = block_excl_scan<int64_t>(v[1], sh, &tot);
+      if (o < d.n_b) a.c_seq_base[d.cb0 + o * d.g] = base[1] + ex1;
+    }
+  }
+  if (d.rlo + o0 < d.rhi) {  // send list
+    const int64_t ex = block_excl_scan<int64_t>(v[2], sh, &tot);
+    if (v[2] > 0) {
+      const int64_t cb = a.seq_chunk_base[a.bag_seq[d.rlo + o]];
+      for (int kk = 0; kk < (int)v[2]; ++kk) a.send_idx[send_off + base[2] + ex + kk] = (int32_t)(cb + kk);
+    }
+  }
+  if (d.lo + o0 < d.hi) {  // reverse receive order: sequences in buffer order, chunks ascending
+    const int64_t ex = block_excl_scan<int64_t>(v[3], sh, &tot);
+    int tie = 0;  // a sequence shorter than its bag: empty chunks with equal (segment, start)
+    if (d.lo + o < d.hi) {
+      const int gs = (int)v[3];
+      tie = (gs > 1 && a.lens[d.lo + o] < gs) ? 1 : 0;
+      const int64_t cb = a.seq_chunk_base[d.lo + o];
+      for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[send_off + base[3] + ex + kk] = (int32_t)(cb + kk);
+    }
+    tie = __syncthreads_or(tie);
+    if (tid == 0 && tie) atomicOr(&a.list_tie[r], 1);
+  }
+}
+
 
 // -------------------------------------------------------------- k_finalize
 __global__ void k_finalize(PlanArgs a) {
@@ -845,6 +876,10 @@ __global__ void k_finalize(PlanArgs a) {
     else wir = __ddiv_rn(hi, lo);
     *a.wir = wir;
   }
+  // ranks whose reverse receive order can tie: replay std::sort now that
+  // send[r] (its input order) is complete; one lane per rank
+  for (int r = threadIdx.x; r < a.W; r += blockDim.x)
+    if (a.list_tie[r]) fix_rev_ties(a, r, a.send_off[r], a.send_off[r + 1] - a.send_off[r]);
 }
 
 }  // namespace sb
@@ -1027,7 +1062,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.rep_total = p->rep_total; a.sentinel = p->sentinel; a.bag_count = p->bag_count;
   a.bag_rows = p->bag_rows; a.rep_chunks = p->rep_chunks; a.send_count = p->send_count;
   a.rep_cbase = p->rep_cbase; a.bag_seq = p->bag_seq;
-  a.tile_cnt = p->tile_cnt; a.bag_cbase = p->bag_cbase; a.bag_sbase = p->bag_sbase;
+  a.tile_cnt = p->tile_cnt; a.list_sum = p->list_sum; a.list_tie = p->list_tie; a.bag_cbase = p->bag_cbase; a.bag_sbase = p->bag_sbase;
   a.n_chunks = p->n_chunks; a.n_seqs = p->n_seqs;
   a.c_id = p->c_id; a.c_idx = p->c_idx; a.c_src = p->c_src; a.c_dst = p->c_dst;
   a.c_start = p->c_start; a.c_end = p->c_end; a.c_src_row = p->c_src_row; a.c_dst_row = p->c_dst_row;
@@ -1054,7 +1089,8 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
   dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
   dalloc(&p->rep_cbase, R + 1); dalloc(&p->bag_seq, N);
-  dalloc(&p->tile_cnt, R * ((N + 1023) / 1024) * M); dalloc(&p->bag_cbase, R * M); dalloc(&p->bag_sbase, R * M);
+  dalloc(&p->tile_cnt, R * ((N + 1023) / 1024) * M); dalloc(&p->list_sum, W * ((N + 1023) / 1024) * 4);
+  dalloc(&p->list_tie, W); dalloc(&p->bag_cbase, R * M); dalloc(&p->bag_sbase, R * M);
   dalloc(&p->recv_count, W);
   dalloc(&p->n_chunks, 1); dalloc(&p->n_seqs, 1);
   dalloc(&p->c_id, C); dalloc(&p->c_idx, C); dalloc(&p->c_src, C); dalloc(&p->c_dst, C);
@@ -1099,7 +1135,7 @@ static void planner_free(sb_planner* p) {
                   p->violations, p->status,
                   p->stage_ids, p->stage_lens, p->stage_w, p->stage_off,
                   p->seg_off, p->seg_id, p->seg_first, p->seg_len, p->recv_count, p->ck_hi, p->ck_lo,
-                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv, p->rep_cbase, p->bag_seq, p->tile_cnt,
+                  p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv, p->rep_cbase, p->bag_seq, p->tile_cnt, p->list_sum, p->list_tie,
                   p->bag_cbase, p->bag_sbase};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -1232,12 +1268,15 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   k_emit_chunks<<<(int)((p->max_chunks + 255) / 256), 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[4], s));
-  k_lists<<<p->W, 1024, 0, s>>>(a);
+  const dim3 lg((unsigned)((p->max_seqs + kListTile - 1) / kListTile), (unsigned)p->W);
+  k_lists_count<<<lg, kListTile, 0, s>>>(a);
+  SB_CHECK_LAUNCH();
+  k_lists<<<lg, kListTile, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
-  count_launch(6);  // greedy, emit count, emit, emit chunks, lists, finalize
+  count_launch(7);  // greedy, emit count, emit, emit chunks, lists count, lists, finalize (+ tie replay)
 }
 
 static void run_identity(sb_planner* p, cudaStream_t s) {
