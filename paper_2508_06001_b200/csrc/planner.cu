@@ -218,14 +218,38 @@ __device__ __forceinline__ int replica_of(const PlanArgs& a, int64_t g) {
   return lo;
 }
 
-__global__ void __launch_bounds__(1024) k_sort_tiles(PlanArgs a) {
+// Sorted runs of kRunTile records, one record per thread: a 512-record
+// register bitonic is ~4.5 us on one SM, so several small tiles on several
+// SMs plus merge passes beat one 2048-record tile (48 us, issue-bound).
+constexpr int kSortThreads = 512;
+constexpr int kRunTile = kSortThreads;
+static_assert(kRunTile <= kSortTile, "run tile fits the staging buffers");
+
+template <int T, int RPT>
+__device__ __forceinline__ void sort_tile_out(const PlanArgs& a, uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int cnt,
+                                              int64_t base) {
+  uint64_t h[RPT], l[RPT];
+  uint32_t v[RPT];
+  reg_bitonic<T, RPT, kSortThreads>(s_hi, s_lo, s_v, cnt, h, l, v);
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int x = threadIdx.x + r * kSortThreads;
+    if (x < cnt) {
+      a.sk_hi[base + x] = h[r];
+      a.sk_lo[base + x] = l[r];
+      a.sk_v[base + x] = v[r];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_tiles(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (!seqs_ok(a)) return;
   int b = blockIdx.x, rep = -1;
   int64_t lo = 0, n = 0;
   for (int r = 0; r < a.R; ++r) {
     const int64_t rl = a.rank_off[r * a.U], rn = a.rank_off[r * a.U + a.U] - rl;
-    const int tiles = (int)((rn + kSortTile - 1) / kSortTile);
+    const int tiles = (int)((rn + kRunTile - 1) / kRunTile);
     if (b < tiles) {
       rep = r;
       lo = rl;
@@ -235,45 +259,27 @@ __global__ void __launch_bounds__(1024) k_sort_tiles(PlanArgs a) {
     b -= tiles;
   }
   if (rep < 0) return;
-  const int64_t t0 = (int64_t)b * kSortTile;
-  const int cnt = (int)(n - t0 < kSortTile ? n - t0 : kSortTile);
+  const int64_t t0 = (int64_t)b * kRunTile;
+  const int cnt = (int)(n - t0 < kRunTile ? n - t0 : kRunTile);
   uint64_t* s_hi = reinterpret_cast<uint64_t*>(smem);
   uint64_t* s_lo = s_hi + kSortTile;
   uint32_t* s_v = reinterpret_cast<uint32_t*>(s_lo + kSortTile);
-  int tile = 64;
-  while (tile < cnt) tile <<= 1;
-  for (int i = threadIdx.x; i < tile; i += blockDim.x) {
-    if (i < cnt) {
-      const double wv = a.w[lo + t0 + i];
-      s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);  // -0.0 ties +0.0
-      s_lo[i] = a.ids[lo + t0 + i];
-      s_v[i] = (uint32_t)(t0 + i);
-    } else {
-      s_hi[i] = ~0ull;
-      s_lo[i] = ~0ull;
-      s_v[i] = 0xffffffffu;
-    }
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const double wv = a.w[lo + t0 + i];
+    s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);  // -0.0 ties +0.0
+    s_lo[i] = a.ids[lo + t0 + i];
+    s_v[i] = (uint32_t)(t0 + i);
   }
   __syncthreads();
-  for (int k = 2; k <= tile; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < tile / 2; i += blockDim.x) {
-        const int l = 2 * j * (i / j) + (i % j), h = l + j;
-        const bool up = (l & k) == 0;
-        const uint64_t lh = s_hi[l], ll = s_lo[l], hh = s_hi[h], hl = s_lo[h];
-        const uint32_t lv = s_v[l], hv = s_v[h];
-        if (rec_less(hh, hl, hv, lh, ll, lv) == up) {
-          s_hi[l] = hh; s_lo[l] = hl; s_v[l] = hv;
-          s_hi[h] = lh; s_lo[h] = ll; s_v[h] = lv;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    a.sk_hi[lo + t0 + i] = s_hi[i];
-    a.sk_lo[lo + t0 + i] = s_lo[i];
-    a.sk_v[lo + t0 + i] = s_v[i];
+  // register bitonic (block_sort.cuh), unrolled for the tile's power of two
+  int tile = 64;
+  while (tile < cnt) tile <<= 1;
+  const int64_t base = lo + t0;
+  switch (tile) {
+    case 64: sort_tile_out<64, 1>(a, s_hi, s_lo, s_v, cnt, base); break;
+    case 128: sort_tile_out<128, 1>(a, s_hi, s_lo, s_v, cnt, base); break;
+    case 256: sort_tile_out<256, 1>(a, s_hi, s_lo, s_v, cnt, base); break;
+    default: sort_tile_out<512, 1>(a, s_hi, s_lo, s_v, cnt, base); break;
   }
 }
 
@@ -1165,11 +1171,15 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
 // chunks: 363 vs 286 us; tools/plan_profile.py, profiles/r01b).
 constexpr int64_t kSmallChunks = 8192;
 
+constexpr int64_t kSmallAutoSeqs = 1536;
+
 static bool use_small_path(const sb_planner* p) {
   if (p->path == 2) return false;
   const bool fits = p->max_seqs <= kSmallSeqs && p->W <= 1024 && p->M <= kMaxBags;
   if (p->path == 1) return fits;
-  return fits && p->max_chunks <= kSmallChunks;
+  // auto: the fused CTA wins up to ~1K sequences (one launch, no inter-kernel
+  // gaps); at 2K the multi-kernel path's parallel sort / emission is ~10 % faster
+  return fits && p->max_seqs <= kSmallAutoSeqs && p->max_chunks <= kSmallChunks;
 }
 
 // The serial FP64 totals fork onto the planner's side stream as soon as the
@@ -1196,13 +1206,13 @@ static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool o
   int launches = 0;
   if (order) {
     const int64_t N = p->max_seqs;
-    const int tiles = (int)((N + kSortTile - 1) / kSortTile) + p->R;
-    k_sort_tiles<<<tiles, 1024, kSortSmemBytes, s>>>(a);
+    const int tiles = (int)((N + kRunTile - 1) / kRunTile) + p->R;
+    k_sort_tiles<<<tiles, kSortThreads, kSortSmemBytes, s>>>(a);
     SB_CHECK_LAUNCH();
     uint64_t *shi = p->sk_hi, *slo = p->sk_lo, *dhi = p->tk_hi, *dlo = p->tk_lo;
     uint32_t *sv = p->sk_v, *dv = p->tk_v;
     const int blocks = (int)((N + 255) / 256);
-    for (int64_t width = kSortTile; width < N; width <<= 1) {
+    for (int64_t width = kRunTile; width < N; width <<= 1) {
       k_merge_pass<<<blocks, 256, 0, s>>>(a, width, shi, slo, sv, dhi, dlo, dv);
       SB_CHECK_LAUNCH();
       std::swap(shi, dhi);

@@ -96,97 +96,12 @@ __device__ void smem_bitonic(uint64_t* hi, uint64_t* lo, uint32_t* v, int n, int
   }
 }
 
-// Branch-free (key, id, index) order for the register sort.
-__device__ __forceinline__ bool rec_less_bf(uint64_t ahi, uint64_t alo, uint32_t av, uint64_t bhi, uint64_t blo,
-                                            uint32_t bv) {
-  return (ahi < bhi) | ((ahi == bhi) & ((alo < blo) | ((alo == blo) & (av < bv))));
-}
-
-// Bitonic sort with the records in registers: thread x holds records
-// x + r * B (r < RPT, B = kSmallThreads) of T = pow2 >= n (slots >= n are
-// +inf padding).  T is a template parameter, so all (log2 T)(log2 T + 1)/2
-// stages unroll: partners at distance j < 32 are exchanged by shuffles,
-// 32 <= j < B through shared memory (the only barriers: n = 256 has 6 of
-// 36 stages), j == B inside the thread.  Leaves the record of rank
-// x + r * B in (h, l, v)[r].
-template <int T, int RPT>
-__device__ void reg_bitonic(uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int n, uint64_t (&h)[RPT],
-                            uint64_t (&l)[RPT], uint32_t (&v)[RPT]) {
-  constexpr int B = kSmallThreads;
-  static_assert(T <= RPT * B && (RPT == 1 || T == RPT * B), "register bitonic shape");
-  const int tid = threadIdx.x;
-  const bool live = RPT > 1 || (tid & ~31) < T;  // warp-uniform
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int x = tid + r * B;
-    h[r] = x < n ? s_hi[x] : ~0ull;
-    l[r] = x < n ? s_lo[x] : ~0ull;
-    v[r] = x < n ? s_v[x] : 0xffffffffu;
-  }
-#pragma unroll
-  for (int k = 2; k <= T; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= B) {  // RPT == 2, j == B: the partner is this thread's other record; k > B, so ascending
-        if (rec_less_bf(h[RPT - 1], l[RPT - 1], v[RPT - 1], h[0], l[0], v[0])) {
-          const uint64_t a = h[0], b = l[0];
-          const uint32_t c = v[0];
-          h[0] = h[RPT - 1]; l[0] = l[RPT - 1]; v[0] = v[RPT - 1];
-          h[RPT - 1] = a; l[RPT - 1] = b; v[RPT - 1] = c;
-        }
-        continue;
-      }
-      uint64_t ph[RPT], pl[RPT];
-      uint32_t pv[RPT];
-      if (j >= 32) {
-        __syncthreads();  // the previous exchange's reads are done
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int x = tid + r * B;
-          if (x < T) {
-            s_hi[x] = h[r];
-            s_lo[x] = l[r];
-            s_v[x] = v[r];
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int x = tid + r * B;
-          const int p = x < T ? (x ^ j) : x;  // x >= T: padding stays (never read back)
-          ph[r] = x < T ? s_hi[p] : h[r];
-          pl[r] = x < T ? s_lo[p] : l[r];
-          pv[r] = x < T ? s_v[p] : v[r];
-        }
-      } else {
-        if (!live) continue;
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          ph[r] = __shfl_xor_sync(0xffffffffu, h[r], j);
-          pl[r] = __shfl_xor_sync(0xffffffffu, l[r], j);
-          pv[r] = __shfl_xor_sync(0xffffffffu, v[r], j);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int x = tid + r * B;
-        const bool up = (x & k) == 0, lower = (x & j) == 0;
-        const bool pless = rec_less_bf(ph[r], pl[r], pv[r], h[r], l[r], v[r]);
-        const bool take = (lower == up) ? pless : !pless;  // records are unique; equal padding swaps to itself
-        h[r] = take ? ph[r] : h[r];
-        l[r] = take ? pl[r] : l[r];
-        v[r] = take ? pv[r] : v[r];
-      }
-    }
-  }
-}
-
 template <int T, int RPT>
 __device__ void reg_sort_emit(const PlanArgs& a, uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int32_t* s_sorted,
                               int64_t lo, int n) {
   uint64_t h[RPT], l[RPT];
   uint32_t v[RPT];
-  reg_bitonic<T, RPT>(s_hi, s_lo, s_v, n, h, l, v);
+  reg_bitonic<T, RPT, kSmallThreads>(s_hi, s_lo, s_v, n, h, l, v);
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     const int x = threadIdx.x + r * kSmallThreads;
