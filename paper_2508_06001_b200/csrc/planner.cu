@@ -1251,8 +1251,7 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
 
 static void run_plan(sb_planner* p, cudaStream_t s) {
   PlanArgs a = make_args(p);
-  if (use_small_path(p)) {
-    SB_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int32_t), s));
+  if (use_small_path(p)) {  // one launch: the kernel clears the status word itself
     if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
     k_plan_small<<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
     SB_CHECK_LAUNCH();

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
     s_flag = 0;
     s_viol = 0;
     s_biglen = 0;
+    *a.status = 0;  // no memset node before the launch; every atomicOr below follows this barrier
   }
   __syncthreads();
   const int64_t N = s_roff[W];

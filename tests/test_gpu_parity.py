@@ -321,3 +321,35 @@ def test_many_replicas_vs_oracle(world, topo, path):
     E.status()
     assert E.compare(A) == 0 and D.compare(B) == 0
     assert Cw.checksum() == A.checksum()
+
+
+@pytest.mark.parametrize("path", ["small", "large"])
+def test_empty_replicas_vs_oracle(path):
+    """Whole replicas without sequences (first and last of three): chunk bases,
+    manifests and the data path skip them exactly like the reference."""
+    rng = np.random.default_rng(5)
+    world = 24  # g2n4: three replicas of eight ranks
+    lens = [[] for _ in range(8)] + [rng.integers(0, 2000, size=3).tolist() for _ in range(8)] + [[] for _ in range(8)]
+    meta = oracle.meta_explicit(lens)
+    planner = sb.Planner("g2n4", world, max_seqs=sum(len(x) for x in lens))
+    planner.set_path(path)
+    planner.plan(device_meta(meta))
+    hp = planner.download()
+    plan, rep = oracle.plan_routing(meta, oracle.parse_topology("g2n4"))
+    got = host_plan_as_oracle(hp, meta)
+    assert got.chunk_rows() == plan.chunk_rows()
+    assert got.send == plan.send and got.recv == plan.recv
+    assert [dbits(x) for x in hp.per_gpu_workload] == [dbits(x) for x in rep.per_gpu_workload]
+    assert hp.rev_recv == oracle.reverse_plan(plan).recv
+    rows = int(sum(sum(x) for x in lens))
+    mk = lambda: sb.World(world, 24, [192], capacity_rows=max(1, rows), max_bag=planner.max_bag)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    dm = device_meta(meta)
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    sb.route(planner, A, B)
+    sb.pre_attn(planner, B, Cw)
+    sb.post_attn(planner, Cw, D)
+    sb.reverse_route(planner, D, E)
+    E.status()
+    assert E.compare(A) == 0 and D.compare(B) == 0
