@@ -7,5 +7,6 @@ reference headers lives in ``include/seqbal/*.hpp`` / ``lib/libseqbal.so``.
 """
 from ._capi import (CapacityError, CommError, ConfigError, CudaError, IntegrityError, ParseError,  # noqa: F401
                     SeqbalError)
+from .hostmem import pinned_host  # noqa: F401
 from .api import (DeviceMeta, Driver, HostPlan, Model, Planner, Scenario, Schedule, Topology,  # noqa: F401
                   UniformBalancer, World, kernel_launches, parse_topology, post_attn, pre_attn, reverse_route, route)

@@ -30,6 +30,7 @@ import numpy as np
 from . import _capi
 from ._capi import call
 from .api import DeviceMeta, Planner, World, post_attn, pre_attn, reverse_route, route
+from .hostmem import pinned_host
 
 
 def partition(world_size: int, n_procs: int, proc: int):
@@ -315,8 +316,8 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     # out the origin world, runs the step and downloads the restored ranks.
     rows_local = int(sum(int(x.sum()) for x in all_lens[first:first + n_local]))
     sizes = [rows_local * meta_b, rows_local * payload, rows_local * rope_b]
-    h_in = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for n in sizes]
-    h_out = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for n in sizes]
+    h_in = [pinned_host(n) for n in sizes]
+    h_out = [pinned_host(n) for n in sizes]
     A.download([h.data_ptr() for h in h_in], sizes)
     torch.cuda.synchronize()
 

@@ -1,52 +1,49 @@
-"""Why the e2e upload runs below the PCIe probe: time the same 224 MB
-host->device image through sb_world_upload and through torch copies,
-from the same pinned buffer (diagnostics)."""
+"""Why the e2e upload sometimes runs below the PCIe probe: H2D bandwidth of a
+224 MB image from pinned buffers allocated three ways (diagnostics):
+torch pin_memory=True (cudaHostAlloc), and anonymous mmap + MADV_HUGEPAGE +
+cudaHostRegister (2 MB pages: fewer IOMMU translations)."""
+import mmap
 import os
-import sys
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_2508_06001_b200 as sb  # noqa: E402
-
-rows = 36372
-sizes = [rows * 16, rows * 6144, rows * 16]
-host = [torch.empty(n, dtype=torch.uint8).pin_memory() for n in sizes]
-w = sb.World(8, 24, [6144], capacity_rows=rows, n_aux=1, aux_row_bytes=16) if False else None
+N = 36372 * 6144
+print("THP:", open("/sys/kernel/mm/transparent_hugepage/enabled").read().strip()
+      if os.path.exists("/sys/kernel/mm/transparent_hugepage/enabled") else "n/a")
 s = torch.cuda.Stream()
+dev = torch.empty(N, dtype=torch.uint8, device="cuda")
 
 
-def t(fn, reps=8):
-    fn()
+def rate(h, reps=8):
+    with torch.cuda.stream(s):
+        dev.copy_(h, non_blocking=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    for _ in range(reps):
-        fn()
+    with torch.cuda.stream(s):
+        for _ in range(reps):
+            dev.copy_(h, non_blocking=True)
     e1.record(s)
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    return N * reps / e0.elapsed_time(e1) / 1e6
 
 
-dev = [torch.empty(n, dtype=torch.uint8, device="cuda") for n in sizes]
+def thp_pinned(n):
+    m = mmap.mmap(-1, n + (2 << 20), flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    m.madvise(mmap.MADV_HUGEPAGE)
+    t = torch.frombuffer(m, dtype=torch.uint8)
+    t.fill_(0)  # fault the pages in (as huge pages where possible)
+    off = (-t.data_ptr()) % (2 << 20)
+    t = t[off:off + n]
+    rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), n, 0)
+    assert int(rc) == 0, rc
+    return t, m
 
 
-def torch_copy():
-    with torch.cuda.stream(s):
-        for d, h in zip(dev, host):
-            d.copy_(h, non_blocking=True)
-
-
-big_h = torch.empty(sizes[1], dtype=torch.uint8, pin_memory=True)
-
-
-def torch_copy_fresh():
-    with torch.cuda.stream(s):
-        dev[1].copy_(big_h, non_blocking=True)
-
-
-for name, fn, nbytes in (("torch copy, .pin_memory() buffers", torch_copy, sum(sizes)),
-                         ("torch copy, pin_memory=True buffer", torch_copy_fresh, sizes[1])):
-    ms = t(fn)
-    print(f"{name}: {ms:.3f} ms  {nbytes / ms / 1e6:.1f} GB/s")
-print("host ptr alignment", [h.data_ptr() % 4096 for h in host], big_h.data_ptr() % 4096)
+for trial in range(3):
+    a = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+    b, keep = thp_pinned(N)
+    c = torch.empty(N, dtype=torch.uint8).pin_memory()
+    print(f"trial {trial}: pin_memory=True {rate(a):.1f} GB/s  thp+register {rate(b):.1f} GB/s  "
+          f".pin_memory() {rate(c):.1f} GB/s")
+    del a, c
