@@ -423,6 +423,51 @@ __device__ __forceinline__ uint64_t greedy_key(bool feasible, double occ) {
 
 constexpr int kGreedyChunk = 1024;  // `hook(p0)` runs before every chunk of this many steps
 
+// One bag per replica (g8n1, g4n1, ...): every pick is bag 0 (balancer.cpp:44-62
+// with m == 1), so the argmin chain disappears.  What stays serial is the FP64
+// prefix in greedy order -- `capacity - assigned >= w` decides the violation
+// count (balancer.cpp:159-163) and `assigned` the occupancy and per-GPU load --
+// one DADD per sequence on lane 0; the other lanes write the picks.
+template <int CHUNK, class GetW, class Hook>
+__device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, int64_t n, double target, GetW getw,
+                                                  Hook hook, int32_t* pick_out, int32_t* bagcnt_out,
+                                                  int* viol_out) {
+  const int lane = threadIdx.x & 31;
+  const int nn = (int)n;
+  const int size = a.bag_size[0];
+  const double cap = __dmul_rn((double)size, target);  // balancer.cpp:30
+  double asg = 0.0;
+  int viol = 0;
+  auto run = [&](int p0, int p1) {
+    for (int p = p0 + lane; p < p1; p += 32) pick_out[p] = 0;
+    if (lane == 0) {
+#pragma unroll 8
+      for (int p = p0; p < p1; ++p) {
+        const double w = getw(p);
+        viol += __dsub_rn(cap, asg) >= w ? 0 : 1;
+        asg = __dadd_rn(asg, w);
+      }
+    }
+    __syncwarp();
+  };
+  if constexpr (CHUNK == 0) {
+    run(0, nn);
+  } else {
+    hook(0);
+    for (int p0 = 0; p0 < nn; p0 += CHUNK) {
+      if (p0 > 0) hook(p0);
+      run(p0, nn - p0 < CHUNK ? nn : p0 + CHUNK);
+    }
+  }
+  if (lane != 0) return;
+  if (bagcnt_out) bagcnt_out[rep] = nn;
+  a.bag_count[rep] = nn;
+  a.per_bag_occ[rep] = occupancy(asg, cap);  // balancer.cpp:170-175
+  const double per = __ddiv_rn(asg, (double)size);  // balancer.cpp:199-202
+  for (int k = 0; k < size; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[0] + k]] = per;
+  atomicAdd(viol_out, viol);
+}
+
 // CHUNK > 0: `hook(p0)` runs before every CHUNK steps (the large path's
 // shared-memory ring); CHUNK == 0: one flat loop (the nested form costs the
 // fused planner ~45 cycles per sequence in code generation).
@@ -431,6 +476,10 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
                                             Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out) {
   const int lane = threadIdx.x & 31;
   const double target = __ddiv_rn(total_rep, (double)a.U);  // balancer.cpp:26
+  if (a.M == 1) {
+    greedy_single_bag<CHUNK>(a, rep, n, target, getw, hook, pick_out, bagcnt_out, viol_out);
+    return;
+  }
   double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
   uint64_t key[BPL];
   int cnt[BPL];
