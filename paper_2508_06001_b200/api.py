@@ -38,7 +38,17 @@ def kernel_launches() -> int:
     return int(_capi.load().sb_kernel_launches())
 
 
+def _destroy(fn, h):
+    """Release a C-ABI handle from __del__; at interpreter shutdown the module
+    globals may already be torn down, and the process exit frees the device."""
+    try:
+        getattr(_capi.load(), fn)(h)
+    except (TypeError, AttributeError):
+        pass
+
+
 # ---------------------------------------------------------------- topology
+
 @dataclass
 class Topology:
     """topology.hpp:16-34: bags of contiguous unit-local ranks, textual order."""
@@ -237,7 +247,7 @@ class Planner:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _capi.load().sb_planner_destroy(h)
+            _destroy("sb_planner_destroy", h)
             self._h = None
 
     @property
@@ -351,7 +361,7 @@ class World:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and getattr(self, "_owned", True):
-            _capi.load().sb_world_destroy(h)
+            _destroy("sb_world_destroy", h)
             self._h = None
 
     @property
@@ -480,7 +490,7 @@ class Scenario:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _capi.load().sb_scenario_destroy(h)
+            _destroy("sb_scenario_destroy", h)
             self._h = None
 
 
@@ -504,7 +514,7 @@ class Schedule:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _capi.load().sb_schedule_destroy(h)
+            _destroy("sb_schedule_destroy", h)
             self._h = None
 
     def generate(self, step: int, meta: DeviceMeta | None = None, stream=None) -> DeviceMeta:
@@ -532,7 +542,7 @@ class Driver:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _capi.load().sb_driver_destroy(h)
+            _destroy("sb_driver_destroy", h)
             self._h = None
 
     @property
@@ -592,7 +602,7 @@ class UniformBalancer:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _capi.load().sb_uniform_destroy(h)
+            _destroy("sb_uniform_destroy", h)
             self._h = None
 
     def plan(self, counts, stream=None):

@@ -133,6 +133,7 @@ struct sb_planner {
   // side stream for work that overlaps the main planner chain (serial totals)
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t gfork_ev = nullptr, gjoin_ev = nullptr;  // single-bag greedy chain (overlaps emission)
 
   // timing
   bool timing = false;

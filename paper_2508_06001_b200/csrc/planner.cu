@@ -439,14 +439,30 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
   double asg = 0.0;
   int viol = 0;
   auto run = [&](int p0, int p1) {
-    for (int p = p0 + lane; p < p1; p += 32) pick_out[p] = 0;
+    if (pick_out)
+      for (int p = p0 + lane; p < p1; p += 32) pick_out[p] = 0;
     if (lane == 0) {
-#pragma unroll 8
-      for (int p = p0; p < p1; ++p) {
+      // the DADD on `asg` is the only chain: eight violation counters keep the
+      // predicated increments off it (one counter was a second ~8-cycle chain)
+      int v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int p = p0;
+      for (; p + 8 <= p1; p += 8) {
+        double w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = getw(p + k);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] += __dsub_rn(cap, asg) >= w[k] ? 0 : 1;
+          asg = __dadd_rn(asg, w[k]);
+        }
+      }
+      for (; p < p1; ++p) {
         const double w = getw(p);
-        viol += __dsub_rn(cap, asg) >= w ? 0 : 1;
+        v[0] += __dsub_rn(cap, asg) >= w ? 0 : 1;
         asg = __dadd_rn(asg, w);
       }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) viol += v[k];
     }
     __syncwarp();
   };
@@ -461,7 +477,7 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
   }
   if (lane != 0) return;
   if (bagcnt_out) bagcnt_out[rep] = nn;
-  a.bag_count[rep] = nn;
+  if (pick_out) a.bag_count[rep] = nn;  // else k_single_bag_fill wrote picks and counts
   a.per_bag_occ[rep] = occupancy(asg, cap);  // balancer.cpp:170-175
   const double per = __ddiv_rn(asg, (double)size);  // balancer.cpp:199-202
   for (int k = 0; k < size; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[0] + k]] = per;
@@ -571,7 +587,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
 constexpr int kGreedyStage = 24576;  // 192 KB of workloads
 
 template <int BPL>
-__global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
+__global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a, bool picks) {
   extern __shared__ __align__(16) double stage[];
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, lane = threadIdx.x;
@@ -580,12 +596,12 @@ __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
   const double* sw = a.sorted_w + lo;
   for (int i = lane; i < n; i += 32) stage[i] = sw[i];
   __syncwarp();
-  greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
-                      nullptr, a.violations);
+  greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {},
+                      picks ? a.pick + lo : nullptr, nullptr, a.violations);
 }
 
 template <int BPL>
-__global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
+__global__ void __launch_bounds__(32) k_greedy(PlanArgs a, bool picks) {
   __shared__ double ring[2][kGreedyChunk];
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, lane = threadIdx.x;
@@ -602,8 +618,18 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
     __syncwarp();
   };
   greedy_warp<BPL, kGreedyChunk>(a, rep, n, a.rep_total[rep],
-                   [&](int p) { return ring[(p / kGreedyChunk) & 1][p % kGreedyChunk]; }, hook, a.pick + lo,
-                   nullptr, a.violations);
+                   [&](int p) { return ring[(p / kGreedyChunk) & 1][p % kGreedyChunk]; }, hook,
+                   picks ? a.pick + lo : nullptr, nullptr, a.violations);
+}
+
+// One bag per replica: the picks (all bag 0) and bag counts (replica sizes)
+// are known before the serial FP64 prefix runs, so emission and the lists
+// start at once while greedy_single_bag's chain runs on the side stream.
+__global__ void __launch_bounds__(256) k_single_bag_fill(PlanArgs a) {
+  if (!seqs_ok(a)) return;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < a.rank_off[a.W]) a.pick[p] = 0;
+  if (p < a.R) a.bag_count[p] = (int32_t)(a.rank_off[p * a.U + a.U] - a.rank_off[p * a.U]);
 }
 
 // ------------------------------------------------------------------ k_emit
@@ -1176,6 +1202,8 @@ static void planner_alloc(sb_planner* p) {
   SB_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   SB_CUDA(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming));
   SB_CUDA(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming));
+  SB_CUDA(cudaEventCreateWithFlags(&p->gfork_ev, cudaEventDisableTiming));
+  SB_CUDA(cudaEventCreateWithFlags(&p->gjoin_ev, cudaEventDisableTiming));
 }
 
 static void planner_free(sb_planner* p) {
@@ -1198,6 +1226,8 @@ static void planner_free(sb_planner* p) {
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   if (p->fork_ev) cudaEventDestroy(p->fork_ev);
   if (p->join_ev) cudaEventDestroy(p->join_ev);
+  if (p->gfork_ev) cudaEventDestroy(p->gfork_ev);
+  if (p->gjoin_ev) cudaEventDestroy(p->gjoin_ev);
   if (p->side) cudaStreamDestroy(p->side);
   for (cudaEvent_t e : p->copy_ev) cudaEventDestroy(e);
   for (auto& sl : p->slots) {
@@ -1279,8 +1309,20 @@ static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool o
 
 // k_greedy_staged when every replica fits the staging buffer (the planner's
 // sequence capacity bounds every replica), else the ring-fed k_greedy.
-static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
+// fork: a single-bag chain runs on the side stream; the caller joins gjoin_ev
+// (run_plan: before k_finalize).
+static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool fork) {
   const bool wide = (p->M + 31) / 32 > 1;
+  const bool single = fork && p->M == 1;
+  cudaStream_t gs = s;
+  if (single) {
+    k_single_bag_fill<<<(int)((std::max<int64_t>(p->max_seqs, p->R) + 255) / 256), 256, 0, s>>>(a);
+    SB_CHECK_LAUNCH();
+    SB_CUDA(cudaEventRecord(p->gfork_ev, s));
+    SB_CUDA(cudaStreamWaitEvent(p->side, p->gfork_ev, 0));
+    gs = p->side;
+    count_launch(1);
+  }
   if (p->max_seqs <= kGreedyStage) {
     const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
     static int set_to[2] = {0, 0};
@@ -1289,13 +1331,14 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
       else SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       set_to[wide] = smem;
     }
-    if (wide) k_greedy_staged<2><<<p->R, 32, smem, s>>>(a);
-    else k_greedy_staged<1><<<p->R, 32, smem, s>>>(a);
+    if (wide) k_greedy_staged<2><<<p->R, 32, smem, gs>>>(a, !single);
+    else k_greedy_staged<1><<<p->R, 32, smem, gs>>>(a, !single);
   } else {
-    if (wide) k_greedy<2><<<p->R, 32, 0, s>>>(a);
-    else k_greedy<1><<<p->R, 32, 0, s>>>(a);
+    if (wide) k_greedy<2><<<p->R, 32, 0, gs>>>(a, !single);
+    else k_greedy<1><<<p->R, 32, 0, gs>>>(a, !single);
   }
   SB_CHECK_LAUNCH();
+  if (single) SB_CUDA(cudaEventRecord(p->gjoin_ev, p->side));
 }
 
 static void run_plan(sb_planner* p, cudaStream_t s) {
@@ -1316,7 +1359,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[1], s));
   launch_sort(p, a, s, true);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[2], s));
-  launch_greedy(p, a, s);
+  launch_greedy(p, a, s, true);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[3], s));
   const dim3 eg((unsigned)((p->max_seqs + kEmitTile - 1) / kEmitTile), (unsigned)p->R);
   k_emit_count<<<eg, kEmitTile, 0, s>>>(a);
@@ -1331,6 +1374,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   SB_CHECK_LAUNCH();
   k_lists<<<lg, kListTile, 0, s>>>(a);
   SB_CHECK_LAUNCH();
+  if (p->M == 1) SB_CUDA(cudaStreamWaitEvent(s, p->gjoin_ev, 0));  // single-bag greedy chain joined
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
@@ -1618,7 +1662,7 @@ extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t*
   sb::launch_totals(p, a, s);
   sb::launch_prep(p, a, s);
   sb::launch_sort(p, a, s, true);
-  sb::launch_greedy(p, a, s);
+  sb::launch_greedy(p, a, s, false);
   sb::count_launch(2);
   SB_CUDA(cudaStreamSynchronize(s));
   int32_t st = 0;
