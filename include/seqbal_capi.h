@@ -153,6 +153,11 @@ SB_API sb_status sb_planner_set_path(sb_planner* p, int path);
 /* Self-test: the planner's fast correctly-rounded division against
  * __ddiv_rn on n random operand pairs; *mismatches must be 0. */
 SB_API sb_status sb_selftest_div(int64_t n, uint64_t seed, int64_t* mismatches);
+/* Self-test: the planner's block-parallel serial FP64 sum (serial_sum.cuh)
+ * against the one-thread chain, `blocks` sums of 1..max_len generated values
+ * of law `mode` (0..6), result and every prefix; *mismatches must be 0. */
+SB_API sb_status sb_selftest_serial_sum(int64_t blocks, int64_t max_len, uint64_t seed, int mode,
+                                        int64_t* mismatches);
 /* Diagnostics: per-phase clock64() stamps of the fused planner (16 slots). */
 SB_API sb_status sb_planner_trace(sb_planner* p, int enable, int64_t* out16);
 

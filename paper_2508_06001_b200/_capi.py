@@ -93,6 +93,7 @@ _SIGS = {
     "sb_planner_set_path": (C.c_int, [C.c_void_p, C.c_int]),
     "sb_planner_trace": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "sb_selftest_div": (C.c_int, [C.c_int64, C.c_uint64, C.c_void_p]),
+    "sb_selftest_serial_sum": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_void_p]),
     "sb_planner_timing": (C.c_int, [C.c_void_p] * 6),
     "sb_world_create": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sb_world_destroy": (C.c_int, [C.c_void_p]),

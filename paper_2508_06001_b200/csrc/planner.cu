@@ -32,6 +32,7 @@
 #include "block_sort.cuh"
 #include "common.cuh"
 #include "internal.hpp"
+#include "serial_sum.cuh"
 #include "stdsort.cuh"
 
 namespace sb {
@@ -324,16 +325,29 @@ __global__ void k_sort_finish(PlanArgs a, const uint32_t* __restrict__ sv) {
   a.sorted_w[g] = a.w[s];
 }
 
-// Serial FP64 totals (dependent chains): per replica in gather order
-// (balancer.cpp:24-25) and BalanceReport::total_workload over every replica
-// (balancer.cpp:147).  One CTA per sum: all threads stage 2048-workload
-// chunks into shared memory (double-buffered) while thread 0 runs the add
-// chain over the previous chunk, so the chain never waits on global loads.
-// Runs on the planner's side stream, concurrently with the sort.
-constexpr int kTotalsChunk = 2048;
+// Serial FP64 totals: per replica in gather order (balancer.cpp:24-25) and
+// BalanceReport::total_workload over every replica (balancer.cpp:147).  One
+// CTA per sum, computed by block_serial_sum (serial_sum.cuh): bit-identical
+// to the one-thread DADD chain, ~log2(total / first) block scans instead of
+// one ~8-cycle dependent add per sequence.  Workloads are recomputed from the
+// lengths (bit-identical to k_prep_seq's), so the sums start with the plan.
+// Runs on the planner's side stream, concurrently with the prep and the sort.
+constexpr int kSumThreads = 512;
+constexpr int kSumPerThread = 8;
+constexpr int64_t kSumStage = 24576;  // workloads staged in shared memory (192 KB) up to this many
 
-__global__ void __launch_bounds__(256) k_totals(PlanArgs a) {
-  __shared__ double buf[2][kTotalsChunk];
+// Stage x_j = f(j), j < n, into dynamic shared memory when the launch gave
+// room for them (every restart of block_serial_sum re-reads its window).
+template <class F>
+__device__ __forceinline__ bool sum_stage(double* stage, int64_t cap, int64_t n, F f) {
+  if (n > cap) return false;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) stage[j] = f(j);
+  __syncthreads();
+  return true;
+}
+
+__global__ void __launch_bounds__(kSumThreads) k_totals(PlanArgs a, int64_t stage_cap) {
+  extern __shared__ __align__(16) double stage[];
   if (!seqs_ok(a)) return;
   const int b = blockIdx.x;
   int64_t lo, hi;
@@ -344,45 +358,10 @@ __global__ void __launch_bounds__(256) k_totals(PlanArgs a) {
     lo = 0;
     hi = a.rank_off[a.W];
   }
-  const int64_t n = hi - lo;
-  const int chunks = (int)((n + kTotalsChunk - 1) / kTotalsChunk);
-  double s = 0.0;
-  // workloads recomputed from the lengths (bit-identical to k_prep_seq's),
-  // so the chain starts with the plan instead of after the per-sequence pass
-  for (int64_t i = threadIdx.x; i < kTotalsChunk && i < n; i += blockDim.x) buf[0][i] = seq_workload(a, lo + i);
-  __syncthreads();
-  for (int c = 0; c < chunks; ++c) {
-    const int64_t nb = (int64_t)(c + 1) * kTotalsChunk;
-    for (int64_t i = threadIdx.x; i < kTotalsChunk && nb + i < n; i += blockDim.x)
-      buf[(c + 1) & 1][i] = seq_workload(a, lo + nb + i);
-    if (threadIdx.x == 0) {
-      const double* x = buf[c & 1];
-      const int cnt = (int)(n - (int64_t)c * kTotalsChunk < kTotalsChunk ? n - (int64_t)c * kTotalsChunk
-                                                                          : kTotalsChunk);
-      // software-pipelined: the next 8 loads are in flight under this 8-add chain
-      int i = 0;
-      double v[8], u[8];
-      if (cnt >= 8) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = x[k];
-      }
-      for (; i + 16 <= cnt; i += 8) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) u[k] = x[i + 8 + k];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = u[k];
-      }
-      if (i + 8 <= cnt) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
-        i += 8;
-      }
-      for (; i < cnt; ++i) s = __dadd_rn(s, x[i]);
-    }
-    __syncthreads();
-  }
+  auto f = [&](int64_t j) { return seq_workload(a, lo + j); };
+  const bool st = sum_stage(stage, stage_cap, hi - lo, f);
+  const double s = block_serial_sum<kSumThreads, kSumPerThread>(
+      hi - lo, [&](int64_t j) { return st ? stage[j] : f(j); }, [](int64_t, double, double) {});
   if (threadIdx.x != 0) return;
   if (b < a.R) {
     a.rep_total[b] = s;
@@ -630,6 +609,79 @@ __global__ void __launch_bounds__(256) k_single_bag_fill(PlanArgs a) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p < a.rank_off[a.W]) a.pick[p] = 0;
   if (p < a.R) a.bag_count[p] = (int32_t)(a.rank_off[p * a.U + a.U] - a.rank_off[p * a.U]);
+}
+
+// One bag per replica, large path: the occupancy replay (balancer.cpp:159-166)
+// over the greedy order is a serial FP64 prefix of the sorted workloads;
+// block_serial_sum yields every prefix exactly, so each sequence's
+// `capacity - assigned >= w` test runs in parallel.  Outputs as greedy_warp.
+__global__ void __launch_bounds__(kSumThreads) k_single_bag_chain(PlanArgs a, int64_t stage_cap) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ int s_viol;
+  if (!seqs_ok(a)) return;
+  const int rep = blockIdx.x;
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  const double target = __ddiv_rn(a.rep_total[rep], (double)a.U);  // balancer.cpp:26
+  const int size = a.bag_size[0];
+  const double cap = __dmul_rn((double)size, target);  // balancer.cpp:30
+  if (threadIdx.x == 0) s_viol = 0;
+  __syncthreads();
+  int viol = 0;
+  const double* sw = a.sorted_w + lo;
+  const bool st = sum_stage(stage, stage_cap, hi - lo, [&](int64_t j) { return sw[j]; });
+  const double asg = block_serial_sum<kSumThreads, kSumPerThread>(
+      hi - lo, [&](int64_t j) { return st ? stage[j] : sw[j]; },
+      [&](int64_t, double before, double w) { viol += __dsub_rn(cap, before) >= w ? 0 : 1; });
+  viol = __reduce_add_sync(0xffffffffu, viol);
+  if ((threadIdx.x & 31) == 0 && viol) atomicAdd(&s_viol, viol);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  a.per_bag_occ[rep] = occupancy(asg, cap);  // balancer.cpp:170-175
+  const double per = __ddiv_rn(asg, (double)size);  // balancer.cpp:199-202
+  for (int k = 0; k < size; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[0] + k]] = per;
+  if (s_viol) atomicAdd(a.violations, s_viol);
+}
+
+// Self-test of block_serial_sum against the one-thread chain: block b sums
+// len_b generated values (mode picks the law: reals, integers and halves --
+// frequent round-half-even ties --, zeros over 120 binades, workloads,
+// power-of-two tie patterns, overflow to +inf) and checks the result and
+// every emitted prefix bit-for-bit.
+__device__ __forceinline__ double selftest_value(uint64_t seed, int mode, int b, int64_t j) {
+  const uint64_t r = splitmix64(seed ^ ((uint64_t)b << 40) ^ (uint64_t)j);
+  switch (mode) {
+    case 0: return (double)(r >> 11) * 0x1.0p-53 * 1e15;
+    case 1: return (double)(r % 1000000007ull);
+    case 2: return (double)(r % 4096) * 0.5;
+    case 3: return (r & 3) == 0 ? 0.0 : ldexp((double)(r >> 11) * 0x1.0p-53, (int)((r >> 3) % 120) - 60);
+    case 4: {
+      const double l = 64.0 + (double)(r % 4096);
+      return __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(24.0, l), 3072.0), 3072.0),
+                       __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(0.49, 4.0), l), l), 3072.0));
+    }
+    case 5: return j < 5 ? 0.0 : ldexp(1.0, (int)(r % 40)) + (((r >> 20) & 1) ? ldexp(1.0, (int)(r % 40) - 53) : 0.0);
+    default: return (r & 1) ? 1e300 * (double)((r >> 1) % 3) : 1.0;
+  }
+}
+
+__global__ void __launch_bounds__(kSumThreads) k_selftest_sum(uint64_t seed, int mode, int64_t max_len,
+                                                              double* prefix, unsigned long long* mismatches) {
+  const int b = blockIdx.x;
+  const int64_t n = 1 + (int64_t)(splitmix64(seed ^ 0xabcdefull ^ (uint64_t)b) % (uint64_t)max_len);
+  double* pre = prefix + (int64_t)b * max_len;
+  const double s = block_serial_sum<kSumThreads, kSumPerThread>(
+      n, [&](int64_t j) { return selftest_value(seed, mode, b, j); },
+      [&](int64_t j, double before, double) { pre[j] = before; });
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned long long bad = 0;
+  double t = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (__double_as_longlong(pre[j]) != __double_as_longlong(t)) ++bad;
+    t = __dadd_rn(t, selftest_value(seed, mode, b, j));
+  }
+  if (__double_as_longlong(s) != __double_as_longlong(t)) ++bad;
+  if (bad) atomicAdd(mismatches, bad);
 }
 
 // ------------------------------------------------------------------ k_emit
@@ -1261,13 +1313,28 @@ static bool use_small_path(const sb_planner* p) {
   return fits && p->max_seqs <= kSmallAutoSeqs && p->max_chunks <= kSmallChunks;
 }
 
+// Shared-memory staging capacity of the serial-sum kernels (workloads of one
+// replica / the whole gather); the attribute is raised once per process.
+static int64_t sum_stage_cap(const sb_planner* p) {
+  const int64_t cap = std::min<int64_t>(std::max<int64_t>(p->max_seqs, 1), kSumStage);
+  static int64_t set_to = 0;
+  if (cap > set_to) {
+    const int bytes = (int)(cap * sizeof(double));
+    SB_CUDA(cudaFuncSetAttribute(k_totals, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    SB_CUDA(cudaFuncSetAttribute(k_single_bag_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    set_to = cap;
+  }
+  return cap;
+}
+
 // The serial FP64 totals fork onto the planner's side stream as soon as the
 // metadata is there (they recompute workloads from lengths) and join before
 // the greedy: the chain overlaps the per-sequence pass and the sort.
 static void launch_totals(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
   SB_CUDA(cudaEventRecord(p->fork_ev, s));
   SB_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
-  k_totals<<<p->R + 1, 256, 0, p->side>>>(a);
+  const int64_t cap = sum_stage_cap(p);
+  k_totals<<<p->R + 1, kSumThreads, (size_t)cap * sizeof(double), p->side>>>(a, cap);
   SB_CHECK_LAUNCH();
   SB_CUDA(cudaEventRecord(p->join_ev, p->side));
   count_launch(1);
@@ -1312,17 +1379,23 @@ static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool o
 // fork: a single-bag chain runs on the side stream; the caller joins gjoin_ev
 // (run_plan: before k_finalize).
 static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool fork) {
-  const bool wide = (p->M + 31) / 32 > 1;
-  const bool single = fork && p->M == 1;
-  cudaStream_t gs = s;
-  if (single) {
+  if (p->M == 1) {  // picks and counts up front; the occupancy replay forks when asked
     k_single_bag_fill<<<(int)((std::max<int64_t>(p->max_seqs, p->R) + 255) / 256), 256, 0, s>>>(a);
     SB_CHECK_LAUNCH();
-    SB_CUDA(cudaEventRecord(p->gfork_ev, s));
-    SB_CUDA(cudaStreamWaitEvent(p->side, p->gfork_ev, 0));
-    gs = p->side;
-    count_launch(1);
+    cudaStream_t gs = s;
+    if (fork) {
+      SB_CUDA(cudaEventRecord(p->gfork_ev, s));
+      SB_CUDA(cudaStreamWaitEvent(p->side, p->gfork_ev, 0));
+      gs = p->side;
+    }
+    const int64_t cap = sum_stage_cap(p);
+    k_single_bag_chain<<<p->R, kSumThreads, (size_t)cap * sizeof(double), gs>>>(a, cap);
+    SB_CHECK_LAUNCH();
+    if (fork) SB_CUDA(cudaEventRecord(p->gjoin_ev, p->side));
+    count_launch(1);  // the callers count one greedy launch
+    return;
   }
+  const bool wide = (p->M + 31) / 32 > 1;
   if (p->max_seqs <= kGreedyStage) {
     const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
     static int set_to[2] = {0, 0};
@@ -1331,14 +1404,13 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool
       else SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       set_to[wide] = smem;
     }
-    if (wide) k_greedy_staged<2><<<p->R, 32, smem, gs>>>(a, !single);
-    else k_greedy_staged<1><<<p->R, 32, smem, gs>>>(a, !single);
+    if (wide) k_greedy_staged<2><<<p->R, 32, smem, s>>>(a, true);
+    else k_greedy_staged<1><<<p->R, 32, smem, s>>>(a, true);
   } else {
-    if (wide) k_greedy<2><<<p->R, 32, 0, gs>>>(a, !single);
-    else k_greedy<1><<<p->R, 32, 0, gs>>>(a, !single);
+    if (wide) k_greedy<2><<<p->R, 32, 0, s>>>(a, true);
+    else k_greedy<1><<<p->R, 32, 0, s>>>(a, true);
   }
   SB_CHECK_LAUNCH();
-  if (single) SB_CUDA(cudaEventRecord(p->gjoin_ev, p->side));
 }
 
 static void run_plan(sb_planner* p, cudaStream_t s) {
@@ -1374,7 +1446,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   SB_CHECK_LAUNCH();
   k_lists<<<lg, kListTile, 0, s>>>(a);
   SB_CHECK_LAUNCH();
-  if (p->M == 1) SB_CUDA(cudaStreamWaitEvent(s, p->gjoin_ev, 0));  // single-bag greedy chain joined
+  if (p->M == 1) SB_CUDA(cudaStreamWaitEvent(s, p->gjoin_ev, 0));  // single-bag occupancy replay joined
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
@@ -1554,6 +1626,30 @@ extern "C" sb_status sb_selftest_div(int64_t n, uint64_t seed, int64_t* mismatch
   const cudaError_t e = cudaGetLastError();
   unsigned long long h = 0;
   cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) throw Error{SB_ERR_CUDA, cudaGetErrorString(e)};
+  *mismatches = (int64_t)h;
+  SB_API_END
+}
+
+extern "C" sb_status sb_selftest_serial_sum(int64_t blocks, int64_t max_len, uint64_t seed, int mode,
+                                           int64_t* mismatches) {
+  SB_API_BEGIN
+  if (!mismatches || blocks < 1 || max_len < 1 || mode < 0 || mode > 6)
+    throw Error{SB_ERR_CONFIG, "sb_selftest_serial_sum: bad arguments"};
+  unsigned long long* d = nullptr;
+  double* pre = nullptr;
+  SB_CUDA(cudaMalloc(&d, sizeof *d));
+  if (cudaMalloc(&pre, sizeof(double) * blocks * max_len) != cudaSuccess) {
+    cudaFree(d);
+    throw Error{SB_ERR_CUDA, "sb_selftest_serial_sum: scratch allocation"};
+  }
+  cudaMemset(d, 0, sizeof *d);
+  sb::k_selftest_sum<<<(unsigned)blocks, sb::kSumThreads>>>(seed, mode, max_len, pre, d);
+  const cudaError_t e = cudaGetLastError();
+  unsigned long long h = 0;
+  cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(pre);
   cudaFree(d);
   if (e != cudaSuccess) throw Error{SB_ERR_CUDA, cudaGetErrorString(e)};
   *mismatches = (int64_t)h;
