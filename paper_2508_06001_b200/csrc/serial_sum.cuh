@@ -69,10 +69,20 @@ __device__ __forceinline__ int64_t sum_inc(const SumElem& e, int64_t par) {
   return e.m + (e.tie ? ((par + e.m) & 1) : e.rb);
 }
 
-// Block-wide serial sum of x_j = load(j), j in [0, n).  All NT threads of the
-// CTA call it with the same n and get the same result.  emit(j, s_j, x_j) runs
-// exactly once for every j (on some thread) with the serially-rounded sum of
-// x_0..x_{j-1}.  Requires blockDim.x == NT.
+// Named barrier 1 over threads [0, NT): the sum can run on the first warps of a
+// larger CTA (the fused planner) while the others wait at their next barrier.
+template <int NT>
+__device__ __forceinline__ void sum_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+// Serial sum of x_j = load(j), j in [0, n), by threads [0, NT) of the CTA
+// (whole warps; all of them call with the same n and get the same result).
+// emit(j, s_j, x_j) runs exactly once for every j (on some thread) with the
+// serially-rounded sum of x_0..x_{j-1}.  Every restart (one per binade
+// crossing and per NT*E-element window) costs several thousand cycles, so a
+// one-thread chain (~10 cycles per element) stays cheaper below a few thousand
+// elements: the planner uses this on its large path only.
 template <int NT, int E, class Load, class Emit>
 __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
   static_assert(NT % 32 == 0 && NT <= 1024, "whole warps");
@@ -99,10 +109,10 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
       }
       s_next = t;
     }
-    __syncthreads();
+    sum_bar<NT>();
     s = s_next;
     i = h;
-    __syncthreads();
+    sum_bar<NT>();
   }
   while (i < n) {
     if (!(s < __longlong_as_double(0x7ff0000000000000ll))) {  // +inf absorbs everything that follows
@@ -112,16 +122,16 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
     if (s == 0.0) {  // RN(0 + x) = x: skip the leading zeros of the window, take the first non-zero
       const int64_t w1 = i + WIN < n ? i + WIN : n;
       if (tid == 0) s_jstar = ~0ull;
-      __syncthreads();
+      sum_bar<NT>();
       for (int64_t j = i + tid; j < w1; j += NT)
         if (load(j) != 0.0) atomicMin(&s_jstar, (unsigned long long)j);
-      __syncthreads();
+      sum_bar<NT>();
       const unsigned long long js = s_jstar;
       const int64_t last = js == ~0ull ? w1 : (int64_t)js + 1;
       for (int64_t j = i + tid; j < last; j += NT) emit(j, 0.0, load(j));
       if (js != ~0ull) s = load((int64_t)js);
       i = last;
-      __syncthreads();  // s_jstar reuse
+      sum_bar<NT>();  // s_jstar reuse
       continue;
     }
     if (s < 0x1p-960) {  // tiny running sum (its ulp would be subnormal): one scalar step
@@ -161,7 +171,7 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
     }
     if (lane == 31) s_wp[warp] = inc;
     if (tid == 0) s_jstar = ~0ull;
-    __syncthreads();
+    sum_bar<NT>();
     if (warp == 0) {
       SumPair x = lane < NW ? s_wp[lane] : SumPair{0, 0};
       SumPair xi = x;
@@ -179,7 +189,7 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
       if (lane < NW) s_wp[lane] = ex;
       if (lane == NW - 1) s_wp[NW] = xi;
     }
-    __syncthreads();
+    sum_bar<NT>();
     // exclusive prefix of this thread = (warp prefix) o (lanes before it in the warp)
     SumPair lex;
     lex.a0 = __shfl_up_sync(0xffffffffu, inc.a0, 1);
@@ -201,7 +211,7 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
       }
     }
     if (cross < E) atomicMin(&s_jstar, (unsigned long long)(j0 + cross));
-    __syncthreads();
+    sum_bar<NT>();
     const unsigned long long js = s_jstar;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -212,7 +222,7 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
         if ((unsigned long long)j == js) s_next = __dadd_rn(sb4, xv[k]);
       }
     }
-    __syncthreads();
+    sum_bar<NT>();
     if (js != ~0ull) {
       s = s_next;
       i = (int64_t)js + 1;
@@ -220,7 +230,7 @@ __device__ double block_serial_sum(int64_t n, Load load, Emit emit) {
       s = __dmul_rn((double)(K + (p0 ? tot.a1 : tot.a0)), q);
       i = i + WIN < n ? i + WIN : n;
     }
-    __syncthreads();  // s_next / s_wp / s_jstar reuse
+    sum_bar<NT>();  // s_next / s_wp / s_jstar reuse
   }
   return s;
 }
