@@ -240,6 +240,34 @@ def test_random_plans_vs_oracle(topo, path):
         assert hp.rev_recv == rev.recv
 
 
+@pytest.mark.parametrize("topo", ["g8n1", "g2n4", "g4n1+g2n1+g1n2"])
+def test_plans_beyond_shared_staging_vs_oracle(topo):
+    """More sequences than the serial-sum kernels stage in shared memory
+    (kSumStage = 24 576): the large path's totals and one-bag occupancy replay
+    read global memory; zero lengths and repeated lengths (exact workload
+    ties) included.  Report bit-exact against the oracle."""
+    rng = np.random.default_rng(29)
+    W = 8
+    lens = []
+    for r in range(W):
+        x = rng.integers(0, 4096, size=3300)
+        x[rng.random(3300) < 0.05] = 0
+        lens.append(x.tolist())
+    meta = oracle.meta_explicit(lens)
+    planner = sb.Planner(topo, W, max_seqs=W * 3300)
+    planner.plan(device_meta(meta))
+    hp = planner.download()
+    plan, rep = oracle.plan_routing(meta, oracle.parse_topology(topo))
+    got = host_plan_as_oracle(hp, meta)
+    assert got.chunk_rows() == plan.chunk_rows()
+    assert got.send == plan.send and got.recv == plan.recv
+    assert [dbits(x) for x in hp.per_gpu_workload] == [dbits(x) for x in rep.per_gpu_workload]
+    assert [dbits(x) for x in hp.per_bag_occupancy] == [dbits(x) for x in rep.per_bag_occupancy]
+    assert hp.capacity_violations == rep.capacity_violations
+    assert dbits(hp.total_workload) == dbits(rep.total_workload)
+    assert dbits(hp.wir) == dbits(rep.wir)
+
+
 def test_full_width_c1_roundtrip_bit_exact():
     """C1 at the bench width (768 doubles == 3072 bf16 == 6144 B/row)."""
     meta = oracle.meta_c1(8, 32, seed=1, step=0)
