@@ -175,25 +175,33 @@ __global__ void __launch_bounds__(256) k_prep_seq(PlanArgs a) {
   }
 }
 
-// Per rank: origin packing offsets (block scan of the lengths in buffer order).
-__global__ void __launch_bounds__(256) k_prep_rows(PlanArgs a) {
+// Per rank: origin packing offsets (block scan of the lengths in buffer
+// order), one pass: each thread owns a contiguous slice, one block scan of the
+// slice sums.  Runs on the side stream beside the totals (nothing before the
+// greedy reads it).
+constexpr int kPrepRowsThreads = 1024;
+
+__global__ void __launch_bounds__(kPrepRowsThreads) k_prep_rows(PlanArgs a) {
   __shared__ int64_t sh[33];
   const int r = blockIdx.x;
   if (!seqs_ok(a)) return;
   const int64_t lo = a.rank_off[r], hi = a.rank_off[r + 1];
-  int64_t carry = 0;
-  for (int64_t base = lo; base < hi; base += blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const bool valid = i < hi;
-    int64_t len = valid ? a.lens[i] : 0;
-    len = len < 0 ? 0 : len;
-    int64_t tot;
-    const int64_t ex = block_excl_scan<int64_t>(len, sh, &tot);
-    if (valid) a.seq_off[i] = carry + ex;
-    carry += tot;
+  const int64_t per = (hi - lo + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = lo + (int64_t)threadIdx.x * per, b1 = b0 + per < hi ? b0 + per : hi;
+  int64_t loc = 0;
+  for (int64_t i = b0; i < b1; ++i) {
+    const int64_t len = a.lens[i];
+    loc += len < 0 ? 0 : len;
+  }
+  int64_t tot;
+  int64_t run = block_excl_scan<int64_t>(loc, sh, &tot);
+  for (int64_t i = b0; i < b1; ++i) {
+    a.seq_off[i] = run;
+    const int64_t len = a.lens[i];
+    run += len < 0 ? 0 : len;
   }
   if (threadIdx.x == 0) {
-    a.origin_rows[r] = carry;
+    a.origin_rows[r] = tot;
     a.send_count[r] = 0;
   }
 }
@@ -1385,25 +1393,26 @@ static int64_t sum_stage_cap(const sb_planner* p) {
   return cap;
 }
 
-// The serial FP64 totals fork onto the planner's side stream as soon as the
-// metadata is there (they recompute workloads from lengths) and join before
-// the greedy: the chain overlaps the per-sequence pass and the sort.
+// The serial FP64 totals and the origin row offsets fork onto the planner's
+// side stream as soon as the metadata is there (the totals recompute workloads
+// from lengths) and join before the greedy: they overlap the per-sequence
+// pass and the sort.
 static void launch_totals(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
   SB_CUDA(cudaEventRecord(p->fork_ev, s));
   SB_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
   const int64_t cap = sum_stage_cap(p);
   k_totals<<<p->R + 1, kSumThreads, (size_t)cap * sizeof(double), p->side>>>(a, cap);
   SB_CHECK_LAUNCH();
+  k_prep_rows<<<p->W, kPrepRowsThreads, 0, p->side>>>(a);
+  SB_CHECK_LAUNCH();
   SB_CUDA(cudaEventRecord(p->join_ev, p->side));
-  count_launch(1);
+  count_launch(2);
 }
 
 static void launch_prep(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
   k_prep_seq<<<(int)((p->max_seqs + 255) / 256), 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
-  k_prep_rows<<<p->W, 256, 0, s>>>(a);
-  SB_CHECK_LAUNCH();
-  count_launch(2);
+  count_launch(1);
 }
 
 static void launch_sort(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool order) {
