@@ -302,16 +302,45 @@ class Planner:
         call("sb_plan_get", self._h, C.byref(v))
         return v
 
-    def download(self, stream=None) -> HostPlan:
+    def host_buffers(self, pinned: bool = True) -> dict:
+        """Caller-owned host arrays for ``download(out=...)``, sized for the
+        planner's capacity; pinned (page-locked) so the device copies run
+        asynchronously at PCIe speed.  Reused by every download into them."""
+        torch = _torch()
+        W = self.world_size
+        nc = int(self.max_seqs) * int(self.max_bag)  # every sequence splits into at most max_bag chunks
+        nb = self.replicas * len(self.topology.bag_sizes)
+        spec = dict(c_id=(nc, torch.int64, np.uint64), c_idx=(nc, torch.int32, None),
+                    c_start=(nc, torch.int64, None), c_end=(nc, torch.int64, None), c_src=(nc, torch.int32, None),
+                    c_dst=(nc, torch.int32, None), send_off=(W + 1, torch.int64, None),
+                    send_idx=(nc, torch.int32, None), recv_off=(W + 1, torch.int64, None),
+                    recv_idx=(nc, torch.int32, None), rev_recv_idx=(nc, torch.int32, None),
+                    target_rows=(W, torch.int64, None), per_gpu_workload=(W, torch.float64, None),
+                    per_bag_occupancy=(nb, torch.float64, None))
+        out = {}
+        for k, (n, dt, view) in spec.items():
+            a = torch.empty(max(1, n), dtype=dt, pin_memory=pinned).numpy()
+            out[k] = a.view(view) if view is not None else a
+        return out
+
+    def download(self, stream=None, out: dict | None = None) -> HostPlan:
+        """The plan in host arrays (sb_plan_download).  ``out``: buffers from
+        host_buffers() to download into (the returned plan views them)."""
         nc, _ = self.sizes(stream)
         W = self.world_size
         nb = self.replicas * len(self.topology.bag_sizes)
-        a = dict(c_id=np.zeros(nc, np.uint64), c_idx=np.zeros(nc, np.int32), c_start=np.zeros(nc, np.int64),
-                 c_end=np.zeros(nc, np.int64), c_src=np.zeros(nc, np.int32), c_dst=np.zeros(nc, np.int32),
-                 send_off=np.zeros(W + 1, np.int64), send_idx=np.zeros(nc, np.int32),
-                 recv_off=np.zeros(W + 1, np.int64), recv_idx=np.zeros(nc, np.int32),
-                 rev_recv_idx=np.zeros(nc, np.int32), target_rows=np.zeros(W, np.int64),
-                 per_gpu_workload=np.zeros(W, np.float64), per_bag_occupancy=np.zeros(nb, np.float64))
+        if out is None:
+            a = dict(c_id=np.zeros(nc, np.uint64), c_idx=np.zeros(nc, np.int32), c_start=np.zeros(nc, np.int64),
+                     c_end=np.zeros(nc, np.int64), c_src=np.zeros(nc, np.int32), c_dst=np.zeros(nc, np.int32),
+                     send_off=np.zeros(W + 1, np.int64), send_idx=np.zeros(nc, np.int32),
+                     recv_off=np.zeros(W + 1, np.int64), recv_idx=np.zeros(nc, np.int32),
+                     rev_recv_idx=np.zeros(nc, np.int32), target_rows=np.zeros(W, np.int64),
+                     per_gpu_workload=np.zeros(W, np.float64), per_bag_occupancy=np.zeros(nb, np.float64))
+        else:
+            if nc > len(out["c_id"]):
+                raise _capi.CapacityError("download: plan larger than the host buffers")
+            lens = dict(send_off=W + 1, recv_off=W + 1, target_rows=W, per_gpu_workload=W, per_bag_occupancy=nb)
+            a = {k: v[:lens.get(k, nc)] for k, v in out.items()}
         h = _capi.PlanHost(*[x.ctypes.data for x in a.values()])
         call("sb_plan_download", self._h, C.byref(h), _stream(stream))
         return HostPlan(W, *a.values(), capacity_violations=int(h.capacity_violations),

@@ -88,6 +88,9 @@ struct sb_planner {
   uint64_t *ck_hi = nullptr, *ck_lo = nullptr, *ck_thi = nullptr, *ck_tlo = nullptr;
   uint32_t *ck_v = nullptr, *ck_tv = nullptr;
 
+  // pinned host scalars for read-backs: [0] status (int32), [1] n_chunks, [2] n_seqs
+  int64_t* h_small = nullptr;
+
   // plan (device)
   int64_t* n_chunks = nullptr;
   int64_t* n_seqs = nullptr;

@@ -1278,6 +1278,7 @@ static PlanArgs make_args(sb_planner* p) {
 
 static void planner_alloc(sb_planner* p) {
   const int64_t N = p->max_seqs, C = p->max_chunks, W = p->W, R = p->R, M = p->M;
+  SB_CUDA(cudaHostAlloc(&p->h_small, 4 * sizeof(int64_t), cudaHostAllocDefault));
   dalloc(&p->d_bag_off, M + 1); dalloc(&p->d_bag_ranks, p->U); dalloc(&p->d_bag_size, M);
   dalloc(&p->d_rank_bag, p->U); dalloc(&p->d_rank_member, p->U);
   dalloc(&p->w, N); dalloc(&p->seq_rank, N); dalloc(&p->seq_off, N); dalloc(&p->hash, 2 * N);
@@ -1340,6 +1341,7 @@ static void planner_free(sb_planner* p) {
                   p->bag_cbase, p->bag_sbase};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  if (p->h_small) cudaFreeHost(p->h_small);
   for (int i = 0; i < 6; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   if (p->fork_ev) cudaEventDestroy(p->fork_ev);
@@ -1894,10 +1896,17 @@ extern "C" sb_status sb_plan_get(const sb_planner* p, sb_plan_dev* o) {
   SB_API_END
 }
 
+// One read-back per call: status, chunk count and (for planned metadata) the
+// sequence count land in pinned scalars with one stream synchronisation.
 static void check_plan_status(sb_planner* p, cudaStream_t s) {
+  int32_t* st_h = reinterpret_cast<int32_t*>(&p->h_small[0]);
+  SB_CUDA(cudaMemcpyAsync(st_h, p->status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaMemcpyAsync(&p->h_small[1], p->n_chunks, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  p->h_small[2] = 0;
+  if (!p->uploaded && p->rank_off)  // uploaded plans carry no sequence metadata
+    SB_CUDA(cudaMemcpyAsync(&p->h_small[2], p->rank_off + p->W, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   SB_CUDA(cudaStreamSynchronize(s));
-  int32_t st = 0;
-  SB_CUDA(cudaMemcpy(&st, p->status, sizeof st, cudaMemcpyDeviceToHost));
+  const int32_t st = *st_h;
   if (st & sb::ST_CAPACITY)
     throw Error{SB_ERR_CAPACITY, "plan_routing: more sequences than the planner capacity"};
   if (st & sb::ST_NEG_LENGTH) throw Error{SB_ERR_CONFIG, "seq_len must be >= 0"};
@@ -1910,12 +1919,8 @@ extern "C" sb_status sb_plan_sizes(sb_planner* p, sb_stream stream, int64_t* n_c
   SB_API_BEGIN
   if (!p) throw Error{SB_ERR_CONFIG, "sb_plan_sizes: null planner"};
   check_plan_status(p, (cudaStream_t)stream);
-  int64_t c = 0, n = 0;
-  SB_CUDA(cudaMemcpy(&c, p->n_chunks, sizeof c, cudaMemcpyDeviceToHost));
-  if (!p->uploaded && p->rank_off)  // uploaded plans carry no sequence metadata
-    SB_CUDA(cudaMemcpy(&n, p->rank_off + p->W, sizeof n, cudaMemcpyDeviceToHost));
-  if (n_chunks) *n_chunks = c;
-  if (n_seqs) *n_seqs = n;
+  if (n_chunks) *n_chunks = p->h_small[1];
+  if (n_seqs) *n_seqs = p->h_small[2];
   SB_API_END
 }
 
@@ -1929,8 +1934,7 @@ extern "C" sb_status sb_plan_download(sb_planner* p, sb_plan_host* o, sb_stream 
   if (!p || !o) throw Error{SB_ERR_CONFIG, "sb_plan_download: null argument"};
   cudaStream_t s = (cudaStream_t)stream;
   check_plan_status(p, s);
-  int64_t c = 0;
-  SB_CUDA(cudaMemcpy(&c, p->n_chunks, sizeof c, cudaMemcpyDeviceToHost));
+  const int64_t c = p->h_small[1];
   d2h(o->chunk_id, p->c_id, c, s);
   d2h(o->chunk_index, p->c_idx, c, s);
   d2h(o->chunk_start, p->c_start, c, s);

@@ -268,6 +268,24 @@ def test_plans_beyond_shared_staging_vs_oracle(topo):
     assert dbits(hp.wir) == dbits(rep.wir)
 
 
+def test_download_into_pinned_buffers_matches():
+    """Planner.download(out=host_buffers()) -- page-locked caller buffers,
+    reused across plans -- returns the same plan as a fresh download."""
+    rng = np.random.default_rng(5)
+    planner = sb.Planner("g2n4", 8, max_seqs=512)
+    host = planner.host_buffers(pinned=True)
+    for trial in range(3):
+        lens = [rng.integers(0, 3000, size=rng.integers(1, 60)).tolist() for _ in range(8)]
+        meta = oracle.meta_explicit(lens)
+        planner.plan(device_meta(meta))
+        a, b = planner.download(), planner.download(out=host)
+        for f in ("c_id", "c_idx", "c_start", "c_end", "c_src", "c_dst", "send_off", "send_idx", "recv_off",
+                  "recv_idx", "rev_recv_idx", "target_rows", "per_gpu_workload", "per_bag_occupancy"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        assert (a.capacity_violations, dbits(a.total_workload), dbits(a.wir)) == \
+            (b.capacity_violations, dbits(b.total_workload), dbits(b.wir))
+
+
 def test_full_width_c1_roundtrip_bit_exact():
     """C1 at the bench width (768 doubles == 3072 bf16 == 6144 B/row)."""
     meta = oracle.meta_c1(8, 32, seed=1, step=0)
