@@ -227,17 +227,42 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
     __syncthreads();
   }
   SB_PHASE(3);
-  // ---- phase 3: duplicate sample ids inside a replica (divergence)
-  if (!a.w_in) {
+  // ---- phases 3+4 side by side: warps 0-1 run the serial FP64 totals
+  // (balancer.cpp:24-25, :147) while warps 2.. check for duplicate sample ids
+  // inside each replica (divergence); named barrier 2 syncs
+  // the checking warps only.  One replica: its total is the report total
+  // (same additions, same order).
+  if (warp == 0) {
+    if (lane == 0) {
+      double s = 0.0;
+      for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_w[i]);
+      *a.total = s;
+      *a.n_seqs = N;
+      if (R == 1) {
+        s_reptot[0] = s;
+        a.rep_total[0] = s;
+      }
+    }
+  } else if (warp == 1) {
+    if (R > 1)
+      for (int rep = lane; rep < R; rep += 32) {
+        double s = 0.0;
+        for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
+        s_reptot[rep] = s;
+        a.rep_total[rep] = s;
+      }
+  } else if (!a.w_in) {
     // open-addressing set per replica in the (not yet used) sort scratch:
     // s_hi and s_lo are contiguous, 2T slots >= 2 * replica size, EMPTY = ~0
+    const int t = tid - 64, nt = (int)blockDim.x - 64;
+    auto bar = [nt]() { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); };
     for (int rep = 0; rep < R; ++rep) {
       const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
       const int tsz = 2 * L.T;
-      for (int i = tid; i < tsz; i += blockDim.x) s_hi[i] = ~0ull;
-      if (tid == 0) s_v[0] = 0;  // count of ids equal to the EMPTY marker
-      __syncthreads();
-      for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
+      for (int i = t; i < tsz; i += nt) s_hi[i] = ~0ull;
+      if (t == 0) s_v[0] = 0;  // count of ids equal to the EMPTY marker
+      bar();
+      for (int64_t i = lo + t; i < hi; i += nt) {
         const uint64_t id = s_ids[i];
         if (id == ~0ull) {
           if (atomicAdd(&s_v[0], 1u) > 0) s_flag = 1;
@@ -255,26 +280,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
           slot = (slot + 1) & (uint32_t)(tsz - 1);
         }
       }
-      __syncthreads();
+      bar();
     }
-    if (s_flag && tid == 0) atomicOr(a.status, ST_DUP_ID);
-  }
-  SB_PHASE(4);
-  // ---- phase 4: serial FP64 totals (balancer.cpp:24-25, :147)
-  if (tid == 0) {
-    double s = 0.0;
-    for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_w[i]);
-    *a.total = s;
-    *a.n_seqs = N;
-  } else if (lane == 0 && warp >= 1) {
-    for (int rep = warp - 1; rep < R; rep += nw - 1) {
-      double s = 0.0;
-      for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
-      s_reptot[rep] = s;
-      a.rep_total[rep] = s;
-    }
+    if (s_flag && t == 0) atomicOr(a.status, ST_DUP_ID);
   }
   __syncthreads();
+  SB_PHASE(4);
   SB_PHASE(5);
   // ---- phase 5: per replica sort by (workload desc, id asc) (balancer.cpp:37-40)
   for (int rep = 0; rep < R; ++rep) {
