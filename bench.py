@@ -981,6 +981,7 @@ def main():
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
                 "h2d_busy_ms_per_step": h2d_busy_ms, "h2d_start_period_ms": h2d_period_ms,
                 "h2d_alone_ms": h2d_alone_ms,
+                "host_buffers": sb.hostmem.choice(),
                 "host_enqueue_ms_per_step": host_enqueue_ms,
                 "result": "content_checksum of the restored world, computed on the device and checked against "
                           "the input's every step",
