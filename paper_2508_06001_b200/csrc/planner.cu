@@ -472,7 +472,8 @@ constexpr int kGreedyChunk = 1024;  // `hook(p0)` runs before every chunk of thi
 // with m == 1), so the argmin chain disappears.  What stays serial is the FP64
 // prefix in greedy order -- `capacity - assigned >= w` decides the violation
 // count (balancer.cpp:159-163) and `assigned` the occupancy and per-GPU load --
-// one DADD per sequence on lane 0; the other lanes write the picks.
+// one DADD per sequence on lane 0; the other lanes write the picks.  Used by
+// the fused planner (the large path runs k_single_bag_fill + k_single_bag_chain).
 template <int CHUNK, class GetW, class Hook>
 __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, int64_t n, double target, GetW getw,
                                                   Hook hook, int32_t* pick_out, int32_t* bagcnt_out,
@@ -484,8 +485,7 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
   double asg = 0.0;
   int viol = 0;
   auto run = [&](int p0, int p1) {
-    if (pick_out)
-      for (int p = p0 + lane; p < p1; p += 32) pick_out[p] = 0;
+    for (int p = p0 + lane; p < p1; p += 32) pick_out[p] = 0;
     if (lane == 0) {
       // the DADD on `asg` is the only chain: eight violation counters keep the
       // predicated increments off it (one counter was a second ~8-cycle chain)
@@ -522,7 +522,7 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
   }
   if (lane != 0) return;
   if (bagcnt_out) bagcnt_out[rep] = nn;
-  if (pick_out) a.bag_count[rep] = nn;  // else k_single_bag_fill wrote picks and counts
+  a.bag_count[rep] = nn;
   a.per_bag_occ[rep] = occupancy(asg, cap);  // balancer.cpp:170-175
   const double per = __ddiv_rn(asg, (double)size);  // balancer.cpp:199-202
   for (int k = 0; k < size; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[0] + k]] = per;
@@ -632,7 +632,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
 constexpr int kGreedyStage = 24576;  // 192 KB of workloads
 
 template <int BPL>
-__global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a, bool picks) {
+__global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
   extern __shared__ __align__(16) double stage[];
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, lane = threadIdx.x;
@@ -641,12 +641,12 @@ __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a, bool picks) {
   const double* sw = a.sorted_w + lo;
   for (int i = lane; i < n; i += 32) stage[i] = sw[i];
   __syncwarp();
-  greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {},
-                      picks ? a.pick + lo : nullptr, nullptr, a.violations);
+  greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
+                      nullptr, a.violations);
 }
 
 template <int BPL>
-__global__ void __launch_bounds__(32) k_greedy(PlanArgs a, bool picks) {
+__global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
   __shared__ double ring[2][kGreedyChunk];
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, lane = threadIdx.x;
@@ -663,8 +663,8 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a, bool picks) {
     __syncwarp();
   };
   greedy_warp<BPL, kGreedyChunk>(a, rep, n, a.rep_total[rep],
-                   [&](int p) { return ring[(p / kGreedyChunk) & 1][p % kGreedyChunk]; }, hook,
-                   picks ? a.pick + lo : nullptr, nullptr, a.violations);
+                   [&](int p) { return ring[(p / kGreedyChunk) & 1][p % kGreedyChunk]; }, hook, a.pick + lo,
+                   nullptr, a.violations);
 }
 
 // One bag per replica: the picks (all bag 0) and bag counts (replica sizes)
@@ -1480,11 +1480,11 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool
       else SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       set_to[wide] = smem;
     }
-    if (wide) k_greedy_staged<2><<<p->R, 32, smem, s>>>(a, true);
-    else k_greedy_staged<1><<<p->R, 32, smem, s>>>(a, true);
+    if (wide) k_greedy_staged<2><<<p->R, 32, smem, s>>>(a);
+    else k_greedy_staged<1><<<p->R, 32, smem, s>>>(a);
   } else {
-    if (wide) k_greedy<2><<<p->R, 32, 0, s>>>(a, true);
-    else k_greedy<1><<<p->R, 32, 0, s>>>(a, true);
+    if (wide) k_greedy<2><<<p->R, 32, 0, s>>>(a);
+    else k_greedy<1><<<p->R, 32, 0, s>>>(a);
   }
   SB_CHECK_LAUNCH();
 }
