@@ -399,7 +399,7 @@ __global__ void k_sort_finish(PlanArgs a, const uint32_t* __restrict__ sv) {
 // lengths (bit-identical to k_prep_seq's), so the sums start with the plan.
 // Runs on the planner's side stream, concurrently with the prep and the sort.
 constexpr int kSumThreads = 512;  // measured: 512 beats 128 at 16K (fewer window restarts)
-constexpr int kSumPerThread = 8;
+constexpr int kSumPerThread = 4;  // measured at 16K: 2 -> 55 us, 4 -> 47, 8 -> 48-52, 16 -> 59-70
 constexpr int64_t kSumStage = 24576;  // workloads staged in shared memory (192 KB) up to this many
 
 // Stage x_j = f(j), j < n, into dynamic shared memory when the launch gave
