@@ -201,8 +201,31 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   }
   __syncthreads();
   SB_PHASE(2);
-  // ---- phase 2: origin packing offsets (block scan of lens in gather order)
-  {
+  // ---- phase 2: origin packing offsets (exclusive scan of lens in gather
+  // order, rebased per rank).  One replica: warp 1 does it inside phases 3+4,
+  // beside the totals and the duplicate check (origin_offsets_warp below)
+  auto origin_offsets_warp = [&]() {
+    int64_t carry = 0;
+    for (int64_t base = 0; base < N; base += 32) {
+      const int64_t i = base + lane;
+      const int64_t v = i < N ? s_lens[i] : 0;
+      const int64_t inc = warp_incl_scan<int64_t>(v);
+      if (i < N) s_soff[i] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncwarp();
+    for (int r = lane; r <= W; r += 32) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : carry;
+    __syncwarp();
+    for (int64_t i = lane; i < N; i += 32) {
+      s_soff[i] -= s_rpre[s_rank[i]];
+      a.seq_off[i] = s_soff[i];
+    }
+    for (int r = lane; r < W; r += 32) {
+      a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+      s_sendcnt[r] = 0;
+    }
+  };
+  if (R > 1) {
     const int64_t per = (N + blockDim.x - 1) / blockDim.x;
     const int64_t b0 = tid * per, b1 = b0 + per < N ? b0 + per : N;
     int64_t loc = 0;
@@ -244,7 +267,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       }
     }
   } else if (warp == 1) {
-    if (R > 1)
+    if (R == 1) origin_offsets_warp();
+    else
       for (int rep = lane; rep < R; rep += 32) {
         double s = 0.0;
         for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
@@ -537,13 +561,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   SB_PHASE(12);
   // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
   __syncthreads();
-  if (tid == 0) {
-    double lo = a.per_gpu[0], hi = a.per_gpu[0];
-    for (int r = 0; r < W; ++r) {
-      lo = fmin(lo, a.per_gpu[r]);
-      hi = fmax(hi, a.per_gpu[r]);
+  if (warp == 0) {  // min and max are order-independent (no NaN): one warp, loads in parallel
+    double lo = a.per_gpu[0], hi = lo;
+    for (int r = lane; r < W; r += 32) {
+      const double v = a.per_gpu[r];
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
     }
-    *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0)
+      *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
   }
   SB_PHASE(13);
 }
