@@ -457,6 +457,31 @@ def run_c5(args):
     return 0
 
 
+# ------------------------------------------------- N-process self-launch
+def spawn_workers(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: launch N worker processes
+    (one per GPU, torch.distributed.run on 127.0.0.1) running this same
+    command, relay rank 0's JSON line, and fail (rc != 0) if they do."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    p = subprocess.run(cmd, stdout=subprocess.PIPE, text=True)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    for ln in lines:
+        print(ln, flush=True)
+    if p.returncode != 0:
+        sys.stderr.write(f"bench.py: {n} worker processes failed (rc {p.returncode})\n")
+        return p.returncode
+    if not lines:
+        sys.stderr.write("bench.py: workers printed no result line\n")
+        return 1
+    return 0
+
+
 # ------------------------------------------------------------ our arm
 def main():
     args = parse_args()
@@ -464,6 +489,12 @@ def main():
     topology = args.topology or cfg["topology"]
     rank = int(os.environ.get("RANK", "0"))
     world_procs = int(os.environ.get("WORLD_SIZE", "1"))
+    if (args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ
+            and args.config not in ("c4", "c5")):
+        return spawn_workers(args.gpus)
+    if args.impl == "ours" and args.gpus != world_procs and args.config not in ("c4", "c5"):
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_procs}\n")
+        return 2
 
     if args.impl == "reference":
         if rank != 0:

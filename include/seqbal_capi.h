@@ -77,7 +77,11 @@ typedef struct sb_planner_desc {
 
 /* Validates like WorkloadModel::validate (workload_model.cpp:15-31),
  * replicate (topology.cpp:81-93) and plan_routing's head check
- * (balancer.cpp:114-120); SB_ERR_CONFIG with the reference's message. */
+ * (balancer.cpp:114-120); SB_ERR_CONFIG with the reference's message.
+ * Limits: at most 64 bags per replica (SB_ERR_CONFIG "more than 64 bags per
+ * replica"; the reference has none).  All four shape fields 0 create an
+ * assignment-only planner for sb_assign_to_bags (no model, no head check);
+ * sb_plan / sb_plan_identity refuse it. */
 SB_API sb_status sb_planner_create(const sb_planner_desc* desc, sb_planner** out);
 SB_API sb_status sb_planner_destroy(sb_planner* p);
 
@@ -448,6 +452,14 @@ SB_API sb_status sb_barrier_destroy(sb_barrier* b);
 SB_API sb_status sb_barrier_buffer(const sb_barrier* b, void** buf, int64_t* bytes);
 SB_API sb_status sb_barrier_set_peers(sb_barrier* b, const uint64_t* bases, int n_procs);
 SB_API sb_status sb_barrier_wait(sb_barrier* b, sb_stream stream);
+/* Bounded wait: a barrier that does not complete within the timeout
+ * (default 60 s, env SEQBAL_BARRIER_TIMEOUT_MS) records which process did
+ * not arrive; sb_barrier_status synchronises the stream and returns
+ * SB_ERR_COMM with that process and epoch (failure detection).
+ * The epoch counter is device-resident, so barriers replay inside CUDA
+ * graphs; *epoch (optional) receives the last completed epoch. */
+SB_API sb_status sb_barrier_set_timeout(sb_barrier* b, double timeout_ms);
+SB_API sb_status sb_barrier_status(sb_barrier* b, uint64_t* epoch, sb_stream stream);
 
 /* Device time of the copy kernels launched while timing was enabled
  * (sb_planner_enable_timing): op 0 route, 1 reverse_route, 2 pre_attn,

@@ -77,11 +77,11 @@ def parse_topology(spec: str) -> Topology:
     """Grammar of topology.cpp:31-65: term ('+' term)*, term := 'g' INT 'n' INT."""
     if not spec:
         raise ParseError("empty topology spec (at offset 0)")
-    sizes, pos = [], 0
+    terms, pos = [], 0
 
     def num(p, what):
         q, v = p, 0
-        while q < len(spec) and spec[q].isdigit():
+        while q < len(spec) and "0" <= spec[q] <= "9":  # ASCII digits only, as parse_int
             v = v * 10 + ord(spec[q]) - 48
             if v > (1 << 20):
                 raise ParseError(f"{what} value too large (at offset {p})")
@@ -99,12 +99,19 @@ def parse_topology(spec: str) -> Topology:
         if pos >= len(spec) or spec[pos] != "n":
             raise ParseError(f"expected 'n' (at offset {pos})")
         n, pos = num(pos + 1, "bag count")
-        sizes += [g] * n
+        terms.append((g, n))
         if pos == len(spec):
             break
         if spec[pos] != "+":
             raise ParseError(f"expected '+' or end of spec (at offset {pos})")
         pos += 1
+    sizes, unit = [], 0
+    for g, n in terms:  # topology.cpp:51-62: the unit-size check runs after the whole spec parsed
+        for _ in range(n):
+            unit += g
+            if unit > (1 << 20):
+                raise ParseError("unit size too large (at offset 0)")
+            sizes.append(g)
     return Topology(sizes)
 
 

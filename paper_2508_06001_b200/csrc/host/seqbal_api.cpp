@@ -694,22 +694,17 @@ std::vector<SequenceAssignment> assign_to_bags(std::vector<SequenceWorkload> wor
   k.bag_off.push_back(0);
   int g_all = 0;
   for (const ComputeBag& b : bags) {
+    // Divergence (documented in DESIGN.md): the reference gives an empty bag
+    // capacity 0 and occupancy 0/inf; the device planner rejects it.
     if (b.size() < 1) throw ConfigError("assign_to_bags: empty bag");
     for (int i = 0; i < b.size(); ++i) k.bag_ranks.push_back(g_all + i);
     g_all += b.size();
     k.bag_off.push_back(g_all);
   }
   k.W = k.U = g_all;
-  // a shape every bag size divides (heads = lcm-free: product of sizes is
-  // enough for validation; the assignment itself never looks at heads)
-  k.n_heads = 1;
-  for (const ComputeBag& b : bags) {
-    const int g = b.size();
-    if (k.n_heads % g) k.n_heads *= g;
-  }
-  k.d_head = 1;
-  k.d_model = k.n_heads;
-  k.n_blocks = 1;
+  // assignment-only planner (all shape fields 0): the greedy never reads the
+  // model, so there is no head-divisibility check to satisfy
+  k.n_heads = k.d_head = k.d_model = k.n_blocks = 0;
   k.gamma = 1.0;
   k.k = 1.0;
   std::lock_guard<std::mutex> lock(dev().mu);
@@ -767,9 +762,11 @@ RoutingPlan identity_plan(const std::vector<std::vector<SequenceInfo>>& per_rank
     RoutingPlan empty;
     return empty;
   }
+  // identity planning never reads the bag tables: one 1-rank bag replicated
+  // W times keeps the planner at one bag per replica for any world size
   Topology t;
-  for (int r = 0; r < W; ++r) t.bags.push_back(ComputeBag{r, {r}});
-  t.unit_size = W;
+  t.bags.push_back(ComputeBag{0, {0}});
+  t.unit_size = 1;
   WorkloadModel model;
   std::lock_guard<std::mutex> lock(dev().mu);
   const FlatMeta f = flatten(per_rank_seqs);
@@ -1077,6 +1074,7 @@ std::uint64_t content_checksum(const World& world) {
   std::vector<int> all(W);
   std::iota(all.begin(), all.end(), 0);
   upload_world(dw, world, all);
+  std::lock_guard<std::mutex> lock(dev().mu);  // meta_buf is the process-wide staging buffer
   DeviceMeta& m = meta_buf(1, 1);
   std::uint64_t zero = 0, acc = 0;
   void* host0[3] = {&zero, nullptr, nullptr};

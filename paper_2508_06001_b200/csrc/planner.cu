@@ -1566,8 +1566,11 @@ extern "C" sb_status sb_planner_create(const sb_planner_desc* d, sb_planner** ou
   SB_API_BEGIN
   if (!d || !out) throw Error{SB_ERR_CONFIG, "sb_planner_create: null argument"};
   *out = nullptr;
+  // All four shape fields 0: an assignment-only planner (sb_assign_to_bags);
+  // no workload model, no head check, sb_plan / sb_plan_identity refuse it.
+  const bool assign_only = d->d_model == 0 && d->n_heads == 0 && d->d_head == 0 && d->n_blocks == 0;
   // WorkloadModel::validate (workload_model.cpp:15-31)
-  if (d->d_model < 1 || d->n_heads < 1 || d->d_head < 1 || d->n_blocks < 1)
+  if (!assign_only && (d->d_model < 1 || d->n_heads < 1 || d->d_head < 1 || d->n_blocks < 1))
     throw Error{SB_ERR_CONFIG, "model shape fields must be >= 1"};
   if ((int64_t)d->n_heads * d->d_head != d->d_model)
     throw Error{SB_ERR_CONFIG, "n_heads * d_head must equal d_model (" + std::to_string(d->n_heads) + " * " +
@@ -1611,7 +1614,7 @@ extern "C" sb_status sb_planner_create(const sb_planner_desc* d, sb_planner** ou
       throw Error{SB_ERR_CONFIG, "empty bag"};
     }
     // plan_routing head check (balancer.cpp:114-120)
-    if (d->n_heads % g != 0) {
+    if (!assign_only && d->n_heads % g != 0) {
       delete p;
       throw Error{SB_ERR_CONFIG, "bag of " + std::to_string(g) + " GPUs does not divide n_heads " +
                                      std::to_string(d->n_heads)};
@@ -1682,6 +1685,7 @@ extern "C" sb_status sb_plan(sb_planner* p, const uint64_t* d_ids, const int64_t
                              const int64_t* d_rank_off, sb_stream stream) {
   SB_API_BEGIN
   if (!p || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_plan: null argument"};
+  if (p->n_heads == 0) throw Error{SB_ERR_CONFIG, "sb_plan: planner was created for assign_to_bags only"};
   p->ids = d_ids;
   p->lens = d_lens;
   p->rank_off = d_rank_off;
@@ -1856,6 +1860,7 @@ extern "C" sb_status sb_plan_identity(sb_planner* p, const uint64_t* d_ids, cons
                                       const int64_t* d_rank_off, sb_stream stream) {
   SB_API_BEGIN
   if (!p || !d_rank_off) throw Error{SB_ERR_CONFIG, "sb_plan_identity: null argument"};
+  if (p->n_heads == 0) throw Error{SB_ERR_CONFIG, "sb_plan_identity: planner was created for assign_to_bags only"};
   p->ids = d_ids;
   p->lens = d_lens;
   p->rank_off = d_rank_off;

@@ -58,6 +58,50 @@ def exchange_bytes(c_src, c_dst, c_start, c_end, world_size, n_procs, row_bytes)
     return sent.astype(np.int64), recv.astype(np.int64)
 
 
+def phase_bytes(hp, op: str, topology, world_size: int, n_procs: int, payload_row_bytes, aux_row_bytes=(),
+                meta_bytes: int = 16):
+    """(sent, recv) bytes per process to / from OTHER processes for one
+    exchange phase of the device plan `hp` (HostPlan).
+
+    route / reverse_route move whole rows (exchange.cpp:127-198).  pre_attn
+    sends, for chunk (q, m) on member m, head slice d of every payload tensor
+    plus the whole metadata / aux row to member d (exchange.cpp:298-325);
+    post_attn gathers slice m from every member m and metadata / aux from
+    member 0 only (exchange.cpp:406-431).  Same decomposition as the device
+    job builders (ulysses_job in csrc/exchange.cu)."""
+    n = (np.asarray(hp.c_end, np.int64) - np.asarray(hp.c_start, np.int64))
+    src, dst = np.asarray(hp.c_src, np.int64), np.asarray(hp.c_dst, np.int64)
+    per = world_size // n_procs
+    full = meta_bytes + int(sum(payload_row_bytes)) + int(sum(aux_row_bytes))
+    if op in ("route", "reverse_route"):
+        s, r = exchange_bytes(src, dst, hp.c_start, hp.c_end, world_size, n_procs, full)
+        return (s, r) if op == "route" else (r, s)
+    sizes = np.asarray(topology.bag_sizes, np.int64)
+    U = int(sizes.sum())
+    rank_bag = np.repeat(np.arange(len(sizes)), sizes)
+    g = sizes[rank_bag[dst % U]]
+    idx = np.asarray(hp.c_idx, np.int64)
+    cq0 = np.arange(len(n), dtype=np.int64) - idx
+    sent = np.zeros(n_procs, np.int64)
+    recv = np.zeros(n_procs, np.int64)
+    whole = meta_bytes + int(sum(aux_row_bytes))
+    for G in np.unique(g[g > 1]):
+        sel = np.nonzero(g == G)[0]
+        sl = int(sum(rb // G for rb in payload_row_bytes))
+        for other in range(int(G)):
+            peer = dst[cq0[sel] + other]  # pre: member d's rank; post: member m's rank
+            if op == "pre_attn":
+                a, b = dst[sel] // per, peer // per
+                nb = n[sel] * (sl + whole)
+            else:
+                a, b = peer // per, dst[sel] // per
+                nb = n[sel] * (sl + (whole if other == 0 else 0))
+            x = a != b
+            sent += np.bincount(a[x], weights=nb[x], minlength=n_procs).astype(np.int64)
+            recv += np.bincount(b[x], weights=nb[x], minlength=n_procs).astype(np.int64)
+    return sent, recv
+
+
 class PeerGroup:
     """Control plane over torch.distributed plus device-buffer sharing."""
 
@@ -113,6 +157,20 @@ class PeerGroup:
         else:
             s.synchronize()
             self.dist.barrier()
+
+    def set_timeout(self, ms: float):
+        if self._barrier is not None:
+            call("sb_barrier_set_timeout", self._barrier, C.c_double(ms))
+
+    def barrier_status(self, stream=None) -> int:
+        """Synchronise; CommError if a device barrier timed out (a peer did
+        not arrive).  Returns the last completed barrier epoch."""
+        if self._barrier is None:
+            return 0
+        s = stream if stream is not None else self.torch.cuda.current_stream()
+        e = C.c_uint64()
+        call("sb_barrier_status", self._barrier, C.byref(e), C.c_void_p(s.cuda_stream))
+        return int(e.value)
 
     def max_over_ranks(self, x: float) -> float:
         t = self.torch.tensor([x], dtype=self.torch.float64)
@@ -202,21 +260,42 @@ class MetaGather:
             self._h = None
 
 
-def step(group: PeerGroup, gather: MetaGather, planner: Planner, A, B, Cw, D, E, ulysses: bool, stream=None):
-    """One pass of the hot path on every process (all phases peer-closed)."""
-    meta = gather.gather(stream)
-    planner.plan(meta, stream)
-    route(planner, A, B, stream)
-    group.barrier(stream)
-    if ulysses:
-        pre_attn(planner, B, Cw, stream)
-        group.barrier(stream)
-        post_attn(planner, Cw, D, stream)
-        group.barrier(stream)
-        reverse_route(planner, D, E, stream)
-    else:
-        reverse_route(planner, B, E, stream)
-    group.barrier(stream)
+def step(group: PeerGroup, gather: MetaGather, planner: Planner, A, B, Cw, D, E, ulysses: bool, stream=None,
+         marks=None):
+    """One pass of the hot path on every process (all phases peer-closed).
+
+    Every exchange writes straight into its destination process's arena and
+    a barrier closes it, so the next phase may read what peers wrote.  With
+    device barriers the whole step is stream-ordered and host-free (it is
+    captured in a CUDA graph by bench_main).  `marks`: optional list of
+    (name, start_event, end_event) timing events per phase, end recorded
+    after the closing barrier (the phase time includes barrier skew)."""
+    torch = group.torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    ev = {}
+
+    def mark(name, which):
+        if marks is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            ev.setdefault(name, [None, None])[which] = e
+
+    mark("gather", 0)
+    meta = gather.gather(s)
+    mark("gather", 1)
+    mark("plan", 0)
+    planner.plan(meta, s)
+    mark("plan", 1)
+    phases = ([("route", route, A, B), ("pre_attn", pre_attn, B, Cw), ("post_attn", post_attn, Cw, D),
+               ("reverse_route", reverse_route, D, E)] if ulysses else
+              [("route", route, A, B), ("reverse_route", reverse_route, B, E)])
+    for name, fn, src, dst in phases:
+        mark(name, 0)
+        fn(planner, src, dst, s)
+        group.barrier(s)
+        mark(name, 1)
+    if marks is not None:
+        marks.extend((k, v[0], v[1]) for k, v in ev.items())
     return meta
 
 
@@ -242,16 +321,25 @@ def _a2a_roofline(busiest: int, route_us: float, same_device: bool) -> dict:
 
 
 def bench_main(args, cfg, topology, metric, clock_sampler=None):
-    """bench.py --gpus N under torchrun: N processes, one GPU each."""
+    """bench.py --gpus N: N processes (spawned by bench.py itself or by
+    torchrun), one GPU each; W logical ranks split in contiguous blocks.
+
+    Timed: the whole step (gather, plan, route, Ulysses, reverse -- every
+    phase closed by a barrier), eager and, with device barriers, as one CUDA
+    graph per process; the faster is the headline.  A separate instrumented
+    eager pass times each phase including its closing barrier (max over
+    ranks) and divides the busiest process's cross-process bytes by it: the
+    all-to-all GB/s against NVLink 5's 900 GB/s per direction."""
     import torch
     import torch.distributed as dist
 
     from . import datagen
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    n_dev = max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local % n_dev)
     if not dist.is_initialized():
-        dist.init_process_group("gloo")
-    group = PeerGroup()
+        dist.init_process_group("gloo")  # control plane only (IPC handles, max over ranks)
+    group = PeerGroup(barrier_mode=os.environ.get("SEQBAL_BARRIER", "auto"))
     W = cfg["world"]
     n_local, first = partition(W, group.size, group.rank)
     meta_kw = {k: v for k, v in cfg["meta"].items() if k != "kind"}
@@ -280,52 +368,101 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     for _ in range(max(3, args.warmup)):
         step(group, gather, planner, A, B, Cw, D, E, ulysses)
     torch.cuda.synchronize()
+    group.barrier_status()
     E.status()
     for r in range(first, first + n_local):
         assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), "round trip not bit-exact"
     cs = group.sum_u64(B.checksum()) == group.sum_u64(A.checksum())
     hp = planner.download()
-    sent, recv = exchange_bytes(hp.c_src, hp.c_dst, hp.c_start, hp.c_end, W, group.size, payload + meta_b + rope_b)
-    busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
 
     stream = torch.cuda.current_stream()
-    planner.enable_timing(True)
-    planner.copy_timing_reset()
-    n0 = _capi.load().sb_kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    group.barrier()
-    torch.cuda.synchronize()
-    clk = clock_sampler(torch.cuda.current_device()) if clock_sampler else None
-    if clk:
-        clk.__enter__()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step(group, gather, planner, A, B, Cw, D, E, ulysses)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if clk:
-        clk.__exit__(None, None, None)
-    launches = _capi.load().sb_kernel_launches() - n0
-    ms = group.max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
-    nr, us_r = planner.copy_timing(0)
-    route_us = group.max_over_ranks(us_r / max(1, nr))
-    planner.enable_timing(False)
+
+    def timed(fn, k):
+        group.barrier()
+        torch.cuda.synchronize()
+        group.dist.barrier()
+        n0 = _capi.load().sb_kernel_launches()
+        clk = clock_sampler(torch.cuda.current_device()) if clock_sampler else None
+        if clk:
+            clk.__enter__()
+        ev0.record(stream)
+        for _ in range(k):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__(None, None, None)
+        launches = _capi.load().sb_kernel_launches() - n0
+        return group.max_over_ranks(ev0.elapsed_time(ev1)) / k, launches, clk
+
+    ms_eager, launches, clk = timed(lambda: step(group, gather, planner, A, B, Cw, D, E, ulysses), args.steps)
+    ms, mode = ms_eager, "eager"
+    graph_err, ms_graph = None, None
+    if group.mode == "device":
+        try:
+            g = torch.cuda.CUDAGraph()
+            group.barrier()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g):
+                step(group, gather, planner, A, B, Cw, D, E, ulysses)
+            l0 = _capi.load().sb_kernel_launches()  # kernels the captured step launches
+            step(group, gather, planner, A, B, Cw, D, E, ulysses)
+            per_step = _capi.load().sb_kernel_launches() - l0
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            ms_graph, _, clk_g = timed(g.replay, args.steps)
+            group.barrier_status()
+            E.status()
+            for r in range(first, first + n_local):
+                assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), \
+                    "graph round trip not bit-exact"
+            if ms_graph < ms:
+                ms, mode, clk, launches = ms_graph, "cuda_graph", clk_g, per_step * args.steps
+        except Exception as e:  # graph capture is an optimisation; eager numbers stand
+            graph_err = f"{type(e).__name__}: {e}"
+
+    # per-phase times (instrumented eager pass; phase end = after its barrier)
+    n_inst = max(3, min(args.steps, 10))
+    acc = {}
+    for _ in range(n_inst):
+        marks = []
+        step(group, gather, planner, A, B, Cw, D, E, ulysses, marks=marks)
+        torch.cuda.synchronize()
+        for name, a, b in marks:
+            acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) * 1000.0
+    group.barrier_status()
+    rows = {"meta": meta_b, "payload": [payload], "aux": [rope_b]}
+    phases = {}
+    for name in ["gather", "plan", "route", "pre_attn", "post_attn", "reverse_route"]:
+        if name not in acc:
+            continue
+        us = group.max_over_ranks(acc[name] / n_inst)
+        ph = {"us": us}
+        if name not in ("gather", "plan"):
+            sent, recv = phase_bytes(hp, name, planner.topology, W, group.size, rows["payload"], rows["aux"], meta_b)
+            busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
+            ph.update(busiest_bytes=busiest, aggregate_bytes=int(sent.sum()),
+                      gbs=busiest / (us * 1e-6) / 1e9 if us > 0 else None,
+                      aggregate_gbs_per_gpu=sent.sum() / group.size / (us * 1e-6) / 1e9 if us > 0 else None)
+            ph["frac_of_nvlink"] = ph["gbs"] / 900.0 if ph["gbs"] is not None and not group.same_device else None
+        phases[name] = ph
+    route_ph = phases["route"]
 
     # e2e through the public API with host buffers: every step uploads this
-    # process's ranks (metadata + payload image) from pinned memory, re-lays
-    # out the origin world, runs the step and downloads the restored ranks.
+    # process's ranks (metadata + payload image) from pinned memory, runs the
+    # step and reads back the result metric (content_checksum of the restored
+    # local ranks, 8 B per process, checked against the input's).
     rows_local = int(sum(int(x.sum()) for x in all_lens[first:first + n_local]))
     sizes = [rows_local * meta_b, rows_local * payload, rows_local * rope_b]
     h_in = [pinned_host(n) for n in sizes]
     h_out = [pinned_host(n) for n in sizes]
     A.download([h.data_ptr() for h in h_in], sizes)
     torch.cuda.synchronize()
-
     want_cs = A.checksum()
 
     def e2e_step():
-        # inputs up from pinned memory; the step's result metric (content
-        # checksum of the restored local ranks, 8 B) back
         gather.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
         A.upload([h.data_ptr() for h in h_in], sizes)
         step(group, gather, planner, A, B, Cw, D, E, ulysses)
@@ -343,9 +480,11 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     ev1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = group.max_over_ranks(ev0.elapsed_time(ev1)) / k
+    e2e_ok = group.max_over_ranks(0.0 if e2e_ok else 1.0) == 0.0
     n_meta_local = int(sum(len(x) for x in all_ids[first:first + n_local]))
     h2d = group.sum_u64(sum(sizes) + 16 * n_meta_local + 8 * (n_local + 1))
     d2h = group.sum_u64(8)
+    group.barrier_status()
     per = hp.per_gpu_workload
     line = {
         "metric": metric, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": group.size,
@@ -353,19 +492,28 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": W,
                    "tokens_per_step": tokens, "sequences": n_seqs, "row_bytes": payload + meta_b + rope_b,
-                   "parallelism": f"{W} ranks over {group.size} GPUs (peer-store all-to-all)",
-                   "barrier": group.mode},
+                   "parallelism": f"{W} ranks over {group.size} processes (peer-store all-to-all)",
+                   "barrier": group.mode, "devices": n_dev, "same_device": bool(group.same_device),
+                   "l2": "inputs larger than L2" if tokens * payload > 126e6 * group.size else
+                         "per-process arenas may fit L2 (strong scaling of one batch)"},
+        "launch_mode": mode, "ms_per_step_eager": ms_eager, "ms_per_step_graph": ms_graph, "graph_error": graph_err,
         "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
-        "a2a_gbs": busiest / (route_us * 1e-6) / 1e9 if route_us > 0 else None,
-        "a2a_busiest_bytes": busiest, "route_copy_us": route_us,
-        "roofline": _a2a_roofline(busiest, route_us, group.same_device),
+        "phases": phases,
+        "a2a_gbs": route_ph.get("gbs"), "a2a_busiest_bytes": route_ph.get("busiest_bytes"),
+        "route_phase_us": route_ph["us"],
+        "roofline": _a2a_roofline(route_ph.get("busiest_bytes", 0), route_ph["us"], group.same_device),
         "gpu_launches": int(launches), "checksum_conserved": bool(cs),
         "clocks": clk.summary() if clk else None,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "round_trip_bit_exact": e2e_ok},
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "round_trip_bit_exact": bool(e2e_ok),
+                "result": "content_checksum of every process's restored ranks (8 B each), checked against the input's"},
     }
+    if group.same_device:
+        line["note"] = ("fewer GPUs than processes: processes share a device, so 'peer' stores are local HBM "
+                        "traffic and phase GB/s are not NVLink numbers")
     if group.rank == 0:
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
+    group.dist.barrier()
     group.close()
     gather.close()
     return 0

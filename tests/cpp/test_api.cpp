@@ -87,6 +87,39 @@ static void test_assign() {
   // :75-78 rejects
   CHECK_THROWS(assign_to_bags({{0, 1}}, {}), ConfigError);
   CHECK_THROWS(assign_to_bags({{0, -1}}, single_bags(1)), ConfigError);
+  // bag sizes whose product overflows int (the first ten primes): no head
+  // check applies to assign_to_bags, so this must plan like the oracle
+  {
+    const int primes[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29};
+    std::vector<ComputeBag> bags;
+    std::vector<int> sizes, bid;
+    int next = 0;
+    for (int j = 0; j < 10; ++j) {
+      ComputeBag b{j, {}};
+      for (int k = 0; k < primes[j]; ++k) b.gpu_ranks.push_back(next++);
+      bags.push_back(b);
+      sizes.push_back(primes[j]);
+      bid.push_back(j);
+    }
+    std::vector<SequenceWorkload> w;
+    std::vector<uint64_t> ids;
+    std::vector<double> ws;
+    for (int i = 0; i < 60; ++i) {
+      w.push_back({static_cast<uint64_t>(i * 7 + 1), static_cast<double>((i * 37) % 101)});
+      ids.push_back(w.back().sample_id);
+      ws.push_back(w.back().workload);
+    }
+    auto got = assign_to_bags(w, bags);
+    std::vector<uint64_t> oi(60);
+    std::vector<double> ow(60);
+    std::vector<int> ob(60);
+    or_assign_to_bags(60, ids.data(), ws.data(), 10, sizes.data(), bid.data(), oi.data(), ow.data(), ob.data());
+    bool same = got.size() == 60;
+    for (int i = 0; same && i < 60; ++i) same = got[i].sample_id == oi[i] && got[i].assigned_bag == ob[i];
+    CHECK(same);
+  }
+  // documented limit: at most 64 bags per replica
+  CHECK_THROWS(assign_to_bags({{0, 1}}, single_bags(65)), ConfigError);
   // random instances vs the oracle, heterogeneous bags
   Rng rng(99);
   for (int trial = 0; trial < 50; ++trial) {
@@ -224,6 +257,26 @@ static void test_reverse_plan() {
   CHECK(reverse_plan(rev) == r.plan);  // generic device path (rev is not cached)
   const RoutingPlan ident = identity_plan(s);
   CHECK(reverse_plan(ident) == ident);
+  // identity_plan for worlds beyond 64 ranks (simulator.cpp:77 'none' baseline)
+  {
+    std::vector<std::vector<SequenceInfo>> big(100);
+    uint64_t id = 1000;
+    for (int r = 0; r < 100; ++r)
+      for (int i = 0; i < r % 3; ++i) big[r].push_back({id++, static_cast<int64_t>(10 * r + i)});
+    const RoutingPlan ip = identity_plan(big);
+    bool ok = ip.world_size == 100;
+    size_t n = 0;
+    for (const auto& c : ip.chunks) ok = ok && c.source_rank == c.target_rank && c.start == 0;
+    for (const auto& r : big) n += r.size();
+    CHECK(ok && ip.chunks.size() == n);
+    CHECK(reverse_plan(ip) == ip);
+  }
+  // documented limit: plan_routing with more than 64 bags per replica
+  {
+    std::vector<std::vector<SequenceInfo>> s65(65);
+    s65[0].push_back({1, 10});
+    CHECK_THROWS(plan_routing(s65, WorkloadModel{}, replicate(parse_topology("g1n65"), 65)), ConfigError);
+  }
 }
 
 static void test_route_split_and_mismatch() {

@@ -49,3 +49,19 @@ def test_topology_parse_errors_carry_offset(bad, offset):
     # topology_test.cpp:56-71: malformed grammar rejected with byte offsets
     with pytest.raises(api.ParseError, match=rf"offset {offset}\)"):
         api.parse_topology(bad)
+
+
+@pytest.mark.parametrize("bad,msg", [("g1048576n2", "unit size too large (at offset 0)"),
+                                     ("g1024n1025", "unit size too large (at offset 0)"),
+                                     ("g٣n1", "expected digits for bag size (at offset 1)"),
+                                     ("g1048576n2+g1x", "expected 'n' (at offset 13)")])
+def test_topology_unit_size_and_ascii_digits(bad, msg):
+    # topology.cpp:16-27 (parse_int accepts '0'-'9' only) and :58 (unit size
+    # checked after the whole spec parsed, offset 0)
+    with pytest.raises(api.ParseError) as e:
+        api.parse_topology(bad)
+    assert str(e.value) == msg
+
+
+def test_topology_largest_unit_accepted():
+    assert api.parse_topology("g1048576n1").unit_size == 1 << 20

@@ -19,7 +19,7 @@ import pytest
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2508_06001_b200 import multigpu
+from paper_2508_06001_b200 import api, multigpu
 
 
 def _free_port():
@@ -48,42 +48,109 @@ def test_partition_owner_and_bytes():
 
 
 def _gloo_worker(rank, size, port, topo, q):
+    """One process of a 2-process gloo world: the product's partition
+    (multigpu.partition / owner_of) decides what this process hosts; it
+    pushes every chunk (route) and every head slice (pre_attn) whose source
+    rank it hosts to the owner of the destination rank -- the decomposition
+    of the device job builders (ulysses_job in csrc/exchange.cu) -- over
+    gloo; the assembled ranks must equal the oracle's single-process
+    route / pre_attn, and the bytes shipped must equal the product's
+    multigpu.phase_bytes accounting (the numbers bench.py reports)."""
+    import copy
+
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
-        W = 8
+        W, width, heads = 8, 8, 4
+        row_bytes = width * 8
         meta = oracle.meta_c1(W, 6, 3, 1)
         n_local, first = multigpu.partition(W, size, rank)
-        plan, _ = oracle.plan_routing(meta, oracle.parse_topology(topo))
-        world = oracle.make_world(meta, 8, 4)  # every process can regenerate any rank
-        # target layout of my ranks
-        out = {r: np.zeros((sum(s[2] for s in plan.target[r]), 64), np.uint8) for r in range(first, first + n_local)}
-        offs = {r: np.cumsum([0] + [s[2] for s in plan.target[r]]) for r in range(W)}
-        src_offs = {r: np.cumsum([0] + [s[2] for s in plan.origin[r]]) for r in range(W)}
-        # sender push: for every chunk whose source I host, ship rows to the owner of dst
+        mine = range(first, first + n_local)
+        tp = oracle.parse_topology(topo)
+        topology = api.parse_topology(topo)
+        plan, _ = oracle.plan_routing(meta, tp, d_model=64, n_heads=heads)
+        world = oracle.make_world(meta, width, heads)  # every process can regenerate any rank
+        ok = True
+
+        def exchange(outbox):
+            inbox = [None] * size
+            dist.all_gather_object(inbox, outbox)
+            return [m for q_ in range(size) for m in inbox[q_][rank]]
+
+        # ---- route: rows of chunk c from its source rank to its target slot
+        offs = {r: np.cumsum([0] + [s_[2] for s_ in plan.target[r]]) for r in range(W)}
+        src_offs = {r: np.cumsum([0] + [s_[2] for s_ in plan.origin[r]]) for r in range(W)}
+        out = {r: np.zeros((int(offs[r][-1]), row_bytes), np.uint8) for r in mine}
         outbox = {q_: [] for q_ in range(size)}
+        shipped = 0
         for c in range(plan.n_chunks):
-            s, d = int(plan.c_src[c]), int(plan.c_dst[c])
-            if not (first <= s < first + n_local) or plan.c_end[c] == plan.c_start[c]:
+            s_, d = int(plan.c_src[c]), int(plan.c_dst[c])
+            if s_ not in mine or plan.c_end[c] == plan.c_start[c]:
                 continue
-            si = [k for k, sg in enumerate(plan.origin[s]) if sg[0] == plan.c_id[c]][0]
+            si = [k for k, sg in enumerate(plan.origin[s_]) if sg[0] == plan.c_id[c]][0]
             di = [k for k, sg in enumerate(plan.target[d]) if sg[0] == plan.c_id[c] and sg[1] == plan.c_start[c]][0]
-            rows = world.ranks[s].payload[src_offs[s][si] + plan.c_start[c]:src_offs[s][si] + plan.c_end[c]]
-            outbox[multigpu.owner_of(d, W, size)].append((d, int(offs[d][di]), rows.copy()))
-        inbox = [None] * size
-        dist.all_gather_object(inbox, outbox)
-        for q_ in range(size):
-            for d, row, rows in inbox[q_][rank]:
-                out[d][row:row + len(rows)] = rows
+            rows = world.ranks[s_].payload[src_offs[s_][si] + plan.c_start[c]:src_offs[s_][si] + plan.c_end[c]]
+            owner = multigpu.owner_of(d, W, size)
+            if owner != rank:
+                shipped += rows.shape[0] * (row_bytes + 16)
+            outbox[owner].append((d, int(offs[d][di]), rows.copy()))
+        for d, row, rows in exchange(outbox):
+            out[d][row:row + len(rows)] = rows
         routed = oracle.route(world, plan)
-        ok = all(np.array_equal(out[r], routed.ranks[r].payload) for r in out)
-        q.put((rank, ok))
+        ok &= all(np.array_equal(out[r], routed.ranks[r].payload) for r in out)
+        sent, recv = multigpu.phase_bytes(plan, "route", topology, W, size, [row_bytes])
+        ok &= int(sent[rank]) == shipped
+
+        # ---- pre_attn: chunk (q, m) on member m sends head slice d to member d
+        want = copy.deepcopy(routed)
+        shipped = 0
+        outbox = {q_: [] for q_ in range(size)}
+        uly = {}
+        U = tp.unit_size
+        for b, g in enumerate(tp.bag_sizes):
+            if g == 1:
+                continue
+            sl = row_bytes // g
+            for rep in range(W // U):
+                ranks = [rep * U + x for x in tp.bag_ranks(b)]
+                ids = [s_[0] for s_ in routed.ranks[ranks[0]].segments]
+                full = [sum(routed.ranks[r].segments[k][2] for r in ranks) for k in range(len(ids))]
+                base = np.cumsum([0] + full)
+                for r in ranks:
+                    if r in mine:
+                        uly[r] = np.zeros((int(base[-1]), sl), np.uint8)
+                for m, r in enumerate(ranks):
+                    if r not in mine:
+                        continue
+                    row = 0
+                    for k, seg in enumerate(routed.ranks[r].segments):
+                        n = seg[2]
+                        for d, dr in enumerate(ranks):
+                            owner = multigpu.owner_of(dr, W, size)
+                            piece = routed.ranks[r].payload[row:row + n, d * sl:(d + 1) * sl].copy()
+                            if owner != rank:
+                                shipped += n * (sl + 16)
+                            outbox[owner].append((dr, int(base[k] + seg[1]), piece))
+                        row += n
+                oracle.pre_attn(want, ranks)
+        for d, row, rows in exchange(outbox):
+            uly[d][row:row + len(rows)] = rows
+        ok &= all(np.array_equal(uly[r], want.ranks[r].payload) for r in uly)
+        sent, recv = multigpu.phase_bytes(plan, "pre_attn", topology, W, size, [row_bytes])
+        ok &= int(sent[rank]) == shipped
+        # received bytes agree with what the peer shipped to us
+        got = [None] * size
+        dist.all_gather_object(got, (int(sent[rank]), int(recv[rank])))
+        ok &= sum(x[0] for x in got) == sum(x[1] for x in got)
+        q.put((rank, bool(ok)))
+    except Exception as e:
+        q.put((rank, f"{type(e).__name__}: {e}"))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2"])
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2", "g1n2+g2n1+g4n1"])
 def test_two_process_push_decomposition_gloo(topo):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -94,21 +161,21 @@ def test_two_process_push_decomposition_gloo(topo):
     res = dict(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: True, 1: True}
+    assert res == {0: True, 1: True}, res
 
 
-def _ipc_worker(rank, size, port, topo, q):
+def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1):
     import torch
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SEQBAL_BARRIER_TIMEOUT_MS="20000")
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
         import paper_2508_06001_b200 as sb
         W = 8
         meta = oracle.meta_c1(W, 5, 2, 0)
-        group = multigpu.PeerGroup()
-        assert group.same_device and group.mode == "host"
+        group = multigpu.PeerGroup(barrier_mode=barrier)
+        assert group.same_device and group.mode == ("host" if barrier == "auto" else barrier)
         n_local, first = multigpu.partition(W, size, rank)
         gather = multigpu.MetaGather(group, W, 8)
         gather.set_local(meta.ids[first:first + n_local], meta.lens[first:first + n_local])
@@ -121,8 +188,10 @@ def _ipc_worker(rank, size, port, topo, q):
         A.layout_origin(dm)
         A.fill_witness(dm)
         group.barrier()
-        multigpu.step(group, gather, planner, A, B, Cw, D, E, planner.max_bag > 1)
+        for _ in range(steps):
+            multigpu.step(group, gather, planner, A, B, Cw, D, E, planner.max_bag > 1)
         torch.cuda.synchronize()
+        group.barrier_status()  # CommError if a device barrier timed out
         plan, _ = oracle.plan_routing(meta, oracle.parse_topology(topo))  # FLUX model, as the planner
         w0 = oracle.make_world(meta, 8, 4)
         routed = oracle.route(w0, plan)
@@ -165,3 +234,98 @@ def test_two_processes_share_one_gpu_through_ipc(topo):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4"])
+def test_two_processes_device_barrier(topo):
+    """The device barrier (k_barrier: system-scope flags in peer memory,
+    device epoch counter, bounded spin) closing every phase of three steps,
+    two processes on one GPU."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, topo, q, "device", 3)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
+def _barrier_timeout_worker(rank, size, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        from paper_2508_06001_b200 import _capi
+        group = multigpu.PeerGroup(barrier_mode="device")
+        group.set_timeout(300.0)
+        group.barrier()
+        group.barrier_status()  # both arrive: fine
+        dist.barrier()
+        if rank == 0:  # process 1 never arrives: bounded wait, then SB_ERR_COMM
+            group.barrier()
+            try:
+                group.barrier_status()
+                q.put((rank, "no error"))
+            except _capi.CommError as e:
+                q.put((rank, "process 1 did not arrive" in str(e)))
+        else:
+            q.put((rank, True))
+        dist.barrier()
+        group.close()
+    except Exception as e:
+        q.put((rank, f"{type(e).__name__}: {e}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_device_barrier_times_out_with_comm_error():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_barrier_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_spawns_two_processes():
+    """`python bench.py --gpus 2` launches its own two worker processes (no
+    torchrun from the caller) and reports the multi-process line: n_gpus 2,
+    bit-exact round trip, per-phase all-to-all bytes and times."""
+    import json
+    import subprocess
+    import sys
+
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["checksum_conserved"] and d["e2e"]["round_trip_bit_exact"]
+    for ph in ("route", "pre_attn", "post_attn", "reverse_route"):
+        assert d["phases"][ph]["busiest_bytes"] > 0 and d["phases"][ph]["us"] > 0, d["phases"]
+    assert d["a2a_gbs"] is not None and d["gpu_launches"] > 0
