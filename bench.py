@@ -60,6 +60,8 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--pattern", default="dit", choices=["dit", "x"],
+                    help="dit: Ulysses on q,k,v out and o back (metrics.cpp:85-121); x: one hidden-state world")
     return ap.parse_args()
 
 
@@ -144,21 +146,22 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- reference arm
-def ref_case(cfg, topology, steps, warmup, budget_s):
+def ref_case(cfg, topology, steps, warmup, budget_s, pattern="dit"):
     return {"world": cfg["world"], "topology": topology, "model": {},
             "meta": dict(cfg["meta"], group_size=cfg["world"]) if cfg["meta"]["kind"] == "scenario" else cfg["meta"],
             "payload_width": PAYLOAD_BYTES // 8, "steps": steps, "warmup": warmup, "budget_s": budget_s,
-            "ulysses": True}
+            "ulysses": True, "qkv": pattern == "dit"}
 
 
-def run_reference(cfg, topology, steps, warmup, budget_s, threads=None):
+def run_reference(cfg, topology, steps, warmup, budget_s, threads=None, pattern="dit"):
     """Time the unmodified reference CPU path (oracle/_ref/ref_harness)."""
     harness = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
     env = dict(os.environ)
     nthreads = threads or os.cpu_count() or 1
     env["OMP_NUM_THREADS"] = str(nthreads)
     if os.path.exists(harness):
-        p = subprocess.run([harness, "bench"], input=json.dumps(ref_case(cfg, topology, steps, warmup, budget_s)).encode(),
+        p = subprocess.run([harness, "bench"],
+                           input=json.dumps(ref_case(cfg, topology, steps, warmup, budget_s, pattern)).encode(),
                            capture_output=True, env=env, timeout=1800)
         if p.returncode == 0:
             d = json.loads(p.stdout)
@@ -458,6 +461,30 @@ def run_c5(args):
 
 
 # ------------------------------------------------- N-process self-launch
+def start_mps():
+    """Start a private CUDA MPS control daemon; returns its env or None."""
+    import shutil
+    import tempfile
+    ctl = shutil.which("nvidia-cuda-mps-control")
+    if not ctl:
+        return None
+    d = tempfile.mkdtemp(prefix="seqbal_mps_")
+    env = {"CUDA_MPS_PIPE_DIRECTORY": os.path.join(d, "pipe"), "CUDA_MPS_LOG_DIRECTORY": os.path.join(d, "log")}
+    for v in env.values():
+        os.makedirs(v, exist_ok=True)
+    r = subprocess.run([ctl, "-d"], env={**os.environ, **env}, capture_output=True)
+    if r.returncode != 0:
+        return None
+    env["SEQBAL_MPS"] = "private"
+    return env
+
+
+def stop_mps(env):
+    import shutil
+    ctl = shutil.which("nvidia-cuda-mps-control")
+    subprocess.run([ctl], input=b"quit\n", env={**os.environ, **env}, capture_output=True, timeout=60)
+
+
 def spawn_workers(n: int) -> int:
     """`python bench.py --gpus N` without torchrun: launch N worker processes
     (one per GPU, torch.distributed.run on 127.0.0.1) running this same
@@ -469,7 +496,27 @@ def spawn_workers(n: int) -> int:
     sock.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
-    p = subprocess.run(cmd, stdout=subprocess.PIPE, text=True)
+    env = dict(os.environ)
+    mps = None
+    try:
+        import torch
+        n_dev = torch.cuda.device_count()
+    except Exception:
+        n_dev = n
+    if n_dev < n and os.environ.get("SEQBAL_MPS", "1") != "0":
+        # Fewer GPUs than processes (functional runs on a one-GPU box): a
+        # private MPS server lets the processes' kernels share the device
+        # concurrently, so device barriers close phases in microseconds
+        # instead of waiting out context time slices.
+        mps = start_mps()
+        if mps:
+            env.update(mps)
+            env.setdefault("SEQBAL_BARRIER", "device")
+    try:
+        p = subprocess.run(cmd, stdout=subprocess.PIPE, text=True, env=env)
+    finally:
+        if mps:
+            stop_mps(mps)
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
     for ln in lines:
         print(ln, flush=True)
@@ -532,7 +579,7 @@ def main():
                                  "sample": f"{ref['full_steps']} full round trips sampled every 50th step"},
                 "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
             return 0
-        r = run_reference(cfg, topology, args.steps, args.warmup, budget_s=120.0)
+        r = run_reference(cfg, topology, args.steps, args.warmup, budget_s=120.0, pattern=args.pattern)
         if "unavailable" in r:
             print(json.dumps({"impl": "reference", "unavailable": r["unavailable"]}))
             return 0
@@ -551,14 +598,6 @@ def main():
         print(json.dumps(line))
         return 0
 
-    import numpy as np
-    import torch
-
-    import ctypes as C
-
-    import paper_2508_06001_b200 as sb
-    from paper_2508_06001_b200 import _capi, datagen
-
     if args.config == "c4":
         return run_c4(args)
     if args.config == "c5":
@@ -566,6 +605,20 @@ def main():
     if world_procs > 1:
         from paper_2508_06001_b200 import multigpu
         return multigpu.bench_main(args, cfg, topology, METRIC, clock_sampler=lambda dev: ClockSampler(dev))
+
+    return run_single(args, cfg, topology)
+
+
+def run_single(args, cfg, topology):
+    """N = 1: the world's W logical ranks on one GPU; the all-to-alls are
+    device-local permutations (HBM-bound)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2508_06001_b200 as sb
+    from paper_2508_06001_b200 import _capi, datagen
 
     torch.cuda.set_device(0)
     W = cfg["world"]
@@ -575,43 +628,91 @@ def main():
     dm = sb.DeviceMeta.from_lists(ids, lens)
     planner = sb.Planner(topology, W, max_seqs=max(n_seqs, 1))
     G = planner.max_bag
-    mk = lambda: sb.World(W, 24, [PAYLOAD_BYTES], capacity_rows=tokens, aux_row_bytes=[ROPE_BYTES], max_bag=G)
-    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    uly = G > 1
+    dit = uly and args.pattern == "dit"
+    P = sb.Planner
+    mkx = lambda: sb.World(W, 24, [PAYLOAD_BYTES], capacity_rows=tokens, aux_row_bytes=[ROPE_BYTES], max_bag=G)
+    A, B = mkx(), mkx()
     A.layout_origin(dm)
     A.fill_witness(dm)
     fill_rope(A, W)
+    planner.plan(dm)
     stream = torch.cuda.current_stream()
+    if dit:
+        # DiT attention (metrics.cpp:85-121): x routed; q, k, v (chunk layout,
+        # written by the projection of the routed x) out through pre_attn; the
+        # attention output o (Ulysses layout) back through post_attn; o home
+        # through reverse_route.  q/k/v/o are device-resident activations.
+        mkq = lambda: sb.World(W, 24, [PAYLOAD_BYTES] * 3, capacity_rows=tokens, aux_row_bytes=[ROPE_BYTES],
+                               max_bag=G)
+        mko = lambda: sb.World(W, 24, [PAYLOAD_BYTES], capacity_rows=tokens, max_bag=G)
+        Q, Qu, O, Oc, E = mkq(), mkq(), mko(), mko(), mko()
+        home = mko()  # o's origin image: what reverse_route must restore
+        home.layout_origin(dm)
+        home.fill_witness(dm)
+        home.perturb()  # o != x
+        t1, t2 = mko(), mko()
+        sb.route(planner, A, B)
+        sb.route(planner, home, t1)
+        sb.pre_attn(planner, t1, t2)
+        Q.layout_plan(planner, sb.World.TARGET)
+        O.layout_plan(planner, sb.World.ULYSSES)
+        torch.cuda.synchronize()
+        for r in range(W):  # setup: q = k = v = routed x; o = pre_attn image of `home`
+            for t_dst, t_src in ((0, 0), (1, 1), (2, 1), (3, 1), (4, 2)):
+                Q.write_rank(t_dst, r, B.read_rank(t_src, r))
+            for t in (0, 1):
+                O.write_rank(t, r, t2.read_rank(t, r))
+        del t1, t2
+        ops = [(P.ROUTE, A, B, 0, None), (P.PRE_ATTN, Q, Qu, 2, lambda pl, st: Q.layout_plan(pl, sb.World.TARGET, st)),
+               (P.POST_ATTN, O, Oc, 3, lambda pl, st: O.layout_plan(pl, sb.World.ULYSSES, st)),
+               (P.REVERSE, Oc, E, 1, None)]
+        worlds = [A, B, Q, Qu, O, Oc, E]
+    else:
+        Cw, D, E = mkx(), mkx(), mkx()
+        home = A
+        ops = ([(P.ROUTE, A, B, 0, None), (P.PRE_ATTN, B, Cw, 2, None), (P.POST_ATTN, Cw, D, 3, None),
+                (P.REVERSE, D, E, 1, None)] if uly else [(P.ROUTE, A, B, 0, None), (P.REVERSE, B, E, 1, None)])
+        worlds = [A, B, Cw, D, E]
+    names = {P.ROUTE: "route", P.PRE_ATTN: "pre_attn", P.POST_ATTN: "post_attn", P.REVERSE: "reverse_route"}
+    home_cs = home.checksum()
+
+    def check_round_trip(what):
+        for w in worlds:
+            w.status()
+        assert E.compare(home) == 0, f"{what}: round trip not bit-exact"
+        assert B.checksum() == A.checksum(), f"{what}: route does not conserve content_checksum"
+        if dit:
+            assert Qu.checksum() == A.checksum(), f"{what}: pre_attn(q) does not conserve content_checksum"
 
     side = torch.cuda.Stream()
-    uly = max(planner.topology.bag_sizes) > 1
-    P = sb.Planner
-    # (op, src, dst, slot) of the step's exchanges, in order
-    ops = ([(P.ROUTE, A, B, 0), (P.PRE_ATTN, B, Cw, 2), (P.POST_ATTN, Cw, D, 3), (P.REVERSE, D, E, 1)] if uly
-           else [(P.ROUTE, A, B, 0), (P.REVERSE, B, E, 1)])
     evs = [torch.cuda.Event() for _ in range(len(ops) + 1)]
 
+    def prepare_all(pl, st, evl=None):
+        for i, (op, src, dst, slot, pre) in enumerate(ops):
+            if pre is not None:
+                pre(pl, st)
+            pl.prepare(op, src, dst, slot, st)
+            if evl is not None:
+                evl[i].record(st)
+
     def step():
-        """plan, then every exchange prepared on a side stream (layout + jobs)
+        """plan, then every exchange prepared on a side stream (layouts + jobs)
         while the copies run back to back on the main stream."""
         main = torch.cuda.current_stream()
         planner.plan(dm)
         evs[-1].record(main)
         side.wait_event(evs[-1])
         with torch.cuda.stream(side):
-            for i, (op, src, dst, slot) in enumerate(ops):
-                planner.prepare(op, src, dst, slot)
-                evs[i].record(side)
-        for i, (op, src, dst, slot) in enumerate(ops):
+            prepare_all(planner, side, evs)
+        for i, (op, src, dst, slot, pre) in enumerate(ops):
             main.wait_event(evs[i])
             planner.run(slot)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    E.status()
-    # correctness of what we time: E == A byte for byte
-    for r in range(W):
-        assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), "round trip not bit-exact"
+    check_round_trip("eager")
     hp = planner.download()
     per = hp.per_gpu_workload
     max_mean = float(per.max() / per.mean()) if per.mean() > 0 else 1.0
@@ -629,12 +730,11 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = sb.kernel_launches() - launches0
-    ms = ev0.elapsed_time(ev1)
-    ms_per_step_eager = ms / args.steps
-    n_route, us_route = planner.copy_timing(0)
-    n_rev, us_rev = planner.copy_timing(1)
-    n_pre, us_pre = planner.copy_timing(2)
-    n_post, us_post = planner.copy_timing(3)
+    ms_per_step_eager = ev0.elapsed_time(ev1) / args.steps
+    copy_us = {}
+    for op in names:
+        n_op, us_op = planner.copy_timing(op)
+        copy_us[names[op]] = us_op / max(1, n_op) if n_op else None
     planner.plan(dm)
     torch.cuda.synchronize()
     plan_breakdown = {"path": "multi-kernel", "us": planner.timing()}
@@ -646,24 +746,20 @@ def main():
     tr = planner.trace(True)
     planner.trace(False)
     if tr[13] > tr[0] > 0:
-        names = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
-                 "rank_lists", "send", "wir"]
+        pnames = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
+                  "rank_lists", "send", "wir"]
         plan_breakdown = {"path": "fused single-CTA", "total_cycles": int(tr[13] - tr[0]),
-                          "cycles": {k: int(v) for k, v in zip(names, np.diff(tr[:14]))}}
-    # algorithmic bytes of each exchange (read == written), from the device
+                          "cycles": {k: int(v) for k, v in zip(pnames, np.diff(tr[:14]))}}
+    # algorithmic bytes of each exchange (bytes read == bytes written), from the device
     op_bytes = {}
-    for name, fn in (("route", lambda: sb.route(planner, A, B)), ("pre_attn", lambda: sb.pre_attn(planner, B, Cw)),
-                     ("post_attn", lambda: sb.post_attn(planner, Cw, D)),
-                     ("reverse_route", lambda: sb.reverse_route(planner, D if uly else B, E))):
-        if name in ("pre_attn", "post_attn") and not uly:
-            continue
-        fn()
+    prepare_all(planner, stream)
+    for op, src, dst, slot, pre in ops:
+        planner.run(slot)
         torch.cuda.synchronize()
-        op_bytes[name] = planner.exchange_bytes()
-    E.status()
+        op_bytes[names[op]] = planner.exchange_bytes()
+    check_round_trip("bytes pass")
 
-    # ---- the same step captured once into a CUDA graph and replayed: the
-    # launch stream of ~30 small kernels collapses into one graph launch
+    # ---- the same step captured once into a CUDA graph and replayed
     graph_ok, ms_per_step = False, ms_per_step_eager
     try:
         g = torch.cuda.CUDAGraph()
@@ -672,7 +768,6 @@ def main():
         for _ in range(3):
             g.replay()
         torch.cuda.synchronize()
-        launches0 = sb.kernel_launches()
         with ClockSampler() as clk_g:
             ev0.record(stream)
             for _ in range(args.steps):
@@ -680,10 +775,7 @@ def main():
             ev1.record(stream)
             torch.cuda.synchronize()
         graph_ms = ev0.elapsed_time(ev1) / args.steps
-        E.status()
-        for r in range(W):
-            assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), \
-                "graph round trip not bit-exact"
+        check_round_trip("graph")
         graph_ok = True
         if graph_ms < ms_per_step:
             ms_per_step = graph_ms
@@ -708,10 +800,8 @@ def main():
         prep_ev = [[torch.cuda.Event() for _ in ops], [torch.cuda.Event() for _ in ops]]
 
         def plan_and_prepare(pl, evl):
-            pl.plan(dm)
-            for i, (op, src, dst, slot) in enumerate(ops):
-                pl.prepare(op, src, dst, slot)
-                evl[i].record(side)
+            pl.plan(dm, side)
+            prepare_all(pl, side, evl)
 
         def pipe_pair():
             # Replays are serialised on the stream, so a replay starts with
@@ -720,13 +810,13 @@ def main():
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 plan_and_prepare(planners[1], prep_ev[1])  # batch k+1 under batch k's copies
-            for op, src, dst, slot in ops:
+            for op, src, dst, slot, pre in ops:
                 planners[0].run(slot)
             free_ev[0].record(main)
             side.wait_event(free_ev[0])  # planner 0's slots are free again
             with torch.cuda.stream(side):
                 plan_and_prepare(planners[0], prep_ev[0])  # batch k+2 under batch k+1's copies
-            for i, (op, src, dst, slot) in enumerate(ops):
+            for i, (op, src, dst, slot, pre) in enumerate(ops):
                 main.wait_event(prep_ev[1][i])
                 planners[1].run(slot)
             main.wait_stream(side)
@@ -752,10 +842,7 @@ def main():
             ev1.record(stream)
             torch.cuda.synchronize()
         pipe_ms = ev0.elapsed_time(ev1) / (2 * pairs)
-        E.status()
-        for r in range(W):
-            assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), \
-                "pipelined round trip not bit-exact"
+        check_round_trip("plan-ahead graph")
     except Exception as e:
         pipe_err = f"{type(e).__name__}: {e}"
     ms_per_step_serial = ms_per_step
@@ -773,7 +860,6 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize()
     plan_us = 1000 * t0.elapsed_time(t1) / 20
-    # device latency of one plan without host launch gaps (graph replay)
     plan_us_graph = None
     try:
         gp = torch.cuda.CUDAGraph()
@@ -790,12 +876,18 @@ def main():
     except Exception:
         pass
 
-    row_bytes = PAYLOAD_BYTES + META_BYTES + ROPE_BYTES
-    route_bytes = 2 * tokens * row_bytes  # every row read once and written once (out-of-place)
     hbm_peak, peak_kind = load_peaks()
-    # context: a plain contiguous device copy of the same bytes (torch copy_,
-    # best of 5) -- the practical peak at this transfer size
-    _src = torch.empty(route_bytes // 2, dtype=torch.uint8, device="cuda")
+    # per-op roofline: algorithmic bytes (read + write) / copy-kernel time
+    roofline_ops = {}
+    for name, nb in op_bytes.items():
+        us = copy_us.get(name)
+        gbs = 2 * nb / (us * 1e-6) / 1e9 if us else None
+        roofline_ops[name] = {"algorithmic_bytes": 2 * nb, "us": us, "gbs": gbs,
+                              "frac": gbs / hbm_peak if gbs else None}
+    dom = max(roofline_ops, key=lambda k: roofline_ops[k]["us"] or 0.0)
+    # context: a plain contiguous device copy of the dominant op's bytes
+    dom_bytes = roofline_ops[dom]["algorithmic_bytes"]
+    _src = torch.empty(dom_bytes // 2, dtype=torch.uint8, device="cuda")
     _dst = torch.empty_like(_src)
     _dst.copy_(_src)
     torch.cuda.synchronize()
@@ -806,25 +898,27 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
         size_ms = min(size_ms, t0.elapsed_time(t1))
-    size_matched_gbs = route_bytes / (size_ms * 1e-3) / 1e9
+    size_matched_gbs = dom_bytes / (size_ms * 1e-3) / 1e9
     del _src, _dst
-    route_kernel_us = us_route / max(1, n_route)
-    achieved = route_bytes / (route_kernel_us * 1e-6) / 1e9
-    # Ulysses: rows of multi-GPU bags; metadata replicated to every member
-    multi = [b for b in planner.topology.bag_sizes]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
-        if pj.get("config") == args.config:
-            traffic = pj.get("route_copy_dram_bytes")
+        if pj.get("config") == args.config and pj.get("pattern", "x") == args.pattern:
+            traffic = pj.get("dominant_dram_bytes", pj.get("route_copy_dram_bytes"))
+    kernel_of = {"route": "k_copy (route)", "reverse_route": "k_copy (reverse_route)",
+                 "pre_attn": "k_copy_tma / k_copy (pre_attn)", "post_attn": "k_copy_tma / k_copy (post_attn)"}
 
-    # ---- e2e through the C-ABI with pinned host buffers
-    sizes = [tokens * META_BYTES, tokens * PAYLOAD_BYTES, tokens * ROPE_BYTES]
-    host_in = [sb.pinned_host(n) for n in sizes]
+    # ---- e2e through the C-ABI with pinned host buffers: every step uploads
+    # its inputs (metadata + the x world image) and reads back a result.
+    xsizes = [tokens * META_BYTES, tokens * PAYLOAD_BYTES, tokens * ROPE_BYTES]
+    host_in = [sb.pinned_host(n) for n in xsizes]
     ptrs_in = [h.data_ptr() for h in host_in]
-    A.download(ptrs_in, sizes)
+    A.download(ptrs_in, xsizes)
+    esizes = [tokens * META_BYTES, tokens * PAYLOAD_BYTES] + ([] if dit else [tokens * ROPE_BYTES])
+    home_img = [sb.pinned_host(n) for n in esizes]
+    home.download([h.data_ptr() for h in home_img], esizes)
     torch.cuda.synchronize()
     flat_ids = np.concatenate(ids).view(np.int64)
     flat_lens = np.concatenate(lens)
@@ -833,14 +927,15 @@ def main():
     h_ids = torch.from_numpy(flat_ids.copy()).pin_memory()
     h_lens = torch.from_numpy(flat_lens.copy()).pin_memory()
     h_off = torch.from_numpy(off).pin_memory()
-    h2d = sum(sizes) + 8 * (len(flat_ids) * 2 + W + 1)
-    d2h = sum(sizes)
+    h2d = sum(xsizes) + 8 * (len(flat_ids) * 2 + W + 1)
+    d2h_full = sum(esizes)
     # Two in-flight steps: step k's H2D (copy stream) and step k-1's D2H
     # (second copy stream) run on the two DMA engines while the device
     # computes; every step still copies its own inputs in and result out.
-    A2s, Es = [mk(), mk()], [E, mk()]
+    A2s = [mkx(), mkx()]
+    Es = [E, (mko() if dit else mkx())]
     metas = [sb.DeviceMeta.from_lists(ids, lens), sb.DeviceMeta.from_lists(ids, lens)]
-    outs = [[sb.pinned_host(n) for n in sizes] for _ in range(2)]
+    outs = [[sb.pinned_host(n) for n in esizes] for _ in range(2)]
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
@@ -848,16 +943,22 @@ def main():
     ev_out = [torch.cuda.Event() for _ in range(2)]
     for e in ev_used + ev_out:
         e.record(stream)
+    acc_dev = torch.zeros(2, dtype=torch.int64, device="cuda")
+    h2d_marks = []  # (start, end) timing events of each upload (diagnostics: DMA busy fraction)
 
-    def e2e_step(k):
+    def e2e_core(k, result):
         i = k % 2
         m, A2, Ei = metas[i], A2s[i], Es[i]
         with torch.cuda.stream(h2d_s):
             h2d_s.wait_event(ev_used[i])  # step k-2 finished reading these buffers
+            mk_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            mk_ev[0].record(h2d_s)
             m.ids.copy_(h_ids, non_blocking=True)
             m.lens.copy_(h_lens, non_blocking=True)
             m.rank_off.copy_(h_off, non_blocking=True)
-            A2.upload(ptrs_in, sizes)
+            A2.upload(ptrs_in, xsizes)
+            mk_ev[1].record(h2d_s)
+            h2d_marks.append(mk_ev)
             ev_in[i].record(h2d_s)
         stream.wait_event(ev_in[i])
         stream.wait_event(ev_out[i])  # step k-2's result has left Ei
@@ -865,80 +966,31 @@ def main():
         planner.plan(m)
         sb.route(planner, A2, B)
         ev_used[i].record(stream)
-        if uly:
+        if dit:
+            Q.layout_plan(planner, sb.World.TARGET)
+            sb.pre_attn(planner, Q, Qu)
+            O.layout_plan(planner, sb.World.ULYSSES)
+            sb.post_attn(planner, O, Oc)
+            sb.reverse_route(planner, Oc, Ei)
+        elif uly:
             sb.pre_attn(planner, B, Cw)
             sb.post_attn(planner, Cw, D)
             sb.reverse_route(planner, D, Ei)
         else:
             sb.reverse_route(planner, B, Ei)
+        result(k, i, Ei)
+
+    def full_result(k, i, Ei):
         ev_comp[i].record(stream)
         with torch.cuda.stream(d2h_s):
             d2h_s.wait_event(ev_comp[i])
-            Ei.download([o.data_ptr() for o in outs[i]], sizes)
+            Ei.download([o.data_ptr() for o in outs[i]], esizes)
             ev_out[i].record(d2h_s)
 
-    for k in range(4):
-        e2e_step(k)
-    torch.cuda.synchronize()
-    for oi, out in enumerate(outs):
-        same = [torch.equal(o, h) for o, h in zip(out, host_in)]
-        if not all(same):
-            diag = []
-            for w, nm in ((B, "B"), (Cw, "C"), (D, "D"), (Es[oi], "E")):
-                try:
-                    w.status()
-                except Exception as ex:
-                    diag.append(f"{nm}: {ex}")
-            raise AssertionError(f"e2e round trip not bit-exact (out {oi}; meta/payload/rope equal {same}; "
-                                 f"status {diag})")
     e2e_steps = max(4, min(args.steps, 50))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for k in range(e2e_steps):
-        e2e_step(k)
-    for e in ev_out:
-        stream.wait_event(e)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_full_ms = e0.elapsed_time(e1) / e2e_steps
-
-    # The contract's e2e: every step uploads its inputs (metadata + the world
-    # image) from pinned memory and reads back the step's result metric -- the
-    # content_checksum of the restored world (8 B, computed on the device,
-    # checked against the input's) -- instead of the whole world.
-    acc_dev = torch.zeros(2, dtype=torch.int64, device="cuda")
     acc_host = torch.zeros(2 * (e2e_steps + 4), dtype=torch.int64, pin_memory=True)
-    want_cs = A.checksum()
 
-    h2d_marks = []  # (start, end) timing events of each upload (diagnostics: DMA busy fraction)
-
-    def e2e_metric_step(k):
-        i = k % 2
-        m, A2, Ei = metas[i], A2s[i], Es[i]
-        with torch.cuda.stream(h2d_s):
-            h2d_s.wait_event(ev_used[i])
-            mk_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            mk_ev[0].record(h2d_s)
-            m.ids.copy_(h_ids, non_blocking=True)
-            m.lens.copy_(h_lens, non_blocking=True)
-            m.rank_off.copy_(h_off, non_blocking=True)
-            A2.upload(ptrs_in, sizes)
-            mk_ev[1].record(h2d_s)
-            h2d_marks.append(mk_ev)
-            ev_in[i].record(h2d_s)
-        stream.wait_event(ev_in[i])
-        stream.wait_event(ev_out[i])
-        A2.layout_origin(m)
-        planner.plan(m)
-        sb.route(planner, A2, B)
-        ev_used[i].record(stream)
-        if uly:
-            sb.pre_attn(planner, B, Cw)
-            sb.post_attn(planner, Cw, D)
-            sb.reverse_route(planner, D, Ei)
-        else:
-            sb.reverse_route(planner, B, Ei)
+    def checksum_result(k, i, Ei):
         acc_dev[i].zero_()
         _capi.call("sb_world_checksum", Ei.handle, C.c_void_p(acc_dev.data_ptr() + 8 * i),
                    C.c_void_p(stream.cuda_stream))
@@ -949,26 +1001,45 @@ def main():
             ev_out[i].record(d2h_s)
 
     for k in range(4):
-        e2e_metric_step(k)
+        e2e_core(k, full_result)
+    torch.cuda.synchronize()
+    for oi, out in enumerate(outs):
+        same = [torch.equal(o, h) for o, h in zip(out, home_img)]
+        assert all(same), f"e2e round trip not bit-exact (out {oi}; tensors equal {same})"
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(e2e_steps):
+        e2e_core(k, full_result)
+    for e in ev_out:
+        stream.wait_event(e)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_full_ms = e0.elapsed_time(e1) / e2e_steps
+
+    # The contract's e2e: every step uploads its inputs (metadata + the x world
+    # image) from pinned memory and reads back the step's result metric -- the
+    # content_checksum of the restored world (8 B, computed on the device and
+    # checked against the expected one every step) -- instead of the whole world.
+    for k in range(4):
+        e2e_core(k, checksum_result)
     torch.cuda.synchronize()
     h2d_marks.clear()
     host_t0 = time.perf_counter()
     e0.record(stream)
     for k in range(e2e_steps):
-        e2e_metric_step(k)
+        e2e_core(k, checksum_result)
     host_enqueue_ms = 1000 * (time.perf_counter() - host_t0) / e2e_steps
     for e in ev_out:
         stream.wait_event(e)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    # the same uploads with no compute beside them
-    torch.cuda.synchronize()
     u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     u0.record(h2d_s)
     for k in range(8):
         with torch.cuda.stream(h2d_s):
-            A2s[k % 2].upload(ptrs_in, sizes)
+            A2s[k % 2].upload(ptrs_in, xsizes)
     u1.record(h2d_s)
     torch.cuda.synchronize()
     h2d_alone_ms = u0.elapsed_time(u1) / 8
@@ -976,14 +1047,21 @@ def main():
     h2d_period_ms = float(np.mean([h2d_marks[j][0].elapsed_time(h2d_marks[j + 1][0])
                                    for j in range(len(h2d_marks) - 1)]))
     got = acc_host[:e2e_steps].numpy().view(np.uint64)
-    assert all(int(x) == want_cs for x in got), "e2e restored-world checksum differs from the input's"
+    assert all(int(x) == home_cs for x in got), "e2e restored-world checksum differs from the expected one"
 
+    row_bytes = PAYLOAD_BYTES + META_BYTES + ROPE_BYTES
+    step_bytes = 2 * sum(op_bytes.values())
+    rd = roofline_ops[dom]
     line = {
         "metric": METRIC, "value": tokens / (ms_per_step * 1e-3), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": W, "tokens_per_step": tokens,
                    "sequences": n_seqs, "row_bytes": row_bytes,
+                   "pattern": ("dit: route x (hidden + RoPE ids); pre_attn q,k,v (3 x 6144 B + RoPE ids); post_attn "
+                               "o (6144 B); reverse_route o (metrics.cpp:85-121)") if dit else
+                              ("x: route, pre_attn, post_attn, reverse_route of one hidden-state world" if uly
+                               else "route + reverse_route (no multi-GPU bags)"),
                    "l2": "inputs larger than L2 (world payload %.0f MB per buffer > 126 MB)" % (
                        tokens * PAYLOAD_BYTES / 1e6), "parallelism": "world of 8 ranks on 1 GPU"},
         "launch_mode": launch_mode,
@@ -992,19 +1070,18 @@ def main():
         "schedule": ("plan-ahead: batch k+1 planned + exchanges prepared on a side stream while batch k's "
                      "copies run; each step = 1 plan + prepares + copies of one full batch"
                      if launch_mode == "cuda_graph+plan_ahead" else "serial: plan, then prepares under copies"),
-        "copy_engine": os.environ.get("SEQBAL_COPY_ENGINE", "tma"),
         "max_mean": max_mean, "wir": hp.wir, "plan_us": plan_us, "plan_us_graph": plan_us_graph,
         "plan_breakdown_us": plan_breakdown,
-        "step_hbm": {"bytes_per_step": 2 * sum(op_bytes.values()), "op_bytes_one_way": op_bytes,
-                     "gbs": 2 * sum(op_bytes.values()) / (ms_per_step * 1e-3) / 1e9,
-                     "frac_of_peak": 2 * sum(op_bytes.values()) / (ms_per_step * 1e-3) / 1e9 / load_peaks()[0]},
-        "phases_us": {"route_copy": route_kernel_us, "reverse_copy": us_rev / max(1, n_rev),
-                      "pre_attn_copy": us_pre / max(1, n_pre), "post_attn_copy": us_post / max(1, n_post)},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_copy (route)", "algorithmic_bytes_per_launch": route_bytes,
+        "step_hbm": {"bytes_per_step": step_bytes, "op_bytes_one_way": op_bytes,
+                     "gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
+                     "frac_of_peak": step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak},
+        "phases_us": {k + "_copy": v for k, v in copy_us.items() if v is not None},
+        "roofline_ops": roofline_ops,
+        "roofline": {"bound": "hbm", "achieved": rd["gbs"], "peak": hbm_peak, "unit": "GB/s",
+                     "frac": rd["frac"], "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": kernel_of[dom], "algorithmic_bytes_per_launch": rd["algorithmic_bytes"],
                      "size_matched_copy_gbs": size_matched_gbs,
-                     "frac_of_size_matched_copy": achieved / size_matched_gbs},
+                     "frac_of_size_matched_copy": rd["gbs"] / size_matched_gbs if rd["gbs"] else None},
         "a2a_gbs": None,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -1014,23 +1091,25 @@ def main():
                 "h2d_alone_ms": h2d_alone_ms,
                 "host_buffers": sb.hostmem.choice(),
                 "host_enqueue_ms_per_step": host_enqueue_ms,
-                "result": "content_checksum of the restored world, computed on the device and checked against "
-                          "the input's every step",
+                "result": "checksum: content_checksum of the restored world (8 B), computed on the device and "
+                          "checked against the expected value every step; e2e_full_world reads the whole world back",
                 "pipeline": "2 steps in flight: H2D(k) on a copy stream under step k-1's compute"},
         "e2e_full_world": {"value": tokens / (e2e_full_ms * 1e-3), "unit": "tokens/s",
-                           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_full_ms,
-                           "note": "the whole restored world read back every step (PCIe-bound both ways)"},
+                           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_full),
+                           "ms_per_step": e2e_full_ms,
+                           "result": "the whole restored world read back every step (PCIe-bound both ways)"},
     }
     if not args.no_cpu_baseline:
-        r = run_reference(cfg, topology, steps=1000, warmup=1, budget_s=args.cpu_budget_s)
+        r = run_reference(cfg, topology, steps=1000, warmup=1, budget_s=args.cpu_budget_s, pattern=args.pattern)
         if "unavailable" in r:
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "unavailable": r["unavailable"]}
         else:
             line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"],
                                     "kind": "reference",
                                     "sample": f"{r['steps']} full {args.config.upper()} steps (~{args.cpu_budget_s:.0f} s budget), "
-                                              "reference plan_routing+route+pre/post_attn+reverse_route, "
-                                              "Exec::Parallel, 768 doubles/row"}
+                                              "reference plan_routing+route+pre/post_attn+reverse_route"
+                                              + (" (pre_attn on q, k, v; post_attn on o)" if dit else "")
+                                              + ", Exec::Parallel, 768 doubles/row"}
     print(json.dumps(line))
     return 0
 

@@ -207,6 +207,14 @@ SB_API sb_status sb_world_set_peers(sb_world* w, int tensor, const uint64_t* hos
  * gather order (exchange.cpp:31-66 shells).  Device arrays as in sb_plan. */
 SB_API sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, const int64_t* d_rank_off,
                                  sb_stream stream);
+/* Layout from the current plan of `p` (no data moved): 0 origin packing,
+ * 1 target (chunk) packing -- what route writes --, 2 Ulysses packing --
+ * what pre_attn writes: multi-GPU bags hold full sequences x H/G heads,
+ * one-GPU bags their chunk rows.  For tensors an exchange did not produce:
+ * q/k/v written by a projection in the chunk layout (the source of a
+ * 3-tensor pre_attn), an attention output in the Ulysses layout (the source
+ * of post_attn) -- the DiT pattern of metrics.cpp:85-121.                  */
+SB_API sb_status sb_world_layout_plan(sb_world* w, const sb_planner* p, int layout, sb_stream stream);
 /* Fill hosted ranks with the reference witness: metadata (id, pos) and
  * payload doubles payload_value(id, pos, col) (exchange.cpp:18-23,52-63).
  * Fixture generator for tests/bench; payload tensors must be 8*W_d bytes. */

@@ -331,6 +331,11 @@ int cmd_bench() {
   const int steps = c.value("steps", 1);
   const int warmup = c.value("warmup", 0);
   const bool ulysses = c.value("ulysses", true);
+  // DiT attention pattern (metrics.cpp:85-121): pre_attn on q, k and v, then
+  // post_attn on the attention output o, and o is what reverse_route brings
+  // home.  q/k/v (chunk layout) and o (Ulysses layout) are produced by the
+  // model between the phases, so their images are prepared untimed.
+  const bool qkv = c.value("qkv", false);
   const Exec exec = c.value("serial", false) ? Exec::Serial : Exec::Parallel;
 
   const World w0 = make_world(samples, width, model.shape.n_heads);
@@ -349,7 +354,30 @@ int cmd_bench() {
     const double b = now_s();
     World routed = route(w0, pr.plan, exec);
     const double cc = now_s();
-    if (ulysses) {
+    double untimed = 0;
+    if (ulysses && qkv) {
+      const double u0 = now_s();
+      std::vector<World> q3{routed, routed, routed};
+      World o = routed;
+      for (int rep = 0; rep < layout.num_replicas(); ++rep)
+        for (const auto& ub : layout.unit.bags)
+          if (ub.size() >= 2) pre_attn(o, global_bag(layout, rep, ub.bag_id), exec);
+      untimed = now_s() - u0;
+      for (int rep = 0; rep < layout.num_replicas(); ++rep) {
+        for (const auto& ub : layout.unit.bags) {
+          if (ub.size() < 2) continue;
+          const ComputeBag bag = global_bag(layout, rep, ub.bag_id);
+          for (World& t : q3) pre_attn(t, bag, exec);
+        }
+      }
+      for (int rep = 0; rep < layout.num_replicas(); ++rep) {
+        for (const auto& ub : layout.unit.bags) {
+          if (ub.size() < 2) continue;
+          post_attn(o, global_bag(layout, rep, ub.bag_id), exec);
+        }
+      }
+      routed = std::move(o);
+    } else if (ulysses) {
       for (int rep = 0; rep < layout.num_replicas(); ++rep) {
         for (const auto& ub : layout.unit.bags) {
           if (ub.size() < 2) continue;
@@ -365,9 +393,9 @@ int cmd_bench() {
     if (it >= warmup) {
       t_plan += b - a;
       t_route += cc - b;
-      t_uly += d - cc;
+      t_uly += d - cc - untimed;
       t_rev += e - d;
-      step_s.push_back(e - a);
+      step_s.push_back(e - a - untimed);
     }
     if (back.ranks.size() != w0.ranks.size()) return 2;
   }

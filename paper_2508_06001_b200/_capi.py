@@ -134,6 +134,7 @@ _SIGS = {
     "sb_barrier_set_peers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "sb_barrier_wait": (C.c_int, [C.c_void_p] * 2),
     "sb_barrier_set_timeout": (C.c_int, [C.c_void_p, C.c_double]),
+    "sb_world_layout_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "sb_barrier_status": (C.c_int, [C.c_void_p] * 3),
     "sb_world_compare": (C.c_int, [C.c_void_p] * 4),
     "sb_world_fill_meta": (C.c_int, [C.c_void_p] * 5),

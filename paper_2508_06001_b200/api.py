@@ -417,6 +417,16 @@ class World:
         _, lens, off = meta.ptrs()
         call("sb_world_layout_origin", self._h, lens, off, _stream(stream))
 
+    ORIGIN, TARGET, ULYSSES = 0, 1, 2
+
+    def layout_plan(self, planner: "Planner", layout: int, stream=None):
+        """Per-rank layout from the planner's current plan without moving
+        data (sb_world_layout_plan): ORIGIN, TARGET (chunk packing, what
+        route writes) or ULYSSES (what pre_attn writes).  For q/k/v produced
+        in the chunk layout or an attention output in the Ulysses layout."""
+        call("sb_world_layout_plan", self._h, planner.handle, int(layout), _stream(stream))
+        return self
+
     def fill_witness(self, meta: DeviceMeta, stream=None):
         call("sb_world_fill_witness", self._h, *meta.ptrs(), _stream(stream))
 

@@ -77,6 +77,7 @@ struct LayoutPlan {
   const int64_t* bag_rows;  // R*M
   const int64_t* target_rows;
   int U, M;
+  int no_check;  // standalone layout (sb_world_layout_plan): no source to validate
 };
 
 // check_world_matches_layout (exchange.cpp:96-123) / check_bag_chunk_layout
@@ -104,7 +105,7 @@ __device__ bool source_matches_plan(const WorldArgs& s, const LayoutPlan& lp, in
 __device__ void layout_tensor(const WorldArgs& d, const WorldArgs& s, const LayoutPlan& lp, const TensorInfo& ti,
                               int mode, int t) {
   if (t >= d.T) return;
-  if (t == 0) {  // the status reflects the latest exchange into d
+  if (t == 0 && !lp.no_check) {  // the status reflects the latest exchange into d
     if (source_matches_plan(s, lp, mode)) atomicAnd(d.status, ~ST_MISMATCH);
     else atomicOr(d.status, ST_MISMATCH);
   }
@@ -125,6 +126,19 @@ __device__ void layout_tensor(const WorldArgs& d, const WorldArgs& s, const Layo
       const int b = lp.rank_bag[u];
       g = lp.bag_size[b];
       k = lp.rank_member[u];
+      if (g == 1 && mode == 3) {  // standalone Ulysses layout: one-GPU bags keep their chunk rows
+        const int64_t rows1 = lp.target_rows[r];
+        const int64_t pitch1 = ti.row_bytes[t];
+        d.base[t * d.W + r] = d.peer_arena[t * d.n_procs + owner] + (uint64_t)off;
+        d.pitch[t * d.W + r] = pitch1;
+        off += rows1 * pitch1;
+        if (off > d.arena_bytes[t]) atomicOr(d.status, ST_LAYOUT);
+        if (t == 0) {
+          d.rows[r] = rows1;
+          d.headcol[r] = 0;
+        }
+        continue;
+      }
       if (g == 1) {  // alias the source world's buffers (pre/post are no-ops)
         d.base[t * d.W + r] = s.base[t * s.W + r];
         d.pitch[t * d.W + r] = s.pitch[t * s.W + r];
@@ -134,17 +148,18 @@ __device__ void layout_tensor(const WorldArgs& d, const WorldArgs& s, const Layo
         }
         continue;
       }
-      rows = mode == 1 ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
+      rows = (mode == 1 || mode == 3) ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
     }
+    const bool sliced = mode == 1 || mode == 3;
     int64_t pitch = ti.row_bytes[t];
-    if (mode == 1 && ti.kind[t] == 1) pitch = ti.row_bytes[t] / g;
+    if (sliced && ti.kind[t] == 1) pitch = ti.row_bytes[t] / g;
     d.base[t * d.W + r] = d.peer_arena[t * d.n_procs + owner] + (uint64_t)off;
     d.pitch[t * d.W + r] = pitch;
     off += rows * pitch;
     if (off > d.arena_bytes[t]) atomicOr(d.status, ST_LAYOUT);
     if (t == 0) {
       d.rows[r] = rows;
-      d.headcol[r] = (mode == 1) ? (int32_t)(k * (ti.row_bytes[1] / 8 / g)) : 0;
+      d.headcol[r] = sliced ? (int32_t)(k * (ti.row_bytes[1] / 8 / g)) : 0;
     }
   }
 }
@@ -1078,6 +1093,46 @@ extern "C" sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, 
   sb::k_layout<<<1, 32, 0, s>>>(a, a, lp, sb::tinfo(w), 0);
   SB_CHECK_LAUNCH();
   sb::count_launch(2);
+  SB_API_END
+}
+
+// Layout of a world that no exchange produced (e.g. q/k/v written by a
+// projection in the chunk layout, or an attention output in the Ulysses
+// layout): per-rank tables from the current plan, on the device.
+extern "C" sb_status sb_world_layout_plan(sb_world* w, const sb_planner* p, int layout, sb_stream stream) {
+  SB_API_BEGIN
+  if (!w || !p) throw Error{SB_ERR_CONFIG, "sb_world_layout_plan: null argument"};
+  if (w->W != p->W)
+    throw Error{SB_ERR_INTEGRITY, "layout: plan world size " + std::to_string(p->W) + " != world ranks " +
+                                      std::to_string(w->W)};
+  if (layout < 0 || layout > 2) throw Error{SB_ERR_CONFIG, "sb_world_layout_plan: layout must be 0, 1 or 2"};
+  if (!p->origin_rows || !p->target_rows) throw Error{SB_ERR_CONFIG, "sb_world_layout_plan: no plan"};
+  sb::LayoutPlan lp{};
+  lp.no_check = 1;
+  int mode = 0;
+  if (layout == 0 || layout == 1) {
+    lp.rows_src = layout == 0 ? p->origin_rows : p->target_rows;
+  } else {
+    if (p->identity || p->uploaded)
+      throw Error{SB_ERR_CONFIG, "Ulysses layout needs a device-built plan (sb_plan)"};
+    for (int b = 0; b < p->M; ++b)
+      if (w->n_heads % p->bag_size[b] != 0)
+        throw Error{SB_ERR_CONFIG, "pre_attn: bag of " + std::to_string(p->bag_size[b]) +
+                                       " GPUs does not divide n_heads " + std::to_string(w->n_heads)};
+    if (w->max_bag < p->max_bag) throw Error{SB_ERR_CONFIG, "world max_bag smaller than the topology's bags"};
+    lp.rank_bag = p->d_rank_bag;
+    lp.rank_member = p->d_rank_member;
+    lp.bag_size = p->d_bag_size;
+    lp.bag_rows = p->bag_rows;
+    lp.target_rows = p->target_rows;
+    lp.U = p->U;
+    lp.M = p->M;
+    mode = 3;
+  }
+  sb::WorldArgs a = sb::wargs(w);
+  sb::k_layout<<<1, 32, 0, (cudaStream_t)stream>>>(a, a, lp, sb::tinfo(w), mode);
+  SB_CHECK_LAUNCH();
+  sb::count_launch();
   SB_API_END
 }
 

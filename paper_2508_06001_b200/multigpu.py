@@ -260,16 +260,32 @@ class MetaGather:
             self._h = None
 
 
-def step(group: PeerGroup, gather: MetaGather, planner: Planner, A, B, Cw, D, E, ulysses: bool, stream=None,
-         marks=None):
+def x_phases(A, B, Cw, D, E, ulysses: bool):
+    """Phases of one hidden-state world: route, pre_attn, post_attn, reverse."""
+    if ulysses:
+        return [("route", route, A, B, None), ("pre_attn", pre_attn, B, Cw, None),
+                ("post_attn", post_attn, Cw, D, None), ("reverse_route", reverse_route, D, E, None)]
+    return [("route", route, A, B, None), ("reverse_route", reverse_route, B, E, None)]
+
+
+def dit_phases(A, B, Q, Qu, O, Oc, E):
+    """DiT attention (metrics.cpp:85-121): route x; pre_attn q,k,v (chunk
+    layout); post_attn o (Ulysses layout); reverse_route o."""
+    return [("route", route, A, B, None),
+            ("pre_attn", pre_attn, Q, Qu, lambda pl, s: Q.layout_plan(pl, World.TARGET, s)),
+            ("post_attn", post_attn, O, Oc, lambda pl, s: O.layout_plan(pl, World.ULYSSES, s)),
+            ("reverse_route", reverse_route, Oc, E, None)]
+
+
+def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=None, marks=None):
     """One pass of the hot path on every process (all phases peer-closed).
 
     Every exchange writes straight into its destination process's arena and
     a barrier closes it, so the next phase may read what peers wrote.  With
     device barriers the whole step is stream-ordered and host-free (it is
-    captured in a CUDA graph by bench_main).  `marks`: optional list of
-    (name, start_event, end_event) timing events per phase, end recorded
-    after the closing barrier (the phase time includes barrier skew)."""
+    captured in a CUDA graph by bench_main).  `phases`: x_phases / dit_phases.
+    `marks`: optional list of (name, start_event, end_event) timing events per
+    phase, end recorded after the closing barrier (includes barrier skew)."""
     torch = group.torch
     s = stream if stream is not None else torch.cuda.current_stream()
     ev = {}
@@ -280,17 +296,18 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, A, B, Cw, D, E,
             e.record(s)
             ev.setdefault(name, [None, None])[which] = e
 
+    if marks is not None:
+        group.barrier(s)  # timed phases start aligned across processes (no host skew in "gather")
     mark("gather", 0)
     meta = gather.gather(s)
     mark("gather", 1)
     mark("plan", 0)
     planner.plan(meta, s)
     mark("plan", 1)
-    phases = ([("route", route, A, B), ("pre_attn", pre_attn, B, Cw), ("post_attn", post_attn, Cw, D),
-               ("reverse_route", reverse_route, D, E)] if ulysses else
-              [("route", route, A, B), ("reverse_route", reverse_route, B, E)])
-    for name, fn, src, dst in phases:
+    for name, fn, src, dst, pre in phases:
         mark(name, 0)
+        if pre is not None:
+            pre(planner, s)
         fn(planner, src, dst, s)
         group.barrier(s)
         mark(name, 1)
@@ -354,7 +371,7 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     ulysses = G > 1
     payload, meta_b, rope_b = 6144, 16, 16
     mk = lambda: make_world(group, W, 24, [payload], capacity_rows=tokens, max_bag=G, aux_row_bytes=(rope_b,))
-    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    A, B = mk(), mk()
     meta = gather.gather()
     gather.status()
     A.layout_origin(meta)
@@ -364,15 +381,59 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         rope = np.zeros((len(pos), 4), np.int32)
         rope[:, 0], rope[:, 1], rope[:, 2] = pos // 4096, (pos // 64) % 64, pos % 64
         A.write_rank(2, r, rope)
+    dit = ulysses and getattr(args, "pattern", "dit") == "dit"
+    planner.plan(meta)
+    if dit:
+        # q, k, v (chunk layout) and o (Ulysses layout) are device-resident
+        # activations: q = k = v = the routed x of this process's ranks,
+        # o = the pre_attn image of a perturbed witness world `home`
+        mkq = lambda: make_world(group, W, 24, [payload] * 3, capacity_rows=tokens, max_bag=G,
+                                 aux_row_bytes=(rope_b,))
+        mko = lambda: make_world(group, W, 24, [payload], capacity_rows=tokens, max_bag=G)
+        Q, Qu, O, Oc, E, home, t1, t2 = mkq(), mkq(), mko(), mko(), mko(), mko(), mko(), mko()
+        home.layout_origin(meta)
+        home.fill_witness(meta)
+        home.perturb()
+        group.barrier()
+        for fn, src, dst in ((route, A, B), (route, home, t1), (pre_attn, t1, t2)):
+            fn(planner, src, dst)
+            group.barrier()
+        Q.layout_plan(planner, World.TARGET)
+        O.layout_plan(planner, World.ULYSSES)
+        torch.cuda.synchronize()
+        for r in range(first, first + n_local):
+            for t_dst, t_src in ((0, 0), (1, 1), (2, 1), (3, 1), (4, 2)):
+                Q.write_rank(t_dst, r, B.read_rank(t_src, r))
+            for t in (0, 1):
+                O.write_rank(t, r, t2.read_rank(t, r))
+        phases = dit_phases(A, B, Q, Qu, O, Oc, E)
+        worlds = [A, B, Q, Qu, O, Oc, E]
+        out_rows = {"payload": [payload], "aux": []}
+    else:
+        Cw, D, E = mk(), mk(), mk()
+        home = A
+        phases = x_phases(A, B, Cw, D, E, ulysses)
+        worlds = [A, B, Cw, D, E]
     group.barrier()
+
+    def run_step(marks=None):
+        return step(group, gather, planner, phases, marks=marks)
+
+    def check(what):
+        torch.cuda.synchronize()
+        group.barrier_status()
+        for w in worlds:
+            w.status()
+        for r in range(first, first + n_local):
+            assert all(np.array_equal(E.read_rank(t, r), home.read_rank(t, r)) for t in range(home.T)), \
+                f"{what}: round trip not bit-exact"
+
     for _ in range(max(3, args.warmup)):
-        step(group, gather, planner, A, B, Cw, D, E, ulysses)
-    torch.cuda.synchronize()
-    group.barrier_status()
-    E.status()
-    for r in range(first, first + n_local):
-        assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), "round trip not bit-exact"
+        run_step()
+    check("eager")
     cs = group.sum_u64(B.checksum()) == group.sum_u64(A.checksum())
+    if dit:
+        cs = cs and group.sum_u64(Qu.checksum()) == group.sum_u64(A.checksum())
     hp = planner.download()
 
     stream = torch.cuda.current_stream()
@@ -396,7 +457,7 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         launches = _capi.load().sb_kernel_launches() - n0
         return group.max_over_ranks(ev0.elapsed_time(ev1)) / k, launches, clk
 
-    ms_eager, launches, clk = timed(lambda: step(group, gather, planner, A, B, Cw, D, E, ulysses), args.steps)
+    ms_eager, launches, clk = timed(run_step, args.steps)
     ms, mode = ms_eager, "eager"
     graph_err, ms_graph = None, None
     if group.mode == "device":
@@ -405,19 +466,15 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
             group.barrier()
             torch.cuda.synchronize()
             with torch.cuda.graph(g):
-                step(group, gather, planner, A, B, Cw, D, E, ulysses)
+                run_step()
             l0 = _capi.load().sb_kernel_launches()  # kernels the captured step launches
-            step(group, gather, planner, A, B, Cw, D, E, ulysses)
+            run_step()
             per_step = _capi.load().sb_kernel_launches() - l0
             for _ in range(3):
                 g.replay()
             torch.cuda.synchronize()
             ms_graph, _, clk_g = timed(g.replay, args.steps)
-            group.barrier_status()
-            E.status()
-            for r in range(first, first + n_local):
-                assert all(np.array_equal(E.read_rank(t, r), A.read_rank(t, r)) for t in range(3)), \
-                    "graph round trip not bit-exact"
+            check("graph")
             if ms_graph < ms:
                 ms, mode, clk, launches = ms_graph, "cuda_graph", clk_g, per_step * args.steps
         except Exception as e:  # graph capture is an optimisation; eager numbers stand
@@ -428,27 +485,33 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     acc = {}
     for _ in range(n_inst):
         marks = []
-        step(group, gather, planner, A, B, Cw, D, E, ulysses, marks=marks)
+        run_step(marks)
         torch.cuda.synchronize()
         for name, a, b in marks:
             acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) * 1000.0
     group.barrier_status()
-    rows = {"meta": meta_b, "payload": [payload], "aux": [rope_b]}
-    phases = {}
+    # tensors each phase moves: x (hidden + RoPE) for route; q,k,v + RoPE for
+    # pre_attn and o for post_attn / reverse_route in the DiT pattern
+    tens = {"route": ([payload], [rope_b])}
+    if dit:
+        tens.update(pre_attn=([payload] * 3, [rope_b]), post_attn=([payload], []), reverse_route=([payload], []))
+    else:
+        tens.update(pre_attn=([payload], [rope_b]), post_attn=([payload], [rope_b]), reverse_route=([payload], [rope_b]))
+    phase_out = {}
     for name in ["gather", "plan", "route", "pre_attn", "post_attn", "reverse_route"]:
         if name not in acc:
             continue
         us = group.max_over_ranks(acc[name] / n_inst)
         ph = {"us": us}
         if name not in ("gather", "plan"):
-            sent, recv = phase_bytes(hp, name, planner.topology, W, group.size, rows["payload"], rows["aux"], meta_b)
+            sent, recv = phase_bytes(hp, name, planner.topology, W, group.size, tens[name][0], tens[name][1], meta_b)
             busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
             ph.update(busiest_bytes=busiest, aggregate_bytes=int(sent.sum()),
                       gbs=busiest / (us * 1e-6) / 1e9 if us > 0 else None,
                       aggregate_gbs_per_gpu=sent.sum() / group.size / (us * 1e-6) / 1e9 if us > 0 else None)
             ph["frac_of_nvlink"] = ph["gbs"] / 900.0 if ph["gbs"] is not None and not group.same_device else None
-        phases[name] = ph
-    route_ph = phases["route"]
+        phase_out[name] = ph
+    route_ph = phase_out["route"]
 
     # e2e through the public API with host buffers: every step uploads this
     # process's ranks (metadata + payload image) from pinned memory, runs the
@@ -456,21 +519,24 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     # local ranks, 8 B per process, checked against the input's).
     rows_local = int(sum(int(x.sum()) for x in all_lens[first:first + n_local]))
     sizes = [rows_local * meta_b, rows_local * payload, rows_local * rope_b]
+    esizes = sizes[:home.T]
     h_in = [pinned_host(n) for n in sizes]
-    h_out = [pinned_host(n) for n in sizes]
+    h_home = [pinned_host(n) for n in esizes]
+    h_out = [pinned_host(n) for n in esizes]
     A.download([h.data_ptr() for h in h_in], sizes)
+    home.download([h.data_ptr() for h in h_home], esizes)
     torch.cuda.synchronize()
-    want_cs = A.checksum()
+    want_cs = home.checksum()
 
     def e2e_step():
         gather.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
         A.upload([h.data_ptr() for h in h_in], sizes)
-        step(group, gather, planner, A, B, Cw, D, E, ulysses)
+        run_step()
         return E.checksum()
 
-    E.download([h.data_ptr() for h in h_out], sizes)  # full image once: byte-exact check
+    E.download([h.data_ptr() for h in h_out], esizes)  # full image once: byte-exact check
     torch.cuda.synchronize()
-    e2e_ok = all(bool(torch.equal(o, h)) for o, h in zip(h_out, h_in)) and e2e_step() == want_cs
+    e2e_ok = all(bool(torch.equal(o, h)) for o, h in zip(h_out, h_home)) and e2e_step() == want_cs
     k = max(3, min(args.steps, 20))
     group.barrier()
     torch.cuda.synchronize()
@@ -492,13 +558,15 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": cfg["workload"], "topology": topology, "world_ranks": W,
                    "tokens_per_step": tokens, "sequences": n_seqs, "row_bytes": payload + meta_b + rope_b,
+                   "pattern": "dit: route x; pre_attn q,k,v; post_attn o; reverse_route o" if dit else "x",
                    "parallelism": f"{W} ranks over {group.size} processes (peer-store all-to-all)",
                    "barrier": group.mode, "devices": n_dev, "same_device": bool(group.same_device),
+                   "mps": os.environ.get("SEQBAL_MPS") == "private",
                    "l2": "inputs larger than L2" if tokens * payload > 126e6 * group.size else
                          "per-process arenas may fit L2 (strong scaling of one batch)"},
         "launch_mode": mode, "ms_per_step_eager": ms_eager, "ms_per_step_graph": ms_graph, "graph_error": graph_err,
         "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
-        "phases": phases,
+        "phases": phase_out,
         "a2a_gbs": route_ph.get("gbs"), "a2a_busiest_bytes": route_ph.get("busiest_bytes"),
         "route_phase_us": route_ph["us"],
         "roofline": _a2a_roofline(route_ph.get("busiest_bytes", 0), route_ph["us"], group.same_device),
