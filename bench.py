@@ -317,7 +317,7 @@ def run_c4(args):
 C5_STEPS = 1000
 
 
-def run_reference_stream(steps, budget_s, threads=None):
+def run_reference_stream(steps, budget_s, threads=None, full_every=50):
     """The reference on the C5 schedule: plan_routing every step, full data
     path (route + Ulysses + reverse, Exec::Parallel) every 50th step."""
     from paper_2508_06001_b200.scenarios import C5_SCENARIOS, C5_SEED, C5_TOPOLOGY, C5_WORLD
@@ -327,7 +327,7 @@ def run_reference_stream(steps, budget_s, threads=None):
     env = dict(os.environ)
     env["OMP_NUM_THREADS"] = str(threads or os.cpu_count() or 1)
     req = {"world": C5_WORLD, "topology": C5_TOPOLOGY, "scenarios": [{"codes": c} for c in C5_SCENARIOS],
-           "seed": C5_SEED, "steps": steps, "full_every": 50, "payload_width": PAYLOAD_BYTES // 8,
+           "seed": C5_SEED, "steps": steps, "full_every": full_every, "payload_width": PAYLOAD_BYTES // 8,
            "budget_s": budget_s}
     p = subprocess.run([harness, "stream"], input=json.dumps(req).encode(), capture_output=True, env=env,
                        timeout=1800)
@@ -418,6 +418,24 @@ def run_c5(args):
     verify_s = time.time() - t0
     vrecs = vdrv.records()
     same_plans = all(a["wir"] == b["wir"] and a["chunks"] == b["chunks"] for a, b in zip(recs, vrecs))
+    # every step's plan against the unmodified reference's plan_routing on the
+    # same schedule (ref_harness stream, plan only: ~50 us per step)
+    ref_plans, ref_err = run_reference_stream(steps, budget_s=1e9, full_every=0)
+    parity = {"steps": 0, "mismatches": None, "fields": "tokens, sequences, chunks, WIR bits, total_workload bits, "
+                                                        "capacity_violations, max_over_mean",
+              "reference": "oracle/_ref/ref_harness stream (plan_routing per step)"}
+    if ref_plans:
+        bad = 0
+        for g in ref_plans["per_step"]:
+            r = recs[g["step"]]
+            ok = (r["tokens"] == g["tokens"] and r["sequences"] == g["sequences"] and r["chunks"] == g["chunks"]
+                  and f"{np.float64(r['wir']).view(np.uint64):016x}" == g["wir"]
+                  and f"{np.float64(r['total_workload']).view(np.uint64):016x}" == g["total_workload"]
+                  and r["capacity_violations"] == g["violations"] and r["max_over_mean"] == g["max_over_mean"])
+            bad += 0 if ok else 1
+        parity.update(steps=len(ref_plans["per_step"]), mismatches=bad)
+    else:
+        parity["unavailable"] = ref_err
     line = {
         "metric": "sustained round-trip tokens/s over a 1000-step dynamic stream; workload imbalance",
         "value": float(tokens.sum() / (ms * 1e-3)), "unit": "tokens/s", "n_gpus": 1, "steps": steps,
@@ -441,6 +459,7 @@ def run_c5(args):
         "verify": {"steps": vprog["steps_run"], "failed_checks": vprog["failed"], "plans_identical": same_plans,
                    "checks": "route + pre_attn conserve content_checksum; post_attn(pre_attn(x)) == x; perturbed "
                              "payload returns home bitwise (simulator.cpp:106-159)", "wall_s": verify_s},
+        "reference_plan_parity": parity,
         "gpu_launches": int(launches), "gpu_launches_per_step": int(launches_per_step), "clocks": clk.summary(),
         "e2e": {"value": e2e_tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 24, "ms_per_step": e2e_ms,

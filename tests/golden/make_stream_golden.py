@@ -6,7 +6,7 @@ UNMODIFIED reference (oracle/_ref/ref_harness, built by oracle/Makefile).
       (data_sim.cpp:39-76) incl. ParseError offsets;
   tests/golden/uniform.json -- balance_uniform_items / reverse_uniform_plan
       (balancer.cpp:411-462) on hand and random count vectors;
-  tests/golden/stream.json  -- the C5 1000-step schedule's first steps planned
+  tests/golden/stream.json  -- all 1000 steps of the C5 schedule planned
       by plan_routing: per-step tokens, sequences, chunks, WIR and total
       workload bits, capacity violations.
 
@@ -57,7 +57,7 @@ def main():
         json.dump(batches, f, separators=(",", ":"))
     stream = harness("stream", {"world": C5_WORLD, "topology": C5_TOPOLOGY,
                                 "scenarios": [{"codes": c} for c in C5_SCENARIOS], "seed": C5_SEED,
-                                "steps": 60, "full_every": 0})
+                                "steps": 1000, "full_every": 0})
     stream["inputs"] = {"world": C5_WORLD, "topology": C5_TOPOLOGY, "scenarios": C5_SCENARIOS, "seed": C5_SEED}
     with open(os.path.join(HERE, "stream.json"), "w") as f:
         json.dump(stream, f, separators=(",", ":"))

@@ -75,8 +75,12 @@ def _c5_driver(verify=True, cap=128, width=768):
 
 
 def test_driver_c5_matches_reference_and_checks_hold():
-    sch, planner, drv = _c5_driver(width=768)  # 96 doubles per row keeps the test small
+    """All 1000 steps of the C5 schedule: every step's plan (tokens,
+    sequences, chunks, WIR and total-workload bits, violations, max/mean)
+    equals the unmodified reference's, and simulate_step's checks hold."""
     n = STREAM["steps"]
+    assert n == 1000
+    sch, planner, drv = _c5_driver(width=768, cap=n)  # 96 doubles per row keeps the test small
     drv.set_step(0)
     drv.run(n)
     prog = drv.progress()
