@@ -259,6 +259,23 @@ SB_API sb_status sb_post_attn(sb_planner* p, sb_world* src, sb_world* dst, sb_st
 SB_API sb_status sb_exchange_prepare(sb_planner* p, int op, sb_world* src, sb_world* dst, int slot,
                                      sb_stream stream);
 SB_API sb_status sb_exchange_run(sb_planner* p, int slot, sb_stream stream);
+/* Collective transport (the NCCL baseline of the four exchanges above; the
+ * reference's simulated all-to-all is exchange.cpp:127-198 / :255-436).  No
+ * peer mappings: every process builds the exchange's full job list from the
+ * shared plan and packs the jobs whose source it hosts and whose target it
+ * does not into one segment per destination process of `send_buf` (in job
+ * order; local->local jobs copy directly).  d_counts (device, 2P int64)
+ * receives the bytes sent to each process [0, P) and received from each
+ * [P, 2P).  The caller then runs ONE all-to-all-v send_buf -> recv_buf on the
+ * same stream (grouped ncclSend/ncclRecv; NCCL skips zero counts, so the
+ * Ulysses exchanges stay inside each bag) and calls sb_exchange_unpack, which
+ * scatters recv_buf into the destination world.  A plan needing more than
+ * send_cap / recv_cap bytes copies nothing and sb_world_status(dst) reports
+ * SB_ERR_CAPACITY; at most 16 processes. */
+SB_API sb_status sb_exchange_pack(sb_planner* p, int op, sb_world* src, sb_world* dst, void* send_buf,
+                                  int64_t send_cap, void* recv_buf, int64_t recv_cap, int64_t* d_counts,
+                                  sb_stream stream);
+SB_API sb_status sb_exchange_unpack(sb_planner* p, sb_stream stream);
 /* Synchronises and returns the world's device status (layout capacity). */
 SB_API sb_status sb_world_status(sb_world* w, sb_stream stream);
 
@@ -438,7 +455,11 @@ SB_API sb_status sb_ipc_close(void* dptr);
 /* Metadata all-gather (gather_sequence_info, exchange.cpp:68-77, made a real
  * collective): every process pushes its hosted ranks' (id, len) records into
  * slot [rank] of every process's gather buffer (peer stores), then -- after a
- * barrier -- compacts its own buffer into gather order for sb_plan.        */
+ * barrier -- compacts its own buffer into gather order for sb_plan.
+ * Without sb_gather_set_peers only this process's slots are written; the
+ * collective transport then all-gathers the buffer's three sections (counts
+ * [W] i64, ids [W*cap] u64, lens [W*cap] i64; each process owns the
+ * contiguous slots of its ranks) with ncclAllGather before compacting.    */
 typedef struct sb_gather sb_gather;
 SB_API sb_status sb_gather_create(int world_size, int n_local, int first_local, int64_t cap_per_rank,
                                   sb_gather** out);

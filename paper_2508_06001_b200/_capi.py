@@ -109,6 +109,9 @@ _SIGS = {
     "sb_post_attn": (C.c_int, [C.c_void_p] * 4),
     "sb_exchange_prepare": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "sb_exchange_run": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "sb_exchange_pack": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                   C.c_int64, C.c_void_p, C.c_void_p]),
+    "sb_exchange_unpack": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sb_world_status": (C.c_int, [C.c_void_p] * 2),
     "sb_world_upload": (C.c_int, [C.c_void_p] * 4),
     "sb_world_download": (C.c_int, [C.c_void_p] * 4),

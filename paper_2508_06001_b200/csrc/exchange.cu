@@ -177,6 +177,7 @@ struct JobArgs {
   int max_bag;
   SbJob* jobs;
   int64_t* n_jobs;
+  int32_t* owner;  // collective transport: every chunk's jobs, owner[x] = src proc << 16 | dst proc (-1: none)
 };
 
 __device__ __forceinline__ bool is_local(const WorldArgs& w, int r) {
@@ -197,11 +198,13 @@ __device__ __forceinline__ void route_job(const JobArgs& j, const WorldArgs& s, 
     const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
     job.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp);
     job.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp);
-    job.n_rows = (is_local(s, sr) && !(*d.status & ST_MISMATCH)) ? j.c_end[c] - j.c_start[c] : 0;
+    const bool coll = j.owner != nullptr;
+    job.n_rows = (coll || (is_local(s, sr) && !(*d.status & ST_MISMATCH))) ? j.c_end[c] - j.c_start[c] : 0;
     job.width = ti.row_bytes[t];
     job.spitch = sp;
     job.dpitch = dp;
     j.jobs[x] = job;
+    if (coll) j.owner[x] = ((sr / s.n_local) << 16) | (dr / d.n_local);
   }
 }
 
@@ -230,6 +233,8 @@ __device__ __forceinline__ void ulysses_job(const JobArgs& j, const WorldArgs& s
     job.n_rows = 0;
     job.width = 16;
     job.spitch = job.dpitch = 16;
+    const bool coll = j.owner != nullptr;
+    int32_t own = -1;
     const int dst_rank_of_chunk = j.c_dst[c];
     const int g = j.bag_size[j.bag_of_rank[dst_rank_of_chunk % j.U]];
     const int mine = j.c_idx[c];
@@ -266,7 +271,8 @@ __device__ __forceinline__ void ulysses_job(const JobArgs& j, const WorldArgs& s
           active = other == 0;  // metadata once per destination row (exchange.cpp:424)
         }
       }
-      if (active && is_local(s, sr) && !(*d.status & ST_MISMATCH)) {
+      if (active && (coll || (is_local(s, sr) && !(*d.status & ST_MISMATCH)))) {
+        own = ((sr / s.n_local) << 16) | (dr / d.n_local);
         const int64_t sp = s.pitch[t * s.W + sr], dp = d.pitch[t * d.W + dr];
         job.src = s.base[t * s.W + sr] + (uint64_t)(srow * sp + scol);
         job.dst = d.base[t * d.W + dr] + (uint64_t)(drow * dp + dcol);
@@ -277,6 +283,7 @@ __device__ __forceinline__ void ulysses_job(const JobArgs& j, const WorldArgs& s
       }
     }
     j.jobs[x] = job;
+    if (coll) j.owner[x] = own;
   }
 }
 
@@ -351,6 +358,105 @@ __global__ void __launch_bounds__(1024) k_exchange_prep(JobArgs j, WorldArgs s, 
   }
   __syncthreads();
   pieces_body(j.jobs, j.n_jobs, piece_off, bytes_moved);
+}
+
+// ------------------------------------------- collective transport split
+// The NCCL baseline transport (sb_exchange_pack / sb_exchange_unpack): no
+// peer mappings.  Every process builds the FULL job list of the exchange
+// (all processes hold the same plan, so the lists are identical) and splits
+// it: a job whose source rank is local and destination remote is packed, in
+// job order, into the destination process's contiguous segment of a send
+// buffer; a job whose destination is local and source remote is unpacked
+// from the source process's segment of the receive buffer.  Sender and
+// receiver walk the same list in the same order, so every byte offset is
+// known on both sides without exchanging any layout.  Local-to-local jobs
+// copy directly in the pack pass.  Between the two passes the caller runs one
+// all-to-all-v (grouped ncclSend/ncclRecv) with the byte counts written to
+// counts[0, P) (sent to each process) and counts[P, 2P) (received).
+constexpr int kMaxCollProcs = 16;
+
+__global__ void __launch_bounds__(1024) k_collective_split(SbJob* jobs, const int32_t* owner, const int64_t* n_jobs_p,
+                                                           int me, int P, uint64_t send, int64_t send_cap,
+                                                           uint64_t recv, int64_t recv_cap, int32_t* status,
+                                                           int64_t* piece_off, int64_t* bytes_moved, SbJob* ujobs,
+                                                           int64_t* u_n_jobs, int64_t* u_piece_off, int64_t* counts) {
+  __shared__ int64_t sh[33];
+  __shared__ int64_t s_tot[2 * kMaxCollProcs];
+  const int64_t n = *n_jobs_p;
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int64_t per = (n + nt - 1) / nt;
+  const int64_t b = tid * per, e = b + per < n ? b + per : n;
+  int64_t cs[kMaxCollProcs], cr[kMaxCollProcs];
+  for (int q = 0; q < kMaxCollProcs; ++q) cs[q] = cr[q] = 0;
+  for (int64_t i = b; i < e; ++i) {
+    const int32_t o = owner[i];
+    const SbJob jb = jobs[i];
+    if (o < 0 || jb.n_rows <= 0) continue;
+    const int so = o >> 16, dd = o & 0xffff;
+    const int64_t nb = jb.n_rows * jb.width;
+    if (so == me && dd != me) cs[dd] += nb;
+    else if (dd == me && so != me) cr[so] += nb;
+  }
+  for (int q = 0; q < P; ++q) {
+    int64_t tot;
+    cs[q] = block_excl_scan<int64_t>(cs[q], sh, &tot);
+    if (tid == 0) s_tot[q] = tot;
+    cr[q] = block_excl_scan<int64_t>(cr[q], sh, &tot);
+    if (tid == 0) s_tot[kMaxCollProcs + q] = tot;
+  }
+  __syncthreads();
+  int64_t sd[kMaxCollProcs], rd[kMaxCollProcs], st = 0, rt = 0;
+  for (int q = 0; q < P; ++q) {
+    sd[q] = st;
+    rd[q] = rt;
+    st += s_tot[q];
+    rt += s_tot[kMaxCollProcs + q];
+  }
+  const bool fits = st <= send_cap && rt <= recv_cap;
+  const bool copy = fits && !(*status & ST_MISMATCH);
+  if (tid == 0 && !fits) atomicOr(status, ST_CAPACITY);
+  for (int64_t i = b; i < e; ++i) {
+    const int32_t o = owner[i];
+    SbJob pk = jobs[i], up;
+    up.src = up.dst = 0;
+    up.n_rows = 0;
+    up.width = up.spitch = up.dpitch = 16;
+    if (o < 0 || pk.n_rows <= 0) {
+      pk.n_rows = 0;
+    } else {
+      const int so = o >> 16, dd = o & 0xffff;
+      const int64_t nb = pk.n_rows * pk.width;
+      if (so == me) {
+        if (dd != me) {
+          pk.dst = send + (uint64_t)(sd[dd] + cs[dd]);
+          pk.dpitch = pk.width;
+          cs[dd] += nb;
+        }
+      } else {
+        if (dd == me) {
+          up = pk;
+          up.src = recv + (uint64_t)(rd[so] + cr[so]);
+          up.spitch = up.width;
+          cr[so] += nb;
+        }
+        pk.n_rows = 0;
+      }
+    }
+    if (!copy) pk.n_rows = up.n_rows = 0;
+    jobs[i] = pk;
+    ujobs[i] = up;
+  }
+  if (tid == 0) {
+    *u_n_jobs = n;
+    for (int q = 0; q < P; ++q) {
+      counts[q] = s_tot[q];
+      counts[P + q] = s_tot[kMaxCollProcs + q];
+    }
+  }
+  __syncthreads();
+  pieces_body(jobs, n_jobs_p, piece_off, bytes_moved);
+  __syncthreads();
+  pieces_body(ujobs, u_n_jobs, u_piece_off, u_n_jobs + 1);
 }
 
 // ------------------------------------------------------------ copy kernel
@@ -844,6 +950,7 @@ static JobArgs jargs(sb_planner* p) {
   j.max_bag = p->max_bag;
   j.jobs = p->jobs;
   j.n_jobs = p->n_jobs;
+  j.owner = p->coll_mode ? p->x_owner : nullptr;
   return j;
 }
 
@@ -1339,6 +1446,88 @@ extern "C" sb_status sb_post_attn(sb_planner* p, sb_world* src, sb_world* dst, s
   SB_API_END
 }
 
+// Collective transport (the NCCL baseline; see k_collective_split): pack
+// this process's outbound jobs of exchange `op` (0 route, 1 reverse_route,
+// 2 pre_attn, 3 post_attn) into per-destination segments of send_buf and
+// copy local-to-local jobs directly; write the all-to-all-v byte counts to
+// d_counts[0, 2P).  The caller moves send_buf -> recv_buf (ncclSend/ncclRecv
+// grouped, or any all-to-all-v) on the same stream, then calls
+// sb_exchange_unpack.  Worlds need no peer mappings (sb_world_set_peers).
+extern "C" sb_status sb_exchange_pack(sb_planner* p, int op, sb_world* src, sb_world* dst, void* send_buf,
+                                      int64_t send_cap, void* recv_buf, int64_t recv_cap, int64_t* d_counts,
+                                      sb_stream stream) {
+  SB_API_BEGIN
+  if (!p || !src || !dst || !d_counts) throw Error{SB_ERR_CONFIG, "sb_exchange_pack: null argument"};
+  if (op < 0 || op > 3) throw Error{SB_ERR_CONFIG, "sb_exchange_pack: op must be 0..3"};
+  if ((send_cap > 0 && !send_buf) || (recv_cap > 0 && !recv_buf) || send_cap < 0 || recv_cap < 0)
+    throw Error{SB_ERR_CONFIG, "sb_exchange_pack: bad transport buffers"};
+  if (dst->n_procs > sb::kMaxCollProcs)
+    throw Error{SB_ERR_CONFIG, "collective transport supports at most " + std::to_string(sb::kMaxCollProcs) +
+                                   " processes"};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t cap = op < 2 ? p->max_chunks * src->T : p->max_chunks * p->max_bag * src->T;
+  if (cap > p->x_owner_cap) {
+    if (p->x_owner) cudaFree(p->x_owner);
+    p->x_owner = nullptr;
+    p->x_owner_cap = 0;
+    SB_CUDA(cudaMalloc(&p->x_owner, sizeof(int32_t) * (size_t)std::max<int64_t>(1, cap)));
+    p->x_owner_cap = cap;
+  }
+  sb_planner::Slot& u = p->unpack;
+  if (cap > u.cap) {
+    if (u.jobs) cudaFree(u.jobs);
+    if (u.piece_off) cudaFree(u.piece_off);
+    u.jobs = nullptr;
+    u.piece_off = nullptr;
+    u.cap = 0;
+    SB_CUDA(cudaMalloc(&u.jobs, sizeof(SbJob) * (size_t)std::max<int64_t>(1, cap)));
+    SB_CUDA(cudaMalloc(&u.piece_off, sizeof(int64_t) * (size_t)(cap + 1)));
+    u.cap = cap;
+  }
+  if (!u.n_jobs) {
+    SB_CUDA(cudaMalloc(&u.n_jobs, sizeof(int64_t) * 2));
+    SB_CUDA(cudaMemset(u.n_jobs, 0, sizeof(int64_t) * 2));
+  }
+  u.prepared = false;
+  p->coll_mode = true;
+  try {
+    if (op < 2) prepare_route(p, op, op, src, dst, s);
+    else prepare_ulysses(p, op, op == 3, src, dst, s);
+  } catch (...) {
+    p->coll_mode = false;
+    throw;
+  }
+  p->coll_mode = false;
+  sb_planner::Slot& sl = p->slots[op];
+  const int me = dst->first_local / dst->n_local;
+  sb::k_collective_split<<<1, 1024, 0, s>>>(sl.jobs, p->x_owner, sl.n_jobs, me, dst->n_procs, (uint64_t)send_buf,
+                                             send_cap, (uint64_t)recv_buf, recv_cap, dst->d_status, sl.piece_off,
+                                             sl.n_jobs + 1, u.jobs, u.n_jobs, u.piece_off, d_counts);
+  SB_CHECK_LAUNCH();
+  sb::count_launch(1);
+  sl.pieces_done = true;
+  sl.fence_sys = 0;  // every store is local: the send buffer or this process's arena
+  u.prepared = true;
+  u.pieces_done = true;
+  u.tma_ok = sl.tma_ok;
+  u.engine = sl.engine;
+  u.fence_sys = 0;
+  u.op = sl.op;
+  run_slot(p, op, s);
+  SB_API_END
+}
+
+extern "C" sb_status sb_exchange_unpack(sb_planner* p, sb_stream stream) {
+  SB_API_BEGIN
+  if (!p) throw Error{SB_ERR_CONFIG, "sb_exchange_unpack: null planner"};
+  sb_planner::Slot& u = p->unpack;
+  if (!u.prepared) throw Error{SB_ERR_CONFIG, "sb_exchange_unpack: no packed exchange"};
+  p->current_op = u.op;
+  sb::launch_copy(u.jobs, u.piece_off, u.n_jobs, (cudaStream_t)stream, 0, u.tma_ok, u.engine);
+  u.prepared = false;
+  SB_API_END
+}
+
 extern "C" sb_status sb_world_status(sb_world* w, sb_stream stream) {
   SB_API_BEGIN
   if (!w) throw Error{SB_ERR_CONFIG, "null world"};
@@ -1346,6 +1535,7 @@ extern "C" sb_status sb_world_status(sb_world* w, sb_stream stream) {
   int32_t st = 0;
   SB_CUDA(cudaMemcpy(&st, w->d_status, sizeof st, cudaMemcpyDeviceToHost));
   if (st & sb::ST_LAYOUT) throw Error{SB_ERR_CAPACITY, "world arena too small for the requested layout"};
+  if (st & sb::ST_CAPACITY) throw Error{SB_ERR_CAPACITY, "collective transport buffers too small for the exchange"};
   if (st & sb::ST_MISMATCH)
     throw Error{SB_ERR_INTEGRITY, "exchange source world does not match the plan's layout (rows per rank differ); "
                                   "nothing was copied"};

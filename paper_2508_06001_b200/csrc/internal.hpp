@@ -119,6 +119,13 @@ struct sb_planner {
   };
   static constexpr int kSlots = 8;
   Slot slots[kSlots];
+  // collective transport (sb_exchange_pack / _unpack): the full job list's
+  // (source process << 16 | destination process) per job, and the unpack list
+  bool coll_mode = false;  // job builders emit every chunk's jobs + owners
+  int32_t* x_owner = nullptr;
+  int64_t x_owner_cap = 0;
+  Slot unpack;
+  int unpack_op = -1;
   int cur_slot = 0, last_run_slot = 0;
   // current slot's buffers (aliases of slots[cur_slot])
   SbJob* jobs = nullptr;

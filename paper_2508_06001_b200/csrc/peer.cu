@@ -58,6 +58,7 @@ __device__ __forceinline__ int64_t* g_lens(uint64_t base, int W, int64_t cap) {
 __global__ void k_gather_push(GatherArgs a, const uint64_t* ids, const int64_t* lens, const int64_t* local_off) {
   const int dst = blockIdx.y;
   const uint64_t base = a.peers[dst];
+  if (!base) return;  // unmapped peer: the collective transport all-gathers the slots instead
   for (int lr = 0; lr < a.n_local; ++lr) {
     const int r = a.first_local + lr;
     const int64_t lo = local_off[lr], n = local_off[lr + 1] - local_off[lr];

@@ -1350,6 +1350,10 @@ static void planner_free(sb_planner* p) {
   if (p->gjoin_ev) cudaEventDestroy(p->gjoin_ev);
   if (p->side) cudaStreamDestroy(p->side);
   for (cudaEvent_t e : p->copy_ev) cudaEventDestroy(e);
+  if (p->x_owner) cudaFree(p->x_owner);
+  if (p->unpack.jobs) cudaFree(p->unpack.jobs);
+  if (p->unpack.piece_off) cudaFree(p->unpack.piece_off);
+  if (p->unpack.n_jobs) cudaFree(p->unpack.n_jobs);
   for (auto& sl : p->slots) {
     if (sl.jobs) cudaFree(sl.jobs);
     if (sl.piece_off) cudaFree(sl.piece_off);

@@ -191,12 +191,107 @@ class PeerGroup:
             self._barrier = None
 
 
+def device_bytes(ptr: int, nbytes: int):
+    """A uint8 torch view of nbytes of device memory owned by the C library."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_View(), device=torch.device("cuda", torch.cuda.current_device()))
+
+
+OPS = {"route": 0, "reverse_route": 1, "pre_attn": 2, "post_attn": 3}
+
+
+class CollectiveTransport:
+    """The NCCL baseline transport: pack (CUDA) -> one all-to-all-v -> unpack
+    (CUDA) per exchange, and ncclAllGather for the metadata.
+
+    `backend` "nccl": grouped ncclSend/ncclRecv through torch.distributed's
+    NCCL process group (needs one distinct GPU per process -- NCCL rejects
+    two ranks on one device).  "staged": the same pack/unpack kernels with the
+    all-to-all over the gloo control group through pinned host buffers -- the
+    functional stand-in for processes that share a GPU (tests).  The byte
+    counts come off the device before each all-to-all (NCCL needs them on the
+    host), so this transport is not graph-capturable; the peer-store path is.
+    Reference: the simulated all-to-alls exchange.cpp:127-198 / :255-436 and
+    the metadata gather exchange.cpp:68-77."""
+
+    def __init__(self, group: PeerGroup, send_bytes: int, recv_bytes: int, backend: str = "nccl"):
+        import torch
+        import torch.distributed as dist
+        if backend not in ("nccl", "staged"):
+            raise _capi.ConfigError(f"unknown collective backend {backend!r}")
+        if backend == "nccl" and group.same_device:
+            raise _capi.ConfigError("NCCL needs one GPU per process; processes share a device here (use 'staged')")
+        self.torch, self.dist, self.group, self.backend = torch, dist, group, backend
+        self.P = group.size
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.pg = dist.new_group(list(range(self.P)), backend="nccl") if backend == "nccl" else None
+        self.send = torch.empty(max(16, send_bytes), dtype=torch.uint8, device=dev)
+        self.recv = torch.empty(max(16, recv_bytes), dtype=torch.uint8, device=dev)
+        self.counts = torch.zeros(2 * self.P, dtype=torch.int64, device=dev)
+        self.h_counts = torch.zeros(2 * self.P, dtype=torch.int64).pin_memory()
+        if backend == "staged":
+            self.h_send = torch.empty(self.send.numel(), dtype=torch.uint8).pin_memory()
+            self.h_recv = torch.empty(self.recv.numel(), dtype=torch.uint8).pin_memory()
+        self.last_counts = None
+
+    def exchange(self, planner: Planner, op: str, src: World, dst: World, stream=None):
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        sp = C.c_void_p(s.cuda_stream)
+        call("sb_exchange_pack", planner.handle, OPS[op], src.handle, dst.handle, C.c_void_p(self.send.data_ptr()),
+             self.send.numel(), C.c_void_p(self.recv.data_ptr()), self.recv.numel(),
+             C.c_void_p(self.counts.data_ptr()), sp)
+        self.h_counts.copy_(self.counts, non_blocking=True)
+        s.synchronize()
+        c = self.h_counts.tolist()
+        out_splits, in_splits = c[:self.P], c[self.P:]
+        self.last_counts = (out_splits, in_splits)
+        ns, nr = sum(out_splits), sum(in_splits)
+        if ns > self.send.numel() or nr > self.recv.numel():  # nothing was packed; status reports it
+            dst.status(s)
+        if self.backend == "nccl":
+            with torch.cuda.stream(s):
+                self.dist.all_to_all_single(self.recv[:nr], self.send[:ns], in_splits, out_splits, group=self.pg)
+        else:
+            self.h_send[:ns].copy_(self.send[:ns])
+            self.dist.all_to_all_single(self.h_recv[:nr], self.h_send[:ns], in_splits, out_splits)
+            with torch.cuda.stream(s):
+                self.recv[:nr].copy_(self.h_recv[:nr], non_blocking=True)
+        call("sb_exchange_unpack", planner.handle, sp)
+        return dst
+
+    def all_gather(self, out, mine, stream=None):
+        """In-place all-gather: `mine` is this process's slice of `out`."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        if self.backend == "nccl":
+            with torch.cuda.stream(s):
+                self.dist.all_gather_into_tensor(out, mine, group=self.pg)
+        else:
+            s.synchronize()
+            h = out.cpu()
+            self.dist.all_gather_into_tensor(h, mine.cpu().clone())
+            with torch.cuda.stream(s):
+                out.copy_(h, non_blocking=False)
+
+    def barrier(self, stream=None):
+        s = stream if stream is not None else self.torch.cuda.current_stream()
+        s.synchronize()
+        self.dist.barrier()
+
+
 def make_world(group: PeerGroup, world_size: int, n_heads: int, payload_row_bytes, capacity_rows: int,
-               max_bag: int = 1, aux_row_bytes=()) -> World:
+               max_bag: int = 1, aux_row_bytes=(), share: bool = True) -> World:
+    """This process's block of a world; share=False skips the IPC mapping of
+    the arenas (the collective transport needs none)."""
     n_local, first = partition(world_size, group.size, group.rank)
     w = World(world_size, n_heads, payload_row_bytes, capacity_rows, aux_row_bytes, n_local=n_local,
               first_local=first, max_bag=max_bag)
-    for t in range(w.T):
+    for t in range(w.T if share else 0):
         base, _ = w.arena(t)
         w.set_peers(t, group.share(base))
     return w
@@ -206,17 +301,25 @@ class MetaGather:
     """The metadata all-gather over peer memory; result is a DeviceMeta in
     gather order with capacity world_size * cap_per_rank."""
 
-    def __init__(self, group: PeerGroup, world_size: int, cap_per_rank: int):
+    def __init__(self, group: PeerGroup, world_size: int, cap_per_rank: int, transport=None):
         import torch
         self.group, self.W = group, world_size
         self.n_local, self.first = partition(world_size, group.size, group.rank)
+        self.transport = transport  # CollectiveTransport: all-gather the slots instead of peer stores
         h = C.c_void_p()
         call("sb_gather_create", world_size, self.n_local, self.first, cap_per_rank, C.byref(h))
         self._h = h
         buf, nb = C.c_void_p(), C.c_int64()
         call("sb_gather_buffer", h, C.byref(buf), C.byref(nb))
-        peers = np.asarray(group.share(buf.value), np.uint64)
-        call("sb_gather_set_peers", h, peers.ctypes.data, group.size)
+        if transport is None:
+            peers = np.asarray(group.share(buf.value), np.uint64)
+            call("sb_gather_set_peers", h, peers.ctypes.data, group.size)
+        else:
+            # sections of the gather buffer (sb_gather_create): counts, ids, lens
+            raw = device_bytes(buf.value, nb.value)
+            W, c = world_size, cap_per_rank
+            self._sections = [(raw[0:8 * W], 8), (raw[8 * W:8 * W + 8 * W * c], 8 * c),
+                              (raw[8 * W + 8 * W * c:], 8 * c)]
         cap = world_size * cap_per_rank
         dev = torch.device("cuda", torch.cuda.current_device())
         self.out = DeviceMeta(np.zeros(cap, np.uint64), np.zeros(cap, np.int64), np.zeros(world_size + 1, np.int64),
@@ -244,7 +347,12 @@ class MetaGather:
         sp = C.c_void_p(s.cuda_stream)
         call("sb_gather_push", self._h, C.c_void_p(self.local_ids.data_ptr()), C.c_void_p(self.local_lens.data_ptr()),
              C.c_void_p(self.local_off.data_ptr()), sp)
-        self.group.barrier(s)
+        if self.transport is None:
+            self.group.barrier(s)
+        else:  # in-place all-gather of each section: this process owns slots [first, first + n_local)
+            for sec, per_rank in self._sections:
+                lo = self.first * per_rank
+                self.transport.all_gather(sec, sec[lo:lo + self.n_local * per_rank], s)
         ids, lens, off = self.out.ptrs()
         call("sb_gather_compact", self._h, ids, lens, off, sp)
         return self.out
@@ -277,7 +385,7 @@ def dit_phases(A, B, Q, Qu, O, Oc, E):
             ("reverse_route", reverse_route, Oc, E, None)]
 
 
-def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=None, marks=None):
+def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=None, marks=None, transport=None):
     """One pass of the hot path on every process (all phases peer-closed).
 
     Every exchange writes straight into its destination process's arena and
@@ -285,7 +393,10 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=
     device barriers the whole step is stream-ordered and host-free (it is
     captured in a CUDA graph by bench_main).  `phases`: x_phases / dit_phases.
     `marks`: optional list of (name, start_event, end_event) timing events per
-    phase, end recorded after the closing barrier (includes barrier skew)."""
+    phase, end recorded after the closing barrier (includes barrier skew).
+    `transport`: a CollectiveTransport -- each exchange is pack, all-to-all-v,
+    unpack (the collective closes the phase; no barrier), and `gather` must
+    have been built with the same transport."""
     torch = group.torch
     s = stream if stream is not None else torch.cuda.current_stream()
     ev = {}
@@ -308,8 +419,11 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=
         mark(name, 0)
         if pre is not None:
             pre(planner, s)
-        fn(planner, src, dst, s)
-        group.barrier(s)
+        if transport is None:
+            fn(planner, src, dst, s)
+            group.barrier(s)
+        else:
+            transport.exchange(planner, name, src, dst, s)
         mark(name, 1)
     if marks is not None:
         marks.extend((k, v[0], v[1]) for k, v in ev.items())
@@ -480,16 +594,6 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         except Exception as e:  # graph capture is an optimisation; eager numbers stand
             graph_err = f"{type(e).__name__}: {e}"
 
-    # per-phase times (instrumented eager pass; phase end = after its barrier)
-    n_inst = max(3, min(args.steps, 10))
-    acc = {}
-    for _ in range(n_inst):
-        marks = []
-        run_step(marks)
-        torch.cuda.synchronize()
-        for name, a, b in marks:
-            acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) * 1000.0
-    group.barrier_status()
     # tensors each phase moves: x (hidden + RoPE) for route; q,k,v + RoPE for
     # pre_attn and o for post_attn / reverse_route in the DiT pattern
     tens = {"route": ([payload], [rope_b])}
@@ -497,20 +601,66 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         tens.update(pre_attn=([payload] * 3, [rope_b]), post_attn=([payload], []), reverse_route=([payload], []))
     else:
         tens.update(pre_attn=([payload], [rope_b]), post_attn=([payload], [rope_b]), reverse_route=([payload], [rope_b]))
-    phase_out = {}
-    for name in ["gather", "plan", "route", "pre_attn", "post_attn", "reverse_route"]:
-        if name not in acc:
-            continue
-        us = group.max_over_ranks(acc[name] / n_inst)
-        ph = {"us": us}
-        if name not in ("gather", "plan"):
-            sent, recv = phase_bytes(hp, name, planner.topology, W, group.size, tens[name][0], tens[name][1], meta_b)
-            busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
-            ph.update(busiest_bytes=busiest, aggregate_bytes=int(sent.sum()),
-                      gbs=busiest / (us * 1e-6) / 1e9 if us > 0 else None,
-                      aggregate_gbs_per_gpu=sent.sum() / group.size / (us * 1e-6) / 1e9 if us > 0 else None)
-            ph["frac_of_nvlink"] = ph["gbs"] / 900.0 if ph["gbs"] is not None and not group.same_device else None
-        phase_out[name] = ph
+
+    def phase_times(step_fn, nvlink: bool):
+        """Per-phase times (instrumented eager pass; phase end = after its
+        barrier or collective), max over ranks, with busiest-GPU bytes."""
+        n_inst = max(3, min(args.steps, 10))
+        acc = {}
+        for _ in range(n_inst):
+            marks = []
+            step_fn(marks)
+            torch.cuda.synchronize()
+            for name, a, b in marks:
+                acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) * 1000.0
+        out = {}
+        for name in ["gather", "plan", "route", "pre_attn", "post_attn", "reverse_route"]:
+            if name not in acc:
+                continue
+            us = group.max_over_ranks(acc[name] / n_inst)
+            ph = {"us": us}
+            if name not in ("gather", "plan"):
+                sent, recv = phase_bytes(hp, name, planner.topology, W, group.size, tens[name][0], tens[name][1],
+                                         meta_b)
+                busiest = int(max(sent.max(), recv.max())) if len(sent) else 0
+                ph.update(busiest_bytes=busiest, aggregate_bytes=int(sent.sum()),
+                          gbs=busiest / (us * 1e-6) / 1e9 if us > 0 else None,
+                          aggregate_gbs_per_gpu=sent.sum() / group.size / (us * 1e-6) / 1e9 if us > 0 else None)
+                ph["frac_of_nvlink"] = ph["gbs"] / 900.0 if ph["gbs"] is not None and nvlink else None
+            out[name] = ph
+        return out
+
+    phase_out = phase_times(run_step, not group.same_device)
+    group.barrier_status()
+
+    # the NCCL baseline transport beside the peer-store path: pack kernel ->
+    # all-to-all-v (grouped ncclSend/ncclRecv) -> unpack kernel per exchange,
+    # ncclAllGather for the metadata.  Same worlds, same plan.
+    coll_out = {}
+    wanted = os.environ.get("SEQBAL_TRANSPORTS", "nccl" if not group.same_device else "")
+    for backend in [b for b in wanted.split(",") if b and b != "peer"]:
+        try:
+            nbytes = max(sum(w.arena(t)[1] for t in range(w.T)) for w in worlds)
+            tr = CollectiveTransport(group, nbytes, nbytes, backend)
+            cg = MetaGather(group, W, cap, transport=tr)
+            cg.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
+            cstep = lambda marks=None: step(group, cg, planner, phases, marks=marks, transport=tr)
+            for t in range(E.T):  # the collective path must rebuild E from scratch
+                device_bytes(*E.arena(t)).zero_()
+            for _ in range(max(3, args.warmup)):
+                cstep()
+            check(backend)
+            cms, cl, _ = timed(cstep, args.steps)
+            check(backend + " (timed)")
+            coll_out[backend] = {"ms_per_step": cms, "value": tokens / (cms * 1e-3), "gpu_launches": int(cl),
+                                 "round_trip_bit_exact": True,
+                                 "phases": phase_times(cstep, backend == "nccl"),
+                                 "collective": "all_to_all_single (grouped ncclSend/ncclRecv)" if backend == "nccl"
+                                 else "gloo all_to_all_single through pinned host buffers (functional stand-in)"}
+            cg.close()
+        except Exception as e:  # report, keep the headline
+            coll_out[backend] = {"error": f"{type(e).__name__}: {e}"}
+    group.barrier()
     route_ph = phase_out["route"]
 
     # e2e through the public API with host buffers: every step uploads this
@@ -567,6 +717,7 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
         "launch_mode": mode, "ms_per_step_eager": ms_eager, "ms_per_step_graph": ms_graph, "graph_error": graph_err,
         "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
         "phases": phase_out,
+        "transports": dict({"peer": {"ms_per_step": ms, "phases": phase_out}}, **coll_out),
         "a2a_gbs": route_ph.get("gbs"), "a2a_busiest_bytes": route_ph.get("busiest_bytes"),
         "route_phase_us": route_ph["us"],
         "roofline": _a2a_roofline(route_ph.get("busiest_bytes", 0), route_ph["us"], group.same_device),

@@ -164,7 +164,7 @@ def test_two_process_push_decomposition_gloo(topo):
     assert res == {0: True, 1: True}, res
 
 
-def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1):
+def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1, transport=None):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SEQBAL_BARRIER_TIMEOUT_MS="20000")
@@ -177,11 +177,15 @@ def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1):
         group = multigpu.PeerGroup(barrier_mode=barrier)
         assert group.same_device and group.mode == ("host" if barrier == "auto" else barrier)
         n_local, first = multigpu.partition(W, size, rank)
-        gather = multigpu.MetaGather(group, W, 8)
-        gather.set_local(meta.ids[first:first + n_local], meta.lens[first:first + n_local])
         planner = sb.Planner(topo, W, max_seqs=64)
         rows = int(sum(int(x.sum()) for x in meta.lens))
-        mk = lambda: multigpu.make_world(group, W, 4, [64], capacity_rows=rows, max_bag=planner.max_bag)
+        tr = None
+        if transport is not None:  # pack -> all-to-all-v -> unpack; worlds without IPC mappings
+            tr = multigpu.CollectiveTransport(group, 4 * rows * 80, 4 * rows * 80, transport)
+        gather = multigpu.MetaGather(group, W, 8, transport=tr)
+        gather.set_local(meta.ids[first:first + n_local], meta.lens[first:first + n_local])
+        mk = lambda: multigpu.make_world(group, W, 4, [64], capacity_rows=rows, max_bag=planner.max_bag,
+                                         share=tr is None)
         A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
         dm = gather.gather()
         gather.status()
@@ -189,7 +193,8 @@ def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1):
         A.fill_witness(dm)
         group.barrier()
         for _ in range(steps):
-            multigpu.step(group, gather, planner, multigpu.x_phases(A, B, Cw, D, E, planner.max_bag > 1))
+            multigpu.step(group, gather, planner, multigpu.x_phases(A, B, Cw, D, E, planner.max_bag > 1),
+                          transport=tr)
         torch.cuda.synchronize()
         group.barrier_status()  # CommError if a device barrier timed out
         plan, _ = oracle.plan_routing(meta, oracle.parse_topology(topo))  # FLUX model, as the planner
@@ -208,6 +213,14 @@ def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1):
                 bad.append(f"post(pre) r{r}")
         if group.sum_u64(B.checksum()) != oracle.checksum(w0):
             bad.append("checksum")
+        if tr is not None:  # the all-to-all-v carried exactly the cross-process bytes of route
+            hp = planner.download()
+            sent, recv = multigpu.phase_bytes(hp, "reverse_route", planner.topology, W, size, [64])
+            out_splits, in_splits = tr.last_counts
+            if sum(out_splits) != int(sent[rank]) or sum(in_splits) != int(recv[rank]):
+                bad.append(f"a2a bytes {tr.last_counts} vs {sent[rank]},{recv[rank]}")
+            for w in (A, B, Cw, D, E):
+                w.status()
         q.put((rank, True if not bad else ";".join(bad)))
         group.barrier()
         gather.close()
@@ -255,6 +268,86 @@ def test_two_processes_device_barrier(topo):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2", "g1n2+g2n1+g4n1"])
+def test_two_processes_collective_transport(topo):
+    """The NCCL-baseline decomposition (sb_exchange_pack -> all-to-all-v ->
+    sb_exchange_unpack, all-gathered metadata) between two processes on one
+    GPU: worlds carry no IPC mappings, the all-to-all runs over gloo through
+    pinned host buffers ('staged'; NCCL itself refuses two ranks on one
+    device).  Routed payload, ids, post(pre) and the round trip must match
+    the oracle exactly, and the all-to-all must carry exactly the
+    cross-process bytes."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, topo, q, "auto", 2, "staged")) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
+def _nccl_one_worker(port, topo, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        import paper_2508_06001_b200 as sb
+        W = 8
+        meta = oracle.meta_c1(W, 5, 2, 0)
+        group = multigpu.PeerGroup()
+        planner = sb.Planner(topo, W, max_seqs=64)
+        rows = int(sum(int(x.sum()) for x in meta.lens))
+        tr = multigpu.CollectiveTransport(group, 4 * rows * 80, 4 * rows * 80, "nccl")
+        gather = multigpu.MetaGather(group, W, 8, transport=tr)
+        gather.set_local(meta.ids, meta.lens)
+        mk = lambda: multigpu.make_world(group, W, 4, [64], capacity_rows=rows, max_bag=planner.max_bag, share=False)
+        A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+        dm = gather.gather()
+        gather.status()
+        A.layout_origin(dm)
+        A.fill_witness(dm)
+        multigpu.step(group, gather, planner, multigpu.x_phases(A, B, Cw, D, E, planner.max_bag > 1), transport=tr)
+        torch.cuda.synchronize()
+        plan, _ = oracle.plan_routing(meta, oracle.parse_topology(topo))
+        routed = oracle.route(oracle.make_world(meta, 8, 4), plan)
+        bad = [r for r in range(W) if not np.array_equal(B.read_rank(1, r), routed.ranks[r].payload.reshape(-1))
+               or not np.array_equal(E.read_rank(1, r), A.read_rank(1, r))]
+        q.put((0, True if not bad else f"ranks {bad}"))
+        gather.close()
+        group.close()
+    except Exception as e:
+        q.put((0, f"{type(e).__name__}: {e}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4"])
+def test_one_process_nccl_transport(topo):
+    """The NCCL backend itself (torch.distributed NCCL group: all_to_all_single
+    + in-place all_gather_into_tensor) on the one GPU this box has: one
+    process hosting all 8 ranks, so every byte is a local pack->unpack."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_one_worker, args=(_free_port(), topo, q))
+    p.start()
+    res = dict([q.get(timeout=300)])
+    p.join(timeout=60)
+    assert res == {0: True}, res
 
 
 def _barrier_timeout_worker(rank, size, port, q):
