@@ -6,8 +6,13 @@
 // (/root/reference/proj/include/seqbal/{error,topology,workload_model,
 // balancer,exchange,metrics}.hpp): the same namespace, type names, field
 // names and function signatures for everything on the plan -> route ->
-// Ulysses -> reverse path, so reference callers (simulator.cpp, the CLI's
-// `plan`, the benches and tests) recompile against libseqbal.so unchanged.
+// Ulysses -> reverse path, so code that calls only those (the CLI's `plan`,
+// the exchange benches, the balancer/exchange/topology tests) recompiles
+// against libseqbal.so unchanged.  simulator.cpp and the CLI's other
+// subcommands also use the modelled-cost layer (flops_per_block, CostModel,
+// estimate_fbl, tokens_per_second, hardware_flops_utilization, fit_gamma,
+// FitError, ScenarioConfig), which is off the hot path and NOT declared here
+// (INTEGRATION.md section 1).
 //
 // Every planning step and every byte of data movement runs in
 // libseqbal_cuda.so (sm_100a) through the C-ABI in seqbal_capi.h; this layer
