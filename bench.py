@@ -259,6 +259,10 @@ def run_c4(args):
                 r["ref_plan_us"] = 1e6 * x["plan_s"]
                 if "reverse_plan_s" in x:
                     r["ref_reverse_plan_us"] = 1e6 * x["reverse_plan_s"]
+                    # the device plan includes the reverse receive order
+                    # (rev_recv_idx); the reference computes it in
+                    # reverse_plan (balancer.cpp:242-287) on every reverse_route
+                    r["speedup_vs_ref_plan_plus_reverse"] = (r["ref_plan_us"] + r["ref_reverse_plan_us"]) / r["plan_us"]
                 r["speedup_vs_ref"] = r["ref_plan_us"] / r["plan_us"]
     head = next(r for r in rows if r["sequences"] == C4_SIZES[-1] and r["topology"] == "g1n8")
     # e2e at the headline point: metadata from pinned host memory -> device

@@ -560,6 +560,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
   }
   int viol = 0;
   const int nn = (int)n;  // <= max_seqs < 2^31: 32-bit loop arithmetic
+  if (a.trace && rep == 0 && lane == 0) a.trace[14] = clock64();  // diagnostics: setup | chain | epilogue
   auto step = [&](int p) {
     const double w = w_a, wn = w_b;  // w_p and w_{p+1} (0 past the end: unused)
     w_a = w_b;
@@ -607,6 +608,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
       for (int p = p0; p < p1; ++p) step(p);
     }
   }
+  if (a.trace && rep == 0 && lane == 0) a.trace[15] = clock64();
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
     const int j = lane + 32 * i;
@@ -975,7 +977,12 @@ __global__ void __launch_bounds__(kListTile) k_lists_count(PlanArgs a) {
     a.list_tie[r] = 0;
   }
   const int64_t o0 = (int64_t)t * kListTile;
-  if (o0 >= d.n_b && d.rlo + o0 >= d.rhi && d.lo + o0 >= d.hi) return;
+  if (o0 >= d.n_b && d.rlo + o0 >= d.rhi && d.lo + o0 >= d.hi) {
+    // empty tile of this rank: its sums are zero (k_lists adds every tile's,
+    // and the buffer may hold a previous plan's)
+    if (tid < 4) a.list_sum[((int64_t)r * gridDim.x + t) * 4 + tid] = 0;
+    return;
+  }
   int64_t v[4];
   list_values(a, d, r, o0 + tid, v);
 #pragma unroll
@@ -1309,7 +1316,7 @@ static void planner_alloc(sb_planner* p) {
   SB_CUDA(cudaMemcpy(p->d_rank_member, p->rank_member.data(), sizeof(int32_t) * p->U, cudaMemcpyHostToDevice));
   SB_CUDA(cudaFuncSetAttribute(k_sort_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBytes));
   if (p->max_seqs <= kSmallSeqs && p->W <= 1024) {
-    p->small_smem = small_layout((int)p->max_seqs, p->W, p->R * p->M, p->R).total;
+    p->small_smem = small_layout((int)p->max_seqs, p->W, p->R * p->M, p->R, p->U, p->M).total;
     static size_t set_to = 0;  // attribute is per function: keep the largest requested
     if (p->small_smem > set_to) {
       SB_CUDA(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->small_smem));

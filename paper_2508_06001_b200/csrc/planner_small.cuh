@@ -32,11 +32,11 @@ __host__ __device__ inline int small_pow2(int n) {
 
 struct SmallLayout {  // byte offsets into dynamic shared memory
   size_t ids, lens, w, soff, hi, lo, v, rank, sorted, pick, G, cb, bo, rank_off, rpre, bagcnt, bagcb, bagq,
-      sendcnt, sendoff, reptot, tie, total;
+      sendcnt, sendoff, reptot, tie, t_boff, t_branks, t_bsize, t_rbag, t_rmem, pergpu, recvoff, total;
   int T;
 };
 
-__host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int R) {
+__host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int R, int U, int M) {
   SmallLayout L;
   const int T = small_pow2(cap);
   size_t o = 0;
@@ -68,6 +68,13 @@ __host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int 
   L.sendoff = take(8ull * (W + 1));
   L.tie = take(4ull * W);
   L.reptot = take(8ull * R);
+  L.t_boff = take(4ull * (M + 1));  // topology tables, staged once (read by every phase)
+  L.t_branks = take(4ull * U);
+  L.t_bsize = take(4ull * M);
+  L.t_rbag = take(4ull * U);
+  L.t_rmem = take(4ull * U);
+  L.pergpu = take(8ull * W);  // per-GPU workload: the greedy writes it, WIR reads it
+  L.recvoff = take(8ull * W);
   L.total = o;
   return L;
 }
@@ -123,15 +130,16 @@ __device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, 
                       viol_out);
 }
 
-__global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int cap) {
+__global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int64_t sh[33];
   __shared__ int s_flag, s_viol, s_biglen;
   __shared__ int warp_cnt[32][kMaxBags];
   __shared__ int running[kMaxBags];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  PlanArgs a = a_in;  // topology tables and per_gpu redirected to shared memory after phase 0
   const int W = a.W, R = a.R, M = a.M, U = a.U;
-  const SmallLayout L = small_layout(cap, W, R * M, R);
+  const SmallLayout L = small_layout(cap, W, R * M, R, U, M);
   uint64_t* s_ids = reinterpret_cast<uint64_t*>(sm + L.ids);
   int64_t* s_lens = reinterpret_cast<int64_t*>(sm + L.lens);
   double* s_w = reinterpret_cast<double*>(sm + L.w);
@@ -156,8 +164,28 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   double* s_reptot = reinterpret_cast<double*>(sm + L.reptot);
 
   SB_PHASE(0);
-  // ---- phase 0: rank offsets, capacity
+  // ---- phase 0: rank offsets, capacity, topology tables
   for (int r = tid; r <= W; r += blockDim.x) s_roff[r] = a.rank_off[r];
+  {
+    int32_t* t_boff = reinterpret_cast<int32_t*>(sm + L.t_boff);
+    int32_t* t_branks = reinterpret_cast<int32_t*>(sm + L.t_branks);
+    int32_t* t_bsize = reinterpret_cast<int32_t*>(sm + L.t_bsize);
+    int32_t* t_rbag = reinterpret_cast<int32_t*>(sm + L.t_rbag);
+    int32_t* t_rmem = reinterpret_cast<int32_t*>(sm + L.t_rmem);
+    for (int i = tid; i <= M; i += blockDim.x) t_boff[i] = a.bag_off[i];
+    for (int i = tid; i < M; i += blockDim.x) t_bsize[i] = a.bag_size[i];
+    for (int i = tid; i < U; i += blockDim.x) {
+      t_branks[i] = a.bag_ranks[i];
+      t_rbag[i] = a.rank_bag[i];
+      t_rmem[i] = a.rank_member[i];
+    }
+    a.bag_off = t_boff;
+    a.bag_ranks = t_branks;
+    a.bag_size = t_bsize;
+    a.rank_bag = t_rbag;
+    a.rank_member = t_rmem;
+    a.per_gpu = reinterpret_cast<double*>(sm + L.pergpu);
+  }
   if (tid == 0) {
     s_flag = 0;
     s_viol = 0;
@@ -375,24 +403,31 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   }
   __syncthreads();
   SB_PHASE(7);
-  // ---- phase 7: chunk bases of every (replica, bag)
-  if (tid == 0) {
-    int64_t cb = 0;
-    int q = 0;
-    for (int rep = 0; rep < R; ++rep) {
-      int64_t rc = 0;
-      for (int b = 0; b < M; ++b) {
-        s_bagcb[rep * M + b] = cb;
-        s_bagq[rep * M + b] = q;
-        const int64_t c = (int64_t)s_bagcnt[rep * M + b] * a.bag_size[b];
-        cb += c;
-        rc += c;
-        q += s_bagcnt[rep * M + b];
+  // ---- phase 7: chunk bases of every (replica, bag): warp 0 scans the
+  // (replica, bag) counts 32 at a time
+  if (warp == 0) {
+    int64_t cb = 0, q = 0;
+    for (int x0 = 0; x0 < R * M; x0 += 32) {
+      const int x = x0 + lane;
+      const int64_t n = x < R * M ? s_bagcnt[x] : 0;
+      const int64_t c = x < R * M ? n * a.bag_size[x % M] : 0;
+      const int64_t ic = warp_incl_scan<int64_t>(c), iq = warp_incl_scan<int64_t>(n);
+      if (x < R * M) {
+        s_bagcb[x] = cb + ic - c;
+        s_bagq[x] = (int32_t)(q + iq - n);
       }
-      a.rep_chunks[rep] = rc;
+      cb += __shfl_sync(0xffffffffu, ic, 31);
+      q += __shfl_sync(0xffffffffu, iq, 31);
     }
-    *a.n_chunks = cb;
-    *a.violations = s_viol;
+    __syncwarp();
+    for (int rep = lane; rep < R; rep += 32) {
+      const int64_t e = rep + 1 < R ? s_bagcb[(rep + 1) * M] : cb;
+      a.rep_chunks[rep] = e - s_bagcb[rep * M];
+    }
+    if (lane == 0) {
+      *a.n_chunks = cb;
+      *a.violations = s_viol;
+    }
   }
   __syncthreads();
   SB_PHASE(8);
@@ -403,7 +438,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
     for (int b = tid; b < M; b += blockDim.x) running[b] = 0;
     __syncthreads();
     for (int64_t tile = lo; tile < hi; tile += blockDim.x) {
-      for (int e = tid; e < 32 * M; e += blockDim.x) warp_cnt[e / M][e % M] = 0;
+      for (int e = tid; e < nw * M; e += blockDim.x) warp_cnt[e / M][e % M] = 0;
       __syncthreads();
       const int64_t p = tile + tid;
       const bool valid = p < hi;
@@ -412,14 +447,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
       const int rank_in = __popc(peers & lt_mask);
       if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
       __syncthreads();
-      if (tid < M) {
-        int run = running[tid];
-        for (int w2 = 0; w2 < 32; ++w2) {
-          const int c = warp_cnt[w2][tid];
-          warp_cnt[w2][tid] = run;
-          run += c;
-        }
-        running[tid] = run;
+      for (int b2 = warp; b2 < M; b2 += nw) {  // warp b2 scans bag b2's per-warp counts
+        const int c = lane < nw ? warp_cnt[lane][b2] : 0;
+        const int inc = warp_incl_scan<int>(c);
+        const int run = running[b2];
+        __syncwarp();
+        if (lane < nw) warp_cnt[lane][b2] = run + inc - c;
+        if (lane == 31) running[b2] = run + inc;
       }
       __syncthreads();
       if (valid) {
@@ -472,19 +506,29 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   }
   __syncthreads();
   SB_PHASE(9);
-  // ---- phase 9: manifest offsets (balancer.cpp:84-91)
-  if (tid == 0) {
+  // ---- phase 9: manifest offsets (balancer.cpp:84-91), warp 0 scans 32
+  // ranks at a time
+  if (warp == 0) {
     int64_t so = 0, ro = 0;
-    for (int r = 0; r < W; ++r) {
-      s_sendoff[r] = so;
-      a.send_off[r] = so;
-      a.recv_off[r] = ro;
-      so += s_sendcnt[r];
-      ro += s_bagcnt[(r / U) * M + a.rank_bag[r % U]];
+    for (int r0 = 0; r0 < W; r0 += 32) {
+      const int r = r0 + lane;
+      const int64_t sc = r < W ? s_sendcnt[r] : 0;
+      const int64_t rc = r < W ? (int64_t)s_bagcnt[(r / U) * M + a.rank_bag[r % U]] : 0;
+      const int64_t is = warp_incl_scan<int64_t>(sc), ir = warp_incl_scan<int64_t>(rc);
+      if (r < W) {
+        s_sendoff[r] = so + is - sc;
+        a.send_off[r] = so + is - sc;
+        a.recv_off[r] = ro + ir - rc;
+        reinterpret_cast<int64_t*>(sm + L.recvoff)[r] = ro + ir - rc;
+      }
+      so += __shfl_sync(0xffffffffu, is, 31);
+      ro += __shfl_sync(0xffffffffu, ir, 31);
     }
-    s_sendoff[W] = so;
-    a.send_off[W] = so;
-    a.recv_off[W] = ro;
+    if (lane == 0) {
+      s_sendoff[W] = so;
+      a.send_off[W] = so;
+      a.recv_off[W] = ro;
+    }
   }
   __syncthreads();
   SB_PHASE(10);
@@ -494,8 +538,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
     const int b = a.rank_bag[u], k = a.rank_member[u], g = a.bag_size[b];
     const int nb = s_bagcnt[rep * M + b];
     const int bq = s_bagq[rep * M + b];
-    int64_t ro = 0;
-    for (int x = 0; x < r; ++x) ro += s_bagcnt[(x / U) * M + a.rank_bag[x % U]];
+    const int64_t ro = reinterpret_cast<const int64_t*>(sm + L.recvoff)[r];
     // recv list + receive-side rows (target packing, balancer.cpp:93-101)
     int64_t carry = 0, carry2 = 0;
     for (int q0 = 0; q0 < nb; q0 += 32) {
@@ -561,6 +604,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a, int ca
   SB_PHASE(12);
   // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
   __syncthreads();
+  for (int r = tid; r < W; r += blockDim.x) a_in.per_gpu[r] = a.per_gpu[r];
   if (warp == 0) {  // min and max are order-independent (no NaN): one warp, loads in parallel
     double lo = a.per_gpu[0], hi = lo;
     for (int r = lane; r < W; r += 32) {

@@ -240,6 +240,31 @@ def test_random_plans_vs_oracle(topo, path):
         assert hp.rev_recv == rev.recv
 
 
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4"])
+def test_large_path_reused_planner_shrinking_batches(topo):
+    """One planner, multi-kernel path, a batch whose busiest bag receives more
+    than one list tile (kListTile = 1024 sequences) followed by smaller
+    batches: per-tile sums of tiles that are empty in the later plans must
+    not leak into target_rows / the Ulysses bases (compute-sanitizer
+    initcheck found k_lists reading never-written tiles)."""
+    W = 8
+    planner = sb.Planner(topo, W, max_seqs=W * 1400)
+    planner.set_path("large")
+    rng = np.random.default_rng(5)
+    for per_rank in (1400, 37, 700, 3):
+        lens = [rng.integers(1, 3000, size=per_rank).tolist() for _ in range(W)]
+        meta = oracle.meta_explicit(lens)
+        planner.plan(device_meta(meta))
+        hp = planner.download()
+        plan, rep = oracle.plan_routing(meta, oracle.parse_topology(topo))
+        got = host_plan_as_oracle(hp, meta)
+        assert got.chunk_rows() == plan.chunk_rows()
+        assert got.send == plan.send and got.recv == plan.recv
+        want_rows = [sum(sg[2] for sg in plan.target[r]) for r in range(W)]
+        assert hp.target_rows.tolist() == want_rows, per_rank
+        assert hp.rev_recv == oracle.reverse_plan(plan).recv
+
+
 @pytest.mark.parametrize("topo", ["g8n1", "g2n4", "g4n1+g2n1+g1n2"])
 def test_plans_beyond_shared_staging_vs_oracle(topo):
     """More sequences than the serial-sum kernels stage in shared memory

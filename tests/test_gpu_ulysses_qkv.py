@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_2508_06001_b200 import multigpu
 
 pytestmark = pytest.mark.gpu
 
@@ -164,6 +165,8 @@ def test_layout_plan_matches_exchange_layouts():
     mk = lambda: sb.World(W, HEADS, [192, 384], capacity_rows=rows, aux_row_bytes=[16], max_bag=4)
     A, B, C, L = mk(), mk(), mk(), mk()
     A.layout_origin(dm)
+    for t in range(A.T):  # defined bytes (compute-sanitizer initcheck), though only layouts are checked
+        multigpu.device_bytes(*A.arena(t)).zero_()
     sb.route(planner, A, B)
     sb.pre_attn(planner, B, C)
     for which, ref in ((sb.World.TARGET, B), (sb.World.ULYSSES, C), (sb.World.ORIGIN, A)):
