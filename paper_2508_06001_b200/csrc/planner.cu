@@ -553,7 +553,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     cap[i] = __dmul_rn((double)size, target);  // balancer.cpp:30
     rcap[i] = cap[i] > 0.0 ? __drcp_rn(cap[i]) : 0.0;
     asg[i] = 0.0;
-    occ[i] = occupancy(0.0, cap[i]);
+    occ[i] = 0.0;  // occupancy(0, cap): +0 for cap > 0 and for cap == 0 (balancer.cpp:32-35)
     rem[i] = __dsub_rn(cap[i], 0.0);
     key[i] = j < a.M ? greedy_key(rem[i] >= w_a, occ[i]) : ~0ull;
     cnt[i] = 0;

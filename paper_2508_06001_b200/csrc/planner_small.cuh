@@ -172,12 +172,20 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     int32_t* t_bsize = reinterpret_cast<int32_t*>(sm + L.t_bsize);
     int32_t* t_rbag = reinterpret_cast<int32_t*>(sm + L.t_rbag);
     int32_t* t_rmem = reinterpret_cast<int32_t*>(sm + L.t_rmem);
-    for (int i = tid; i <= M; i += blockDim.x) t_boff[i] = a.bag_off[i];
-    for (int i = tid; i < M; i += blockDim.x) t_bsize[i] = a.bag_size[i];
-    for (int i = tid; i < U; i += blockDim.x) {
-      t_branks[i] = a.bag_ranks[i];
-      t_rbag[i] = a.rank_bag[i];
-      t_rmem[i] = a.rank_member[i];
+    // all loads first, then the shared stores (a generic source pointer may
+    // alias shared memory, so interleaving would serialise the round trips)
+    for (int i0 = 0; i0 <= (M > U ? M : U); i0 += blockDim.x) {
+      const int i = i0 + tid;
+      const int32_t bo = i <= M ? a.bag_off[i] : 0, bs = i < M ? a.bag_size[i] : 0;
+      const int32_t br = i < U ? a.bag_ranks[i] : 0, rb = i < U ? a.rank_bag[i] : 0,
+                    rm = i < U ? a.rank_member[i] : 0;
+      if (i <= M) t_boff[i] = bo;
+      if (i < M) t_bsize[i] = bs;
+      if (i < U) {
+        t_branks[i] = br;
+        t_rbag[i] = rb;
+        t_rmem[i] = rm;
+      }
     }
     a.bag_off = t_boff;
     a.bag_ranks = t_branks;
