@@ -708,7 +708,9 @@ def run_single(args, cfg, topology):
         if dit:
             assert Qu.checksum() == A.checksum(), f"{what}: pre_attn(q) does not conserve content_checksum"
 
-    side = torch.cuda.Stream()
+    # high priority: the one-CTA plan / prepare kernels get SMs as soon as a
+    # wave of the copy kernel's CTAs retires instead of after its tail
+    side = torch.cuda.Stream(priority=-1)
     evs = [torch.cuda.Event() for _ in range(len(ops) + 1)]
 
     def prepare_all(pl, st, evl=None):

@@ -87,85 +87,105 @@ struct LayoutPlan {
 // multi-GPU bags).  A mismatch raises ST_MISMATCH on the destination and the
 // job builders then emit empty jobs, so a stale or foreign world is reported
 // as IntegrityError by sb_world_status instead of being read out of bounds.
-__device__ bool source_matches_plan(const WorldArgs& s, const LayoutPlan& lp, int mode) {
-  for (int r = s.first_local; r < s.first_local + s.n_local; ++r) {
-    int64_t want;
-    if (mode == 0) {
-      want = lp.expect_rows[r];
-    } else {
-      const int u = r % lp.U, rep = r / lp.U;
-      const int b = lp.rank_bag[u];
-      want = (mode == 2 && lp.bag_size[b] > 1) ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
-    }
-    if (s.rows[r] != want) return false;
+__device__ __forceinline__ bool rank_matches_plan(const WorldArgs& s, const LayoutPlan& lp, int mode, int r) {
+  int64_t want;
+  if (mode == 0) {
+    want = lp.expect_rows[r];
+  } else {
+    const int u = r % lp.U, rep = r / lp.U;
+    const int b = lp.rank_bag[u];
+    want = (mode == 2 && lp.bag_size[b] > 1) ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
   }
-  return true;
+  return s.rows[r] == want;
 }
 
+// Layout of tensor t, computed by ONE WARP (lane = rank, 32 ranks at a time):
+// rows and pitch per rank by mode, then each rank's byte offset inside its
+// owner process's arena by a segmented exclusive scan (owners hold
+// contiguous blocks of n_local ranks; a segment restarts at every owner's
+// first rank).  Aliased ranks (one-GPU bags under pre/post_attn) take the
+// source's tables and no arena bytes.  All per-rank loads are independent
+// across lanes, so the layout costs a few memory round trips instead of a
+// dependent chain over the world's ranks.
 __device__ void layout_tensor(const WorldArgs& d, const WorldArgs& s, const LayoutPlan& lp, const TensorInfo& ti,
                               int mode, int t) {
   if (t >= d.T) return;
+  const int lane = threadIdx.x & 31;
   if (t == 0 && !lp.no_check) {  // the status reflects the latest exchange into d
-    if (source_matches_plan(s, lp, mode)) atomicAnd(d.status, ~ST_MISMATCH);
-    else atomicOr(d.status, ST_MISMATCH);
-  }
-  int owner = -1;
-  int64_t off = 0;
-  for (int r = 0; r < d.W; ++r) {
-    const int o = r / d.n_local;
-    if (o != owner) {
-      owner = o;
-      off = 0;
+    bool bad = false;
+    for (int r = s.first_local + lane; r < s.first_local + s.n_local; r += 32) bad |= !rank_matches_plan(s, lp, mode, r);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (bad) atomicOr(d.status, ST_MISMATCH);
+      else atomicAnd(d.status, ~ST_MISMATCH);
     }
-    int g = 1, k = 0;
-    int64_t rows;
-    if (mode == 0) {
-      rows = lp.rows_src[r];
-    } else {
-      const int u = r % lp.U, rep = r / lp.U;
-      const int b = lp.rank_bag[u];
-      g = lp.bag_size[b];
-      k = lp.rank_member[u];
-      if (g == 1 && mode == 3) {  // standalone Ulysses layout: one-GPU bags keep their chunk rows
-        const int64_t rows1 = lp.target_rows[r];
-        const int64_t pitch1 = ti.row_bytes[t];
-        d.base[t * d.W + r] = d.peer_arena[t * d.n_procs + owner] + (uint64_t)off;
-        d.pitch[t * d.W + r] = pitch1;
-        off += rows1 * pitch1;
-        if (off > d.arena_bytes[t]) atomicOr(d.status, ST_LAYOUT);
-        if (t == 0) {
-          d.rows[r] = rows1;
-          d.headcol[r] = 0;
+  }
+  int64_t carry = 0;
+  bool overflow = false;
+  for (int r0 = 0; r0 < d.W; r0 += 32) {
+    const int r = r0 + lane;
+    const bool valid = r < d.W;
+    int64_t rows = 0, pitch = ti.row_bytes[t];
+    int32_t headcol = 0;
+    bool alias = false;
+    if (valid) {
+      if (mode == 0) {
+        rows = lp.rows_src[r];
+      } else {
+        const int u = r % lp.U, rep = r / lp.U;
+        const int b = lp.rank_bag[u];
+        const int g = lp.bag_size[b];
+        if (g == 1 && mode == 3) {  // standalone Ulysses layout: one-GPU bags keep their chunk rows
+          rows = lp.target_rows[r];
+        } else if (g == 1) {  // alias the source world's buffers (pre/post are no-ops)
+          alias = true;
+        } else {
+          const bool sliced = mode == 1 || mode == 3;
+          rows = sliced ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
+          if (sliced && ti.kind[t] == 1) pitch = ti.row_bytes[t] / g;
+          if (sliced) headcol = (int32_t)(lp.rank_member[u] * (ti.row_bytes[1] / 8 / g));
         }
-        continue;
       }
-      if (g == 1) {  // alias the source world's buffers (pre/post are no-ops)
+    }
+    const int64_t bytes = valid && !alias ? rows * pitch : 0;
+    bool f = valid && r % d.n_local == 0;  // segment head: first rank of an owner
+    int64_t x = bytes;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan
+      const int64_t nx = __shfl_up_sync(0xffffffffu, x, o);
+      const bool nf = __shfl_up_sync(0xffffffffu, f, o);
+      if (lane >= o && !f) {
+        x += nx;
+        f = nf;
+      }
+    }
+    const int64_t incl = f ? x : x + carry;
+    if (valid) {
+      if (alias) {
         d.base[t * d.W + r] = s.base[t * s.W + r];
         d.pitch[t * d.W + r] = s.pitch[t * s.W + r];
         if (t == 0) {
           d.rows[r] = s.rows[r];
           d.headcol[r] = s.headcol[r];
         }
-        continue;
+      } else {
+        const int owner = r / d.n_local;
+        d.base[t * d.W + r] = d.peer_arena[t * d.n_procs + owner] + (uint64_t)(incl - bytes);
+        d.pitch[t * d.W + r] = pitch;
+        overflow |= incl > d.arena_bytes[t];
+        if (t == 0) {
+          d.rows[r] = rows;
+          d.headcol[r] = headcol;
+        }
       }
-      rows = (mode == 1 || mode == 3) ? lp.bag_rows[rep * lp.M + b] : lp.target_rows[r];
     }
-    const bool sliced = mode == 1 || mode == 3;
-    int64_t pitch = ti.row_bytes[t];
-    if (sliced && ti.kind[t] == 1) pitch = ti.row_bytes[t] / g;
-    d.base[t * d.W + r] = d.peer_arena[t * d.n_procs + owner] + (uint64_t)off;
-    d.pitch[t * d.W + r] = pitch;
-    off += rows * pitch;
-    if (off > d.arena_bytes[t]) atomicOr(d.status, ST_LAYOUT);
-    if (t == 0) {
-      d.rows[r] = rows;
-      d.headcol[r] = sliced ? (int32_t)(k * (ti.row_bytes[1] / 8 / g)) : 0;
-    }
+    carry = __shfl_sync(0xffffffffu, incl, 31);
   }
+  if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(d.status, ST_LAYOUT);
 }
 
 __global__ void k_layout(WorldArgs d, WorldArgs s, LayoutPlan lp, TensorInfo ti, int mode) {
-  layout_tensor(d, s, lp, ti, mode, threadIdx.x);
+  layout_tensor(d, s, lp, ti, mode, threadIdx.x >> 5);  // one warp per tensor
 }
 
 // ----------------------------------------------------------- job builders
@@ -348,7 +368,7 @@ __global__ void __launch_bounds__(1024) k_exchange_prep(JobArgs j, WorldArgs s, 
                                                         LayoutPlan lp, int op, int64_t* piece_off,
                                                         int64_t* bytes_moved) {
   const int mode = op < 2 ? 0 : (op == 2 ? 1 : 2);
-  layout_tensor(d, s, lp, ti, mode, threadIdx.x);
+  layout_tensor(d, s, lp, ti, mode, threadIdx.x >> 5);
   __syncthreads();
   const int64_t n = op < 2 ? *j.n_chunks * s.T : *j.n_chunks * j.max_bag * s.T;
   if (threadIdx.x == 0) *j.n_jobs = n;
@@ -1197,7 +1217,7 @@ extern "C" sb_status sb_world_layout_origin(sb_world* w, const int64_t* d_lens, 
   lp.rows_src = w->d_rows;
   lp.expect_rows = w->d_rows;
   sb::WorldArgs a = sb::wargs(w);
-  sb::k_layout<<<1, 32, 0, s>>>(a, a, lp, sb::tinfo(w), 0);
+  sb::k_layout<<<1, 32 * 16, 0, s>>>(a, a, lp, sb::tinfo(w), 0);
   SB_CHECK_LAUNCH();
   sb::count_launch(2);
   SB_API_END
@@ -1237,7 +1257,7 @@ extern "C" sb_status sb_world_layout_plan(sb_world* w, const sb_planner* p, int 
     mode = 3;
   }
   sb::WorldArgs a = sb::wargs(w);
-  sb::k_layout<<<1, 32, 0, (cudaStream_t)stream>>>(a, a, lp, sb::tinfo(w), mode);
+  sb::k_layout<<<1, 32 * 16, 0, (cudaStream_t)stream>>>(a, a, lp, sb::tinfo(w), mode);
   SB_CHECK_LAUNCH();
   sb::count_launch();
   SB_API_END
@@ -1321,7 +1341,7 @@ static void prepare_route(sb_planner* p, int slot, int reverse, sb_world* src, s
     SB_CHECK_LAUNCH();
     sb::count_launch(1);
   } else {
-    sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
+    sb::k_layout<<<1, 32 * 16, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), 0);
     SB_CHECK_LAUNCH();
     sb::k_jobs_route<<<std::min<int64_t>(1184, (p->max_chunks * src->T + 255) / 256), 256, 0, s>>>(
         sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), reverse);
@@ -1368,7 +1388,7 @@ static void prepare_ulysses(sb_planner* p, int slot, int post, sb_world* src, sb
     SB_CHECK_LAUNCH();
     sb::count_launch(1);
   } else {
-    sb::k_layout<<<1, 32, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), post ? 2 : 1);
+    sb::k_layout<<<1, 32 * 16, 0, s>>>(sb::wargs(dst), sb::wargs(src), lp, sb::tinfo(dst), post ? 2 : 1);
     SB_CHECK_LAUNCH();
     sb::k_jobs_ulysses<<<std::min<int64_t>(1184, (total + 255) / 256), 256, 0, s>>>(
         sb::jargs(p), sb::wargs(src), sb::wargs(dst), sb::tinfo(src), post);
@@ -2036,7 +2056,7 @@ __global__ void __launch_bounds__(1024) k_uniform_prep(const int64_t* counts, co
   LayoutPlan lp{};
   lp.rows_src = rows;
   lp.expect_rows = rows + W;
-  layout_tensor(d, s, lp, ti, 0, threadIdx.x);
+  layout_tensor(d, s, lp, ti, 0, threadIdx.x >> 5);
   __syncthreads();
   const int T = s.T;
   const int64_t total = (int64_t)3 * W * T;

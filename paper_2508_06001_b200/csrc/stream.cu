@@ -645,7 +645,9 @@ extern "C" sb_status sb_driver_create(sb_planner* p, const sb_schedule* s, int n
     SB_CUDA(cudaMalloc(&d->d_acc, sizeof(uint64_t) * 5));
     SB_CUDA(cudaMalloc(&d->d_rec, sizeof(sb_step_record) * (size_t)d->rec_cap));
     SB_CUDA(cudaMemset(d->d_rec, 0, sizeof(sb_step_record) * (size_t)d->rec_cap));
-    SB_CUDA(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
+    int least = 0, greatest = 0;  // high priority: plan / prepare kernels jump the copy kernel's later waves
+    SB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SB_CUDA(cudaStreamCreateWithPriority(&d->side, cudaStreamNonBlocking, greatest));
     for (auto& e : d->ev) SB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   } catch (...) {
     sb_driver_destroy(d);

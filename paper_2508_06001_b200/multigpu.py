@@ -385,7 +385,20 @@ def dit_phases(A, B, Q, Qu, O, Oc, E):
             ("reverse_route", reverse_route, Oc, E, None)]
 
 
-def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=None, marks=None, transport=None):
+_SIDE = {}
+
+
+def _side_stream():
+    """One side stream per device for the exchange preparations."""
+    import torch
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream(priority=-1)  # preparations jump the copy kernel's later waves
+    return _SIDE[dev]
+
+
+def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=None, marks=None, transport=None,
+         overlap_prep: bool = True):
     """One pass of the hot path on every process (all phases peer-closed).
 
     Every exchange writes straight into its destination process's arena and
@@ -396,7 +409,11 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=
     phase, end recorded after the closing barrier (includes barrier skew).
     `transport`: a CollectiveTransport -- each exchange is pack, all-to-all-v,
     unpack (the collective closes the phase; no barrier), and `gather` must
-    have been built with the same transport."""
+    have been built with the same transport.
+    `overlap_prep` (peer path): every phase's preparation (destination layout
+    + copy jobs, one CTA each) runs on a side stream right after the plan, so
+    phase i's copy waits only for its own preparation and phase i-1's
+    barrier; preparations read the plan and world tables, never payload."""
     torch = group.torch
     s = stream if stream is not None else torch.cuda.current_stream()
     ev = {}
@@ -415,16 +432,38 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=
     mark("plan", 0)
     planner.plan(meta, s)
     mark("plan", 1)
-    for name, fn, src, dst, pre in phases:
-        mark(name, 0)
-        if pre is not None:
-            pre(planner, s)
-        if transport is None:
-            fn(planner, src, dst, s)
+    if transport is None and overlap_prep:
+        torch = group.torch
+        side = _side_stream()
+        fork = torch.cuda.Event()
+        fork.record(s)
+        side.wait_event(fork)
+        ready = []
+        with torch.cuda.stream(side):
+            for name, fn, src, dst, pre in phases:
+                if pre is not None:
+                    pre(planner, side)
+                planner.prepare(OPS[name], src, dst, OPS[name], side)
+                e = torch.cuda.Event()
+                e.record(side)
+                ready.append(e)
+        for (name, fn, src, dst, pre), e in zip(phases, ready):
+            mark(name, 0)
+            s.wait_event(e)
+            planner.run(OPS[name], s)
             group.barrier(s)
-        else:
-            transport.exchange(planner, name, src, dst, s)
-        mark(name, 1)
+            mark(name, 1)
+    else:
+        for name, fn, src, dst, pre in phases:
+            mark(name, 0)
+            if pre is not None:
+                pre(planner, s)
+            if transport is None:
+                fn(planner, src, dst, s)
+                group.barrier(s)
+            else:
+                transport.exchange(planner, name, src, dst, s)
+            mark(name, 1)
     if marks is not None:
         marks.extend((k, v[0], v[1]) for k, v in ev.items())
     return meta
