@@ -118,14 +118,27 @@ class PeerGroup:
         self.mode = ("host" if self.same_device else "device") if barrier_mode == "auto" else barrier_mode
         self._opened = []
         self._barrier = None
+        self._extra = []
         if self.mode == "device":
-            h = C.c_void_p()
-            call("sb_barrier_create", self.size, self.rank, C.byref(h))
-            self._barrier = h
-            buf, nb = C.c_void_p(), C.c_int64()
-            call("sb_barrier_buffer", h, C.byref(buf), C.byref(nb))
-            peers = np.asarray(self.share(buf.value), np.uint64)
-            call("sb_barrier_set_peers", h, peers.ctypes.data, self.size)
+            self._barrier = self._new_device_barrier()
+
+    def _new_device_barrier(self):
+        h = C.c_void_p()
+        call("sb_barrier_create", self.size, self.rank, C.byref(h))
+        buf, nb = C.c_void_p(), C.c_int64()
+        call("sb_barrier_buffer", h, C.byref(buf), C.byref(nb))
+        peers = np.asarray(self.share(buf.value), np.uint64)
+        call("sb_barrier_set_peers", h, peers.ctypes.data, self.size)
+        return h
+
+    def make_barrier(self) -> "DeviceBarrier":
+        """An independent device barrier (own flags and epoch), for a second
+        stream that closes its own phases concurrently with the main one."""
+        if self.mode != "device":
+            raise _capi.ConfigError("an extra stream barrier needs device barriers")
+        b = DeviceBarrier(self, self._new_device_barrier())
+        self._extra.append(b)
+        return b
 
     def all_gather_object(self, obj):
         out = [None] * self.size
@@ -183,12 +196,32 @@ class PeerGroup:
         return int(np.int64(t.item()).astype(np.uint64))
 
     def close(self):
+        for b in self._extra:
+            _capi.load().sb_barrier_destroy(b.handle)
+        self._extra = []
         for p in self._opened:
             _capi.load().sb_ipc_close(C.c_void_p(p))
         self._opened = []
         if self._barrier is not None:
             _capi.load().sb_barrier_destroy(self._barrier)
             self._barrier = None
+
+
+class DeviceBarrier:
+    """A second device barrier of a PeerGroup (see PeerGroup.make_barrier)."""
+
+    def __init__(self, group: PeerGroup, handle):
+        self.group, self.handle = group, handle
+
+    def barrier(self, stream=None):
+        s = stream if stream is not None else self.group.torch.cuda.current_stream()
+        call("sb_barrier_wait", self.handle, C.c_void_p(s.cuda_stream))
+
+    def status(self, stream=None) -> int:
+        s = stream if stream is not None else self.group.torch.cuda.current_stream()
+        e = C.c_uint64()
+        call("sb_barrier_status", self.handle, C.byref(e), C.c_void_p(s.cuda_stream))
+        return int(e.value)
 
 
 def device_bytes(ptr: int, nbytes: int):
@@ -341,14 +374,16 @@ class MetaGather:
             self.local_lens[:n].copy_(torch.from_numpy(lens.copy()))
         self.local_off.copy_(torch.from_numpy(off))
 
-    def gather(self, stream=None) -> DeviceMeta:
+    def gather(self, stream=None, barrier=None) -> DeviceMeta:
+        """Push, close (the group's barrier, or `barrier` -- a DeviceBarrier
+        for a gather on a second stream), compact."""
         torch = self.group.torch
         s = stream if stream is not None else torch.cuda.current_stream()
         sp = C.c_void_p(s.cuda_stream)
         call("sb_gather_push", self._h, C.c_void_p(self.local_ids.data_ptr()), C.c_void_p(self.local_lens.data_ptr()),
              C.c_void_p(self.local_off.data_ptr()), sp)
         if self.transport is None:
-            self.group.barrier(s)
+            (barrier or self.group).barrier(s)
         else:  # in-place all-gather of each section: this process owns slots [first, first + n_local)
             for sec, per_rank in self._sections:
                 lo = self.first * per_rank
@@ -467,6 +502,77 @@ def step(group: PeerGroup, gather: MetaGather, planner: Planner, phases, stream=
     if marks is not None:
         marks.extend((k, v[0], v[1]) for k, v in ev.items())
     return meta
+
+
+class PlanAhead:
+    """Two-batch pipeline of the multi-process step (device barriers only).
+
+    Batch k+1's metadata all-gather, plan and every exchange preparation run
+    on the high-priority side stream -- the gather closed by its own device
+    barrier -- while batch k's copies run on the main stream, each closed by
+    the group's barrier.  Two planners and two gather buffers alternate, so
+    batch k+1 never overwrites a plan, a prepared slot or gather slots that
+    batch k (here or on a peer) still reads: a process pushes batch k+1's
+    records only after the side barrier of batch k, which every peer reaches
+    after compacting batch k-1 from the same buffer.  `pair()` moves two
+    batches and is graph-capturable; `prime()` prepares batch 0 first.
+    Same schedule as the N = 1 headline (bench.py run_single)."""
+
+    def __init__(self, group: PeerGroup, gathers, planners, phases):
+        import torch
+        if len(gathers) != 2 or len(planners) != 2:
+            raise _capi.ConfigError("PlanAhead needs two gathers and two planners")
+        self.torch, self.group, self.gathers, self.planners, self.phases = torch, group, gathers, planners, phases
+        self.side = _side_stream()
+        self.side_barrier = group.make_barrier()
+        self.ready = [[torch.cuda.Event() for _ in phases] for _ in range(2)]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def _prepare(self, b):  # on the side stream
+        pl = self.planners[b]
+        meta = self.gathers[b].gather(self.side, barrier=self.side_barrier)
+        pl.plan(meta, self.side)
+        for (name, fn, src, dst, pre), e in zip(self.phases, self.ready[b]):
+            if pre is not None:
+                pre(pl, self.side)
+            pl.prepare(OPS[name], src, dst, OPS[name], self.side)
+            e.record(self.side)
+
+    def _run(self, b, s, wait=True):
+        pl = self.planners[b]
+        for (name, fn, src, dst, pre), e in zip(self.phases, self.ready[b]):
+            if wait:
+                s.wait_event(e)
+            pl.run(OPS[name], s)
+            self.group.barrier(s)
+        self.free[b].record(s)
+
+    def prime(self, stream=None):
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self.side.wait_stream(s)
+        with torch.cuda.stream(self.side):
+            self._prepare(0)
+        s.wait_stream(self.side)
+
+    def pair(self, stream=None):
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self.side.wait_stream(s)
+        with torch.cuda.stream(self.side):
+            self._prepare(1)  # batch k+1 under batch k's copies
+        # batch 0 was prepared before this pair began (prime(), or the join
+        # that ends the previous pair), so its copies need no event wait --
+        # which also keeps a captured pair free of waits on uncaptured work
+        self._run(0, s, wait=False)
+        self.side.wait_event(self.free[0])
+        with torch.cuda.stream(self.side):
+            self._prepare(0)  # batch k+2 under batch k+1's copies
+        self._run(1, s)
+        s.wait_stream(self.side)
+
+    def status(self):
+        self.side_barrier.status(self.side)
 
 
 def _a2a_roofline(busiest: int, route_us: float, same_device: bool) -> dict:
@@ -632,6 +738,47 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
                 ms, mode, clk, launches = ms_graph, "cuda_graph", clk_g, per_step * args.steps
         except Exception as e:  # graph capture is an optimisation; eager numbers stand
             graph_err = f"{type(e).__name__}: {e}"
+    # plan-ahead (the N = 1 headline's schedule): batch k+1 gathered, planned
+    # and prepared on the side stream under batch k's copies; two-batch graph
+    ms_pipe, pipe_err = None, None
+    if group.mode == "device" and os.environ.get("SEQBAL_NO_PIPE") != "1":
+        try:
+            gather2 = MetaGather(group, W, cap)
+            gather2.set_local(all_ids[first:first + n_local], all_lens[first:first + n_local])
+            planner2 = Planner(topology, W, max_seqs=max(1, W * cap))
+            pipe = PlanAhead(group, [gather, gather2], [planner, planner2], phases)
+            torch.cuda.synchronize()
+            for w in (B, E):  # the pipeline must rebuild them (the check is not vacuous)
+                for t in range(w.T):
+                    device_bytes(*w.arena(t)).zero_()
+            torch.cuda.synchronize()
+            group.barrier()
+            pipe.prime()
+            for _ in range(2):  # eager warm-up: allocates planner2's slots outside the capture
+                pipe.pair()
+            torch.cuda.synchronize()
+            gp = torch.cuda.CUDAGraph()
+            group.barrier()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gp):
+                pipe.pair()
+            l0 = _capi.load().sb_kernel_launches()
+            pipe.pair()
+            per_pair = _capi.load().sb_kernel_launches() - l0
+            for _ in range(2):
+                gp.replay()
+            torch.cuda.synchronize()
+            pairs = max(1, args.steps // 2)
+            ms_pair, _, clk_p = timed(gp.replay, pairs)
+            ms_pipe = ms_pair / 2
+            pipe.status()
+            check("plan-ahead graph")
+            if group.sum_u64(B.checksum()) != group.sum_u64(A.checksum()):
+                raise AssertionError("plan-ahead: route does not conserve content_checksum")
+            if ms_pipe < ms:
+                ms, mode, clk, launches = ms_pipe, "cuda_graph+plan_ahead", clk_p, per_pair * pairs
+        except Exception as e:  # the serial step's numbers stand
+            pipe_err = f"{type(e).__name__}: {e}"
 
     # tensors each phase moves: x (hidden + RoPE) for route; q,k,v + RoPE for
     # pre_attn and o for post_attn / reverse_route in the DiT pattern
@@ -754,6 +901,7 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
                    "l2": "inputs larger than L2" if tokens * payload > 126e6 * group.size else
                          "per-process arenas may fit L2 (strong scaling of one batch)"},
         "launch_mode": mode, "ms_per_step_eager": ms_eager, "ms_per_step_graph": ms_graph, "graph_error": graph_err,
+        "ms_per_step_plan_ahead": ms_pipe, "pipeline_error": pipe_err,
         "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0, "wir": hp.wir,
         "phases": phase_out,
         "transports": dict({"peer": {"ms_per_step": ms, "phases": phase_out}}, **coll_out),

@@ -164,7 +164,7 @@ def test_two_process_push_decomposition_gloo(topo):
     assert res == {0: True, 1: True}, res
 
 
-def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1, transport=None):
+def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1, transport=None, pipeline=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SEQBAL_BARRIER_TIMEOUT_MS="20000")
@@ -192,9 +192,19 @@ def _ipc_worker(rank, size, port, topo, q, barrier="auto", steps=1, transport=No
         A.layout_origin(dm)
         A.fill_witness(dm)
         group.barrier()
-        for _ in range(steps):
-            multigpu.step(group, gather, planner, multigpu.x_phases(A, B, Cw, D, E, planner.max_bag > 1),
-                          transport=tr)
+        phases = multigpu.x_phases(A, B, Cw, D, E, planner.max_bag > 1)
+        if pipeline:  # two batches in flight: gather/plan/prepare of k+1 under k's copies
+            gather2 = multigpu.MetaGather(group, W, 8)
+            gather2.set_local(meta.ids[first:first + n_local], meta.lens[first:first + n_local])
+            pipe = multigpu.PlanAhead(group, [gather, gather2], [planner, sb.Planner(topo, W, max_seqs=64)], phases)
+            pipe.prime()
+            for _ in range(steps):
+                pipe.pair()
+            torch.cuda.synchronize()
+            pipe.status()
+        else:
+            for _ in range(steps):
+                multigpu.step(group, gather, planner, phases, transport=tr)
         torch.cuda.synchronize()
         group.barrier_status()  # CommError if a device barrier timed out
         plan, _ = oracle.plan_routing(meta, oracle.parse_topology(topo))  # FLUX model, as the planner
@@ -348,6 +358,28 @@ def test_one_process_nccl_transport(topo):
     res = dict([q.get(timeout=300)])
     p.join(timeout=60)
     assert res == {0: True}, res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("topo", ["g1n8", "g2n4"])
+def test_two_processes_plan_ahead_pipeline(topo):
+    """multigpu.PlanAhead: batch k+1's all-gather (closed by a second device
+    barrier on the side stream), plan and preparations run under batch k's
+    copies, two planners and gather buffers alternating; three pairs of
+    steps between two processes on one GPU, results as the serial step's."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, topo, q, "device", 3, None, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
 
 
 def _barrier_timeout_worker(rank, size, port, q):
