@@ -484,10 +484,21 @@ __global__ void __launch_bounds__(1024) k_collective_split(SbJob* jobs, const in
 //  0: ld.global.nc.L1::no_allocate.L2::256B / st.global.L1::no_allocate
 //  1: ld.global.nc.L1::no_allocate          / st.global.L1::no_allocate
 //  2: ld.global.cs (evict-first)            / st.global.cs
+//  3: as 0, stores with an L2 evict_first policy
+//  4: loads with an L2 evict_first policy, stores as 0
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 template <int HINT>
 __device__ __forceinline__ int4 ld_stream(const void* p) {
   int4 r;
-  if (HINT == 0)
+  if (HINT == 4)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(l2_evict_first()));
+  else if (HINT == 0 || HINT == 3)
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
@@ -503,6 +514,10 @@ template <int HINT>
 __device__ __forceinline__ void st_stream(void* p, const int4& v) {
   if (HINT == 2)
     asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  else if (HINT == 3)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(l2_evict_first())
                  : "memory");
   else
     asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
@@ -676,6 +691,28 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint3
                "r"(bytes)
                : "memory");
 }
+// L2 eviction-priority variants of the bulk copies (SEQBAL_TMA_HINT bits:
+// 1 = stores evict_first, 2 = loads evict_first, 4 = stores evict_last,
+// 8 = loads evict_last); the policy word comes from createpolicy.
+__device__ __forceinline__ uint64_t l2_policy(int evict_last) {
+  uint64_t pol;
+  if (evict_last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* gdst, const void* smem_src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -715,7 +752,7 @@ __device__ __forceinline__ PieceRef piece_of(const SbJob& j, int64_t k) {
 }
 
 __global__ void __launch_bounds__(32) k_copy_tma(const SbJob* __restrict__ jobs, const int64_t* __restrict__ piece_off,
-                                                 const int64_t* __restrict__ n_jobs_p) {
+                                                 const int64_t* __restrict__ n_jobs_p, int hint) {
   extern __shared__ __align__(128) unsigned char stage_mem[];
   __shared__ __align__(8) uint64_t bars[kTmaStages];
   const int64_t n_jobs = *n_jobs_p;
@@ -730,19 +767,27 @@ __global__ void __launch_bounds__(32) k_copy_tma(const SbJob* __restrict__ jobs,
     if (piece_off[mid] <= g0) lo = mid;
     else hi = mid;
   }
+  const uint64_t spol = (hint & 5) ? l2_policy(hint & 4) : 0, lpol = (hint & 10) ? l2_policy(hint & 8) : 0;
   int64_t jl = lo, js = lo;  // job cursors of the load and the store streams
   auto load = [&](int64_t g, int s) {
     while (piece_off[jl + 1] <= g) ++jl;
     const PieceRef p = piece_of(jobs[jl], g - piece_off[jl]);
     char* sm = reinterpret_cast<char*>(stage_mem) + (size_t)s * kPieceBytes;
     mbar_expect_tx(&bars[s], (uint32_t)(p.rows * p.width));
-    for (int64_t r = 0; r < p.rows; ++r) bulk_g2s(sm + r * p.width, p.src + r * p.spitch, (uint32_t)p.width, &bars[s]);
+    if (lpol)
+      for (int64_t r = 0; r < p.rows; ++r)
+        bulk_g2s_hint(sm + r * p.width, p.src + r * p.spitch, (uint32_t)p.width, &bars[s], lpol);
+    else
+      for (int64_t r = 0; r < p.rows; ++r) bulk_g2s(sm + r * p.width, p.src + r * p.spitch, (uint32_t)p.width, &bars[s]);
   };
   auto store = [&](int64_t g, int s) {
     while (piece_off[js + 1] <= g) ++js;
     const PieceRef p = piece_of(jobs[js], g - piece_off[js]);
     const char* sm = reinterpret_cast<const char*>(stage_mem) + (size_t)s * kPieceBytes;
-    for (int64_t r = 0; r < p.rows; ++r) bulk_s2g(p.dst + r * p.dpitch, sm + r * p.width, (uint32_t)p.width);
+    if (spol)
+      for (int64_t r = 0; r < p.rows; ++r) bulk_s2g_hint(p.dst + r * p.dpitch, sm + r * p.width, (uint32_t)p.width, spol);
+    else
+      for (int64_t r = 0; r < p.rows; ++r) bulk_s2g(p.dst + r * p.dpitch, sm + r * p.width, (uint32_t)p.width);
     bulk_commit();
   };
   const int64_t n = g1 - g0;
@@ -1053,17 +1098,24 @@ static void launch_copy(SbJob* jobs, int64_t* piece_off, int64_t* n_jobs, cudaSt
       attr = true;
     }
     copy_grid();
-    k_copy_tma<<<g_num_sms * 2, 32, kTmaSmem, s>>>(jobs, piece_off, n_jobs);
+    static int tma_hint = -1;  // SEQBAL_TMA_HINT (see l2_policy)
+    if (tma_hint < 0) {
+      const char* v = getenv("SEQBAL_TMA_HINT");
+      tma_hint = v ? atoi(v) : 0;
+    }
+    k_copy_tma<<<g_num_sms * 2, 32, kTmaSmem, s>>>(jobs, piece_off, n_jobs, tma_hint);
   } else if (engine == 2) {
     k_copy<3><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
   } else {
-    static int hint = -1;  // SEQBAL_COPY_HINT=0|1|2 (see ld_stream)
+    static int hint = -1;  // SEQBAL_COPY_HINT=0..4 (see ld_stream)
     if (hint < 0) {
       const char* v = getenv("SEQBAL_COPY_HINT");
       hint = v ? atoi(v) : 0;
     }
     if (hint == 1) k_copy<1, 1><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
     else if (hint == 2) k_copy<1, 2><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
+    else if (hint == 3) k_copy<1, 3><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
+    else if (hint == 4) k_copy<1, 4><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
     else k_copy<1, 0><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
   }
   SB_CHECK_LAUNCH();
