@@ -771,10 +771,11 @@ def run_single(args, cfg, topology):
     tr = planner.trace(True)
     planner.trace(False)
     if tr[13] > tr[0] > 0:
-        pnames = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
-                  "rank_lists", "send", "wir"]
+        # phase marks 0..6 and the end mark 13 (planner_small.cuh)
+        pnames = ["load", "seq+totals+offsets", "sort", "greedy+dup", "emit+wir", "lists", "ties"]
+        marks = [int(x) for x in tr[:7]] + [int(tr[13])]
         plan_breakdown = {"path": "fused single-CTA", "total_cycles": int(tr[13] - tr[0]),
-                          "cycles": {k: int(v) for k, v in zip(pnames, np.diff(tr[:14]))}}
+                          "cycles": {k: marks[i + 1] - marks[i] for i, k in enumerate(pnames)}}
     # algorithmic bytes of each exchange (bytes read == bytes written), from the device
     op_bytes = {}
     prepare_all(planner, stream)
@@ -930,7 +931,8 @@ def run_single(args, cfg, topology):
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
-        if pj.get("config") == args.config and pj.get("pattern", "x") == args.pattern:
+        if (pj.get("config") == args.config and pj.get("pattern", "x") == args.pattern
+                and pj.get("dominant_op", "route") == dom):
             traffic = pj.get("dominant_dram_bytes", pj.get("route_copy_dram_bytes"))
     kernel_of = {"route": "k_copy (route)", "reverse_route": "k_copy (reverse_route)",
                  "pre_attn": "k_copy_tma / k_copy (pre_attn)", "post_attn": "k_copy_tma / k_copy (post_attn)"}

@@ -63,7 +63,8 @@ def build(verbose: bool = False, force: bool = False) -> dict:
         objs = []
         for s in srcs:
             o = os.path.join(LIB, os.path.basename(s) + ".o")
-            cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-dc", s, "-o", o]
+            extra = os.environ.get("SEQBAL_NVCC_DEFINES", "").split()  # diagnostics builds (-D...)
+            cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-dc", s, "-o", o]
             if verbose:
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)

@@ -477,7 +477,7 @@ constexpr int kGreedyChunk = 1024;  // `hook(p0)` runs before every chunk of thi
 template <int CHUNK, class GetW, class Hook>
 __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, int64_t n, double target, GetW getw,
                                                   Hook hook, int32_t* pick_out, int32_t* bagcnt_out,
-                                                  int* viol_out) {
+                                                  int* viol_out, int32_t* q_out) {
   const int lane = threadIdx.x & 31;
   const int nn = (int)n;
   const int size = a.bag_size[0];
@@ -485,7 +485,10 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
   double asg = 0.0;
   int viol = 0;
   auto run = [&](int p0, int p1) {
-    for (int p = p0 + lane; p < p1; p += 32) pick_out[p] = 0;
+    for (int p = p0 + lane; p < p1; p += 32) {
+      pick_out[p] = 0;
+      if (q_out) q_out[p] = p;  // every sequence joins bag 0, in greedy order
+    }
     if (lane == 0) {
       // the DADD on `asg` is the only chain: eight violation counters keep the
       // predicated increments off it (one counter was a second ~8-cycle chain)
@@ -532,30 +535,37 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
 // CHUNK > 0: `hook(p0)` runs before every CHUNK steps (the large path's
 // shared-memory ring); CHUNK == 0: one flat loop (the nested form costs the
 // fused planner ~45 cycles per sequence in code generation).
-template <int BPL, int CHUNK, class GetW, class Hook>
+// `q_out` (optional): per greedy position, the sequence's rank inside its
+// bag (the stable bag partition of balancer.cpp:178-192), stored by the
+// winning lane off the chain.
+template <int BPL, int CHUNK, bool QOUT = false, class GetW, class Hook>
 __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t n, double total_rep, GetW getw,
-                                            Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out) {
+                                            Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out,
+                                            int32_t* q_out = nullptr) {
   const int lane = threadIdx.x & 31;
   const double target = __ddiv_rn(total_rep, (double)a.U);  // balancer.cpp:26
   if (a.M == 1) {
-    greedy_single_bag<CHUNK>(a, rep, n, target, getw, hook, pick_out, bagcnt_out, viol_out);
+    greedy_single_bag<CHUNK>(a, rep, n, target, getw, hook, pick_out, bagcnt_out, viol_out, q_out);
     return;
   }
   double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
   uint64_t key[BPL];
   int cnt[BPL];
+  bool act[BPL];  // loop-invariant: a.M is not re-read inside the chain
+  const int M = a.M;
   hook(0);
   double w_a = n > 0 ? getw(0) : 0.0, w_b = n > 1 ? getw(1) : 0.0, w_c = n > 2 ? getw(2) : 0.0;
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
     const int j = lane + 32 * i;
-    const int size = j < a.M ? a.bag_size[j] : 0;
+    act[i] = j < M;
+    const int size = act[i] ? a.bag_size[j] : 0;
     cap[i] = __dmul_rn((double)size, target);  // balancer.cpp:30
     rcap[i] = cap[i] > 0.0 ? __drcp_rn(cap[i]) : 0.0;
     asg[i] = 0.0;
     occ[i] = 0.0;  // occupancy(0, cap): +0 for cap > 0 and for cap == 0 (balancer.cpp:32-35)
     rem[i] = __dsub_rn(cap[i], 0.0);
-    key[i] = j < a.M ? greedy_key(rem[i] >= w_a, occ[i]) : ~0ull;
+    key[i] = act[i] ? greedy_key(rem[i] >= w_a, occ[i]) : ~0ull;
     cnt[i] = 0;
   }
   int viol = 0;
@@ -572,12 +582,11 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     uint32_t best_j = 0xffffffffu;
 #pragma unroll
     for (int i = 0; i < BPL; ++i) {
-      const bool act = lane + 32 * i < a.M;
       nasg[i] = __dadd_rn(asg[i], w);
       nocc[i] = occupancy_sel(nasg[i], cap[i], rcap[i]);
       nrem[i] = __dsub_rn(cap[i], nasg[i]);
-      kwin[i] = act ? greedy_key(nrem[i] >= wn, nocc[i]) : ~0ull;
-      knot[i] = act ? greedy_key(rem[i] >= wn, occ[i]) : ~0ull;
+      kwin[i] = act[i] ? greedy_key(nrem[i] >= wn, nocc[i]) : ~0ull;
+      knot[i] = act[i] ? greedy_key(rem[i] >= wn, occ[i]) : ~0ull;
       if (BPL == 1 || key[i] < best) {  // strict: slot 0 (lower bag id) keeps ties
         best = key[i];
         best_j = (uint32_t)(lane + 32 * i);
@@ -591,6 +600,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
 #pragma unroll
     for (int i = 0; i < BPL; ++i) {
       const bool won = (uint32_t)(lane + 32 * i) == pick;
+      if (QOUT && won) q_out[p] = cnt[i];
       key[i] = won ? kwin[i] : knot[i];
       asg[i] = won ? nasg[i] : asg[i];
       occ[i] = won ? nocc[i] : occ[i];
@@ -891,12 +901,11 @@ __global__ void __launch_bounds__(256) k_emit_chunks(PlanArgs a) {
 // happens to, so replay libstdc++'s algorithm on its input (the incoming
 // chunks in index order == send[r]) with its comparator.  Single thread;
 // lists of <= 16 entries are already identical (insertion sort is stable).
-__device__ void fix_rev_ties(const PlanArgs& a, int r, int64_t off, int64_t n) {
+__device__ void fix_rev_ties(int32_t* rev_recv_idx, const int32_t* send_idx, const int32_t* seq, const int64_t* st,
+                             int64_t off, int64_t n) {
   if (n <= stdsort::kThreshold) return;
-  for (int64_t i = 0; i < n; ++i) a.rev_recv_idx[off + i] = a.send_idx[off + i];
-  const int32_t* seq = a.c_seq;
-  const int64_t* st = a.c_start;
-  stdsort::sort(a.rev_recv_idx + off, n, [&](int32_t x, int32_t y) {
+  for (int64_t i = 0; i < n; ++i) rev_recv_idx[off + i] = send_idx[off + i];
+  stdsort::sort(rev_recv_idx + off, n, [&](int32_t x, int32_t y) {
     if (seq[x] != seq[y]) return seq[x] < seq[y];
     return st[x] < st[y];
   });
@@ -1085,7 +1094,8 @@ __global__ void k_finalize(PlanArgs a) {
   // ranks whose reverse receive order can tie: replay std::sort now that
   // send[r] (its input order) is complete; one lane per rank
   for (int r = threadIdx.x; r < a.W; r += blockDim.x)
-    if (a.list_tie[r]) fix_rev_ties(a, r, a.send_off[r], a.send_off[r + 1] - a.send_off[r]);
+    if (a.list_tie[r])
+      fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, a.send_off[r], a.send_off[r + 1] - a.send_off[r]);
 }
 
 }  // namespace sb

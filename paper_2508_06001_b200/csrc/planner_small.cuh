@@ -1,16 +1,12 @@
 // Single-CTA planner for small batches (up to kSmallSeqs sequences).
 //
 // The multi-kernel pipeline in planner.cu is launch-latency bound when a
-// step carries a few dozen sequences (C2: 30): six launches, each paying a
+// step carries a few dozen sequences (C2: 30): many launches, each paying a
 // kernel start and a cold read of what the previous one wrote.  Here one
-// 1024-thread CTA keeps every per-sequence array in shared memory and runs
-// the same phases back to back, separated by __syncthreads:
-//   load + workload + origin offsets -> duplicate check (sort by id) ->
-//   serial FP64 totals -> sort by (workload desc, id asc) -> greedy (warp
-//   per replica) -> stable bag partition + chunk emission -> manifests,
-//   receive rows, Ulysses bases, reverse order -> WIR.
-// Results are bit-identical to the large path (tests/test_gpu_parity.py
-// runs both on the same inputs).
+// 512-thread CTA keeps every per-sequence array in shared memory and runs
+// the phases back to back (listed above k_plan_small).  Results are
+// bit-identical to the large path (tests/test_gpu_parity.py runs both on the
+// same inputs).
 #pragma once
 
 namespace sb {
@@ -20,9 +16,16 @@ namespace sb {
   do {                                                \
     if (a.trace && threadIdx.x == 0) a.trace[k] = clock64(); \
   } while (0)
+// Sub-phase marks (diagnostics): thread 0's time / the latest warp's time.
+#define SB_MARK(k) SB_PHASE(k)
+#define SB_MARK_MAX(k)                                                                                   \
+  do {                                                                                                   \
+    if (a.trace && (threadIdx.x & 31) == 0)                                                              \
+      atomicMax(reinterpret_cast<unsigned long long*>(a.trace + (k)), (unsigned long long)clock64()); \
+  } while (0)
 
 constexpr int kSmallSeqs = 2048;
-constexpr int kSmallThreads = 512;  // 128 registers per thread: the greedy keeps its speculation in registers
+constexpr int kSmallThreads = 512;  // a 256-thread block measured no faster greedy (same code generation)
 
 __host__ __device__ inline int small_pow2(int n) {
   int t = 32;
@@ -32,7 +35,7 @@ __host__ __device__ inline int small_pow2(int n) {
 
 struct SmallLayout {  // byte offsets into dynamic shared memory
   size_t ids, lens, w, soff, hi, lo, v, rank, sorted, pick, G, cb, bo, rank_off, rpre, bagcnt, bagcb, bagq,
-      sendcnt, sendoff, reptot, tie, t_boff, t_branks, t_bsize, t_rbag, t_rmem, pergpu, recvoff, total;
+      sendcnt, sendoff, reptot, repc, tie, t_boff, t_branks, t_bsize, t_rbag, t_rmem, pergpu, recvoff, q, total;
   int T;
 };
 
@@ -68,6 +71,7 @@ __host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int 
   L.sendoff = take(8ull * (W + 1));
   L.tie = take(4ull * W);
   L.reptot = take(8ull * R);
+  L.repc = take(8ull * R);
   L.t_boff = take(4ull * (M + 1));  // topology tables, staged once (read by every phase)
   L.t_branks = take(4ull * U);
   L.t_bsize = take(4ull * M);
@@ -75,6 +79,7 @@ __host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int 
   L.t_rmem = take(4ull * U);
   L.pergpu = take(8ull * W);  // per-GPU workload: the greedy writes it, WIR reads it
   L.recvoff = take(8ull * W);
+  L.q = take(4ull * cap);  // rank of each greedy position inside its bag
   L.total = o;
   return L;
 }
@@ -104,8 +109,8 @@ __device__ void smem_bitonic(uint64_t* hi, uint64_t* lo, uint32_t* v, int n, int
 }
 
 template <int T, int RPT>
-__device__ void reg_sort_emit(const PlanArgs& a, uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int32_t* s_sorted,
-                              int64_t lo, int n) {
+__device__ void reg_sort_emit(int32_t* sorted_idx, uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int32_t* s_sorted,
+                              const double* s_w, double* s_wsorted, int64_t lo, int n) {
   uint64_t h[RPT], l[RPT];
   uint32_t v[RPT];
   reg_bitonic<T, RPT, kSmallThreads>(s_hi, s_lo, s_v, n, h, l, v);
@@ -114,7 +119,8 @@ __device__ void reg_sort_emit(const PlanArgs& a, uint64_t* s_hi, uint64_t* s_lo,
     const int x = threadIdx.x + r * kSmallThreads;
     if (x < n) {
       s_sorted[lo + x] = (int32_t)(lo + v[r]);
-      a.sorted_idx[lo + x] = (int32_t)(lo + v[r]);
+      s_wsorted[lo + x] = s_w[lo + v[r]];
+      sorted_idx[lo + x] = (int32_t)(lo + v[r]);
     }
   }
 }
@@ -122,21 +128,26 @@ __device__ void reg_sort_emit(const PlanArgs& a, uint64_t* s_hi, uint64_t* s_lo,
 // Warp-level inclusive scan helper over int64.
 __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_incl_scan<int64_t>(x); }
 
-template <int BPL>
-__device__ void small_greedy(const PlanArgs& a, int rep, int64_t lo, int64_t n, const double* s_w, const int32_t* s_sorted,
-                             int32_t* s_pick, int32_t* s_bagcnt, double total_rep, int* viol_out) {
-  const double* ws = s_w + lo;  // workloads already gathered into greedy order
-  greedy_warp<BPL, 0>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo, s_bagcnt,
-                      viol_out);
-}
-
+// Single-CTA plan in seven barrier-separated phases.  Independent work shares
+// a phase on different warps instead of taking its own (the kernel is a
+// latency chain: a phase costs its slowest warp plus a barrier):
+//   0 rank offsets + topology tables -> shared memory
+//   1 per sequence: workload, rank, sort keys (warps 2..) | serial FP64 total
+//     straight from the lengths (warp 0) | origin row offsets (warp 1)
+//   2 sort by (workload desc, id asc); workloads gathered into greedy order
+//   3 greedy, one warp per replica, which also records each sequence's rank
+//     inside its bag and the bag bases | duplicate-id check (other warps)
+//   4 per-sequence chunk emission (stable bag partition from those ranks) |
+//     WIR (warp 0)
+//   5 manifest offsets scanned by every warp, recv / Ulysses / reverse lists
+//     per rank warp, send lists per sequence
+//   6 libstdc++ tie-order replay of the reverse lists (rare)
 __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int64_t sh[33];
   __shared__ int s_flag, s_viol, s_biglen;
-  __shared__ int warp_cnt[32][kMaxBags];
-  __shared__ int running[kMaxBags];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  constexpr unsigned kFull = 0xffffffffu;
   PlanArgs a = a_in;  // topology tables and per_gpu redirected to shared memory after phase 0
   const int W = a.W, R = a.R, M = a.M, U = a.U;
   const SmallLayout L = small_layout(cap, W, R * M, R, U, M);
@@ -152,6 +163,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
   int32_t* s_pick = reinterpret_cast<int32_t*>(sm + L.pick);
   int32_t* s_G = reinterpret_cast<int32_t*>(sm + L.G);
   int64_t* s_cb = reinterpret_cast<int64_t*>(sm + L.cb);
+  double* s_wsorted = reinterpret_cast<double*>(sm + L.cb);  // greedy-order workloads; s_cb is written after the greedy
   int32_t* s_bo = reinterpret_cast<int32_t*>(sm + L.bo);
   int64_t* s_roff = reinterpret_cast<int64_t*>(sm + L.rank_off);
   int64_t* s_rpre = reinterpret_cast<int64_t*>(sm + L.rpre);
@@ -160,11 +172,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
   int32_t* s_bagq = reinterpret_cast<int32_t*>(sm + L.bagq);
   int64_t* s_sendcnt = reinterpret_cast<int64_t*>(sm + L.sendcnt);
   int64_t* s_sendoff = reinterpret_cast<int64_t*>(sm + L.sendoff);
+  int64_t* s_recvoff = reinterpret_cast<int64_t*>(sm + L.recvoff);
   int32_t* s_tie = reinterpret_cast<int32_t*>(sm + L.tie);
   double* s_reptot = reinterpret_cast<double*>(sm + L.reptot);
+  int64_t* s_repc = reinterpret_cast<int64_t*>(sm + L.repc);
+  int32_t* s_q = reinterpret_cast<int32_t*>(sm + L.q);
 
   SB_PHASE(0);
-  // ---- phase 0: rank offsets, capacity, topology tables
+  // ---- phase 0: rank offsets, topology tables
   for (int r = tid; r <= W; r += blockDim.x) s_roff[r] = a.rank_off[r];
   {
     int32_t* t_boff = reinterpret_cast<int32_t*>(sm + L.t_boff);
@@ -194,6 +209,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     a.rank_member = t_rmem;
     a.per_gpu = reinterpret_cast<double*>(sm + L.pergpu);
   }
+  for (int r = tid; r < W; r += blockDim.x) s_sendcnt[r] = 0;
   if (tid == 0) {
     s_flag = 0;
     s_viol = 0;
@@ -206,62 +222,100 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     if (tid == 0) atomicOr(a.status, ST_CAPACITY);
     return;
   }
-  SB_PHASE(1);
-  // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
-  for (int64_t i = tid; i < N; i += blockDim.x) {
-    int lo = 0, hi = W;  // rank r with roff[r] <= i < roff[r+1]
+  auto rank_of = [&](int64_t i) {  // rank r with roff[r] <= i < roff[r+1]
+    int lo = 0, hi = W;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (s_roff[mid] <= i) lo = mid;
       else hi = mid;
     }
-    int64_t len = a.lens[i];
-    if (len < 0) {
-      atomicOr(a.status, ST_NEG_LENGTH);
-      len = 0;
-    }
-    double wv;
-    if (a.w_in) {
-      wv = a.w_in[i];
-      if (!(wv >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
-    } else {
-      wv = gamma_weighted_workload(len, a.d_model, a.gamma);
-    }
-    if (len >= (int64_t)1 << 26) s_biglen = 1;  // 32 lengths no longer sum in 32 bits
-    s_ids[i] = a.ids[i];
-    s_lens[i] = len;
-    s_w[i] = wv;
-    s_rank[i] = lo;
-    a.w[i] = wv;
-    a.seq_rank[i] = lo;
-  }
-  __syncthreads();
-  SB_PHASE(2);
-  // ---- phase 2: origin packing offsets (exclusive scan of lens in gather
-  // order, rebased per rank).  One replica: warp 1 does it inside phases 3+4,
-  // beside the totals and the duplicate check (origin_offsets_warp below)
-  auto origin_offsets_warp = [&]() {
-    int64_t carry = 0;
-    for (int64_t base = 0; base < N; base += 32) {
-      const int64_t i = base + lane;
-      const int64_t v = i < N ? s_lens[i] : 0;
-      const int64_t inc = warp_incl_scan<int64_t>(v);
-      if (i < N) s_soff[i] = carry + inc - v;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    __syncwarp();
-    for (int r = lane; r <= W; r += 32) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : carry;
-    __syncwarp();
-    for (int64_t i = lane; i < N; i += 32) {
-      s_soff[i] -= s_rpre[s_rank[i]];
-      a.seq_off[i] = s_soff[i];
-    }
-    for (int r = lane; r < W; r += 32) {
-      a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-      s_sendcnt[r] = 0;
+    return lo;
+  };
+  auto raw_workload = [&](int64_t i) {  // workload of gather index i (balancer.cpp:144)
+    if (a.w_in) return a.w_in[i];
+    const int64_t len = a.lens[i];
+    return gamma_weighted_workload(len < 0 ? 0 : len, a.d_model, a.gamma);
+  };
+  SB_PHASE(1);
+  // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
+  auto seq_pass = [&](int t0, int nt, bool keys) {
+    for (int64_t i = t0; i < N; i += nt) {
+      const int r = rank_of(i);
+      int64_t len = a.lens[i];
+      if (len < 0) {
+        atomicOr(a.status, ST_NEG_LENGTH);
+        len = 0;
+      }
+      double wv;
+      if (a.w_in) {
+        wv = a.w_in[i];
+        if (!(wv >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
+      } else {
+        wv = gamma_weighted_workload(len, a.d_model, a.gamma);
+      }
+      if (len >= (int64_t)1 << 26) s_biglen = 1;  // 32 lengths no longer sum in 32 bits
+      const uint64_t id = a.ids[i];
+      s_ids[i] = id;
+      s_lens[i] = len;
+      s_w[i] = wv;
+      s_rank[i] = r;
+      a.w[i] = wv;
+      a.seq_rank[i] = r;
+      if (keys) {  // one replica: its sort records, indexed by gather position
+        s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
+        s_lo[i] = id;
+        s_v[i] = (uint32_t)i;
+      }
     }
   };
-  if (R > 1) {
+  if (R == 1) {
+    if (warp == 0) {
+      // serial FP64 total in gather order (balancer.cpp:24-25; the replica
+      // total of :147 is the same sum): the warp recomputes the workloads
+      // from the lengths into the (not yet used) greedy-order scratch, lane 0
+      // chains them
+#pragma unroll 4
+      for (int64_t i = lane; i < N; i += 32) s_wsorted[i] = raw_workload(i);
+      __syncwarp();
+      double s = 0.0;
+      if (lane == 0) {
+#pragma unroll 8
+        for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_wsorted[i]);
+      }
+      SB_MARK_MAX(11);
+      if (lane == 0) {
+        *a.total = s;
+        *a.n_seqs = N;
+        s_reptot[0] = s;
+        a.rep_total[0] = s;
+      }
+    } else if (warp == 1) {
+      // origin packing offsets: exclusive scan of the lengths in gather
+      // order, rebased per rank
+      int64_t carry = 0;
+      for (int64_t base = 0; base < N; base += 32) {
+        const int64_t i = base + lane;
+        int64_t v = i < N ? a.lens[i] : 0;
+        v = v < 0 ? 0 : v;
+        const int64_t inc = warp_incl_scan<int64_t>(v);
+        if (i < N) s_soff[i] = carry + inc - v;
+        carry += __shfl_sync(kFull, inc, 31);
+      }
+      __syncwarp();
+      for (int r = lane; r <= W; r += 32) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : carry;
+      __syncwarp();
+      for (int64_t i = lane; i < N; i += 32) {
+        s_soff[i] -= s_rpre[rank_of(i)];
+        a.seq_off[i] = s_soff[i];
+      }
+      for (int r = lane; r < W; r += 32) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+    } else {
+      seq_pass(tid - 64, (int)blockDim.x - 64, true);
+    }
+    __syncthreads();
+  } else {
+    seq_pass(tid, (int)blockDim.x, false);
+    __syncthreads();
     const int64_t per = (N + blockDim.x - 1) / blockDim.x;
     const int64_t b0 = tid * per, b1 = b0 + per < N ? b0 + per : N;
     int64_t loc = 0;
@@ -279,42 +333,122 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
       s_soff[i] -= s_rpre[s_rank[i]];
       a.seq_off[i] = s_soff[i];
     }
-    for (int r = tid; r < W; r += blockDim.x) {
-      a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-      s_sendcnt[r] = 0;
-    }
-    __syncthreads();
-  }
-  SB_PHASE(3);
-  // ---- phases 3+4 side by side: warps 0-1 run the serial FP64 totals
-  // (balancer.cpp:24-25, :147) while warps 2.. check for duplicate sample ids
-  // inside each replica (divergence); named barrier 2 syncs
-  // the checking warps only.  One replica: its total is the report total
-  // (same additions, same order).
-  if (warp == 0) {
-    if (lane == 0) {
+    for (int r = tid; r < W; r += blockDim.x) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+    // serial totals (balancer.cpp:24-25, :147): global on warp 0, one
+    // replica per lane of warp 1
+    if (warp == 0 && lane == 0) {
       double s = 0.0;
       for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_w[i]);
       *a.total = s;
       *a.n_seqs = N;
-      if (R == 1) {
-        s_reptot[0] = s;
-        a.rep_total[0] = s;
-      }
-    }
-  } else if (warp == 1) {
-    if (R == 1) origin_offsets_warp();
-    else
+    } else if (warp == 1) {
       for (int rep = lane; rep < R; rep += 32) {
         double s = 0.0;
         for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
         s_reptot[rep] = s;
         a.rep_total[rep] = s;
       }
+    }
+    __syncthreads();
+  }
+  SB_PHASE(2);
+  // ---- phase 2: per replica sort by (workload desc, id asc) (balancer.cpp:37-40);
+  // each variant also gathers the workloads into greedy order
+  for (int rep = 0; rep < R; ++rep) {
+    const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
+    if (R > 1) {
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        const double wv = s_w[lo + i];
+        s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
+        s_lo[i] = s_ids[lo + i];
+        s_v[i] = (uint32_t)i;
+      }
+      __syncthreads();
+    }
+    if (n > 32 && n <= 2 * kSmallThreads && blockDim.x == kSmallThreads) {
+      const int nn = (int)n;
+      int32_t* gs = a.sorted_idx;
+      if (nn <= 64) reg_sort_emit<64, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+      else if (nn <= 128) reg_sort_emit<128, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+      else if (nn <= 256) reg_sort_emit<256, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+      else if (nn <= 512) reg_sort_emit<512, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+      else reg_sort_emit<1024, 2>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+    } else if (n <= 1024) {
+      // rank by counting: the key (~bits(w), id, index) is a total order.
+      // k = blockDim/n lanes (power of two <= 32) share one record's count,
+      // each over a slice of the candidates (broadcast smem reads), then a
+      // shuffle reduction inside the k-lane group.
+      const int nn = (int)n;
+      int k = 1;
+      while (k < 32 && 2 * k * nn <= (int)blockDim.x) k <<= 1;
+      const int per = (nn + k - 1) / k;
+      for (int base = 0; base < nn * k; base += blockDim.x) {
+        const int x = base + tid;
+        const int i = x / k, part = x % k;
+        int pos = 0;
+        if (i < nn) {
+          const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
+          const int j0 = part * per, j1 = j0 + per < nn ? j0 + per : nn;
+#pragma unroll 8
+          for (int j = j0; j < j1; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
+        }
+        for (int o = k >> 1; o > 0; o >>= 1) pos += __shfl_xor_sync(kFull, pos, o);
+        if (i < nn && part == 0) {
+          s_sorted[lo + pos] = (int32_t)(lo + i);
+          s_wsorted[lo + pos] = s_w[lo + i];
+          a.sorted_idx[lo + pos] = (int32_t)(lo + i);
+        }
+      }
+    } else {
+      smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
+        s_wsorted[lo + i] = s_w[lo + s_v[i]];
+        a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
+      }
+    }
+    __syncthreads();
+  }
+  SB_PHASE(3);
+  // ---- phase 3: greedy, one warp per replica (balancer.cpp:44-62), beside
+  // the duplicate-id check inside each replica (divergence)
+  const int ng = R < nw - 2 ? R : nw - 2;
+  if (warp < ng) {
+    for (int rep = warp; rep < R; rep += ng) {
+      const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
+      const double* ws = s_wsorted + lo;
+      if (M <= 32)
+        greedy_warp<1, 0, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo,
+                          s_bagcnt, &s_viol, s_q + lo);
+      else
+        greedy_warp<2, 0, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo,
+                          s_bagcnt, &s_viol, s_q + lo);
+      __syncwarp();
+      // replica-local chunk bases of the bags (chunk order: bag, q, k) and
+      // the bags' first slots in the (replica, bag)-grouped sequence list
+      int cb = 0, q = (int)lo;  // <= cap * kMaxBags chunks: 32 bits
+      for (int x0 = 0; x0 < M; x0 += 32) {
+        const int x = x0 + lane;
+        const int nb = x < M ? s_bagcnt[rep * M + x] : 0;
+        const int c = x < M ? nb * a.bag_size[x] : 0;
+        const int ic = warp_incl_scan<int>(c), iq = warp_incl_scan<int>(nb);
+        if (x < M) {
+          s_bagcb[rep * M + x] = cb + ic - c;
+          s_bagq[rep * M + x] = q + iq - nb;
+        }
+        cb += __shfl_sync(kFull, ic, 31);
+        q += __shfl_sync(kFull, iq, 31);
+      }
+      if (lane == 0) {
+        s_repc[rep] = cb;
+        a.rep_chunks[rep] = cb;
+        if (R == 1) *a.n_chunks = cb;
+      }
+    }
   } else if (!a.w_in) {
-    // open-addressing set per replica in the (not yet used) sort scratch:
+    // open-addressing set per replica in the sort scratch (free now):
     // s_hi and s_lo are contiguous, 2T slots >= 2 * replica size, EMPTY = ~0
-    const int t = tid - 64, nt = (int)blockDim.x - 64;
+    const int t = tid - 32 * ng, nt = (int)blockDim.x - 32 * ng;
     auto bar = [nt]() { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); };
     for (int rep = 0; rep < R; ++rep) {
       const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
@@ -345,209 +479,74 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     if (s_flag && t == 0) atomicOr(a.status, ST_DUP_ID);
   }
   __syncthreads();
+  if (R > 1) {
+    // replica chunk bases (chunk order: replica, bag, q, k)
+    if (warp == 0) {
+      int64_t carry = 0;
+      for (int x0 = 0; x0 < R; x0 += 32) {
+        const int x = x0 + lane;
+        const int64_t c = x < R ? s_repc[x] : 0;
+        const int64_t inc = warp_incl_scan<int64_t>(c);
+        if (x < R) s_repc[x] = carry + inc - c;
+        carry += __shfl_sync(kFull, inc, 31);
+      }
+      __syncwarp();
+      for (int e = lane; e < R * M; e += 32) s_bagcb[e] += s_repc[e / M];
+      if (lane == 0) *a.n_chunks = carry;
+    }
+    __syncthreads();
+  }
   SB_PHASE(4);
-  SB_PHASE(5);
-  // ---- phase 5: per replica sort by (workload desc, id asc) (balancer.cpp:37-40)
-  for (int rep = 0; rep < R; ++rep) {
-    const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
-    for (int64_t i = tid; i < n; i += blockDim.x) {
-      const double wv = s_w[lo + i];
-      s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
-      s_lo[i] = s_ids[lo + i];
-      s_v[i] = (uint32_t)i;
-    }
-    __syncthreads();
-    if (n > 32 && n <= 2 * kSmallThreads && blockDim.x == kSmallThreads) {
-      const int nn = (int)n;
-      if (nn <= 64) reg_sort_emit<64, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
-      else if (nn <= 128) reg_sort_emit<128, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
-      else if (nn <= 256) reg_sort_emit<256, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
-      else if (nn <= 512) reg_sort_emit<512, 1>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
-      else reg_sort_emit<1024, 2>(a, s_hi, s_lo, s_v, s_sorted, lo, nn);
-    } else if (n <= 1024) {
-      // rank by counting: the key (~bits(w), id, index) is a total order.
-      // k = blockDim/n lanes (power of two <= 32) share one record's count,
-      // each over a slice of the candidates (broadcast smem reads), then a
-      // shuffle reduction inside the k-lane group.
-      const int nn = (int)n;
-      int k = 1;
-      while (k < 32 && 2 * k * nn <= (int)blockDim.x) k <<= 1;
-      const int per = (nn + k - 1) / k;
-      for (int base = 0; base < nn * k; base += blockDim.x) {
-        const int x = base + tid;
-        const int i = x / k, part = x % k;
-        int pos = 0;
-        if (i < nn) {
-          const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
-          const int j0 = part * per, j1 = j0 + per < nn ? j0 + per : nn;
-#pragma unroll 8
-          for (int j = j0; j < j1; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
-        }
-        for (int o = k >> 1; o > 0; o >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, o);
-        if (i < nn && part == 0) {
-          s_sorted[lo + pos] = (int32_t)(lo + i);
-          a.sorted_idx[lo + pos] = (int32_t)(lo + i);
-        }
-      }
-    } else {
-      smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
-      for (int64_t i = tid; i < n; i += blockDim.x) {
-        s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
-        a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
-      }
-    }
-    __syncthreads();
-  }
-  SB_PHASE(6);
-  // ---- phase 6: greedy, one warp per replica (balancer.cpp:44-62), over the
-  // workloads gathered into greedy order (the sort scratch is free now)
-  double* s_wsorted = reinterpret_cast<double*>(s_hi);
-  for (int64_t i = tid; i < N; i += blockDim.x) s_wsorted[i] = s_w[s_sorted[i]];
-  __syncthreads();
-  for (int rep = warp; rep < R; rep += nw) {
-    const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
-    if (M <= 32) small_greedy<1>(a, rep, lo, n, s_wsorted, nullptr, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
-    else small_greedy<2>(a, rep, lo, n, s_wsorted, nullptr, s_pick, s_bagcnt, s_reptot[rep], &s_viol);
-  }
-  __syncthreads();
-  SB_PHASE(7);
-  // ---- phase 7: chunk bases of every (replica, bag): warp 0 scans the
-  // (replica, bag) counts 32 at a time
+  // ---- phase 4: stable bag partition (balancer.cpp:178-192), one thread per
+  // sequence: the greedy recorded each sequence's rank q in its bag, so its
+  // chunks are [bag base + q * g, + g) and its slot in the grouped list is
+  // bag first slot + q.  Warp 0 computes the WIR beside it.
   if (warp == 0) {
-    int64_t cb = 0, q = 0;
-    for (int x0 = 0; x0 < R * M; x0 += 32) {
-      const int x = x0 + lane;
-      const int64_t n = x < R * M ? s_bagcnt[x] : 0;
-      const int64_t c = x < R * M ? n * a.bag_size[x % M] : 0;
-      const int64_t ic = warp_incl_scan<int64_t>(c), iq = warp_incl_scan<int64_t>(n);
-      if (x < R * M) {
-        s_bagcb[x] = cb + ic - c;
-        s_bagq[x] = (int32_t)(q + iq - n);
-      }
-      cb += __shfl_sync(0xffffffffu, ic, 31);
-      q += __shfl_sync(0xffffffffu, iq, 31);
+    for (int r = lane; r < W; r += 32) a_in.per_gpu[r] = a.per_gpu[r];
+    // min and max are order-independent (no NaN) (metrics.cpp:20-31)
+    double lo = a.per_gpu[0], hi = lo;
+    for (int r = lane; r < W; r += 32) {
+      const double v = a.per_gpu[r];
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
     }
-    __syncwarp();
-    for (int rep = lane; rep < R; rep += 32) {
-      const int64_t e = rep + 1 < R ? s_bagcb[(rep + 1) * M] : cb;
-      a.rep_chunks[rep] = e - s_bagcb[rep * M];
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
     }
     if (lane == 0) {
-      *a.n_chunks = cb;
+      *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
       *a.violations = s_viol;
     }
-  }
-  __syncthreads();
-  SB_PHASE(8);
-  // ---- phase 8: stable bag partition + chunk emission (balancer.cpp:178-218)
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int rep = 0; rep < R; ++rep) {
-    const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
-    for (int b = tid; b < M; b += blockDim.x) running[b] = 0;
-    __syncthreads();
-    for (int64_t tile = lo; tile < hi; tile += blockDim.x) {
-      for (int e = tid; e < nw * M; e += blockDim.x) warp_cnt[e / M][e % M] = 0;
-      __syncthreads();
-      const int64_t p = tile + tid;
-      const bool valid = p < hi;
-      const int b = valid ? s_pick[p] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, b);
-      const int rank_in = __popc(peers & lt_mask);
-      if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
-      __syncthreads();
-      for (int b2 = warp; b2 < M; b2 += nw) {  // warp b2 scans bag b2's per-warp counts
-        const int c = lane < nw ? warp_cnt[lane][b2] : 0;
-        const int inc = warp_incl_scan<int>(c);
-        const int run = running[b2];
-        __syncwarp();
-        if (lane < nw) warp_cnt[lane][b2] = run + inc - c;
-        if (lane == 31) running[b2] = run + inc;
-      }
-      __syncthreads();
-      if (valid) {
-        const int q = warp_cnt[warp][b] + rank_in;
-        const int s = s_sorted[p];
-        const int g = a.bag_size[b];
-        const int64_t cb = s_bagcb[rep * M + b] + (int64_t)q * g;
-        const int src = s_rank[s];
-        s_G[s] = g;
-        s_cb[s] = cb;
-        s_bo[s_bagq[rep * M + b] + q] = s;
-        a.seq_G[s] = g;
-        a.seq_chunk_base[s] = cb;
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sendcnt[src]), (unsigned long long)g);
-      }
-      __syncthreads();
-    }
-  }
-  // chunk emission, one thread per chunk (coalesced stores): bag rb =
-  // (rep, b) holds chunks [bagcb[rb], bagcb[rb] + count * g) in its
-  // sequences' bag order; a chunk finds its bag by binary search
-  {
-    const int RM = R * M;
-    const int64_t total = s_bagcb[RM - 1] + (int64_t)s_bagcnt[RM - 1] * a.bag_size[M - 1];
-    for (int64_t c = tid; c < total; c += blockDim.x) {
-      int blo = 0, bhi = RM;  // last bag with base <= c (empty bags share the base of the next)
-      while (bhi - blo > 1) {
-        const int mid = (blo + bhi) >> 1;
-        if (s_bagcb[mid] <= c) blo = mid;
-        else bhi = mid;
-      }
-      const int rep = blo / M, b = blo - rep * M;
+  } else {
+    for (int64_t p = tid - 32; p < N; p += (int)blockDim.x - 32) {
+      const int s = s_sorted[p];
+      const int b = s_pick[p], q = s_q[p];
+      const int src = s_rank[s];
+      const int rep = src / U;
+      const int rb = rep * M + b;
       const int g = a.bag_size[b];
-      const uint32_t e = (uint32_t)(c - s_bagcb[blo]);
-      const int q = (int)(e / (uint32_t)g), k = (int)(e - (uint32_t)q * (uint32_t)g);
-      const int s = s_bo[s_bagq[blo] + q];
-      int64_t cq;
-      int cr;
-      len_divmod(s_lens[s], g, cq, cr);
-      const int64_t st = (int64_t)k * cq + (k < cr ? k : cr);
-      a.c_id[c] = s_ids[s];
-      a.c_idx[c] = k;
-      a.c_start[c] = st;
-      a.c_end[c] = st + cq + (k < cr ? 1 : 0);
-      a.c_src[c] = s_rank[s];
-      a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
-      a.c_src_row[c] = s_soff[s] + st;
-      a.c_seq[c] = s;
+      const int64_t cb = s_bagcb[rb] + (int64_t)q * g;
+      s_G[s] = g;
+      s_cb[s] = cb;
+      s_bo[s_bagq[rb] + q] = s;
+      a.seq_G[s] = g;
+      a.seq_chunk_base[s] = cb;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&s_sendcnt[src]), (unsigned long long)g);
     }
+    SB_MARK_MAX(10);
   }
   __syncthreads();
-  SB_PHASE(9);
-  // ---- phase 9: manifest offsets (balancer.cpp:84-91), warp 0 scans 32
-  // ranks at a time
-  if (warp == 0) {
-    int64_t so = 0, ro = 0;
-    for (int r0 = 0; r0 < W; r0 += 32) {
-      const int r = r0 + lane;
-      const int64_t sc = r < W ? s_sendcnt[r] : 0;
-      const int64_t rc = r < W ? (int64_t)s_bagcnt[(r / U) * M + a.rank_bag[r % U]] : 0;
-      const int64_t is = warp_incl_scan<int64_t>(sc), ir = warp_incl_scan<int64_t>(rc);
-      if (r < W) {
-        s_sendoff[r] = so + is - sc;
-        a.send_off[r] = so + is - sc;
-        a.recv_off[r] = ro + ir - rc;
-        reinterpret_cast<int64_t*>(sm + L.recvoff)[r] = ro + ir - rc;
-      }
-      so += __shfl_sync(0xffffffffu, is, 31);
-      ro += __shfl_sync(0xffffffffu, ir, 31);
-    }
-    if (lane == 0) {
-      s_sendoff[W] = so;
-      a.send_off[W] = so;
-      a.recv_off[W] = ro;
-    }
-  }
-  __syncthreads();
-  SB_PHASE(10);
-  // ---- phase 10: per rank lists, one warp per rank
-  for (int r = warp; r < W; r += nw) {
+  SB_PHASE(5);
+  // ---- phase 5: manifests (balancer.cpp:84-101, reverse order :259-285)
+  // recv list + receive-side rows (target packing) + Ulysses sequence bases
+  // of rank r, and its reverse receive order: r's sequences in buffer order,
+  // chunks ascending.  Warp-wide; ro / so = r's recv / send list offsets.
+  auto rank_lists = [&](int r, int64_t ro, int64_t so) {
     const int rep = r / U, u = r % U;
     const int b = a.rank_bag[u], k = a.rank_member[u], g = a.bag_size[b];
     const int nb = s_bagcnt[rep * M + b];
     const int bq = s_bagq[rep * M + b];
-    const int64_t ro = reinterpret_cast<const int64_t*>(sm + L.recvoff)[r];
-    // recv list + receive-side rows (target packing, balancer.cpp:93-101)
     int64_t carry = 0, carry2 = 0;
     for (int q0 = 0; q0 < nb; q0 += 32) {
       const int q = q0 + lane;
@@ -569,14 +568,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
         a.recv_idx[ro + q] = (int32_t)c;
         if (k == 0) a.c_seq_base[s_cb[s]] = carry2 + inc2 - l;
       }
-      carry += __shfl_sync(0xffffffffu, inc, 31);
-      if (k == 0) carry2 += __shfl_sync(0xffffffffu, inc2, 31);
+      carry += __shfl_sync(kFull, inc, 31);
+      if (k == 0) carry2 += __shfl_sync(kFull, inc2, 31);
     }
     if (lane == 0) {
       a.target_rows[r] = carry;
       if (k == 0) a.bag_rows[rep * M + b] = carry2;
     }
-    // reverse receive order: r's sequences in buffer order, chunks ascending
     const int64_t s0 = s_roff[r], s1 = s_roff[r + 1];
     int64_t c4 = 0;
     bool tie = false;  // a sequence shorter than its bag: equal (segment, start) keys
@@ -587,46 +585,120 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
       tie |= gs > 1 && s_lens[i] < gs;
       const int64_t inc = warp_incl_scan<int>(gs);  // <= 32 * kMaxBags
       if (valid)
-        for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[s_sendoff[r] + c4 + inc - gs + kk] = (int32_t)(s_cb[i] + kk);
-      c4 += __shfl_sync(0xffffffffu, inc, 31);
+        for (int kk = 0; kk < gs; ++kk) a.rev_recv_idx[so + c4 + inc - gs + kk] = (int32_t)(s_cb[i] + kk);
+      c4 += __shfl_sync(kFull, inc, 31);
     }
-    tie = __any_sync(0xffffffffu, tie);
+    tie = __any_sync(kFull, tie);
     if (lane == 0) s_tie[r] = tie ? 1 : 0;
-  }
-  __syncthreads();
-  SB_PHASE(11);
-  // ---- phase 11: send lists -- r's sequences ordered by first chunk index
-  // position of sequence i in send[r] = chunks of r's sequences with a
-  // smaller first chunk index (counting, no sort, no barrier)
-  for (int64_t i = tid; i < N; i += blockDim.x) {
+  };
+  // send list of the rank of sequence i: r's sequences ordered by first
+  // chunk index (counting, no sort); so = the rank's send offset
+  auto send_list = [&](int64_t i, int64_t so) {
     const int r = s_rank[i];
     const int64_t cb = s_cb[i];
     int64_t pos = 0;
     for (int64_t j = s_roff[r]; j < s_roff[r + 1]; ++j)
       if (s_cb[j] < cb) pos += s_G[j];
-    for (int kk = 0; kk < s_G[i]; ++kk) a.send_idx[s_sendoff[r] + pos + kk] = (int32_t)(cb + kk);
+    for (int kk = 0; kk < s_G[i]; ++kk) a.send_idx[so + pos + kk] = (int32_t)(cb + kk);
+  };
+  // chunk emission (balancer.cpp:194-218), one thread per chunk (coalesced
+  // stores): bag rb = (rep, b) holds chunks [bagcb[rb], bagcb[rb] + count * g)
+  // in its sequences' bag order; a chunk finds its bag by binary search
+  const int RM = R * M;
+  const int64_t n_chunks = s_bagcb[RM - 1] + (int64_t)s_bagcnt[RM - 1] * a.bag_size[M - 1];
+  auto emit_chunk = [&](int64_t c) {
+    int blo = 0, bhi = RM;  // last bag with base <= c (empty bags share the base of the next)
+    while (bhi - blo > 1) {
+      const int mid = (blo + bhi) >> 1;
+      if (s_bagcb[mid] <= c) blo = mid;
+      else bhi = mid;
+    }
+    const int rep = blo / M, b = blo - rep * M;
+    const int g = a.bag_size[b];
+    const uint32_t e = (uint32_t)(c - s_bagcb[blo]);
+    const int q = (int)(e / (uint32_t)g), k = (int)(e - (uint32_t)q * (uint32_t)g);
+    const int s = s_bo[s_bagq[blo] + q];
+    int64_t cq;
+    int cr;
+    len_divmod(s_lens[s], g, cq, cr);
+    const int64_t st = (int64_t)k * cq + (k < cr ? k : cr);
+    a.c_id[c] = s_ids[s];
+    a.c_idx[c] = k;
+    a.c_start[c] = st;
+    a.c_end[c] = st + cq + (k < cr ? 1 : 0);
+    a.c_src[c] = s_rank[s];
+    a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
+    a.c_src_row[c] = s_soff[s] + st;
+    a.c_seq[c] = s;
+  };
+  // chunk emission and send lists go to the highest threads first: warps
+  // without a rank list take them while the rank warps scan
+  const int rtid = (int)blockDim.x - 1 - tid;
+  if (W <= 32) {
+    // every warp scans the per-rank counts itself: lane r holds rank r's
+    // send / recv offsets (no extra barrier)
+    // 32-bit scans: counts are bounded by the plan's chunk capacity
+    const int sc = lane < W ? (int)s_sendcnt[lane] : 0;
+    const int rc = lane < W ? s_bagcnt[(lane / U) * M + a.rank_bag[lane % U]] : 0;
+    const int is = warp_incl_scan<int>(sc), ir = warp_incl_scan<int>(rc);
+    const int so_l = is - sc, ro_l = ir - rc;
+    if (warp == 0) {
+      if (lane < W) {
+        s_sendoff[lane] = so_l;
+        a.send_off[lane] = so_l;
+        a.recv_off[lane] = ro_l;
+      }
+      if (lane == W - 1) {
+        s_sendoff[W] = is;
+        a.send_off[W] = is;
+        a.recv_off[W] = ir;
+      }
+    }
+    SB_MARK(7);
+    for (int r = warp; r < W; r += nw) rank_lists(r, __shfl_sync(kFull, ro_l, r), __shfl_sync(kFull, so_l, r));
+    SB_MARK_MAX(8);
+    for (int64_t c = rtid; c < n_chunks; c += blockDim.x) emit_chunk(c);
+    SB_MARK_MAX(12);
+    for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {  // warp-uniform trip count (the shuffle below)
+      const int64_t i = b0 + rtid;
+      const int r = i < N ? s_rank[i] : 0;
+      const int64_t so = __shfl_sync(kFull, so_l, r);
+      if (i < N) send_list(i, so);
+    }
+    SB_MARK_MAX(9);
+  } else {
+    if (warp == 0) {
+      int64_t so = 0, ro = 0;
+      for (int r0 = 0; r0 < W; r0 += 32) {
+        const int r = r0 + lane;
+        const int64_t sc = r < W ? s_sendcnt[r] : 0;
+        const int64_t rc = r < W ? (int64_t)s_bagcnt[(r / U) * M + a.rank_bag[r % U]] : 0;
+        const int64_t is = warp_incl_scan<int64_t>(sc), ir = warp_incl_scan<int64_t>(rc);
+        if (r < W) {
+          s_sendoff[r] = so + is - sc;
+          a.send_off[r] = so + is - sc;
+          a.recv_off[r] = ro + ir - rc;
+          s_recvoff[r] = ro + ir - rc;
+        }
+        so += __shfl_sync(kFull, is, 31);
+        ro += __shfl_sync(kFull, ir, 31);
+      }
+      if (lane == 0) {
+        s_sendoff[W] = so;
+        a.send_off[W] = so;
+        a.recv_off[W] = ro;
+      }
+    }
+    __syncthreads();
+    for (int r = warp; r < W; r += nw) rank_lists(r, s_recvoff[r], s_sendoff[r]);
+    for (int64_t c = rtid; c < n_chunks; c += blockDim.x) emit_chunk(c);
+    for (int64_t i = rtid; i < N; i += blockDim.x) send_list(i, s_sendoff[s_rank[i]]);
   }
   __syncthreads();  // send lists complete: reverse-order tie replay reads them
+  SB_PHASE(6);
   for (int r = warp; r < W; r += nw)
-    if (lane == 0 && s_tie[r]) fix_rev_ties(a, r, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r]);
-  SB_PHASE(12);
-  // ---- phase 12: WIR (metrics.cpp:20-31); per_gpu written by the greedy
-  __syncthreads();
-  for (int r = tid; r < W; r += blockDim.x) a_in.per_gpu[r] = a.per_gpu[r];
-  if (warp == 0) {  // min and max are order-independent (no NaN): one warp, loads in parallel
-    double lo = a.per_gpu[0], hi = lo;
-    for (int r = lane; r < W; r += 32) {
-      const double v = a.per_gpu[r];
-      lo = fmin(lo, v);
-      hi = fmax(hi, v);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0)
-      *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
-  }
+    if (lane == 0 && s_tie[r])
+      fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r]);
   SB_PHASE(13);
 }
 

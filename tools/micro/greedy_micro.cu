@@ -608,6 +608,82 @@ __global__ void g_diag(const double* w_sorted, int n, int M, const double* caps,
   long long t1 = clock64();
   if (lane == 0) { *cyc = t1 - t0; *replays = nrep; }
 }
+
+// The production greedy_warp step (planner.cu, CHUNK == 0, BPL == 1) and
+// variants, to find what separates it from v5flat:
+//  VAR 0: production (3-ahead prefetch ring, clamped index, picks + q to smem, viol)
+//  VAR 1: no q store       VAR 2: direct w / wn loads (no ring)
+//  VAR 3: no viol          VAR 4: picks to global (as v5flat)   VAR 5: 1 + 2 + 3
+//  VAR 6: VAR 0 inside a 512-thread CTA (128-register cap), the other 15
+//  warps waiting at __syncthreads (the fused planner's situation)
+template <int VAR>
+__global__ void __launch_bounds__(VAR >= 6 ? 512 : 32) g_prod(const double* w_sorted, int n, int M, const double* caps, int* pick, long long* cyc,
+                       int* replays) {
+  extern __shared__ double wsd[];
+  __shared__ int s_pick[4096];  // ring: the store cost is what is measured
+  __shared__ int s_q[4096];
+  const int lane = threadIdx.x;
+  if (VAR >= 6 && threadIdx.x >= 32) {
+    __syncthreads();
+    return;
+  }
+  for (int i = lane; i < n + 2; i += 32) wsd[i] = i < n ? w_sorted[i] : 0.0;
+  __syncwarp();
+  const double* ws = wsd;
+  auto getw = [ws](int p) { return ws[p]; };
+  const double cap = lane < M ? caps[lane] : 0.0;
+  const double rcap = cap > 0.0 ? __drcp_rn(cap) : 0.0;
+  double asg = 0.0, occ = 0.0, rem = __dsub_rn(cap, 0.0);
+  const int nn = n;
+  double w_a = nn > 0 ? getw(0) : 0.0, w_b = nn > 1 ? getw(1) : 0.0, w_c = nn > 2 ? getw(2) : 0.0;
+  uint64_t key = lane < M ? ((((rem >= w_a) ? 0ull : (1ull << 63))) | (uint64_t)__double_as_longlong(occ)) : ~0ull;
+  int cnt = 0, viol = 0;
+  long long t0 = clock64();
+  for (int p = 0; p < nn; ++p) {
+    double w, wn;
+    if (VAR == 2 || VAR == 5) {
+      w = ws[p];
+      wn = ws[p + 1];
+    } else {
+      w = w_a;
+      wn = w_b;
+      w_a = w_b;
+      w_b = w_c;
+      w_c = getw(p + 3 < nn ? p + 3 : nn - 1);
+    }
+    const bool act = lane < M;
+    const double nasg = __dadd_rn(asg, w);
+    const double nocc = occ_sel(nasg, cap, rcap);
+    const double nrem = __dsub_rn(cap, nasg);
+    const uint64_t kwin = act ? ((((nrem >= wn) ? 0ull : (1ull << 63))) | (uint64_t)__double_as_longlong(nocc)) : ~0ull;
+    const uint64_t knot = act ? ((((rem >= wn) ? 0ull : (1ull << 63))) | (uint64_t)__double_as_longlong(occ)) : ~0ull;
+    const uint64_t best = key;
+    const uint32_t best_j = (uint32_t)lane;
+    const uint32_t khi = (uint32_t)(best >> 32), klo = (uint32_t)best;
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+    const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+    const uint32_t pk = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+    if (VAR != 3 && VAR != 5) viol += (int)(m1 >> 31);
+    const bool won = (uint32_t)lane == pk;
+    if (VAR != 1 && VAR != 5 && won) s_q[p & 4095] = cnt;
+    key = won ? kwin : knot;
+    asg = won ? nasg : asg;
+    occ = won ? nocc : occ;
+    rem = won ? nrem : rem;
+    cnt += won ? 1 : 0;
+    if (VAR == 4) {
+      if (lane == 0) pick[p] = (int)pk;
+    } else if (lane == 0) {
+      s_pick[p & 4095] = (int)pk;
+    }
+  }
+  long long t1 = clock64();
+  __syncwarp();
+  if (VAR != 4)
+    for (int i = lane; i < n; i += 32) pick[i] = i < n - 4096 ? -1 : s_pick[i & 4095];
+  if (lane == 0) { *cyc = t1 - t0; *replays = viol + s_q[n / 2] * 0; }
+  if (VAR >= 6 && blockDim.x > 32) __syncthreads();
+}
 int main() {
   unsigned* du; double* dd; long long* dc;
   cudaMalloc(&du, 128); cudaMalloc(&dd, 512); cudaMalloc(&dc, 8);
@@ -675,10 +751,26 @@ int main() {
         cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
         cudaMemcpy(&hrep, drep, 4, cudaMemcpyDeviceToHost);
         cudaMemcpy(h6.data(), p6, n * 4, cudaMemcpyDeviceToHost);
-        int dd = 0; for (int i = 0; i < n; ++i) dd += h5[i] != h6[i];
+        int dd = 0; for (int i = 0; i < n; ++i) dd += h6[i] >= 0 && h5[i] != h6[i];
         printf("  %s %.1f cyc/seq (diffs %d, conflict %d)\n", name, (double)c / n, dd, hrep);
       };
       run(g_diag<0>, "v5flat");
+      run(g_prod<0>, "prod");
+      run(g_prod<1>, "prod-no-q");
+      run(g_prod<2>, "prod-direct-w");
+      run(g_prod<3>, "prod-no-viol");
+      run(g_prod<4>, "prod-pick-global");
+      run(g_prod<5>, "prod-1+2+3");
+      {
+        cudaFuncSetAttribute(g_prod<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
+        for (int r = 0; r < 2; ++r) g_prod<6><<<1, 512, (n + 2) * 8>>>(dw, n, M, dcap, p6, dc, drep);
+        cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+        printf("  prod-in-512-CTA %.1f cyc/seq (%s)\n", (double)c / n, cudaGetErrorString(cudaGetLastError()));
+        for (int r = 0; r < 2; ++r) g_prod<6><<<1, 32, (n + 2) * 8>>>(dw, n, M, dcap, p6, dc, drep);
+        cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+        printf("  prod-bounds512-alone %.1f cyc/seq (%s)\n", (double)c / n, cudaGetErrorString(cudaGetLastError()));
+        cudaFuncSetAttribute(g_prod<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
+      }
       run(g_diag<1>, "redux-chain-only");
       run(g_diag<2>, "division-chain-only");
       run(g_diag<3>, "v9");

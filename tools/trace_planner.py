@@ -1,6 +1,6 @@
 """Per-phase cycle trace of the fused planner (diagnostics, needs a GPU).
 
-    python tools/trace_planner.py [c2|c1]
+    python tools/trace_planner.py [c2|c1] [topology]
 """
 import os
 import sys
@@ -20,6 +20,8 @@ if cfg == "c1":
 else:
     ids, lens = datagen.metadata("scenario", 8, codes=C2, step=0, seed=7)
     topo = "g1n4+g2n2"
+if len(sys.argv) > 2:
+    topo = sys.argv[2]
 dm = sb.DeviceMeta.from_lists(ids, lens)
 p = sb.Planner(topo, 8, max_seqs=sum(len(x) for x in ids))
 p.trace(True)
@@ -27,9 +29,15 @@ for _ in range(5):
     p.plan(dm)
 torch.cuda.synchronize()
 t = p.trace(True)
-names = ["load", "workload", "offsets", "dup", "totals", "sort", "greedy", "bases", "emit", "offsets2",
-         "rank_lists", "send", "wir"]
-d = np.diff(t[:14])
-for n, c in zip(names, d):
-    print(f"{n:12s} {int(c):8d} cycles")
+names = ["load", "seq+totals+offsets", "sort", "greedy+dup", "emit+wir", "lists", "ties"]
+marks = [int(x) for x in t[:7]] + [int(t[13])]
+for i, n in enumerate(names):
+    print(f"{n:20s} {marks[i + 1] - marks[i]:8d} cycles")
 print("total", int(t[13] - t[0]), "cycles")
+sub = {"P1 totals chain done": 11, "P4 per-seq pass done (max)": 10, "P5 offsets done (warp 0)": 7,
+       "P5 rank lists done (max)": 8, "P5 chunk emission done (max)": 12, "P5 send lists done (max)": 9}
+for k, i in sub.items():
+    if t[i] > 0:
+        print(f"  {k:32s} +{int(t[i] - t[0]):8d} cycles from start")
+if t[15] > t[14] > 0:
+    print("greedy chain (replica 0):", int(t[15] - t[14]), "cycles")
