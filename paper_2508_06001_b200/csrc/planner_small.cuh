@@ -125,6 +125,15 @@ __device__ void reg_sort_emit(int32_t* sorted_idx, uint64_t* s_hi, uint64_t* s_l
   }
 }
 
+// The greedy as its own (not inlined) function: inside the fused kernel's
+// body the chain was scheduled ~60 cycles per step slower than the same code
+// compiled alone (tools/micro/greedy_prod.cu).
+template <int BPL>
+__device__ __noinline__ void small_greedy(const PlanArgs& a, int rep, int64_t n, double total_rep, const double* ws,
+                                          int32_t* pick, int32_t* bagcnt, int* viol, int32_t* q) {
+  greedy_warp<BPL, 0, true>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, pick, bagcnt, viol, q);
+}
+
 // Warp-level inclusive scan helper over int64.
 __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_incl_scan<int64_t>(x); }
 
@@ -417,12 +426,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     for (int rep = warp; rep < R; rep += ng) {
       const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
       const double* ws = s_wsorted + lo;
-      if (M <= 32)
-        greedy_warp<1, 0, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo,
-                          s_bagcnt, &s_viol, s_q + lo);
-      else
-        greedy_warp<2, 0, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, s_pick + lo,
-                          s_bagcnt, &s_viol, s_q + lo);
+      if (M <= 32) small_greedy<1>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
+      else small_greedy<2>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
       __syncwarp();
       // replica-local chunk bases of the bags (chunk order: bag, q, k) and
       // the bags' first slots in the (replica, bag)-grouped sequence list

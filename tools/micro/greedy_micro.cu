@@ -660,9 +660,16 @@ __global__ void __launch_bounds__(VAR >= 6 ? 512 : 32) g_prod(const double* w_so
     const uint64_t best = key;
     const uint32_t best_j = (uint32_t)lane;
     const uint32_t khi = (uint32_t)(best >> 32), klo = (uint32_t)best;
-    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
-    const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
-    const uint32_t pk = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+    uint32_t m1, m2, pk;
+    if (VAR == 7) {  // inline-PTX redux.sync (bounds 512): does it avoid the divergence checks?
+      asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m1) : "r"(khi));
+      asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m2) : "r"(khi == m1 ? klo : 0xffffffffu));
+      asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(pk) : "r"((khi == m1 && klo == m2) ? best_j : 0xffffffffu));
+    } else {
+      m1 = __reduce_min_sync(0xffffffffu, khi);
+      m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      pk = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+    }
     if (VAR != 3 && VAR != 5) viol += (int)(m1 >> 31);
     const bool won = (uint32_t)lane == pk;
     if (VAR != 1 && VAR != 5 && won) s_q[p & 4095] = cnt;
@@ -769,6 +776,10 @@ int main() {
         for (int r = 0; r < 2; ++r) g_prod<6><<<1, 32, (n + 2) * 8>>>(dw, n, M, dcap, p6, dc, drep);
         cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
         printf("  prod-bounds512-alone %.1f cyc/seq (%s)\n", (double)c / n, cudaGetErrorString(cudaGetLastError()));
+        cudaFuncSetAttribute(g_prod<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
+        for (int r = 0; r < 2; ++r) g_prod<7><<<1, 512, (n + 2) * 8>>>(dw, n, M, dcap, p6, dc, drep);
+        cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+        printf("  prod-bounds512-asm-redux %.1f cyc/seq (%s)\n", (double)c / n, cudaGetErrorString(cudaGetLastError()));
         cudaFuncSetAttribute(g_prod<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 2) * 8);
       }
       run(g_diag<1>, "redux-chain-only");
