@@ -1120,21 +1120,24 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
   SB_CUDA(cudaMemsetAsync(p->violations, 0, sizeof(int32_t), s));
 }
 
-// Path choice.  The fused single-CTA planner wins while launches dominate
-// (256 sequences: 38 vs 88 us); its chunk phases are one CTA, so with many
-// chunks the multi-kernel path wins (2048 sequences, bags of 8 = 16 K
-// chunks: 363 vs 286 us; tools/plan_profile.py, profiles/r01b).
+// Path choice.  The fused single-CTA planner wins while launches dominate;
+// the multi-kernel path's fixed cost is ~50 us (a dozen launches) but its
+// greedy runs in a 32-thread kernel (~102 cycles per step against ~150 inside
+// the 512-thread fused CTA) and its sort / emission use many SMs.  Measured
+// crossover by graph replay (tools/path_compare.py, profiles/r02): multi-bag
+// 768 sequences 98 vs 103 us fused ahead, 1024 125 vs 118 multi-kernel
+// ahead; one bag per replica 512 46 vs 61 fused ahead, 768 66 vs 61 behind.
 constexpr int64_t kSmallChunks = 8192;
 
-constexpr int64_t kSmallAutoSeqs = 1536;
+constexpr int64_t kSmallAutoSeqs = 896;         // replicas with several bags
+constexpr int64_t kSmallAutoSeqsOneBag = 640;   // one bag per replica (no greedy chain)
 
 static bool use_small_path(const sb_planner* p) {
   if (p->path == 2) return false;
   const bool fits = p->max_seqs <= kSmallSeqs && p->W <= 1024 && p->M <= kMaxBags;
   if (p->path == 1) return fits;
-  // auto: the fused CTA wins up to ~1K sequences (one launch, no inter-kernel
-  // gaps); at 2K the multi-kernel path's parallel sort / emission is ~10 % faster
-  return fits && p->max_seqs <= kSmallAutoSeqs && p->max_chunks <= kSmallChunks;
+  const int64_t lim = p->M == 1 ? kSmallAutoSeqsOneBag : kSmallAutoSeqs;
+  return fits && p->max_seqs <= lim && p->max_chunks <= kSmallChunks;
 }
 
 // Shared-memory staging capacity of the serial-sum kernels (workloads of one
