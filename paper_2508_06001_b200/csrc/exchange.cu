@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
@@ -655,8 +656,14 @@ __global__ void k_rank_rows(const int64_t* lens, const int64_t* off, int64_t* ro
 // flight.  Used when every job is 16-byte aligned and pieces fit a stage
 // (always true for the route/Ulysses layouts here) and the destination is
 // local HBM.
-constexpr int kTmaStages = 3;
-constexpr size_t kTmaSmem = (size_t)kTmaStages * kPieceBytes;
+// Default ring: 2 stages x 3 CTAs per SM (192 KB of stages per SM).  C2 DiT
+// step, profiles/r02/tma_ring_sweep: 2x3 0.3126 ms, 3x2 0.315, 4x1 / 6x1
+// 0.3155 (pre_attn alone faster, 112 vs 116 us, but one 128-192 KB CTA per SM
+// leaves the side-stream plan / prepare kernels less room), 2x2 0.325, 3x1
+// 0.328, 2x1 0.396.  SEQBAL_TMA_RING=stages,ctas_per_sm overrides.
+constexpr int kTmaStages = 2;
+constexpr int kTmaCtasPerSm = 3;
+constexpr int kTmaMaxStages = 6;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -752,14 +759,15 @@ __device__ __forceinline__ PieceRef piece_of(const SbJob& j, int64_t k) {
 }
 
 __global__ void __launch_bounds__(32) k_copy_tma(const SbJob* __restrict__ jobs, const int64_t* __restrict__ piece_off,
-                                                 const int64_t* __restrict__ n_jobs_p, int hint) {
+                                                 const int64_t* __restrict__ n_jobs_p, int hint, int stages) {
   extern __shared__ __align__(128) unsigned char stage_mem[];
-  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  __shared__ __align__(8) uint64_t bars[kTmaMaxStages];
+  const int ns = stages;
   const int64_t n_jobs = *n_jobs_p;
   const int64_t total = piece_off[n_jobs];
   const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
   if (g0 >= g1 || threadIdx.x != 0) return;  // one elected lane drives the DMA ring
-  for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+  for (int s = 0; s < ns; ++s) mbar_init(&bars[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   int64_t lo = 0, hi = n_jobs;
   while (hi - lo > 1) {
@@ -791,16 +799,16 @@ __global__ void __launch_bounds__(32) k_copy_tma(const SbJob* __restrict__ jobs,
     bulk_commit();
   };
   const int64_t n = g1 - g0;
-  for (int64_t k = 0; k < kTmaStages && k < n; ++k) load(g0 + k, (int)k);
+  for (int64_t k = 0; k < ns && k < n; ++k) load(g0 + k, (int)k);
   for (int64_t k = 0; k < n; ++k) {
-    const int s = (int)(k % kTmaStages);
-    mbar_wait(&bars[s], (uint32_t)((k / kTmaStages) & 1));
+    const int s = (int)(k % ns);
+    mbar_wait(&bars[s], (uint32_t)((k / ns) & 1));
     store(g0 + k, s);
     // refill the stage whose store was issued one step ago, once it has
     // been read out of shared memory
-    if (k >= 1 && k - 1 + kTmaStages < n) {
+    if (k >= 1 && k - 1 + ns < n) {
       bulk_wait_read<1>();
-      load(g0 + k - 1 + kTmaStages, (int)((k - 1) % kTmaStages));
+      load(g0 + k - 1 + ns, (int)((k - 1) % ns));
     }
   }
   bulk_wait_all();
@@ -1091,11 +1099,20 @@ static void run_copy(sb_planner* p, cudaStream_t s, int fence_sys, bool tma_ok, 
 static void launch_copy(SbJob* jobs, int64_t* piece_off, int64_t* n_jobs, cudaStream_t s, int fence_sys,
                         bool tma_ok, int engine) {
   if (!fence_sys && tma_ok && engine == 1) {
-    static bool attr = false;
-    if (!attr) {
-      SB_CUDA(cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    static int stages = 0, per_sm = 0;  // ring depth x CTAs per SM
+    if (!stages) {
+      stages = kTmaStages;
+      per_sm = kTmaCtasPerSm;
+      if (const char* v = getenv("SEQBAL_TMA_RING")) {
+        int a = 0, b = 0;
+        if (sscanf(v, "%d,%d", &a, &b) == 2 && a >= 2 && a <= kTmaMaxStages && b >= 1 && b <= 8) {
+          stages = a;
+          per_sm = b;
+        }
+      }
+      SB_CUDA(cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(stages * kPieceBytes)));
       SB_CUDA(cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      attr = true;
     }
     copy_grid();
     static int tma_hint = -1;  // SEQBAL_TMA_HINT (see l2_policy)
@@ -1103,7 +1120,7 @@ static void launch_copy(SbJob* jobs, int64_t* piece_off, int64_t* n_jobs, cudaSt
       const char* v = getenv("SEQBAL_TMA_HINT");
       tma_hint = v ? atoi(v) : 0;
     }
-    k_copy_tma<<<g_num_sms * 2, 32, kTmaSmem, s>>>(jobs, piece_off, n_jobs, tma_hint);
+    k_copy_tma<<<g_num_sms * per_sm, 32, stages * kPieceBytes, s>>>(jobs, piece_off, n_jobs, tma_hint, stages);
   } else if (engine == 2) {
     k_copy<3><<<copy_grid(), kCopyThreads, 0, s>>>(jobs, piece_off, n_jobs, fence_sys);
   } else {

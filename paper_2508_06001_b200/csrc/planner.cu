@@ -637,13 +637,16 @@ __global__ void __launch_bounds__(256) k_emit_chunks(PlanArgs a) {
 // chunks in index order == send[r]) with its comparator.  Single thread;
 // lists of <= 16 entries are already identical (insertion sort is stable).
 __device__ void fix_rev_ties(int32_t* rev_recv_idx, const int32_t* send_idx, const int32_t* seq, const int64_t* st,
-                             int64_t off, int64_t n) {
+                             int64_t off, int64_t n, stdsort::Frame* stack) {
   if (n <= stdsort::kThreshold) return;
   for (int64_t i = 0; i < n; ++i) rev_recv_idx[off + i] = send_idx[off + i];
-  stdsort::sort(rev_recv_idx + off, n, [&](int32_t x, int32_t y) {
-    if (seq[x] != seq[y]) return seq[x] < seq[y];
-    return st[x] < st[y];
-  });
+  stdsort::sort(
+      rev_recv_idx + off, n,
+      [&](int32_t x, int32_t y) {
+        if (seq[x] != seq[y]) return seq[x] < seq[y];
+        return st[x] < st[y];
+      },
+      stack);
 }
 
 // ----------------------------------------------------------------- k_lists
@@ -829,8 +832,11 @@ __global__ void k_finalize(PlanArgs a) {
   // ranks whose reverse receive order can tie: replay std::sort now that
   // send[r] (its input order) is complete; one lane per rank
   for (int r = threadIdx.x; r < a.W; r += blockDim.x)
-    if (a.list_tie[r])
-      fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, a.send_off[r], a.send_off[r + 1] - a.send_off[r]);
+    if (a.list_tie[r]) {
+      stdsort::Frame stk[stdsort::kStackFrames];
+      fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, a.send_off[r], a.send_off[r + 1] - a.send_off[r],
+                   stk);
+    }
 }
 
 }  // namespace sb
@@ -927,10 +933,11 @@ __global__ void __launch_bounds__(1024) k_generic_lists(GenericArgs a) {
   if (tid == 0) {
     const uint64_t* seg = a.ck_hi;
     const int64_t* st = a.c_start;
+    stdsort::Frame stk[stdsort::kStackFrames];
     stdsort::sort(a.rev_recv_idx + s_so, cs, [&](int32_t x, int32_t y) {
       if (seg[x] != seg[y]) return seg[x] < seg[y];
       return st[x] < st[y];
-    });
+    }, stk);
   }
   (void)smem;
 }

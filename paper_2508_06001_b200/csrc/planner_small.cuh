@@ -125,11 +125,11 @@ __device__ void reg_sort_emit(int32_t* sorted_idx, uint64_t* s_hi, uint64_t* s_l
   }
 }
 
-// The greedy as its own (not inlined) function: inside the fused kernel's
-// body the chain was scheduled ~60 cycles per step slower than the same code
-// compiled alone (tools/micro/greedy_prod.cu).
+// The greedy inlined (an out-of-line call gave the same ~150 cycles per step
+// and a larger stack frame that lengthened every launch by ~4 us,
+// tools/plan_latency.py).
 template <int BPL>
-__device__ __noinline__ void small_greedy(const PlanArgs& a, int rep, int64_t n, double total_rep, const double* ws,
+__device__ __forceinline__ void small_greedy(const PlanArgs& a, int rep, int64_t n, double total_rep, const double* ws,
                                           int32_t* pick, int32_t* bagcnt, int* viol, int32_t* q) {
   greedy_warp<BPL, 0, true>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, pick, bagcnt, viol, q);
 }
@@ -702,8 +702,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
   __syncthreads();  // send lists complete: reverse-order tie replay reads them
   SB_PHASE(6);
   for (int r = warp; r < W; r += nw)
-    if (lane == 0 && s_tie[r])
-      fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r]);
+    if (lane == 0 && s_tie[r]) {
+      stdsort::Frame stk[stdsort::kStackFrames];
+      fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r], stk);
+    }
   SB_PHASE(13);
 }
 
