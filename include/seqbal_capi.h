@@ -78,8 +78,8 @@ typedef struct sb_planner_desc {
 /* Validates like WorkloadModel::validate (workload_model.cpp:15-31),
  * replicate (topology.cpp:81-93) and plan_routing's head check
  * (balancer.cpp:114-120); SB_ERR_CONFIG with the reference's message.
- * Limits: at most 64 bags per replica (SB_ERR_CONFIG "more than 64 bags per
- * replica"; the reference has none).  All four shape fields 0 create an
+ * Limits: at most 1024 bags per replica (SB_ERR_CONFIG "more than 1024 bags
+ * per replica"; the reference has none; above 64 the multi-kernel path runs).  All four shape fields 0 create an
  * assignment-only planner for sb_assign_to_bags (no model, no head check);
  * sb_plan / sb_plan_identity refuse it. */
 SB_API sb_status sb_planner_create(const sb_planner_desc* desc, sb_planner** out);

@@ -9,7 +9,8 @@
 
 namespace sb {
 
-constexpr int kMaxBags = 64;  // bags per replica handled by k_emit's shared tables
+constexpr int kMaxBags = 64;         // bags per replica on the fused planner and the register greedy
+constexpr int kMaxBagsLarge = 1024;  // bags per replica on the multi-kernel path (k_greedy_many, k_emit tables)
 
 struct PlanArgs {
   int W, U, M, R;

@@ -414,6 +414,68 @@ __global__ void __launch_bounds__(32) k_greedy(PlanArgs a) {
                    nullptr, a.violations);
 }
 
+// More than kMaxBags bags per replica (up to kMaxBagsLarge): the same
+// decision per step (balancer.cpp:44-62) without the register speculation --
+// every lane walks its bags (j = lane, lane + 32, ...) in shared memory,
+// forms key = (infeasible, bits(occupancy)) with the exact division, keeps the
+// first minimum, and the warp takes the lexicographic (key, bag) minimum by
+// three REDUX; the winner's lane adds the workload.  Same arithmetic as
+// greedy_warp (occupancy_sel == __ddiv_rn, tests/test_gpu_parity.py), so the
+// picks and the FP64 report are identical; ~BPL times slower per step.
+__global__ void __launch_bounds__(32) k_greedy_many(PlanArgs a) {
+  extern __shared__ __align__(16) double gm[];  // cap[M], asg[M], then cnt[M] (int)
+  if (!seqs_ok(a)) return;
+  const int rep = blockIdx.x, lane = threadIdx.x, M = a.M;
+  double* cap = gm;
+  double* asg = gm + M;
+  int* cnt = reinterpret_cast<int*>(gm + 2 * M);
+  const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+  const int n = (int)(hi - lo);
+  const double target = __ddiv_rn(a.rep_total[rep], (double)a.U);  // balancer.cpp:26
+  for (int j = lane; j < M; j += 32) {
+    cap[j] = __dmul_rn((double)a.bag_size[j], target);  // balancer.cpp:30
+    asg[j] = 0.0;
+    cnt[j] = 0;
+  }
+  __syncwarp();
+  const double* sw = a.sorted_w + lo;
+  int viol = 0;
+  double w_next = n > 0 ? sw[0] : 0.0;
+  for (int p = 0; p < n; ++p) {
+    const double w = w_next;
+    w_next = p + 1 < n ? sw[p + 1] : 0.0;  // prefetch under this step
+    uint64_t best = ~0ull;
+    uint32_t best_j = 0xffffffffu;
+    for (int j = lane; j < M; j += 32) {
+      const double o = occupancy(asg[j], cap[j]);
+      const uint64_t key = greedy_key(__dsub_rn(cap[j], asg[j]) >= w, o);
+      if (key < best) {  // strict: the lower bag of this lane keeps ties
+        best = key;
+        best_j = (uint32_t)j;
+      }
+    }
+    const uint32_t khi = (uint32_t)(best >> 32), klo = (uint32_t)best;
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+    const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+    const uint32_t pick = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+    viol += (int)(m1 >> 31);  // winner infeasible: fallback pick == capacity violation
+    if ((int)(pick & 31u) == lane) {
+      asg[pick] = __dadd_rn(asg[pick], w);
+      cnt[pick] += 1;
+    }
+    if (lane == 0) a.pick[lo + p] = (int)pick;
+    __syncwarp();
+  }
+  for (int j = lane; j < M; j += 32) {
+    a.bag_count[rep * M + j] = cnt[j];
+    a.per_bag_occ[rep * M + j] = occupancy(asg[j], cap[j]);  // balancer.cpp:170-175 (replay == greedy)
+    const int g = a.bag_size[j];
+    const double per = __ddiv_rn(asg[j], (double)g);  // balancer.cpp:199-202
+    for (int k = 0; k < g; ++k) a.per_gpu[rep * a.U + a.bag_ranks[a.bag_off[j] + k]] = per;
+  }
+  if (lane == 0) atomicAdd(a.violations, viol);
+}
+
 // One bag per replica: the picks (all bag 0) and bag counts (replica sizes)
 // are known before the serial FP64 prefix runs, so emission and the lists
 // start at once while greedy_single_bag's chain runs on the side stream.
@@ -508,7 +570,7 @@ __global__ void __launch_bounds__(kSumThreads) k_selftest_sum(uint64_t seed, int
 constexpr int kEmitTile = 1024;
 
 __global__ void __launch_bounds__(kEmitTile) k_emit_count(PlanArgs a) {
-  __shared__ int cnt[kMaxBags];
+  extern __shared__ int cnt[];  // M counters
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.y, tile = blockIdx.x;
   const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
@@ -525,12 +587,13 @@ __global__ void __launch_bounds__(kEmitTile) k_emit_count(PlanArgs a) {
   }
   const int64_t p0 = lo + (int64_t)tile * kEmitTile;
   if (p0 >= hi) return;
-  if (threadIdx.x < a.M) cnt[threadIdx.x] = 0;
+  for (int b = threadIdx.x; b < a.M; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
   const int64_t p = p0 + threadIdx.x;
   if (p < hi) atomicAdd(&cnt[a.pick[p]], 1);
   __syncthreads();
-  if (threadIdx.x < a.M) a.tile_cnt[((int64_t)rep * gridDim.x + tile) * a.M + threadIdx.x] = cnt[threadIdx.x];
+  for (int b = threadIdx.x; b < a.M; b += blockDim.x)
+    a.tile_cnt[((int64_t)rep * gridDim.x + tile) * a.M + b] = cnt[b];
 }
 
 // Phase A2 (same grid): q = rank of each pick among its bag's picks in
@@ -539,7 +602,8 @@ __global__ void __launch_bounds__(kEmitTile) k_emit_count(PlanArgs a) {
 // per-sequence fields and the inverse map bag_seq[(bag, q)] = s that lets
 // phase B emit chunks in parallel.
 __global__ void __launch_bounds__(kEmitTile) k_emit(PlanArgs a) {
-  __shared__ int warp_cnt[kEmitTile / 32][kMaxBags];
+  extern __shared__ int wc[];  // per-warp bag counts: [kEmitTile / 32][M]
+  auto warp_cnt = [&](int w, int b) -> int& { return wc[w * a.M + b]; };
   __shared__ int64_t rep_base;
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.y, tile = blockIdx.x;
@@ -561,23 +625,23 @@ __global__ void __launch_bounds__(kEmitTile) k_emit(PlanArgs a) {
   const int b = valid ? a.pick[p] : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, b);
   const int rank_in = __popc(peers & ((1u << lane) - 1u));
-  for (int e = tid; e < (kEmitTile / 32) * a.M; e += blockDim.x) warp_cnt[e / a.M][e % a.M] = 0;
+  for (int e = tid; e < (kEmitTile / 32) * a.M; e += blockDim.x) wc[e] = 0;
   __syncthreads();
-  if (valid && rank_in == 0) warp_cnt[warp][b] = __popc(peers);
+  if (valid && rank_in == 0) warp_cnt(warp, b) = __popc(peers);
   __syncthreads();
-  if (tid < a.M) {  // exclusive prefix over earlier tiles, then over this tile's warps
+  for (int bb = tid; bb < a.M; bb += blockDim.x) {  // exclusive prefix over earlier tiles, then over this tile's warps
     int run = 0;
-    const int* tc = a.tile_cnt + (int64_t)rep * gridDim.x * a.M + tid;
+    const int* tc = a.tile_cnt + (int64_t)rep * gridDim.x * a.M + bb;
     for (int t = 0; t < tile; ++t) run += tc[(int64_t)t * a.M];
     for (int w = 0; w < kEmitTile / 32; ++w) {
-      const int c = warp_cnt[w][tid];
-      warp_cnt[w][tid] = run;
+      const int c = warp_cnt(w, bb);
+      warp_cnt(w, bb) = run;
       run += c;
     }
   }
   __syncthreads();
   if (!valid) return;
-  const int q = warp_cnt[warp][b] + rank_in;
+  const int q = warp_cnt(warp, b) + rank_in;
   const int s = a.sorted_idx[p];
   const int g = a.bag_size[b];
   a.bag_seq[a.bag_sbase[rep * a.M + b] + q] = s;
@@ -604,15 +668,22 @@ __global__ void __launch_bounds__(256) k_emit_chunks(PlanArgs a) {
     }
     rep = l;
   }
-  int64_t rel = c - a.rep_cbase[rep], sq = a.rank_off[rep * a.U];
+  int64_t rel = c - a.rep_cbase[rep];
   int b = 0;
-  for (;; ++b) {
-    const int64_t nb = a.bag_count[rep * a.M + b];
-    const int64_t span = nb * a.bag_size[b];
-    if (rel < span || b == a.M - 1) break;
-    rel -= span;
-    sq += nb;
+  {
+    // last bag whose replica-local chunk base is <= rel (an empty bag shares
+    // its base with the next bag, so the search lands on the non-empty one)
+    const int64_t* cbase = a.bag_cbase + (int64_t)rep * a.M;
+    int l = 0, h = a.M;
+    while (h - l > 1) {
+      const int m = (l + h) >> 1;
+      if (cbase[m] <= rel) l = m;
+      else h = m;
+    }
+    b = l;
+    rel -= cbase[b];
   }
+  const int64_t sq = a.bag_sbase[rep * a.M + b];
   const int g = a.bag_size[b];
   const int64_t q = rel / g;
   const int k = (int)(rel - q * g);
@@ -1237,6 +1308,12 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool
     count_launch(1);  // the callers count one greedy launch
     return;
   }
+  if (p->M > kMaxBags) {
+    const int smem = (int)((2 * sizeof(double) + sizeof(int)) * p->M);
+    k_greedy_many<<<p->R, 32, smem, s>>>(a);
+    SB_CHECK_LAUNCH();
+    return;
+  }
   const bool wide = (p->M + 31) / 32 > 1;
   if (p->max_seqs <= kGreedyStage) {
     const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
@@ -1276,9 +1353,17 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   launch_greedy(p, a, s, true);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[3], s));
   const dim3 eg((unsigned)((p->max_seqs + kEmitTile - 1) / kEmitTile), (unsigned)p->R);
-  k_emit_count<<<eg, kEmitTile, 0, s>>>(a);
+  const int emit_smem = (int)(sizeof(int) * (kEmitTile / 32) * p->M);
+  if (emit_smem > 48 * 1024) {
+    static int set_to = 0;
+    if (emit_smem > set_to) {
+      SB_CUDA(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, emit_smem));
+      set_to = emit_smem;
+    }
+  }
+  k_emit_count<<<eg, kEmitTile, sizeof(int) * p->M, s>>>(a);
   SB_CHECK_LAUNCH();
-  k_emit<<<eg, kEmitTile, 0, s>>>(a);
+  k_emit<<<eg, kEmitTile, emit_smem, s>>>(a);
   SB_CHECK_LAUNCH();
   k_emit_chunks<<<(int)((p->max_chunks + 255) / 256), 256, 0, s>>>(a);
   SB_CHECK_LAUNCH();
@@ -1352,8 +1437,8 @@ extern "C" sb_status sb_planner_create(const sb_planner_desc* d, sb_planner** ou
   if (d->world_size % d->unit_size != 0)
     throw Error{SB_ERR_CONFIG, "world_size " + std::to_string(d->world_size) +
                                    " is not a multiple of the sharding unit " + std::to_string(d->unit_size)};
-  if (d->n_bags > sb::kMaxBags)
-    throw Error{SB_ERR_CONFIG, "more than " + std::to_string(sb::kMaxBags) + " bags per replica"};
+  if (d->n_bags > sb::kMaxBagsLarge)
+    throw Error{SB_ERR_CONFIG, "more than " + std::to_string(sb::kMaxBagsLarge) + " bags per replica"};
   auto* p = new sb_planner();
   p->W = d->world_size;
   p->U = d->unit_size;

@@ -118,8 +118,27 @@ static void test_assign() {
     for (int i = 0; same && i < 60; ++i) same = got[i].sample_id == oi[i] && got[i].assigned_bag == ob[i];
     CHECK(same);
   }
-  // documented limit: at most 64 bags per replica
-  CHECK_THROWS(assign_to_bags({{0, 1}}, single_bags(65)), ConfigError);
+  // more than 64 bags (the multi-kernel path's k_greedy_many) vs the oracle;
+  // documented limit: at most 1024 bags per replica
+  {
+    const int m = 100, n = 700;
+    std::vector<SequenceWorkload> w;
+    std::vector<uint64_t> ids, oi(n);
+    std::vector<double> ws, ow(n);
+    std::vector<int> sizes(m, 1), bid(m), ob(n);
+    for (int j = 0; j < m; ++j) bid[j] = j;
+    for (int i = 0; i < n; ++i) {
+      w.push_back({static_cast<uint64_t>(i * 13 + 5), static_cast<double>((i * 7919) % 997 + (i % 3 == 0 ? 0 : 1000))});
+      ids.push_back(w.back().sample_id);
+      ws.push_back(w.back().workload);
+    }
+    auto got = assign_to_bags(w, single_bags(m));
+    or_assign_to_bags(n, ids.data(), ws.data(), m, sizes.data(), bid.data(), oi.data(), ow.data(), ob.data());
+    bool same = got.size() == static_cast<size_t>(n);
+    for (int i = 0; same && i < n; ++i) same = got[i].sample_id == oi[i] && got[i].assigned_bag == ob[i];
+    CHECK(same);
+  }
+  CHECK_THROWS(assign_to_bags({{0, 1}}, single_bags(1025)), ConfigError);
   // random instances vs the oracle, heterogeneous bags
   Rng rng(99);
   for (int trial = 0; trial < 50; ++trial) {
@@ -271,11 +290,11 @@ static void test_reverse_plan() {
     CHECK(ok && ip.chunks.size() == n);
     CHECK(reverse_plan(ip) == ip);
   }
-  // documented limit: plan_routing with more than 64 bags per replica
+  // documented limit: plan_routing with more than 1024 bags per replica
   {
-    std::vector<std::vector<SequenceInfo>> s65(65);
-    s65[0].push_back({1, 10});
-    CHECK_THROWS(plan_routing(s65, WorkloadModel{}, replicate(parse_topology("g1n65"), 65)), ConfigError);
+    std::vector<std::vector<SequenceInfo>> s1025(1025);
+    s1025[0].push_back({1, 10});
+    CHECK_THROWS(plan_routing(s1025, WorkloadModel{}, replicate(parse_topology("g1n1025"), 1025)), ConfigError);
   }
 }
 

@@ -407,6 +407,45 @@ def test_many_replicas_vs_oracle(world, topo, path):
     assert Cw.checksum() == A.checksum()
 
 
+@pytest.mark.parametrize("world,topo", [(96, "g1n96"), (96, "g1n64+g2n16"), (400, "g2n200"), (130, "g1n65")])
+def test_many_bags_vs_oracle(world, topo):
+    """More than 64 bags per replica (multi-kernel path, k_greedy_many and the
+    emission tables in dynamic shared memory): plan, report and data path equal
+    the reference's; the reference has no bag limit, the device path 1024."""
+    rng = np.random.default_rng(len(topo) + world)
+    lens = [rng.integers(0, 4000, size=rng.integers(0, 9)).tolist() for _ in range(world)]
+    meta = oracle.meta_explicit(lens)
+    planner = sb.Planner(topo, world, max_seqs=max(1, sum(len(x) for x in lens)))
+    planner.plan(device_meta(meta))
+    hp = planner.download()
+    plan, rep = oracle.plan_routing(meta, oracle.parse_topology(topo))
+    got = host_plan_as_oracle(hp, meta)
+    assert got.chunk_rows() == plan.chunk_rows()
+    assert got.send == plan.send and got.recv == plan.recv
+    assert [dbits(x) for x in hp.per_gpu_workload] == [dbits(x) for x in rep.per_gpu_workload]
+    assert [dbits(x) for x in hp.per_bag_occupancy] == [dbits(x) for x in rep.per_bag_occupancy]
+    assert dbits(hp.wir) == dbits(rep.wir) and dbits(hp.total_workload) == dbits(rep.total_workload)
+    assert hp.capacity_violations == rep.capacity_violations
+    assert hp.rev_recv == oracle.reverse_plan(plan).recv
+    rows = int(sum(sum(x) for x in lens))
+    mk = lambda: sb.World(world, 24, [192], capacity_rows=max(1, rows), max_bag=planner.max_bag)
+    A, B, Cw, D, E = mk(), mk(), mk(), mk(), mk()
+    dm = device_meta(meta)
+    A.layout_origin(dm)
+    A.fill_witness(dm)
+    sb.route(planner, A, B)
+    sb.pre_attn(planner, B, Cw)
+    sb.post_attn(planner, Cw, D)
+    sb.reverse_route(planner, D, E)
+    E.status()
+    assert E.compare(A) == 0 and D.compare(B) == 0
+
+
+def test_bag_limit_is_config_error():
+    with pytest.raises(sb.ConfigError, match="more than 1024 bags per replica"):
+        sb.Planner("g1n1025", 1025, max_seqs=8)
+
+
 @pytest.mark.parametrize("path", ["small", "large"])
 def test_empty_replicas_vs_oracle(path):
     """Whole replicas without sequences (first and last of three): chunk bases,
