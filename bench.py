@@ -246,7 +246,8 @@ def run_c4(args):
                 graph_us = 1000 * t0.elapsed_time(t1) / k
                 hp = planner.download()
                 per = hp.per_gpu_workload
-                rows.append({"sequences": n, "topology": topo, "chunks": hp.n_chunks, "plan_us": graph_us,
+                rows.append({"sequences": n, "topology": topo, "path": planner.last_path(), "chunks": hp.n_chunks,
+                             "plan_us": graph_us,
                              "plan_us_eager": eager_us, "wir": hp.wir,
                              "max_mean": float(per.max() / per.mean()) if per.mean() > 0 else 1.0})
                 del g, planner
@@ -770,7 +771,12 @@ def run_single(args, cfg, topology):
     torch.cuda.synchronize()
     tr = planner.trace(True)
     planner.trace(False)
-    if tr[13] > tr[0] > 0:
+    if planner.last_path() == "hybrid" and tr[13] > tr[11] > 0 and tr[12] > tr[0] > 0:
+        # three kernels on (possibly) different SMs: per-kernel cycle spans
+        parts = {"prefix (load, seq, sort)": int(tr[12] - tr[0]), "greedy kernel chain": int(tr[15] - tr[14]),
+                 "suffix (reload, bases+dup, emit+wir, lists, ties)": int(tr[13] - tr[11])}
+        plan_breakdown = {"path": "hybrid", "total_cycles": sum(parts.values()), "cycles": parts}
+    elif tr[13] > tr[0] > 0:
         # phase marks 0..6 and the end mark 13 (planner_small.cuh)
         pnames = ["load", "seq+totals+offsets", "sort", "greedy+dup", "emit+wir", "lists", "ties"]
         marks = [int(x) for x in tr[:7]] + [int(tr[13])]

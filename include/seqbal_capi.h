@@ -150,10 +150,14 @@ typedef struct sb_plan_host {
 } sb_plan_host;
 SB_API sb_status sb_plan_download(sb_planner* p, sb_plan_host* out, sb_stream stream);
 
-/* Planner pipeline: 0 = auto (single-CTA fused planner when the capacity is
- * at most 2048 sequences, else the multi-kernel pipeline), 1 = force the
- * fused planner, 2 = force the multi-kernel pipeline.  Both are bit-exact. */
+/* Planner pipeline: 0 = auto (by capacity: the single-CTA fused planner for
+ * small batches, the hybrid -- fused prefix, 32-thread greedy kernel, fused
+ * suffix -- up to 2048 sequences, else the multi-kernel pipeline), 1 = force
+ * the fused planner, 2 = force the multi-kernel pipeline, 3 = force the
+ * hybrid.  All are bit-exact. */
 SB_API sb_status sb_planner_set_path(sb_planner* p, int path);
+/* The pipeline the last sb_plan ran: 1 fused, 2 multi-kernel, 3 hybrid. */
+SB_API sb_status sb_planner_last_path(sb_planner* p, int* path);
 /* Self-test: the planner's fast correctly-rounded division against
  * __ddiv_rn on n random operand pairs; *mismatches must be 0. */
 SB_API sb_status sb_selftest_div(int64_t n, uint64_t seed, int64_t* mismatches);

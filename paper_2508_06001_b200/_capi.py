@@ -91,6 +91,7 @@ _SIGS = {
     "sb_plan_download": (C.c_int, [C.c_void_p] * 3),
     "sb_planner_enable_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "sb_planner_set_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "sb_planner_last_path": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "sb_planner_trace": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "sb_selftest_div": (C.c_int, [C.c_int64, C.c_uint64, C.c_void_p]),
     "sb_selftest_serial_sum": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_void_p]),

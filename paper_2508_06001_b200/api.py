@@ -282,8 +282,15 @@ class Planner:
         call("sb_exchange_run", self._h, slot, _stream(stream))
 
     def set_path(self, path: str):
-        """'auto' | 'small' (fused single-CTA planner) | 'large' (multi-kernel)."""
-        call("sb_planner_set_path", self._h, {"auto": 0, "small": 1, "large": 2}[path])
+        """'auto' | 'small' (fused single-CTA planner) | 'large' (multi-kernel) |
+        'hybrid' (fused prefix, 32-thread greedy kernel, fused suffix)."""
+        call("sb_planner_set_path", self._h, {"auto": 0, "small": 1, "large": 2, "hybrid": 3}[path])
+
+    def last_path(self) -> str:
+        """Which pipeline the last plan ran ('small', 'large', 'hybrid'; '' before any)."""
+        v = C.c_int()
+        call("sb_planner_last_path", self._h, C.byref(v))
+        return {0: "", 1: "small", 2: "large", 3: "hybrid"}[v.value]
 
     def trace(self, enable: bool = True):
         """Per-phase clock64 deltas of the fused planner's last run (diagnostics)."""

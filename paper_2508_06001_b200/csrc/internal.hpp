@@ -31,7 +31,8 @@ struct sb_planner {
   bool identity = false;
   bool any_multi_bag = false;
   bool uploaded = false;  // current plan came from sb_plan_upload (no bag tables)
-  int path = 0;           // planner pipeline: 0 auto, 1 single-CTA small, 2 multi-kernel
+  int path = 0;           // planner pipeline: 0 auto, 1 single-CTA small, 2 multi-kernel, 3 hybrid
+  int last_path = 0;      // what the last sb_plan ran: 1 single-CTA, 2 multi-kernel, 3 hybrid
   long long* trace = nullptr;  // per-phase clock64 stamps of the fused planner (diagnostics)
   size_t small_smem = 0;  // dynamic shared memory of the small path
   // origin layout of an uploaded plan (segment CSR), kept for reverse_plan
@@ -66,6 +67,7 @@ struct sb_planner {
   int32_t* sorted_idx = nullptr;
   int32_t* pick = nullptr;
   int32_t* seq_bag = nullptr;
+  int32_t* greedy_q = nullptr;  // hybrid path: rank of each greedy position inside its bag
   int32_t* seq_G = nullptr;
   int64_t* seq_chunk_base = nullptr;
 

@@ -31,6 +31,7 @@ struct PlanArgs {
   int32_t* sorted_idx;
   int32_t* pick;
   int32_t *seq_bag, *seq_G;
+  int32_t* greedy_q;  // hybrid path: the greedy kernel's per-position rank inside the bag
   int64_t* seq_chunk_base;
   double* rep_total;
   int32_t* sentinel;

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kSumThreads) k_totals(PlanArgs a, int64_t stag
 // sequence); larger ones stream through the ring.
 constexpr int kGreedyStage = 24576;  // 192 KB of workloads
 
-template <int BPL>
+template <int BPL, bool QOUT = false>
 __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
   extern __shared__ __align__(16) double stage[];
   if (!seqs_ok(a)) return;
@@ -388,8 +388,8 @@ __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
   const double* sw = a.sorted_w + lo;
   for (int i = lane; i < n; i += 32) stage[i] = sw[i];
   __syncwarp();
-  greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
-                      nullptr, a.violations);
+  greedy_warp<BPL, 0, QOUT>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {},
+                            a.pick + lo, nullptr, a.violations, QOUT ? a.greedy_q + lo : nullptr);
 }
 
 template <int BPL>
@@ -1088,6 +1088,7 @@ static PlanArgs make_args(sb_planner* p) {
   a.sk_v = p->sk_v; a.tk_v = p->tk_v;
   a.sorted_w = p->sorted_w; a.sorted_idx = p->sorted_idx; a.pick = p->pick;
   a.seq_bag = p->seq_bag; a.seq_G = p->seq_G; a.seq_chunk_base = p->seq_chunk_base;
+  a.greedy_q = p->greedy_q;
   a.rep_total = p->rep_total; a.sentinel = p->sentinel; a.bag_count = p->bag_count;
   a.bag_rows = p->bag_rows; a.rep_chunks = p->rep_chunks; a.send_count = p->send_count;
   a.rep_cbase = p->rep_cbase; a.bag_seq = p->bag_seq;
@@ -1115,7 +1116,7 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->sk_hi, N); dalloc(&p->sk_lo, N); dalloc(&p->tk_hi, N); dalloc(&p->tk_lo, N);
   dalloc(&p->sk_v, N); dalloc(&p->tk_v, N);
   dalloc(&p->sorted_w, N); dalloc(&p->sorted_idx, N); dalloc(&p->pick, N);
-  dalloc(&p->seq_bag, N); dalloc(&p->seq_G, N); dalloc(&p->seq_chunk_base, N);
+  dalloc(&p->seq_bag, N); dalloc(&p->seq_G, N); dalloc(&p->seq_chunk_base, N); dalloc(&p->greedy_q, N);
   dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
   dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
   dalloc(&p->rep_cbase, R + 1); dalloc(&p->bag_seq, N);
@@ -1142,7 +1143,9 @@ static void planner_alloc(sb_planner* p) {
     p->small_smem = small_layout((int)p->max_seqs, p->W, p->R * p->M, p->R, p->U, p->M).total;
     static size_t set_to = 0;  // attribute is per function: keep the largest requested
     if (p->small_smem > set_to) {
-      SB_CUDA(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->small_smem));
+      SB_CUDA(cudaFuncSetAttribute(k_plan_small<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->small_smem));
+      SB_CUDA(cudaFuncSetAttribute(k_plan_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->small_smem));
+      SB_CUDA(cudaFuncSetAttribute(k_plan_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->small_smem));
       set_to = p->small_smem;
     }
   }
@@ -1168,7 +1171,7 @@ static void planner_free(sb_planner* p) {
                   p->stage_ids, p->stage_lens, p->stage_w, p->stage_off,
                   p->seg_off, p->seg_id, p->seg_first, p->seg_len, p->recv_count, p->ck_hi, p->ck_lo,
                   p->ck_thi, p->ck_tlo, p->ck_v, p->ck_tv, p->rep_cbase, p->bag_seq, p->tile_cnt, p->list_sum, p->list_tie,
-                  p->bag_cbase, p->bag_sbase};
+                  p->bag_cbase, p->bag_sbase, p->greedy_q};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->h_small) cudaFreeHost(p->h_small);
@@ -1201,21 +1204,30 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
 // Path choice.  The fused single-CTA planner wins while launches dominate;
 // the multi-kernel path's fixed cost is ~50 us (a dozen launches) but its
 // greedy runs in a 32-thread kernel (~102 cycles per step against ~150 inside
-// the 512-thread fused CTA) and its sort / emission use many SMs.  Measured
-// crossover by graph replay (tools/path_compare.py, profiles/r02): multi-bag
-// 768 sequences 98 vs 103 us fused ahead, 1024 125 vs 118 multi-kernel
-// ahead; one bag per replica 512 46 vs 61 fused ahead, 768 66 vs 61 behind.
+// the 512-thread fused CTA) and its sort / emission use many SMs; the hybrid
+// (fused prefix, 32-thread greedy kernel, fused suffix) pays two kernel
+// boundaries and a reload for the faster chain.  Measured by graph replay
+// (tools/path_compare.py, profiles/r02/s3_planner/path_compare.txt), g1n8:
+// 256 sequences fused 35 / hybrid 37 / multi-kernel 65 us, 512 64 / 60 / 84,
+// 768 96 / 91 / 99, 1024 126 / 113-125 / 116-118 (g2n4, g4n2 favour the
+// multi-kernel path there); one bag per replica 512 46 vs 61 fused ahead,
+// 768 66 vs 61 behind.
 constexpr int64_t kSmallChunks = 8192;
 
-constexpr int64_t kSmallAutoSeqs = 896;         // replicas with several bags
 constexpr int64_t kSmallAutoSeqsOneBag = 640;   // one bag per replica (no greedy chain)
+constexpr int64_t kHybridAutoSeqs = 384;        // hybrid from here (see choose_path) ...
+constexpr int64_t kHybridAutoMaxSeqs = 896;     // ... up to here, multi-kernel above
 
-static bool use_small_path(const sb_planner* p) {
-  if (p->path == 2) return false;
+// 1 = fused single CTA, 2 = multi-kernel, 3 = hybrid (fused prefix, 32-thread
+// greedy kernel, fused suffix).
+static int choose_path(const sb_planner* p) {
   const bool fits = p->max_seqs <= kSmallSeqs && p->W <= 1024 && p->M <= kMaxBags;
-  if (p->path == 1) return fits;
-  const int64_t lim = p->M == 1 ? kSmallAutoSeqsOneBag : kSmallAutoSeqs;
-  return fits && p->max_seqs <= lim && p->max_chunks <= kSmallChunks;
+  if (p->path == 2 || !fits) return 2;
+  if (p->path == 1) return 1;
+  if (p->path == 3) return 3;
+  if (p->M == 1) return p->max_seqs <= kSmallAutoSeqsOneBag && p->max_chunks <= kSmallChunks ? 1 : 2;
+  if (p->max_chunks > kSmallChunks || p->max_seqs > kHybridAutoMaxSeqs) return 2;
+  return p->max_seqs < kHybridAutoSeqs ? 1 : 3;
 }
 
 // Shared-memory staging capacity of the serial-sum kernels (workloads of one
@@ -1334,13 +1346,55 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool
 
 static void run_plan(sb_planner* p, cudaStream_t s) {
   PlanArgs a = make_args(p);
-  if (use_small_path(p)) {  // one launch: the kernel clears the status word itself
+  p->last_path = choose_path(p);
+  if (p->last_path == 1) {  // one launch: the kernel clears the status word itself
     if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
-    k_plan_small<<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
+    k_plan_small<0><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
     SB_CHECK_LAUNCH();
     if (p->timing)
       for (int i = 1; i < 6; ++i) SB_CUDA(cudaEventRecord(p->ev[i], s));
     count_launch(1);
+    return;
+  }
+  if (p->last_path == 3) {
+    // hybrid: prefix (phases 0-2; clears status and violations) -> 32-thread
+    // greedy kernel -> suffix (phases 3-6); the duplicate-id check runs on the
+    // side stream beside the greedy kernel.  (Measured slower: forking the
+    // check before the prefix behind a status memset, 256 sequences 42 vs 37
+    // us, and programmatic dependent launch of the last two kernels.)
+    if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
+    k_plan_small<1><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
+    SB_CHECK_LAUNCH();
+    {
+      const int dsmem = (int)(sizeof(uint64_t) * 2 * small_pow2((int)p->max_seqs));
+      static int dset = 0;
+      if (dsmem > 48 * 1024 && dsmem > dset) {
+        SB_CUDA(cudaFuncSetAttribute(k_dup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
+        dset = dsmem;
+      }
+      SB_CUDA(cudaEventRecord(p->fork_ev, s));
+      SB_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
+      k_dup_small<<<1, kSmallThreads, dsmem, p->side>>>(a, (int)p->max_seqs);
+      SB_CHECK_LAUNCH();
+      SB_CUDA(cudaEventRecord(p->join_ev, p->side));
+    }
+    const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
+    static int set_to[2] = {0, 0};
+    const bool wide = p->M > 32;
+    if (smem > set_to[wide]) {
+      if (wide) SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      else SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      set_to[wide] = smem;
+    }
+    if (wide) k_greedy_staged<2, true><<<p->R, 32, smem, s>>>(a);
+    else k_greedy_staged<1, true><<<p->R, 32, smem, s>>>(a);
+    SB_CHECK_LAUNCH();
+    SB_CUDA(cudaStreamWaitEvent(s, p->join_ev, 0));  // duplicate check joined
+    k_plan_small<2><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
+    SB_CHECK_LAUNCH();
+    if (p->timing)
+      for (int i = 1; i < 6; ++i) SB_CUDA(cudaEventRecord(p->ev[i], s));
+    count_launch(4);
     return;
   }
   plan_common_prologue(p, s);
@@ -1607,10 +1661,17 @@ extern "C" sb_status sb_planner_trace(sb_planner* p, int enable, int64_t* out16)
 
 extern "C" sb_status sb_planner_set_path(sb_planner* p, int path) {
   SB_API_BEGIN
-  if (!p || path < 0 || path > 2) throw Error{SB_ERR_CONFIG, "sb_planner_set_path: path must be 0, 1 or 2"};
-  if (path == 1 && !(p->max_seqs <= sb::kSmallSeqs && p->W <= 1024))
+  if (!p || path < 0 || path > 3) throw Error{SB_ERR_CONFIG, "sb_planner_set_path: path must be 0, 1, 2 or 3"};
+  if ((path == 1 || path == 3) && !(p->max_seqs <= sb::kSmallSeqs && p->W <= 1024))
     throw Error{SB_ERR_CONFIG, "sb_planner_set_path: capacity too large for the single-CTA planner"};
   p->path = path;
+  SB_API_END
+}
+
+extern "C" sb_status sb_planner_last_path(sb_planner* p, int* path) {
+  SB_API_BEGIN
+  if (!p || !path) throw Error{SB_ERR_CONFIG, "null argument"};
+  *path = p->last_path;
   SB_API_END
 }
 

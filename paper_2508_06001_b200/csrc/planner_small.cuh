@@ -151,6 +151,14 @@ __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_inc
 //   5 manifest offsets scanned by every warp, recv / Ulysses / reverse lists
 //     per rank warp, send lists per sequence
 //   6 libstdc++ tie-order replay of the reverse lists (rare)
+//
+// MODE 0 runs all of it.  The hybrid path (planner.cu run_plan) splits it
+// around the 32-thread greedy kernel, whose chain runs ~100 cycles per step
+// against ~150 inside this 512-thread kernel: MODE 1 runs
+// phases 0-2 and leaves the greedy-order workloads in global memory,
+// k_greedy_staged<.., true> picks, and MODE 2 reloads the per-sequence state
+// and runs phases 3-6 with the bag bases in place of the greedy.
+template <int MODE>
 __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int64_t sh[33];
@@ -187,7 +195,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
   int64_t* s_repc = reinterpret_cast<int64_t*>(sm + L.repc);
   int32_t* s_q = reinterpret_cast<int32_t*>(sm + L.q);
 
-  SB_PHASE(0);
+  if (MODE != 2) SB_PHASE(0);
   // ---- phase 0: rank offsets, topology tables
   for (int r = tid; r <= W; r += blockDim.x) s_roff[r] = a.rank_off[r];
   {
@@ -216,14 +224,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     a.bag_size = t_bsize;
     a.rank_bag = t_rbag;
     a.rank_member = t_rmem;
-    a.per_gpu = reinterpret_cast<double*>(sm + L.pergpu);
+    if (MODE == 0) a.per_gpu = reinterpret_cast<double*>(sm + L.pergpu);  // the hybrid's greedy writes it globally
   }
   for (int r = tid; r < W; r += blockDim.x) s_sendcnt[r] = 0;
   if (tid == 0) {
     s_flag = 0;
     s_viol = 0;
     s_biglen = 0;
-    *a.status = 0;  // no memset node before the launch; every atomicOr below follows this barrier
+    if (MODE != 2) *a.status = 0;  // no memset node before the launch; every atomicOr below follows this barrier
+    if (MODE == 1) *a.violations = 0;  // the greedy kernel adds to it
   }
   __syncthreads();
   const int64_t N = s_roff[W];
@@ -245,6 +254,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     const int64_t len = a.lens[i];
     return gamma_weighted_workload(len < 0 ? 0 : len, a.d_model, a.gamma);
   };
+  if constexpr (MODE != 2) {
   SB_PHASE(1);
   // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
   auto seq_pass = [&](int t0, int nt, bool keys) {
@@ -291,7 +301,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
 #pragma unroll 8
         for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_wsorted[i]);
       }
-      SB_MARK_MAX(11);
       if (lane == 0) {
         *a.total = s;
         *a.n_seqs = N;
@@ -418,6 +427,28 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     }
     __syncthreads();
   }
+  if constexpr (MODE == 1) {  // hand the greedy-order workloads to the greedy kernel
+    for (int64_t p = tid; p < N; p += blockDim.x) a.sorted_w[p] = s_wsorted[p];
+    SB_PHASE(12);  // trace: prefix end (the hybrid's kernels run on different SMs)
+    return;
+  }
+  } else {
+  SB_PHASE(11);  // trace: suffix start
+  // ---- MODE 2: reload what phases 0-2 and the greedy kernel left in global memory
+  for (int64_t i = tid; i < N; i += blockDim.x) {
+    const int64_t len = a.lens[i] < 0 ? 0 : a.lens[i];
+    if (len >= (int64_t)1 << 26) s_biglen = 1;
+    s_ids[i] = a.ids[i];
+    s_lens[i] = len;
+    s_rank[i] = a.seq_rank[i];
+    s_soff[i] = a.seq_off[i];
+    s_sorted[i] = a.sorted_idx[i];
+    s_pick[i] = a.pick[i];
+    s_q[i] = a.greedy_q[i];
+  }
+  for (int e = tid; e < R * M; e += blockDim.x) s_bagcnt[e] = a.bag_count[e];
+  __syncthreads();
+  }
   SB_PHASE(3);
   // ---- phase 3: greedy, one warp per replica (balancer.cpp:44-62), beside
   // the duplicate-id check inside each replica (divergence)
@@ -425,10 +456,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
   if (warp < ng) {
     for (int rep = warp; rep < R; rep += ng) {
       const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
-      const double* ws = s_wsorted + lo;
-      if (M <= 32) small_greedy<1>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
-      else small_greedy<2>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
-      __syncwarp();
+      if constexpr (MODE == 0) {
+        const double* ws = s_wsorted + lo;
+        if (M <= 32) small_greedy<1>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
+        else small_greedy<2>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
+        __syncwarp();
+      }
       // replica-local chunk bases of the bags (chunk order: bag, q, k) and
       // the bags' first slots in the (replica, bag)-grouped sequence list
       int cb = 0, q = (int)lo;  // <= cap * kMaxBags chunks: 32 bits
@@ -450,7 +483,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
         if (R == 1) *a.n_chunks = cb;
       }
     }
-  } else if (!a.w_in) {
+  } else if (MODE == 0 && !a.w_in) {  // the hybrid runs k_dup_small beside its greedy kernel
     // open-addressing set per replica in the sort scratch (free now):
     // s_hi and s_lo are contiguous, 2T slots >= 2 * replica size, EMPTY = ~0
     const int t = tid - 32 * ng, nt = (int)blockDim.x - 32 * ng;
@@ -507,7 +540,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
   // chunks are [bag base + q * g, + g) and its slot in the grouped list is
   // bag first slot + q.  Warp 0 computes the WIR beside it.
   if (warp == 0) {
-    for (int r = lane; r < W; r += 32) a_in.per_gpu[r] = a.per_gpu[r];
+    if (MODE == 0)
+      for (int r = lane; r < W; r += 32) a_in.per_gpu[r] = a.per_gpu[r];
     // min and max are order-independent (no NaN) (metrics.cpp:20-31)
     double lo = a.per_gpu[0], hi = lo;
     for (int r = lane; r < W; r += 32) {
@@ -521,7 +555,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     }
     if (lane == 0) {
       *a.wir = hi == 0.0 ? 1.0 : (lo == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : __ddiv_rn(hi, lo));
-      *a.violations = s_viol;
+      if (MODE == 0) *a.violations = s_viol;
     }
   } else {
     for (int64_t p = tid - 32; p < N; p += (int)blockDim.x - 32) {
@@ -663,7 +697,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     for (int r = warp; r < W; r += nw) rank_lists(r, __shfl_sync(kFull, ro_l, r), __shfl_sync(kFull, so_l, r));
     SB_MARK_MAX(8);
     for (int64_t c = rtid; c < n_chunks; c += blockDim.x) emit_chunk(c);
-    SB_MARK_MAX(12);
     for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {  // warp-uniform trip count (the shuffle below)
       const int64_t i = b0 + rtid;
       const int r = i < N ? s_rank[i] : 0;
@@ -707,6 +740,44 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
       fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r], stk);
     }
   SB_PHASE(13);
+}
+
+// Hybrid path: the duplicate-id check inside each replica (divergence, see
+// DESIGN.md) on a side stream beside the greedy kernel -- the same
+// open-addressing set as phase 3 of k_plan_small, in its own shared memory.
+__global__ void __launch_bounds__(kSmallThreads) k_dup_small(PlanArgs a, int cap) {
+  extern __shared__ __align__(16) unsigned long long tab[];  // 2T slots
+  __shared__ unsigned n_empty;
+  __shared__ int flag;
+  const int64_t N = a.rank_off[a.W];
+  if (N > cap || a.w_in) return;
+  const int tsz = 2 * small_pow2(cap);
+  if (threadIdx.x == 0) flag = 0;
+  for (int rep = 0; rep < a.R; ++rep) {
+    const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
+    for (int i = threadIdx.x; i < tsz; i += blockDim.x) tab[i] = ~0ull;
+    if (threadIdx.x == 0) n_empty = 0;
+    __syncthreads();
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const uint64_t id = a.ids[i];
+      if (id == ~0ull) {
+        if (atomicAdd(&n_empty, 1u) > 0) flag = 1;
+        continue;
+      }
+      uint32_t slot = (uint32_t)(hash_slot(id) & (uint64_t)(tsz - 1));
+      for (;;) {
+        const unsigned long long old = atomicCAS(&tab[slot], ~0ull, (unsigned long long)id);
+        if (old == ~0ull) break;
+        if (old == id) {
+          flag = 1;
+          break;
+        }
+        slot = (slot + 1) & (uint32_t)(tsz - 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && flag) atomicOr(a.status, ST_DUP_ID);
 }
 
 }  // namespace sb

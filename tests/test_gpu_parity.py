@@ -105,11 +105,14 @@ def test_device_plan_and_exchange_match_reference(name):
     check_report(report_as_oracle(hp), ref["report"])
     check_plan(reverse_as_oracle(hp, fwd), ref["reverse"])  # libstdc++ tie order replayed
 
-    # the other planner pipeline (fused single-CTA vs multi-kernel) must agree bit for bit
-    other = make_planner(case, meta)
+    # the other planner pipelines (fused single-CTA, hybrid, multi-kernel) must agree bit for bit
     n_seqs = sum(len(x) for x in meta.ids)
-    other.set_path("large" if n_seqs <= 2048 else "auto")
-    planner_paths_equal(hp, other.plan(dm).download())
+    for path in (["large", "small", "hybrid"] if n_seqs <= 2048 else []):
+        other = make_planner(case, meta)
+        other.set_path(path)
+        planner_paths_equal(hp, other.plan(dm).download())
+        if len(other.topology.bag_sizes) <= 64:
+            assert other.last_path() == path
 
     # identity_plan on the same planner slots
     planner.plan_identity(dm)
@@ -151,7 +154,7 @@ def test_device_plan_and_exchange_match_reference(name):
     check_dev_world(E, ref["returned"])
 
 
-@pytest.mark.parametrize("path", ["small", "large"])
+@pytest.mark.parametrize("path", ["small", "large", "hybrid"])
 @pytest.mark.parametrize("topo", ["g8n1", "g4n2", "g2n1+g1n2+g4n1"])
 def test_reverse_ties_match_std_sort(topo, path):
     """Sequences shorter than their bag make reverse_plan's sort keys tie; the
@@ -215,7 +218,7 @@ def test_capacity_exceeded_is_loud():
         planner.sizes()
 
 
-@pytest.mark.parametrize("path", ["small", "large"])
+@pytest.mark.parametrize("path", ["small", "large", "hybrid"])
 @pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2", "g8n1", "g1n2+g2n1+g4n1"])
 def test_random_plans_vs_oracle(topo, path):
     rng = np.random.default_rng(sum(map(ord, topo)))
@@ -371,7 +374,7 @@ def test_world_plan_mismatch_is_integrity_error():
         assert np.array_equal(E.read_rank(1, r), A.read_rank(1, r))
 
 
-@pytest.mark.parametrize("path", ["small", "large"])
+@pytest.mark.parametrize("path", ["small", "large", "hybrid"])
 @pytest.mark.parametrize("world,topo", [(64, "g2n4"), (256, "g4n2+g8n1"), (96, "g1n4+g2n2+g4n1")])
 def test_many_replicas_vs_oracle(world, topo, path):
     """Large worlds: many replicas planned independently (balancer.cpp:136-219),
@@ -446,7 +449,7 @@ def test_bag_limit_is_config_error():
         sb.Planner("g1n1025", 1025, max_seqs=8)
 
 
-@pytest.mark.parametrize("path", ["small", "large"])
+@pytest.mark.parametrize("path", ["small", "large", "hybrid"])
 def test_empty_replicas_vs_oracle(path):
     """Whole replicas without sequences (first and last of three): chunk bases,
     manifests and the data path skip them exactly like the reference."""

@@ -1,5 +1,6 @@
-"""Fused single-CTA planner vs the multi-kernel path: plan latency by CUDA
-graph replay (C1 law, 8 ranks) -- picks the auto-path threshold (diagnostics).
+"""Fused single-CTA planner vs hybrid vs the multi-kernel path: plan latency
+by CUDA graph replay (C1 law, 8 ranks) -- picks the auto-path thresholds
+(diagnostics).
 
     python tools/path_compare.py
 """
@@ -33,12 +34,13 @@ def plan_us(p, dm, reps=20):
     return 1000 * e0.elapsed_time(e1) / reps
 
 
-for n in (256, 512, 768, 1024, 1536, 2048):
-    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
+sizes = [int(x) for x in sys.argv[1:]] or [64, 128, 256, 512, 768, 1024, 1536, 2048]
+for n in sizes:
+    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=max(1, n // 8))
     dm = sb.DeviceMeta.from_lists(ids, lens)
     row = []
-    for topo in ("g1n8", "g2n4", "g8n1"):
-        for path in ("small", "large"):
+    for topo in ("g1n8", "g2n4", "g4n2"):
+        for path in ("small", "hybrid", "large"):
             p = sb.Planner(topo, 8, max_seqs=n)
             p.set_path(path)
             row.append(f"{topo}/{path} {plan_us(p, dm):7.1f}")

@@ -1,6 +1,6 @@
 """Per-phase cycle trace of the fused planner (diagnostics, needs a GPU).
 
-    python tools/trace_planner.py [c2|c1] [topology]
+    python tools/trace_planner.py [c2|c1] [topology] [small|hybrid|large]
 """
 import os
 import sys
@@ -24,11 +24,17 @@ if len(sys.argv) > 2:
     topo = sys.argv[2]
 dm = sb.DeviceMeta.from_lists(ids, lens)
 p = sb.Planner(topo, 8, max_seqs=sum(len(x) for x in ids))
+if len(sys.argv) > 3:
+    p.set_path(sys.argv[3])
 p.trace(True)
 for _ in range(5):
     p.plan(dm)
 torch.cuda.synchronize()
 t = p.trace(True)
+if p.last_path() == "hybrid":  # three kernels: per-kernel spans (clocks of different SMs)
+    print("hybrid: prefix", int(t[12] - t[0]), "greedy chain", int(t[15] - t[14]), "suffix", int(t[13] - t[11]),
+          "cycles")
+    sys.exit(0)
 names = ["load", "seq+totals+offsets", "sort", "greedy+dup", "emit+wir", "lists", "ties"]
 marks = [int(x) for x in t[:7]] + [int(t[13])]
 for i, n in enumerate(names):
