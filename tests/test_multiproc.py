@@ -281,6 +281,28 @@ def test_two_processes_device_barrier(topo):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("topo", ["g2n4", "g4n2"])
+def test_four_processes_device_barrier(topo):
+    """Four processes (two ranks each) on one GPU: peer maps, the device
+    barrier's all-to-all flag pattern and the per-process job split beyond
+    the two-process case (what an N = 4 / 8 box runs), checked against the
+    oracle for two steps."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 4, port, topo, q, "device", 2)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True, 2: True, 3: True}, res
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("topo", ["g1n8", "g2n4", "g4n2", "g1n2+g2n1+g4n1"])
 def test_two_processes_collective_transport(topo):
     """The NCCL-baseline decomposition (sb_exchange_pack -> all-to-all-v ->
