@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <vector>
 #include <algorithm>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 __global__ void lat_redux(int iters, unsigned* out, long long* cyc) {
@@ -691,6 +692,79 @@ __global__ void __launch_bounds__(VAR >= 6 ? 512 : 32) g_prod(const double* w_so
   if (lane == 0) { *cyc = t1 - t0; *replays = viol + s_q[n / 2] * 0; }
   if (VAR >= 6 && blockDim.x > 32) __syncthreads();
 }
+
+// Two-REDUX argmin with exact block replay (candidate for greedy_warp):
+// the second REDUX runs on the low word with its 5 low bits replaced by the
+// lane, so it returns the winner directly; a lane of the winner's 32-ulp
+// bucket other than the winner flags the step as ambiguous.  Per block of K
+// steps the state is saved; an ambiguous block is replayed with the exact
+// three-REDUX step.
+template <int K>
+__global__ void __launch_bounds__(32) g_fast(const double* w_sorted, int n, int M, const double* caps, int* pick,
+                                             long long* cyc, int* replays) {
+  extern __shared__ double wsd[];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n + 2; i += 32) wsd[i] = i < n ? w_sorted[i] : 0.0;
+  __syncwarp();
+  const double* ws = wsd;
+  const double cap = lane < M ? caps[lane] : 0.0;
+  const double rcap = cap > 0.0 ? __drcp_rn(cap) : 0.0;
+  const bool act = lane < M;
+  double asg = 0.0, occ = 0.0, rem = __dsub_rn(cap, 0.0);
+  const int nn = n;
+  double w_a = ws[0], w_b = ws[1], w_c = ws[2];
+  uint64_t key = act ? ((((rem >= w_a) ? 0ull : (1ull << 63))) | (uint64_t)__double_as_longlong(occ)) : ~0ull;
+  int cnt = 0, viol = 0, nrep = 0;
+  auto step = [&](int p, auto ex) -> bool {
+    constexpr bool EXACT = decltype(ex)::value;
+    const double w = w_a, wn = w_b;
+    w_a = w_b;
+    w_b = w_c;
+    w_c = ws[p + 3 < nn ? p + 3 : nn - 1];
+    const double nasg = __dadd_rn(asg, w);
+    const double nocc = occ_sel(nasg, cap, rcap);
+    const double nrem = __dsub_rn(cap, nasg);
+    const uint64_t kwin = act ? ((((nrem >= wn) ? 0ull : (1ull << 63))) | (uint64_t)__double_as_longlong(nocc)) : ~0ull;
+    const uint64_t knot = act ? ((((rem >= wn) ? 0ull : (1ull << 63))) | (uint64_t)__double_as_longlong(occ)) : ~0ull;
+    const uint32_t khi = (uint32_t)(key >> 32), klo = (uint32_t)key;
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, khi);
+    uint32_t pk;
+    bool amb = false;
+    if constexpr (EXACT) {
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+      pk = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? (uint32_t)lane : 0xffffffffu);
+    } else {
+      const uint32_t m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? ((klo & ~31u) | (uint32_t)lane) : 0xffffffffu);
+      pk = m2 & 31u;
+      amb = khi == m1 && (klo | 31u) == (m2 | 31u) && (uint32_t)lane != pk;
+    }
+    viol += (int)(m1 >> 31);
+    const bool won = (uint32_t)lane == pk;
+    key = won ? kwin : knot;
+    asg = won ? nasg : asg;
+    occ = won ? nocc : occ;
+    rem = won ? nrem : rem;
+    cnt += won ? 1 : 0;
+    if (lane == 0) pick[p] = (int)pk;
+    return amb;
+  };
+  long long t0 = clock64();
+  for (int p0 = 0; p0 < nn; p0 += K) {
+    const int p1 = p0 + K < nn ? p0 + K : nn;
+    const uint64_t key0 = key;
+    const double asg0 = asg, occ0 = occ, rem0 = rem, wa0 = w_a, wb0 = w_b, wc0 = w_c;
+    const int cnt0 = cnt, viol0 = viol;
+    bool amb = false;
+    for (int p = p0; p < p1; ++p) amb |= step(p, std::false_type{});
+    if (__any_sync(0xffffffffu, amb)) {
+      ++nrep;
+      key = key0; asg = asg0; occ = occ0; rem = rem0; w_a = wa0; w_b = wb0; w_c = wc0; cnt = cnt0; viol = viol0;
+      for (int p = p0; p < p1; ++p) step(p, std::true_type{});
+    }
+  }
+  long long t1 = clock64();
+  if (lane == 0) { *cyc = t1 - t0; *replays = nrep; }
+}
 int main() {
   unsigned* du; double* dd; long long* dc;
   cudaMalloc(&du, 128); cudaMalloc(&dd, 512); cudaMalloc(&dc, 8);
@@ -762,6 +836,9 @@ int main() {
         printf("  %s %.1f cyc/seq (diffs %d, conflict %d)\n", name, (double)c / n, dd, hrep);
       };
       run(g_diag<0>, "v5flat");
+      run(g_fast<32>, "fast2-K32");
+      run(g_fast<16>, "fast2-K16");
+      run(g_fast<64>, "fast2-K64");
       run(g_prod<0>, "prod");
       run(g_prod<1>, "prod-no-q");
       run(g_prod<2>, "prod-direct-w");
