@@ -21,6 +21,7 @@ plan_routing (balancer.cpp:105-225), route/reverse_route
 from __future__ import annotations
 
 import ctypes as C
+import datetime
 import json
 import os
 import socket
@@ -261,7 +262,9 @@ class CollectiveTransport:
         self.torch, self.dist, self.group, self.backend = torch, dist, group, backend
         self.P = group.size
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.pg = dist.new_group(list(range(self.P)), backend="nccl") if backend == "nccl" else None
+        # bounded: a peer that failed before this point turns a hang into an error
+        self.pg = (dist.new_group(list(range(self.P)), backend="nccl", timeout=datetime.timedelta(seconds=180))
+                   if backend == "nccl" else None)
         self.send = torch.empty(max(16, send_bytes), dtype=torch.uint8, device=dev)
         self.recv = torch.empty(max(16, recv_bytes), dtype=torch.uint8, device=dev)
         self.counts = torch.zeros(2 * self.P, dtype=torch.int64, device=dev)
@@ -614,7 +617,8 @@ def bench_main(args, cfg, topology, metric, clock_sampler=None):
     n_dev = max(1, torch.cuda.device_count())
     torch.cuda.set_device(local % n_dev)
     if not dist.is_initialized():
-        dist.init_process_group("gloo")  # control plane only (IPC handles, max over ranks)
+        # control plane only (IPC handles, max over ranks); bounded collectives
+        dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=600))
     group = PeerGroup(barrier_mode=os.environ.get("SEQBAL_BARRIER", "auto"))
     W = cfg["world"]
     n_local, first = partition(W, group.size, group.rank)
