@@ -537,7 +537,10 @@ def spawn_workers(n: int) -> int:
             env.update(mps)
             env.setdefault("SEQBAL_BARRIER", "device")
     try:
-        p = subprocess.run(cmd, stdout=subprocess.PIPE, text=True, env=env)
+        p = subprocess.run(cmd, stdout=subprocess.PIPE, text=True, env=env, timeout=1800)
+    except subprocess.TimeoutExpired:
+        sys.stderr.write(f"bench.py: {n} worker processes did not finish within 30 min\n")
+        return 3
     finally:
         if mps:
             stop_mps(mps)
