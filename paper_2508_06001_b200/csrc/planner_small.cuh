@@ -25,6 +25,7 @@ namespace sb {
   } while (0)
 
 constexpr int kSmallSeqs = 2048;
+constexpr int kSmallScanSeqs = 128;  // up to here one warp computes the origin offsets (phase 1)
 constexpr int kSmallThreads = 512;  // a 256-thread block measured no faster greedy (same code generation)
 
 __host__ __device__ inline int small_pow2(int n) {
@@ -293,23 +294,39 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
       // total of :147 is the same sum): the warp recomputes the workloads
       // from the lengths into the (not yet used) greedy-order scratch, lane 0
       // chains them
+      const int n = (int)N;
 #pragma unroll 4
-      for (int64_t i = lane; i < N; i += 32) s_wsorted[i] = raw_workload(i);
+      for (int i = lane; i < n; i += 32) s_wsorted[i] = raw_workload(i);
       __syncwarp();
       double s = 0.0;
       if (lane == 0) {
-#pragma unroll 8
-        for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_wsorted[i]);
+        // 16-byte loads, the next group's issued before this group's DADDs
+        // (the chain is the only serial part: ~8 cycles per element)
+        const double2* v2 = reinterpret_cast<const double2*>(s_wsorted);
+        int i = 0;
+        if (n >= 8) {
+          double2 c0 = v2[0], c1 = v2[1], c2 = v2[2], c3 = v2[3];
+          for (i = 8; i + 8 <= n; i += 8) {
+            const double2 d0 = v2[i / 2], d1 = v2[i / 2 + 1], d2 = v2[i / 2 + 2], d3 = v2[i / 2 + 3];
+            s = __dadd_rn(s, c0.x); s = __dadd_rn(s, c0.y); s = __dadd_rn(s, c1.x); s = __dadd_rn(s, c1.y);
+            s = __dadd_rn(s, c2.x); s = __dadd_rn(s, c2.y); s = __dadd_rn(s, c3.x); s = __dadd_rn(s, c3.y);
+            c0 = d0; c1 = d1; c2 = d2; c3 = d3;
+          }
+          s = __dadd_rn(s, c0.x); s = __dadd_rn(s, c0.y); s = __dadd_rn(s, c1.x); s = __dadd_rn(s, c1.y);
+          s = __dadd_rn(s, c2.x); s = __dadd_rn(s, c2.y); s = __dadd_rn(s, c3.x); s = __dadd_rn(s, c3.y);
+        }
+        for (; i < n; ++i) s = __dadd_rn(s, s_wsorted[i]);
       }
+      if (MODE == 0) SB_MARK_MAX(11);  // diagnostics: totals chain done
       if (lane == 0) {
         *a.total = s;
         *a.n_seqs = N;
         s_reptot[0] = s;
         a.rep_total[0] = s;
       }
-    } else if (warp == 1) {
-      // origin packing offsets: exclusive scan of the lengths in gather
-      // order, rebased per rank
+    } else if (N <= kSmallScanSeqs && warp == 1) {
+      // origin packing offsets, few sequences: one warp scans the lengths in
+      // gather order (32 per step) and rebases them per rank
       int64_t carry = 0;
       for (int64_t base = 0; base < N; base += 32) {
         const int64_t i = base + lane;
@@ -327,8 +344,47 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
         a.seq_off[i] = s_soff[i];
       }
       for (int r = lane; r < W; r += 32) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-    } else {
+      if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
+    } else if (N <= kSmallScanSeqs) {
       seq_pass(tid - 64, (int)blockDim.x - 64, true);
+    } else {
+      // warps 1..: the per-sequence pass, then the origin packing offsets
+      // (exclusive scan of the lengths in gather order, rebased per rank) as
+      // a scan over these warps only, closed by named barrier 1 (one warp
+      // walking 32 lengths per dependent step was the phase's critical path)
+      const int t = tid - 32, nt = (int)blockDim.x - 32, tw = t >> 5, ntw = nt >> 5;
+      auto bar = [nt]() { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); };
+      seq_pass(t, nt, true);
+      bar();
+      const int n = (int)N;
+      const int per = (n + nt - 1) / nt, b0 = t * per < n ? t * per : n, b1 = b0 + per < n ? b0 + per : n;
+      int64_t loc = 0;
+      for (int i = b0; i < b1; ++i) loc += s_lens[i];
+      const int64_t inc = warp_incl_scan<int64_t>(loc);
+      if (lane == 31) sh[tw] = inc;
+      bar();
+      if (tw == 0) {
+        const int64_t x = lane < ntw ? sh[lane] : 0;
+        const int64_t xi = warp_incl_scan<int64_t>(x);
+        __syncwarp();
+        if (lane < ntw) sh[lane] = xi - x;
+        if (lane == ntw - 1) sh[32] = xi;
+      }
+      bar();
+      int64_t run = sh[tw] + inc - loc;
+      for (int i = b0; i < b1; ++i) {
+        s_soff[i] = run;
+        run += s_lens[i];
+      }
+      bar();
+      for (int r = t; r <= W; r += nt) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : sh[32];
+      bar();
+      for (int i = t; i < n; i += nt) {
+        s_soff[i] -= s_rpre[s_rank[i]];
+        a.seq_off[i] = s_soff[i];
+      }
+      for (int r = t; r < W; r += nt) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+      if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
     }
     __syncthreads();
   } else {

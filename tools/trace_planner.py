@@ -40,8 +40,8 @@ marks = [int(x) for x in t[:7]] + [int(t[13])]
 for i, n in enumerate(names):
     print(f"{n:20s} {marks[i + 1] - marks[i]:8d} cycles")
 print("total", int(t[13] - t[0]), "cycles")
-sub = {"P1 totals chain done": 11, "P4 per-seq pass done (max)": 10, "P5 offsets done (warp 0)": 7,
-       "P5 rank lists done (max)": 8, "P5 chunk emission done (max)": 12, "P5 send lists done (max)": 9}
+sub = {"P1 totals chain done": 11, "P1 origin offsets done": 12, "P4 per-seq pass done (max)": 10,
+       "P5 offsets done (warp 0)": 7, "P5 rank lists done (max)": 8, "P5 send lists done (max)": 9}
 for k, i in sub.items():
     if t[i] > 0:
         print(f"  {k:32s} +{int(t[i] - t[0]):8d} cycles from start")
