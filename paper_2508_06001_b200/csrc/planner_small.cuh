@@ -255,255 +255,255 @@ __global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int
     const int64_t len = a.lens[i];
     return gamma_weighted_workload(len < 0 ? 0 : len, a.d_model, a.gamma);
   };
-  if constexpr (MODE != 2) {
-  SB_PHASE(1);
-  // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
-  auto seq_pass = [&](int t0, int nt, bool keys) {
-    for (int64_t i = t0; i < N; i += nt) {
-      const int r = rank_of(i);
-      int64_t len = a.lens[i];
-      if (len < 0) {
-        atomicOr(a.status, ST_NEG_LENGTH);
-        len = 0;
+  if constexpr (MODE != 2) {  // phases 1-2 (fused, hybrid prefix)
+    SB_PHASE(1);
+    // ---- phase 1: metadata, workloads, ranks (balancer.cpp:139-149)
+    auto seq_pass = [&](int t0, int nt, bool keys) {
+      for (int64_t i = t0; i < N; i += nt) {
+        const int r = rank_of(i);
+        int64_t len = a.lens[i];
+        if (len < 0) {
+          atomicOr(a.status, ST_NEG_LENGTH);
+          len = 0;
+        }
+        double wv;
+        if (a.w_in) {
+          wv = a.w_in[i];
+          if (!(wv >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
+        } else {
+          wv = gamma_weighted_workload(len, a.d_model, a.gamma);
+        }
+        if (len >= (int64_t)1 << 26) s_biglen = 1;  // 32 lengths no longer sum in 32 bits
+        const uint64_t id = a.ids[i];
+        s_ids[i] = id;
+        s_lens[i] = len;
+        s_w[i] = wv;
+        s_rank[i] = r;
+        a.w[i] = wv;
+        a.seq_rank[i] = r;
+        if (keys) {  // one replica: its sort records, indexed by gather position
+          s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
+          s_lo[i] = id;
+          s_v[i] = (uint32_t)i;
+        }
       }
-      double wv;
-      if (a.w_in) {
-        wv = a.w_in[i];
-        if (!(wv >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);
-      } else {
-        wv = gamma_weighted_workload(len, a.d_model, a.gamma);
-      }
-      if (len >= (int64_t)1 << 26) s_biglen = 1;  // 32 lengths no longer sum in 32 bits
-      const uint64_t id = a.ids[i];
-      s_ids[i] = id;
-      s_lens[i] = len;
-      s_w[i] = wv;
-      s_rank[i] = r;
-      a.w[i] = wv;
-      a.seq_rank[i] = r;
-      if (keys) {  // one replica: its sort records, indexed by gather position
-        s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
-        s_lo[i] = id;
-        s_v[i] = (uint32_t)i;
-      }
-    }
-  };
-  if (R == 1) {
-    if (warp == 0) {
-      // serial FP64 total in gather order (balancer.cpp:24-25; the replica
-      // total of :147 is the same sum): the warp recomputes the workloads
-      // from the lengths into the (not yet used) greedy-order scratch, lane 0
-      // chains them
-      const int n = (int)N;
-#pragma unroll 4
-      for (int i = lane; i < n; i += 32) s_wsorted[i] = raw_workload(i);
-      __syncwarp();
-      double s = 0.0;
-      if (lane == 0) {
-        // 16-byte loads, the next group's issued before this group's DADDs
-        // (the chain is the only serial part: ~8 cycles per element)
-        const double2* v2 = reinterpret_cast<const double2*>(s_wsorted);
-        int i = 0;
-        if (n >= 8) {
-          double2 c0 = v2[0], c1 = v2[1], c2 = v2[2], c3 = v2[3];
-          for (i = 8; i + 8 <= n; i += 8) {
-            const double2 d0 = v2[i / 2], d1 = v2[i / 2 + 1], d2 = v2[i / 2 + 2], d3 = v2[i / 2 + 3];
+    };
+    if (R == 1) {
+      if (warp == 0) {
+        // serial FP64 total in gather order (balancer.cpp:24-25; the replica
+        // total of :147 is the same sum): the warp recomputes the workloads
+        // from the lengths into the (not yet used) greedy-order scratch, lane 0
+        // chains them
+        const int n = (int)N;
+  #pragma unroll 4
+        for (int i = lane; i < n; i += 32) s_wsorted[i] = raw_workload(i);
+        __syncwarp();
+        double s = 0.0;
+        if (lane == 0) {
+          // 16-byte loads, the next group's issued before this group's DADDs
+          // (the chain is the only serial part: ~8 cycles per element)
+          const double2* v2 = reinterpret_cast<const double2*>(s_wsorted);
+          int i = 0;
+          if (n >= 8) {
+            double2 c0 = v2[0], c1 = v2[1], c2 = v2[2], c3 = v2[3];
+            for (i = 8; i + 8 <= n; i += 8) {
+              const double2 d0 = v2[i / 2], d1 = v2[i / 2 + 1], d2 = v2[i / 2 + 2], d3 = v2[i / 2 + 3];
+              s = __dadd_rn(s, c0.x); s = __dadd_rn(s, c0.y); s = __dadd_rn(s, c1.x); s = __dadd_rn(s, c1.y);
+              s = __dadd_rn(s, c2.x); s = __dadd_rn(s, c2.y); s = __dadd_rn(s, c3.x); s = __dadd_rn(s, c3.y);
+              c0 = d0; c1 = d1; c2 = d2; c3 = d3;
+            }
             s = __dadd_rn(s, c0.x); s = __dadd_rn(s, c0.y); s = __dadd_rn(s, c1.x); s = __dadd_rn(s, c1.y);
             s = __dadd_rn(s, c2.x); s = __dadd_rn(s, c2.y); s = __dadd_rn(s, c3.x); s = __dadd_rn(s, c3.y);
-            c0 = d0; c1 = d1; c2 = d2; c3 = d3;
           }
-          s = __dadd_rn(s, c0.x); s = __dadd_rn(s, c0.y); s = __dadd_rn(s, c1.x); s = __dadd_rn(s, c1.y);
-          s = __dadd_rn(s, c2.x); s = __dadd_rn(s, c2.y); s = __dadd_rn(s, c3.x); s = __dadd_rn(s, c3.y);
+          for (; i < n; ++i) s = __dadd_rn(s, s_wsorted[i]);
         }
-        for (; i < n; ++i) s = __dadd_rn(s, s_wsorted[i]);
-      }
-      if (MODE == 0) SB_MARK_MAX(11);  // diagnostics: totals chain done
-      if (lane == 0) {
-        *a.total = s;
-        *a.n_seqs = N;
-        s_reptot[0] = s;
-        a.rep_total[0] = s;
-      }
-    } else if (N <= kSmallScanSeqs && warp == 1) {
-      // origin packing offsets, few sequences: one warp scans the lengths in
-      // gather order (32 per step) and rebases them per rank
-      int64_t carry = 0;
-      for (int64_t base = 0; base < N; base += 32) {
-        const int64_t i = base + lane;
-        int64_t v = i < N ? a.lens[i] : 0;
-        v = v < 0 ? 0 : v;
-        const int64_t inc = warp_incl_scan<int64_t>(v);
-        if (i < N) s_soff[i] = carry + inc - v;
-        carry += __shfl_sync(kFull, inc, 31);
-      }
-      __syncwarp();
-      for (int r = lane; r <= W; r += 32) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : carry;
-      __syncwarp();
-      for (int64_t i = lane; i < N; i += 32) {
-        s_soff[i] -= s_rpre[rank_of(i)];
-        a.seq_off[i] = s_soff[i];
-      }
-      for (int r = lane; r < W; r += 32) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-      if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
-    } else if (N <= kSmallScanSeqs) {
-      seq_pass(tid - 64, (int)blockDim.x - 64, true);
-    } else {
-      // warps 1..: the per-sequence pass, then the origin packing offsets
-      // (exclusive scan of the lengths in gather order, rebased per rank) as
-      // a scan over these warps only, closed by named barrier 1 (one warp
-      // walking 32 lengths per dependent step was the phase's critical path)
-      const int t = tid - 32, nt = (int)blockDim.x - 32, tw = t >> 5, ntw = nt >> 5;
-      auto bar = [nt]() { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); };
-      seq_pass(t, nt, true);
-      bar();
-      const int n = (int)N;
-      const int per = (n + nt - 1) / nt, b0 = t * per < n ? t * per : n, b1 = b0 + per < n ? b0 + per : n;
-      int64_t loc = 0;
-      for (int i = b0; i < b1; ++i) loc += s_lens[i];
-      const int64_t inc = warp_incl_scan<int64_t>(loc);
-      if (lane == 31) sh[tw] = inc;
-      bar();
-      if (tw == 0) {
-        const int64_t x = lane < ntw ? sh[lane] : 0;
-        const int64_t xi = warp_incl_scan<int64_t>(x);
+        if (MODE == 0) SB_MARK_MAX(11);  // diagnostics: totals chain done
+        if (lane == 0) {
+          *a.total = s;
+          *a.n_seqs = N;
+          s_reptot[0] = s;
+          a.rep_total[0] = s;
+        }
+      } else if (N <= kSmallScanSeqs && warp == 1) {
+        // origin packing offsets, few sequences: one warp scans the lengths in
+        // gather order (32 per step) and rebases them per rank
+        int64_t carry = 0;
+        for (int64_t base = 0; base < N; base += 32) {
+          const int64_t i = base + lane;
+          int64_t v = i < N ? a.lens[i] : 0;
+          v = v < 0 ? 0 : v;
+          const int64_t inc = warp_incl_scan<int64_t>(v);
+          if (i < N) s_soff[i] = carry + inc - v;
+          carry += __shfl_sync(kFull, inc, 31);
+        }
         __syncwarp();
-        if (lane < ntw) sh[lane] = xi - x;
-        if (lane == ntw - 1) sh[32] = xi;
+        for (int r = lane; r <= W; r += 32) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : carry;
+        __syncwarp();
+        for (int64_t i = lane; i < N; i += 32) {
+          s_soff[i] -= s_rpre[rank_of(i)];
+          a.seq_off[i] = s_soff[i];
+        }
+        for (int r = lane; r < W; r += 32) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+        if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
+      } else if (N <= kSmallScanSeqs) {
+        seq_pass(tid - 64, (int)blockDim.x - 64, true);
+      } else {
+        // warps 1..: the per-sequence pass, then the origin packing offsets
+        // (exclusive scan of the lengths in gather order, rebased per rank) as
+        // a scan over these warps only, closed by named barrier 1 (one warp
+        // walking 32 lengths per dependent step was the phase's critical path)
+        const int t = tid - 32, nt = (int)blockDim.x - 32, tw = t >> 5, ntw = nt >> 5;
+        auto bar = [nt]() { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); };
+        seq_pass(t, nt, true);
+        bar();
+        const int n = (int)N;
+        const int per = (n + nt - 1) / nt, b0 = t * per < n ? t * per : n, b1 = b0 + per < n ? b0 + per : n;
+        int64_t loc = 0;
+        for (int i = b0; i < b1; ++i) loc += s_lens[i];
+        const int64_t inc = warp_incl_scan<int64_t>(loc);
+        if (lane == 31) sh[tw] = inc;
+        bar();
+        if (tw == 0) {
+          const int64_t x = lane < ntw ? sh[lane] : 0;
+          const int64_t xi = warp_incl_scan<int64_t>(x);
+          __syncwarp();
+          if (lane < ntw) sh[lane] = xi - x;
+          if (lane == ntw - 1) sh[32] = xi;
+        }
+        bar();
+        int64_t run = sh[tw] + inc - loc;
+        for (int i = b0; i < b1; ++i) {
+          s_soff[i] = run;
+          run += s_lens[i];
+        }
+        bar();
+        for (int r = t; r <= W; r += nt) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : sh[32];
+        bar();
+        for (int i = t; i < n; i += nt) {
+          s_soff[i] -= s_rpre[s_rank[i]];
+          a.seq_off[i] = s_soff[i];
+        }
+        for (int r = t; r < W; r += nt) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+        if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
       }
-      bar();
-      int64_t run = sh[tw] + inc - loc;
-      for (int i = b0; i < b1; ++i) {
+      __syncthreads();
+    } else {
+      seq_pass(tid, (int)blockDim.x, false);
+      __syncthreads();
+      const int64_t per = (N + blockDim.x - 1) / blockDim.x;
+      const int64_t b0 = tid * per, b1 = b0 + per < N ? b0 + per : N;
+      int64_t loc = 0;
+      for (int64_t i = b0; i < b1; ++i) loc += s_lens[i];
+      int64_t tot;
+      int64_t run = block_excl_scan<int64_t>(loc, sh, &tot);
+      for (int64_t i = b0; i < b1; ++i) {
         s_soff[i] = run;
         run += s_lens[i];
       }
-      bar();
-      for (int r = t; r <= W; r += nt) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : sh[32];
-      bar();
-      for (int i = t; i < n; i += nt) {
+      __syncthreads();
+      for (int r = tid; r <= W; r += blockDim.x) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : tot;
+      __syncthreads();
+      for (int64_t i = tid; i < N; i += blockDim.x) {
         s_soff[i] -= s_rpre[s_rank[i]];
         a.seq_off[i] = s_soff[i];
       }
-      for (int r = t; r < W; r += nt) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-      if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
-    }
-    __syncthreads();
-  } else {
-    seq_pass(tid, (int)blockDim.x, false);
-    __syncthreads();
-    const int64_t per = (N + blockDim.x - 1) / blockDim.x;
-    const int64_t b0 = tid * per, b1 = b0 + per < N ? b0 + per : N;
-    int64_t loc = 0;
-    for (int64_t i = b0; i < b1; ++i) loc += s_lens[i];
-    int64_t tot;
-    int64_t run = block_excl_scan<int64_t>(loc, sh, &tot);
-    for (int64_t i = b0; i < b1; ++i) {
-      s_soff[i] = run;
-      run += s_lens[i];
-    }
-    __syncthreads();
-    for (int r = tid; r <= W; r += blockDim.x) s_rpre[r] = s_roff[r] < N ? s_soff[s_roff[r]] : tot;
-    __syncthreads();
-    for (int64_t i = tid; i < N; i += blockDim.x) {
-      s_soff[i] -= s_rpre[s_rank[i]];
-      a.seq_off[i] = s_soff[i];
-    }
-    for (int r = tid; r < W; r += blockDim.x) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-    // serial totals (balancer.cpp:24-25, :147): global on warp 0, one
-    // replica per lane of warp 1
-    if (warp == 0 && lane == 0) {
-      double s = 0.0;
-      for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_w[i]);
-      *a.total = s;
-      *a.n_seqs = N;
-    } else if (warp == 1) {
-      for (int rep = lane; rep < R; rep += 32) {
+      for (int r = tid; r < W; r += blockDim.x) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
+      // serial totals (balancer.cpp:24-25, :147): global on warp 0, one
+      // replica per lane of warp 1
+      if (warp == 0 && lane == 0) {
         double s = 0.0;
-        for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
-        s_reptot[rep] = s;
-        a.rep_total[rep] = s;
-      }
-    }
-    __syncthreads();
-  }
-  SB_PHASE(2);
-  // ---- phase 2: per replica sort by (workload desc, id asc) (balancer.cpp:37-40);
-  // each variant also gathers the workloads into greedy order
-  for (int rep = 0; rep < R; ++rep) {
-    const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
-    if (R > 1) {
-      for (int64_t i = tid; i < n; i += blockDim.x) {
-        const double wv = s_w[lo + i];
-        s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
-        s_lo[i] = s_ids[lo + i];
-        s_v[i] = (uint32_t)i;
+        for (int64_t i = 0; i < N; ++i) s = __dadd_rn(s, s_w[i]);
+        *a.total = s;
+        *a.n_seqs = N;
+      } else if (warp == 1) {
+        for (int rep = lane; rep < R; rep += 32) {
+          double s = 0.0;
+          for (int64_t i = s_roff[rep * U]; i < s_roff[rep * U + U]; ++i) s = __dadd_rn(s, s_w[i]);
+          s_reptot[rep] = s;
+          a.rep_total[rep] = s;
+        }
       }
       __syncthreads();
     }
-    if (n > 32 && n <= 2 * kSmallThreads && blockDim.x == kSmallThreads) {
-      const int nn = (int)n;
-      int32_t* gs = a.sorted_idx;
-      if (nn <= 64) reg_sort_emit<64, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
-      else if (nn <= 128) reg_sort_emit<128, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
-      else if (nn <= 256) reg_sort_emit<256, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
-      else if (nn <= 512) reg_sort_emit<512, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
-      else reg_sort_emit<1024, 2>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
-    } else if (n <= 1024) {
-      // rank by counting: the key (~bits(w), id, index) is a total order.
-      // k = blockDim/n lanes (power of two <= 32) share one record's count,
-      // each over a slice of the candidates (broadcast smem reads), then a
-      // shuffle reduction inside the k-lane group.
-      const int nn = (int)n;
-      int k = 1;
-      while (k < 32 && 2 * k * nn <= (int)blockDim.x) k <<= 1;
-      const int per = (nn + k - 1) / k;
-      for (int base = 0; base < nn * k; base += blockDim.x) {
-        const int x = base + tid;
-        const int i = x / k, part = x % k;
-        int pos = 0;
-        if (i < nn) {
-          const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
-          const int j0 = part * per, j1 = j0 + per < nn ? j0 + per : nn;
-#pragma unroll 8
-          for (int j = j0; j < j1; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
+    SB_PHASE(2);
+    // ---- phase 2: per replica sort by (workload desc, id asc) (balancer.cpp:37-40);
+    // each variant also gathers the workloads into greedy order
+    for (int rep = 0; rep < R; ++rep) {
+      const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
+      if (R > 1) {
+        for (int64_t i = tid; i < n; i += blockDim.x) {
+          const double wv = s_w[lo + i];
+          s_hi[i] = ~(uint64_t)__double_as_longlong(wv == 0.0 ? 0.0 : wv);
+          s_lo[i] = s_ids[lo + i];
+          s_v[i] = (uint32_t)i;
         }
-        for (int o = k >> 1; o > 0; o >>= 1) pos += __shfl_xor_sync(kFull, pos, o);
-        if (i < nn && part == 0) {
-          s_sorted[lo + pos] = (int32_t)(lo + i);
-          s_wsorted[lo + pos] = s_w[lo + i];
-          a.sorted_idx[lo + pos] = (int32_t)(lo + i);
+        __syncthreads();
+      }
+      if (n > 32 && n <= 2 * kSmallThreads && blockDim.x == kSmallThreads) {
+        const int nn = (int)n;
+        int32_t* gs = a.sorted_idx;
+        if (nn <= 64) reg_sort_emit<64, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+        else if (nn <= 128) reg_sort_emit<128, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+        else if (nn <= 256) reg_sort_emit<256, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+        else if (nn <= 512) reg_sort_emit<512, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+        else reg_sort_emit<1024, 2>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+      } else if (n <= 1024) {
+        // rank by counting: the key (~bits(w), id, index) is a total order.
+        // k = blockDim/n lanes (power of two <= 32) share one record's count,
+        // each over a slice of the candidates (broadcast smem reads), then a
+        // shuffle reduction inside the k-lane group.
+        const int nn = (int)n;
+        int k = 1;
+        while (k < 32 && 2 * k * nn <= (int)blockDim.x) k <<= 1;
+        const int per = (nn + k - 1) / k;
+        for (int base = 0; base < nn * k; base += blockDim.x) {
+          const int x = base + tid;
+          const int i = x / k, part = x % k;
+          int pos = 0;
+          if (i < nn) {
+            const uint64_t hi_i = s_hi[i], lo_i = s_lo[i];
+            const int j0 = part * per, j1 = j0 + per < nn ? j0 + per : nn;
+  #pragma unroll 8
+            for (int j = j0; j < j1; ++j) pos += rec_less(s_hi[j], s_lo[j], (uint32_t)j, hi_i, lo_i, (uint32_t)i);
+          }
+          for (int o = k >> 1; o > 0; o >>= 1) pos += __shfl_xor_sync(kFull, pos, o);
+          if (i < nn && part == 0) {
+            s_sorted[lo + pos] = (int32_t)(lo + i);
+            s_wsorted[lo + pos] = s_w[lo + i];
+            a.sorted_idx[lo + pos] = (int32_t)(lo + i);
+          }
+        }
+      } else {
+        smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
+        for (int64_t i = tid; i < n; i += blockDim.x) {
+          s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
+          s_wsorted[lo + i] = s_w[lo + s_v[i]];
+          a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
         }
       }
-    } else {
-      smem_bitonic(s_hi, s_lo, s_v, (int)n, small_pow2((int)n));
-      for (int64_t i = tid; i < n; i += blockDim.x) {
-        s_sorted[lo + i] = (int32_t)(lo + s_v[i]);
-        s_wsorted[lo + i] = s_w[lo + s_v[i]];
-        a.sorted_idx[lo + i] = (int32_t)(lo + s_v[i]);
-      }
+      __syncthreads();
     }
+    if constexpr (MODE == 1) {  // hand the greedy-order workloads to the greedy kernel
+      for (int64_t p = tid; p < N; p += blockDim.x) a.sorted_w[p] = s_wsorted[p];
+      SB_PHASE(12);  // trace: prefix end (the hybrid's kernels run on different SMs)
+      return;
+    }
+  } else {  // hybrid suffix
+    SB_PHASE(11);  // trace: suffix start
+    // ---- MODE 2: reload what phases 0-2 and the greedy kernel left in global memory
+    for (int64_t i = tid; i < N; i += blockDim.x) {
+      const int64_t len = a.lens[i] < 0 ? 0 : a.lens[i];
+      if (len >= (int64_t)1 << 26) s_biglen = 1;
+      s_ids[i] = a.ids[i];
+      s_lens[i] = len;
+      s_rank[i] = a.seq_rank[i];
+      s_soff[i] = a.seq_off[i];
+      s_sorted[i] = a.sorted_idx[i];
+      s_pick[i] = a.pick[i];
+      s_q[i] = a.greedy_q[i];
+    }
+    for (int e = tid; e < R * M; e += blockDim.x) s_bagcnt[e] = a.bag_count[e];
     __syncthreads();
-  }
-  if constexpr (MODE == 1) {  // hand the greedy-order workloads to the greedy kernel
-    for (int64_t p = tid; p < N; p += blockDim.x) a.sorted_w[p] = s_wsorted[p];
-    SB_PHASE(12);  // trace: prefix end (the hybrid's kernels run on different SMs)
-    return;
-  }
-  } else {
-  SB_PHASE(11);  // trace: suffix start
-  // ---- MODE 2: reload what phases 0-2 and the greedy kernel left in global memory
-  for (int64_t i = tid; i < N; i += blockDim.x) {
-    const int64_t len = a.lens[i] < 0 ? 0 : a.lens[i];
-    if (len >= (int64_t)1 << 26) s_biglen = 1;
-    s_ids[i] = a.ids[i];
-    s_lens[i] = len;
-    s_rank[i] = a.seq_rank[i];
-    s_soff[i] = a.seq_off[i];
-    s_sorted[i] = a.sorted_idx[i];
-    s_pick[i] = a.pick[i];
-    s_q[i] = a.greedy_q[i];
-  }
-  for (int e = tid; e < R * M; e += blockDim.x) s_bagcnt[e] = a.bag_count[e];
-  __syncthreads();
   }
   SB_PHASE(3);
   // ---- phase 3: greedy, one warp per replica (balancer.cpp:44-62), beside
