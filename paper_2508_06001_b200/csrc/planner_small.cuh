@@ -160,7 +160,7 @@ __device__ __forceinline__ int64_t warp_scan_incl64(int64_t x) { return warp_inc
 // k_greedy_staged<.., true> picks, and MODE 2 reloads the per-sequence state
 // and runs phases 3-6 with the bag bases in place of the greedy.
 template <int MODE>
-__global__ void __launch_bounds__(kSmallThreads) k_plan_small(PlanArgs a_in, int cap) {
+__global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, int cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int64_t sh[33];
   __shared__ int s_flag, s_viol, s_biglen;
