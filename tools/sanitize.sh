@@ -2,14 +2,14 @@
 # compute-sanitizer (memcheck, racecheck, synccheck, initcheck) over a subset
 # of the GPU parity tests covering every kernel family: fused single-CTA and
 # multi-kernel planners (sorts, greedy, block serial sums, emission, lists,
-# std::sort replay), exchange prep, LSU + TMA copy engines (mbarrier ring),
+# std::sort replay), the hybrid planner and the >64-bag greedy, exchange prep, LSU + TMA copy engines (mbarrier ring),
 # Ulysses on q/k/v, the stream driver's plan-ahead slots, uniform balancer.
 # Writes gpurun_out/sanitize_<tool>.log; summary in gpurun_out/sanitize_summary.txt
 cd "$(dirname "$0")/.."
 SEL_PARITY="rand07 or rand19 or c2_g1n4 or c3_g4n2 or empty_world or zero_len or c4_n4096_g2n4 or c4_n1024_g8n1"
 TESTS=(
   "tests/test_gpu_parity.py -k ($SEL_PARITY) and device_plan"
-  "tests/test_gpu_parity.py -k test_random_plans_vs_oracle or block_serial_sum or reverse_ties"
+  "tests/test_gpu_parity.py -k test_random_plans_vs_oracle or block_serial_sum or reverse_ties or many_bags or many_replicas"
   "tests/test_gpu_ulysses_qkv.py -k g4n2 or layout_plan"
   "tests/test_gpu_stream.py -k plan_ahead or graph_replay"
   "tests/test_uniform.py"
