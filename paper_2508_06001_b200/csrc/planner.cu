@@ -1207,16 +1207,15 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
 // the 512-thread fused CTA) and its sort / emission use many SMs; the hybrid
 // (fused prefix, 32-thread greedy kernel, fused suffix) pays two kernel
 // boundaries and a reload for the faster chain.  Measured by graph replay
-// (tools/path_compare.py, profiles/r02/s3_planner/path_compare.txt), g1n8:
-// 256 sequences fused 35 / hybrid 37 / multi-kernel 65 us, 512 64 / 60 / 84,
-// 768 96 / 91 / 99, 1024 126 / 113-125 / 116-118 (g2n4, g4n2 favour the
-// multi-kernel path there); one bag per replica 512 46 vs 61 fused ahead,
-// 768 66 vs 61 behind.
+// (tools/path_compare.py, profiles/r02/s3_planner/path_compare*.txt), g1n8:
+// 256 sequences fused 34 / hybrid 36 / multi-kernel 67 us, 512 61 / 56 / 86,
+// 768 91 / 82 / 100, 1024 116 / 102-113 / 114-117, 1536 multi-kernel ahead;
+// one bag per replica 512 46 vs 61 fused ahead, 768 66 vs 61 behind.
 constexpr int64_t kSmallChunks = 8192;
 
 constexpr int64_t kSmallAutoSeqsOneBag = 640;   // one bag per replica (no greedy chain)
 constexpr int64_t kHybridAutoSeqs = 384;        // hybrid from here (see choose_path) ...
-constexpr int64_t kHybridAutoMaxSeqs = 896;     // ... up to here, multi-kernel above
+constexpr int64_t kHybridAutoMaxSeqs = 1152;    // ... up to here, multi-kernel above
 
 // 1 = fused single CTA, 2 = multi-kernel, 3 = hybrid (fused prefix, 32-thread
 // greedy kernel, fused suffix).

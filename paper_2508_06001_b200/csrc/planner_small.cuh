@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
   // in its sequences' bag order; a chunk finds its bag by binary search
   const int RM = R * M;
   const int64_t n_chunks = s_bagcb[RM - 1] + (int64_t)s_bagcnt[RM - 1] * a.bag_size[M - 1];
-  auto emit_chunk = [&](int64_t c) {
+  auto emit_chunk = [&](int64_t c) -> int {  // returns the chunk's source rank
     int blo = 0, bhi = RM;  // last bag with base <= c (empty bags share the base of the next)
     while (bhi - blo > 1) {
       const int mid = (blo + bhi) >> 1;
@@ -725,6 +725,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
     a.c_dst[c] = rep * U + a.bag_ranks[a.bag_off[b] + k];
     a.c_src_row[c] = s_soff[s] + st;
     a.c_seq[c] = s;
+    return s_rank[s];
   };
   // chunk emission and send lists go to the highest threads first: warps
   // without a rank list take them while the rank warps scan
@@ -750,16 +751,61 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       }
     }
     SB_MARK(7);
-    for (int r = warp; r < W; r += nw) rank_lists(r, __shfl_sync(kFull, ro_l, r), __shfl_sync(kFull, so_l, r));
-    SB_MARK_MAX(8);
-    for (int64_t c = rtid; c < n_chunks; c += blockDim.x) emit_chunk(c);
-    for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {  // warp-uniform trip count (the shuffle below)
-      const int64_t i = b0 + rtid;
-      const int r = i < N ? s_rank[i] : 0;
-      const int64_t so = __shfl_sync(kFull, so_l, r);
-      if (i < N) send_list(i, so);
+    if (N > kSmallScanSeqs && 2 * W <= nw) {
+      // send[r] = the chunks of source r in chunk order (finalize_manifests,
+      // balancer.cpp:84-91): a stable filter of the chunk array by source
+      // rank, emitted tile by tile on warps [W, nw) (match_any + per-warp
+      // counts, double-buffered, named barrier 1) while warps [0, W) build
+      // the rank lists -- O(chunks) instead of counting over each rank's
+      // sequences
+      __shared__ int s_wcnt[2][kSmallThreads / 32][32];
+      __shared__ int s_run[32];
+      if (warp < W) {
+        rank_lists(warp, __shfl_sync(kFull, ro_l, warp), __shfl_sync(kFull, so_l, warp));
+        SB_MARK_MAX(8);
+      } else {
+        const int t0 = tid - 32 * W, nt = (int)blockDim.x - 32 * W, tw = warp - W, ntw = nw - W;
+        auto bar = [nt]() { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); };
+        if (t0 < 32) s_run[t0] = 0;
+        const unsigned lt = (1u << lane) - 1u;
+        for (int64_t base = 0, t = 0; base < n_chunks; base += nt, ++t) {
+          const int64_t c = base + t0;
+          const bool valid = c < n_chunks;
+          const int r = valid ? emit_chunk(c) : -1;
+          const unsigned peers = __match_any_sync(kFull, r);
+          const int rank_in = __popc(peers & lt);
+          int* wc = &s_wcnt[t & 1][tw][0];
+          if (lane < W) wc[lane] = 0;
+          __syncwarp();
+          if (valid && rank_in == 0) wc[r] = __popc(peers);
+          bar();
+          if (tw == 0 && lane < W) {  // exclusive prefix over the warps, after the earlier tiles
+            int run = s_run[lane];
+            for (int w = 0; w < ntw; ++w) {
+              const int x = s_wcnt[t & 1][w][lane];
+              s_wcnt[t & 1][w][lane] = run;
+              run += x;
+            }
+            s_run[lane] = run;
+          }
+          bar();
+          const int64_t so = __shfl_sync(kFull, so_l, valid ? r : 0);
+          if (valid) a.send_idx[so + wc[r] + rank_in] = (int32_t)c;
+        }
+        SB_MARK_MAX(9);
+      }
+    } else {
+      for (int r = warp; r < W; r += nw) rank_lists(r, __shfl_sync(kFull, ro_l, r), __shfl_sync(kFull, so_l, r));
+      SB_MARK_MAX(8);
+      for (int64_t c = rtid; c < n_chunks; c += blockDim.x) emit_chunk(c);
+      for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {  // warp-uniform trip count (the shuffle below)
+        const int64_t i = b0 + rtid;
+        const int r = i < N ? s_rank[i] : 0;
+        const int64_t so = __shfl_sync(kFull, so_l, r);
+        if (i < N) send_list(i, so);
+      }
+      SB_MARK_MAX(9);
     }
-    SB_MARK_MAX(9);
   } else {
     if (warp == 0) {
       int64_t so = 0, ro = 0;

@@ -1,6 +1,6 @@
 """Per-phase cycle trace of the fused planner (diagnostics, needs a GPU).
 
-    python tools/trace_planner.py [c2|c1] [topology] [small|hybrid|large]
+    python tools/trace_planner.py [c2|c1|c1:<n>] [topology] [small|hybrid|large]
 """
 import os
 import sys
@@ -14,8 +14,9 @@ from paper_2508_06001_b200 import datagen  # noqa: E402
 
 C2 = ["g2b8i256f1s0", "g2b4i512f1s0", "g2b2i768f1s0", "g2b1i1024f1s0"]
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-if cfg == "c1":
-    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=32)
+if cfg.startswith("c1"):  # c1 (256 sequences) or c1:<n>
+    n = int(cfg.split(":")[1]) if ":" in cfg else 256
+    ids, lens = datagen.metadata("c1", 8, seed=1, step=0, per_rank=n // 8)
     topo = "g1n8"
 else:
     ids, lens = datagen.metadata("scenario", 8, codes=C2, step=0, seed=7)
