@@ -618,13 +618,13 @@ __global__ void g_diag(const double* w_sorted, int n, int M, const double* caps,
 //  VAR 6: VAR 0 inside a 512-thread CTA (128-register cap), the other 15
 //  warps waiting at __syncthreads (the fused planner's situation)
 template <int VAR>
-__global__ void __launch_bounds__(VAR >= 6 ? 512 : 32) g_prod(const double* w_sorted, int n, int M, const double* caps, int* pick, long long* cyc,
+__global__ void __launch_bounds__((VAR == 6 || VAR == 7) ? 512 : 32) g_prod(const double* w_sorted, int n, int M, const double* caps, int* pick, long long* cyc,
                        int* replays) {
   extern __shared__ double wsd[];
   __shared__ int s_pick[4096];  // ring: the store cost is what is measured
   __shared__ int s_q[4096];
   const int lane = threadIdx.x;
-  if (VAR >= 6 && threadIdx.x >= 32) {
+  if ((VAR == 6 || VAR == 7) && threadIdx.x >= 32) {
     __syncthreads();
     return;
   }
@@ -662,7 +662,16 @@ __global__ void __launch_bounds__(VAR >= 6 ? 512 : 32) g_prod(const double* w_so
     const uint32_t best_j = (uint32_t)lane;
     const uint32_t khi = (uint32_t)(best >> 32), klo = (uint32_t)best;
     uint32_t m1, m2, pk;
-    if (VAR == 7) {  // inline-PTX redux.sync (bounds 512): does it avoid the divergence checks?
+    if (VAR == 8) {  // unique-high-word shortcut: ballot, else the two exact REDUX
+      m1 = __reduce_min_sync(0xffffffffu, khi);
+      const unsigned eq = __ballot_sync(0xffffffffu, khi == m1);
+      if (__popc(eq) == 1) {
+        pk = (uint32_t)(__ffs(eq) - 1);
+      } else {
+        m2 = __reduce_min_sync(0xffffffffu, khi == m1 ? klo : 0xffffffffu);
+        pk = __reduce_min_sync(0xffffffffu, (khi == m1 && klo == m2) ? best_j : 0xffffffffu);
+      }
+    } else if (VAR == 7) {  // inline-PTX redux.sync (bounds 512): does it avoid the divergence checks?
       asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m1) : "r"(khi));
       asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(m2) : "r"(khi == m1 ? klo : 0xffffffffu));
       asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(pk) : "r"((khi == m1 && klo == m2) ? best_j : 0xffffffffu));
@@ -690,7 +699,7 @@ __global__ void __launch_bounds__(VAR >= 6 ? 512 : 32) g_prod(const double* w_so
   if (VAR != 4)
     for (int i = lane; i < n; i += 32) pick[i] = i < n - 4096 ? -1 : s_pick[i & 4095];
   if (lane == 0) { *cyc = t1 - t0; *replays = viol + s_q[n / 2] * 0; }
-  if (VAR >= 6 && blockDim.x > 32) __syncthreads();
+  if ((VAR == 6 || VAR == 7) && blockDim.x > 32) __syncthreads();
 }
 
 // Two-REDUX argmin with exact block replay (candidate for greedy_warp):
@@ -840,6 +849,7 @@ int main() {
       run(g_fast<16>, "fast2-K16");
       run(g_fast<64>, "fast2-K64");
       run(g_prod<0>, "prod");
+      run(g_prod<8>, "prod-unique-hi");
       run(g_prod<1>, "prod-no-q");
       run(g_prod<2>, "prod-direct-w");
       run(g_prod<3>, "prod-no-viol");
