@@ -57,12 +57,21 @@ __device__ void reg_bitonic(uint64_t* s_hi, uint64_t* s_lo, uint32_t* s_v, int n
   for (int k = 2; k <= T; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= B) {  // RPT == 2, j == B: the partner is this thread's other record; k > B, so ascending
-        if (rec_less_bf(h[RPT - 1], l[RPT - 1], v[RPT - 1], h[0], l[0], v[0])) {
-          const uint64_t a = h[0], b = l[0];
-          const uint32_t c = v[0];
-          h[0] = h[RPT - 1]; l[0] = l[RPT - 1]; v[0] = v[RPT - 1];
-          h[RPT - 1] = a; l[RPT - 1] = b; v[RPT - 1] = c;
+      if (j >= B) {  // the partner of record r is this thread's record r ^ (j / B)
+        const int d = j / B;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          if ((r & d) != 0) continue;
+          const int r2 = r | d;
+          const int x = tid + r * B;
+          const bool up = (x & k) == 0;  // ascending half of the current bitonic merge
+          const bool lt = rec_less_bf(h[r2], l[r2], v[r2], h[r], l[r], v[r]);
+          if (lt == up) {  // ascending: smaller to r; descending: larger to r
+            const uint64_t a = h[r], b = l[r];
+            const uint32_t c = v[r];
+            h[r] = h[r2]; l[r] = l[r2]; v[r] = v[r2];
+            h[r2] = a; l[r2] = b; v[r2] = c;
+          }
         }
         continue;
       }

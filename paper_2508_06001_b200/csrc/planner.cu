@@ -388,8 +388,37 @@ __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
   const double* sw = a.sorted_w + lo;
   for (int i = lane; i < n; i += 32) stage[i] = sw[i];
   __syncwarp();
-  greedy_warp<BPL, 0, QOUT>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {},
-                            a.pick + lo, nullptr, a.violations, QOUT ? a.greedy_q + lo : nullptr);
+  if constexpr (!QOUT) {
+    greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
+                        nullptr, a.violations);
+  } else {
+    // hybrid path: the picks go to shared memory behind the workloads, then
+    // one pass derives each position's rank inside its bag (the stable bag
+    // partition, match_any per 32 positions) and writes both out coalesced.
+    // Recording the rank inside the chain cost ~16 cycles per step.
+    __shared__ int run[kMaxBags];
+    int32_t* p_stage = reinterpret_cast<int32_t*>(stage + a.max_seqs);
+    greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, p_stage, nullptr,
+                        a.violations);
+    for (int b = lane; b < a.M; b += 32) run[b] = 0;
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int p0 = 0; p0 < n; p0 += 32) {
+      const int p = p0 + lane;
+      const bool valid = p < n;
+      const int b = valid ? p_stage[p] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int rank_in = __popc(peers & lt);
+      const int base = valid ? run[b] : 0;
+      __syncwarp();
+      if (valid && rank_in == 0) run[b] = base + __popc(peers);
+      __syncwarp();
+      if (valid) {
+        a.pick[lo + p] = b;
+        a.greedy_q[lo + p] = base + rank_in;
+      }
+    }
+  }
 }
 
 template <int BPL>
@@ -1377,7 +1406,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaEventRecord(p->join_ev, p->side));
     }
-    const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
+    const int smem = (int)((sizeof(double) + sizeof(int32_t)) * std::max<int64_t>(1, p->max_seqs));
     static int set_to[2] = {0, 0};
     const bool wide = p->M > 32;
     if (smem > set_to[wide]) {

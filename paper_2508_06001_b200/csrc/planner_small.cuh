@@ -439,14 +439,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
         }
         __syncthreads();
       }
-      if (n > 32 && n <= 2 * kSmallThreads && blockDim.x == kSmallThreads) {
+      if (n > 32 && n <= 4 * kSmallThreads && blockDim.x == kSmallThreads) {
         const int nn = (int)n;
         int32_t* gs = a.sorted_idx;
         if (nn <= 64) reg_sort_emit<64, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
         else if (nn <= 128) reg_sort_emit<128, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
         else if (nn <= 256) reg_sort_emit<256, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
         else if (nn <= 512) reg_sort_emit<512, 1>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
-        else reg_sort_emit<1024, 2>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+        else if (nn <= 1024) reg_sort_emit<1024, 2>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
+      else reg_sort_emit<2048, 4>(gs, s_hi, s_lo, s_v, s_sorted, s_w, s_wsorted, lo, nn);
       } else if (n <= 1024) {
         // rank by counting: the key (~bits(w), id, index) is a total order.
         // k = blockDim/n lanes (power of two <= 32) share one record's count,
