@@ -132,7 +132,40 @@ __device__ void reg_sort_emit(int32_t* sorted_idx, uint64_t* s_hi, uint64_t* s_l
 template <int BPL>
 __device__ __forceinline__ void small_greedy(const PlanArgs& a, int rep, int64_t n, double total_rep, const double* ws,
                                           int32_t* pick, int32_t* bagcnt, int* viol, int32_t* q) {
-  greedy_warp<BPL, 0, true>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, pick, bagcnt, viol, q);
+  greedy_warp<BPL, 0>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, pick, bagcnt, viol);
+  // each position's rank inside its bag (the stable bag partition), one
+  // match_any pass after the chain: recording it inside the chain cost more
+  // per step.  `bagcnt` (this replica's M counts, written by the greedy)
+  // serves as the running counters and is restored at the end.
+  const int lane = threadIdx.x & 31, M = a.M;
+  int32_t* cnt = bagcnt + rep * M;
+  __syncwarp();
+  int keep[BPL];
+#pragma unroll
+  for (int i = 0; i < BPL; ++i) {
+    const int j = lane + 32 * i;
+    keep[i] = j < M ? cnt[j] : 0;
+    if (j < M) cnt[j] = 0;
+  }
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int p0 = 0; p0 < (int)n; p0 += 32) {
+    const int p = p0 + lane;
+    const bool valid = p < (int)n;
+    const int b = valid ? pick[p] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int rank_in = __popc(peers & lt);
+    const int base = valid ? cnt[b] : 0;
+    __syncwarp();
+    if (valid && rank_in == 0) cnt[b] = base + __popc(peers);
+    __syncwarp();
+    if (valid) q[p] = base + rank_in;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < BPL; ++i)
+    if (lane + 32 * i < M) cnt[lane + 32 * i] = keep[i];
+  __syncwarp();
 }
 
 // Warp-level inclusive scan helper over int64.
