@@ -146,6 +146,7 @@ struct sb_planner {
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t gfork_ev = nullptr, gjoin_ev = nullptr;  // single-bag greedy chain (overlaps emission)
+  cudaEvent_t dup_ev = nullptr;                         // multi-kernel duplicate-id check (side stream)
 
   // timing
   bool timing = false;

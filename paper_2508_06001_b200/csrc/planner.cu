@@ -59,8 +59,8 @@ __global__ void k_selftest_div(uint64_t seed, int64_t n, unsigned long long* mis
 // ------------------------------------------------------------------ prep
 // Per sequence (grid over the capacity, one thread per gathered sequence):
 // workload (balancer.cpp:144; or the caller's for assign_to_bags), owning
-// rank, length check (workload_model.cpp:66) and the duplicate-id check
-// inside the replica (open addressing in global memory).
+// rank and the length check (workload_model.cpp:66); the duplicate-id check
+// (open addressing in global memory) is k_prep_dup on the side stream.
 __device__ __forceinline__ double seq_workload(const PlanArgs& a, int64_t i) {
   if (a.w_in) return a.w_in[i];
   const int64_t len = a.lens[i];
@@ -80,18 +80,33 @@ __global__ void __launch_bounds__(256) k_prep_seq(PlanArgs a) {
     if (a.rank_off[mid] <= i) lo = mid;
     else hi = mid;
   }
-  const int r = lo, rep = r / a.U;
+  const int r = lo;
   if (a.lens[i] < 0) atomicOr(a.status, ST_NEG_LENGTH);
   const double wi = seq_workload(a, i);
   if (a.w_in && !(wi >= 0.0)) atomicOr(a.status, ST_NEG_LENGTH);  // balancer.cpp:18-20
   a.w[i] = wi;
   a.seq_rank[i] = r;
+}
+
+// The duplicate-id check inside each replica (divergence), on the
+// planner's side stream after the totals: only the status word depends on
+// it, so it runs beside the sort and the greedy and is joined at the end.
+__global__ void __launch_bounds__(256) k_prep_dup(PlanArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!seqs_ok(a) || a.w_in || i >= a.rank_off[a.W]) return;
+  int lo = 0, hi = a.W;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.rank_off[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  const int rep = lo / a.U;
   const int64_t rlo = a.rank_off[rep * a.U], rhi = a.rank_off[rep * a.U + a.U];
   const int64_t tsize = 2 * (rhi - rlo);
   uint64_t* tab = a.hash + 2 * rlo;
   const uint64_t id = a.ids[i];
   if (id == ~0ull) {
-    if (atomicAdd(&a.sentinel[rep], 1) > 0 && !a.w_in) atomicOr(a.status, ST_DUP_ID);
+    if (atomicAdd(&a.sentinel[rep], 1) > 0) atomicOr(a.status, ST_DUP_ID);
     return;
   }
   uint64_t slot = hash_slot(id) % (uint64_t)tsize;
@@ -100,7 +115,7 @@ __global__ void __launch_bounds__(256) k_prep_seq(PlanArgs a) {
         atomicCAS(reinterpret_cast<unsigned long long*>(tab + slot), ~0ull, (unsigned long long)id);
     if (old == ~0ull) break;
     if (old == id) {
-      if (!a.w_in) atomicOr(a.status, ST_DUP_ID);  // assign_to_bags allows repeats
+      atomicOr(a.status, ST_DUP_ID);
       break;
     }
     slot = (slot + 1 == (uint64_t)tsize) ? 0 : slot + 1;
@@ -1185,6 +1200,7 @@ static void planner_alloc(sb_planner* p) {
   SB_CUDA(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming));
   SB_CUDA(cudaEventCreateWithFlags(&p->gfork_ev, cudaEventDisableTiming));
   SB_CUDA(cudaEventCreateWithFlags(&p->gjoin_ev, cudaEventDisableTiming));
+  SB_CUDA(cudaEventCreateWithFlags(&p->dup_ev, cudaEventDisableTiming));
 }
 
 static void planner_free(sb_planner* p) {
@@ -1210,6 +1226,7 @@ static void planner_free(sb_planner* p) {
   if (p->join_ev) cudaEventDestroy(p->join_ev);
   if (p->gfork_ev) cudaEventDestroy(p->gfork_ev);
   if (p->gjoin_ev) cudaEventDestroy(p->gjoin_ev);
+  if (p->dup_ev) cudaEventDestroy(p->dup_ev);
   if (p->side) cudaStreamDestroy(p->side);
   for (cudaEvent_t e : p->copy_ev) cudaEventDestroy(e);
   if (p->x_owner) cudaFree(p->x_owner);
@@ -1285,8 +1302,13 @@ static void launch_totals(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
   k_prep_rows<<<p->W, kPrepRowsThreads, 0, p->side>>>(a);
   SB_CHECK_LAUNCH();
   SB_CUDA(cudaEventRecord(p->join_ev, p->side));
-  count_launch(2);
+  k_prep_dup<<<(int)((p->max_seqs + 255) / 256), 256, 0, p->side>>>(a);  // joined by join_dup()
+  SB_CHECK_LAUNCH();
+  SB_CUDA(cudaEventRecord(p->dup_ev, p->side));
+  count_launch(3);
 }
+
+static void join_dup(sb_planner* p, cudaStream_t s) { SB_CUDA(cudaStreamWaitEvent(s, p->dup_ev, 0)); }
 
 static void launch_prep(sb_planner* p, const PlanArgs& a, cudaStream_t s) {
   k_prep_seq<<<(int)((p->max_seqs + 255) / 256), 256, 0, s>>>(a);
@@ -1458,6 +1480,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
   if (p->M == 1) SB_CUDA(cudaStreamWaitEvent(s, p->gjoin_ev, 0));  // single-bag occupancy replay joined
   k_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
+  join_dup(p, s);
   if (p->timing) SB_CUDA(cudaEventRecord(p->ev[5], s));
   count_launch(7);  // greedy, emit count, emit, emit chunks, lists count, lists, finalize (+ tie replay)
 }
@@ -1474,6 +1497,7 @@ static void run_identity(sb_planner* p, cudaStream_t s) {
   SB_CHECK_LAUNCH();
   k_identity_finalize<<<1, 32, 0, s>>>(a);
   SB_CHECK_LAUNCH();
+  join_dup(p, s);
   count_launch(3);
 }
 
@@ -1779,6 +1803,7 @@ extern "C" sb_status sb_assign_to_bags(sb_planner* p, int64_t n, const uint64_t*
   sb::launch_prep(p, a, s);
   sb::launch_sort(p, a, s, true);
   sb::launch_greedy(p, a, s, false);
+  sb::join_dup(p, s);
   sb::count_launch(2);
   SB_CUDA(cudaStreamSynchronize(s));
   int32_t st = 0;
