@@ -36,6 +36,7 @@
 #include "plan_args.cuh"
 #include "serial_sum.cuh"
 #include "stdsort.cuh"
+#include "tma.cuh"
 
 namespace sb {
 
@@ -395,14 +396,15 @@ constexpr int kGreedyStage = 24576;  // 192 KB of workloads
 
 template <int BPL, bool QOUT = false>
 __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
-  extern __shared__ __align__(16) double stage[];
+  extern __shared__ __align__(16) double stage_raw[];  // max_seqs + 2 doubles (+ max_seqs ints for QOUT)
+  __shared__ __align__(8) uint64_t sbar;
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, lane = threadIdx.x;
   const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
   const int n = (int)(hi - lo);
-  const double* sw = a.sorted_w + lo;
-  for (int i = lane; i < n; i += 32) stage[i] = sw[i];
-  __syncwarp();
+  // greedy-order workloads into shared memory by bulk copy (one warp's
+  // dependent load rounds took ~30 us at 16K sequences)
+  const double* stage = stage_doubles_bulk(stage_raw, a.sorted_w + lo, n, &sbar);
   if constexpr (!QOUT) {
     greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
                         nullptr, a.violations);
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
     // partition, match_any per 32 positions) and writes both out coalesced.
     // Recording the rank inside the chain cost ~16 cycles per step.
     __shared__ int run[kMaxBags];
-    int32_t* p_stage = reinterpret_cast<int32_t*>(stage + a.max_seqs);
+    int32_t* p_stage = reinterpret_cast<int32_t*>(stage_raw + a.max_seqs + 2);
     greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, p_stage, nullptr,
                         a.violations);
     for (int b = lane; b < a.M; b += 32) run[b] = 0;
@@ -1159,7 +1161,8 @@ static void planner_alloc(sb_planner* p) {
   dalloc(&p->w, N); dalloc(&p->seq_rank, N); dalloc(&p->seq_off, N); dalloc(&p->hash, 2 * N);
   dalloc(&p->sk_hi, N); dalloc(&p->sk_lo, N); dalloc(&p->tk_hi, N); dalloc(&p->tk_lo, N);
   dalloc(&p->sk_v, N); dalloc(&p->tk_v, N);
-  dalloc(&p->sorted_w, N); dalloc(&p->sorted_idx, N); dalloc(&p->pick, N);
+  dalloc(&p->sorted_w, N + 2);  // + bulk-copy alignment slack (k_greedy_staged)
+  dalloc(&p->sorted_idx, N); dalloc(&p->pick, N);
   dalloc(&p->seq_bag, N); dalloc(&p->seq_G, N); dalloc(&p->seq_chunk_base, N); dalloc(&p->greedy_q, N);
   dalloc(&p->rep_total, R); dalloc(&p->sentinel, R); dalloc(&p->bag_count, R * M);
   dalloc(&p->bag_rows, R * M); dalloc(&p->rep_chunks, R); dalloc(&p->send_count, W);
@@ -1378,7 +1381,7 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool
   }
   const bool wide = (p->M + 31) / 32 > 1;
   if (p->max_seqs <= kGreedyStage) {
-    const int smem = (int)(sizeof(double) * std::max<int64_t>(1, p->max_seqs));
+    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 2));
     static int set_to[2] = {0, 0};
     if (smem > set_to[wide]) {
       if (wide) SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1428,7 +1431,8 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaEventRecord(p->join_ev, p->side));
     }
-    const int smem = (int)((sizeof(double) + sizeof(int32_t)) * std::max<int64_t>(1, p->max_seqs));
+    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 2) +
+                           sizeof(int32_t) * std::max<int64_t>(1, p->max_seqs));
     static int set_to[2] = {0, 0};
     const bool wide = p->M > 32;
     if (smem > set_to[wide]) {
