@@ -123,7 +123,7 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
 // `q_out` (optional): per greedy position, the sequence's rank inside its
 // bag (the stable bag partition of balancer.cpp:178-192), stored by the
 // winning lane off the chain.
-template <int BPL, int CHUNK, bool QOUT = false, class GetW, class Hook>
+template <int BPL, int CHUNK, bool QOUT = false, bool PADDED = false, class GetW, class Hook>
 __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t n, double total_rep, GetW getw,
                                             Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out,
                                             int32_t* q_out = nullptr) {
@@ -160,7 +160,9 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     const double w = w_a, wn = w_b;  // w_p and w_{p+1} (0 past the end: unused)
     w_a = w_b;
     w_b = w_c;
-    w_c = getw(p + 3 < nn ? p + 3 : nn - 1);  // prefetch under this step (clamped: no branch)
+    // prefetch under this step: clamped, or straight when getw is readable 3
+    // past the end (PADDED: the staged kernels pad their buffer)
+    w_c = getw(PADDED ? p + 3 : (p + 3 < nn ? p + 3 : nn - 1));
     double nasg[BPL], nocc[BPL], nrem[BPL];
     uint64_t kwin[BPL], knot[BPL];
     uint64_t best = ~0ull;

@@ -396,7 +396,7 @@ constexpr int kGreedyStage = 24576;  // 192 KB of workloads
 
 template <int BPL, bool QOUT = false>
 __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
-  extern __shared__ __align__(16) double stage_raw[];  // max_seqs + 2 doubles (+ max_seqs ints for QOUT)
+  extern __shared__ __align__(16) double stage_raw[];  // max_seqs + 6 doubles (+ max_seqs ints for QOUT)
   __shared__ __align__(8) uint64_t sbar;
   if (!seqs_ok(a)) return;
   const int rep = blockIdx.x, lane = threadIdx.x;
@@ -405,18 +405,20 @@ __global__ void __launch_bounds__(32) k_greedy_staged(PlanArgs a) {
   // greedy-order workloads into shared memory by bulk copy (one warp's
   // dependent load rounds took ~30 us at 16K sequences)
   const double* stage = stage_doubles_bulk(stage_raw, a.sorted_w + lo, n, &sbar);
+  if (lane < 4) const_cast<double*>(stage)[n + lane] = 0.0;  // the unclamped prefetch reads 3 past the end
+  __syncwarp();
   if constexpr (!QOUT) {
-    greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, a.pick + lo,
-                        nullptr, a.violations);
+    greedy_warp<BPL, 0, false, true>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {},
+                                     a.pick + lo, nullptr, a.violations);
   } else {
     // hybrid path: the picks go to shared memory behind the workloads, then
     // one pass derives each position's rank inside its bag (the stable bag
     // partition, match_any per 32 positions) and writes both out coalesced.
     // Recording the rank inside the chain cost ~16 cycles per step.
     __shared__ int run[kMaxBags];
-    int32_t* p_stage = reinterpret_cast<int32_t*>(stage_raw + a.max_seqs + 2);
-    greedy_warp<BPL, 0>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {}, p_stage, nullptr,
-                        a.violations);
+    int32_t* p_stage = reinterpret_cast<int32_t*>(stage_raw + a.max_seqs + 6);
+    greedy_warp<BPL, 0, false, true>(a, rep, n, a.rep_total[rep], [&](int p) { return stage[p]; }, [](int) {},
+                                     p_stage, nullptr, a.violations);
     for (int b = lane; b < a.M; b += 32) run[b] = 0;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
@@ -1381,7 +1383,7 @@ static void launch_greedy(sb_planner* p, const PlanArgs& a, cudaStream_t s, bool
   }
   const bool wide = (p->M + 31) / 32 > 1;
   if (p->max_seqs <= kGreedyStage) {
-    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 2));
+    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 6));
     static int set_to[2] = {0, 0};
     if (smem > set_to[wide]) {
       if (wide) SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1431,7 +1433,7 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaEventRecord(p->join_ev, p->side));
     }
-    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 2) +
+    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 6) +
                            sizeof(int32_t) * std::max<int64_t>(1, p->max_seqs));
     static int set_to[2] = {0, 0};
     const bool wide = p->M > 32;

@@ -54,6 +54,19 @@ static double host_workload(int64_t len, double d, double gamma) {
   return lin + att;
 }
 
+// production code with the unclamped prefetch (PADDED: stage has 3 spare slots)
+__global__ void __launch_bounds__(32) k_prod_pad(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n + 4; i += 32) stage[i] = i < n ? sw[i] : 0.0;
+  __syncwarp();
+  const long long t0 = clock64();
+  greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
+                                 a.violations);
+  const long long t1 = clock64();
+  if (lane == 0) *cyc = t1 - t0;
+}
+
 int main(int argc, char** argv) {
   std::vector<int64_t> lens;
   if (argc > 1) {
@@ -113,14 +126,14 @@ int main(int argc, char** argv) {
     a.violations = viol;
     a.trace = nullptr;
     auto run = [&](auto kern, const char* name) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, n * 8);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 4) * 8);
       long long c = 0;
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
-      for (int r = 0; r < 3; ++r) kern<<<1, 32, n * 8>>>(a, dw, n, dc);
+      for (int r = 0; r < 3; ++r) kern<<<1, 32, (n + 4) * 8>>>(a, dw, n, dc);
       cudaEventRecord(e0);
-      kern<<<1, 32, n * 8>>>(a, dw, n, dc);
+      kern<<<1, 32, (n + 4) * 8>>>(a, dw, n, dc);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0.f;
@@ -131,6 +144,7 @@ int main(int argc, char** argv) {
     };
     run(k_prod, "prod");
     run(k_prod_regs, "prod-regs");
+    run(k_prod_pad, "prod-padded");
   }
   return 0;
 }
