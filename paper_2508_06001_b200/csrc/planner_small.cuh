@@ -328,14 +328,22 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
         // from the lengths into the (not yet used) greedy-order scratch, lane 0
         // chains them
         const int n = (int)N;
+        const double* wsrc = s_wsorted;
+        if (N > kSmallScanSeqs) {
+          // the sequence pass (warps 1..) writes s_w; wait for it on barrier 3
+          // (producers only arrive) instead of reloading the lengths here
+          asm volatile("bar.sync 3, %0;" ::"r"((int)blockDim.x) : "memory");
+          wsrc = s_w;
+        } else {
   #pragma unroll 4
-        for (int i = lane; i < n; i += 32) s_wsorted[i] = raw_workload(i);
-        __syncwarp();
+          for (int i = lane; i < n; i += 32) s_wsorted[i] = raw_workload(i);
+          __syncwarp();
+        }
         double s = 0.0;
         if (lane == 0) {
           // 16-byte loads, the next group's issued before this group's DADDs
           // (the chain is the only serial part: ~8 cycles per element)
-          const double2* v2 = reinterpret_cast<const double2*>(s_wsorted);
+          const double2* v2 = reinterpret_cast<const double2*>(wsrc);
           int i = 0;
           if (n >= 8) {
             double2 c0 = v2[0], c1 = v2[1], c2 = v2[2], c3 = v2[3];
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
             s = __dadd_rn(s, c0.x); s = __dadd_rn(s, c0.y); s = __dadd_rn(s, c1.x); s = __dadd_rn(s, c1.y);
             s = __dadd_rn(s, c2.x); s = __dadd_rn(s, c2.y); s = __dadd_rn(s, c3.x); s = __dadd_rn(s, c3.y);
           }
-          for (; i < n; ++i) s = __dadd_rn(s, s_wsorted[i]);
+          for (; i < n; ++i) s = __dadd_rn(s, wsrc[i]);
         }
         if (MODE == 0) SB_MARK_MAX(11);  // diagnostics: totals chain done
         if (lane == 0) {
@@ -388,6 +396,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
         const int t = tid - 32, nt = (int)blockDim.x - 32, tw = t >> 5, ntw = nt >> 5;
         auto bar = [nt]() { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); };
         seq_pass(t, nt, true);
+        asm volatile("bar.arrive 3, %0;" ::"r"((int)blockDim.x) : "memory");  // s_w ready for warp 0
         bar();
         const int n = (int)N;
         const int per = (n + nt - 1) / nt, b0 = t * per < n ? t * per : n, b1 = b0 + per < n ? b0 + per : n;
