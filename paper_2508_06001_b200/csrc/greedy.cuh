@@ -123,14 +123,28 @@ __device__ __forceinline__ void greedy_single_bag(const PlanArgs& a, int rep, in
 // `q_out` (optional): per greedy position, the sequence's rank inside its
 // bag (the stable bag partition of balancer.cpp:178-192), stored by the
 // winning lane off the chain.
-template <int BPL, int CHUNK, bool QOUT = false, bool PADDED = false, class GetW, class Hook>
+struct NoDone {
+  __device__ void operator()() const {}
+};
+
+// `done()` runs once the picks are all stored, before the per-bag epilogue
+// (the fused planner hands the picks to another warp there).  SB_TRACE_P3
+// (diagnostics build) marks the setup and epilogue in trace slots 7, 11, 12.
+template <int BPL, int CHUNK, bool QOUT = false, bool PADDED = false, class GetW, class Hook, class Done = NoDone>
 __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t n, double total_rep, GetW getw,
                                             Hook hook, int32_t* pick_out, int32_t* bagcnt_out, int* viol_out,
-                                            int32_t* q_out = nullptr) {
+                                            int32_t* q_out = nullptr, Done done = Done()) {
   const int lane = threadIdx.x & 31;
+#ifdef SB_TRACE_P3
+  if (a.trace && rep == 0 && lane == 0) a.trace[11] = clock64();
+#endif
   const double target = __ddiv_rn(total_rep, (double)a.U);  // balancer.cpp:26
+#ifdef SB_TRACE_P3
+  if (a.trace && rep == 0 && lane == 0) a.trace[12] = clock64() + (target == 12345.0 ? 1 : 0);
+#endif
   if (a.M == 1) {
     greedy_single_bag<CHUNK>(a, rep, n, target, getw, hook, pick_out, bagcnt_out, viol_out, q_out);
+    done();
     return;
   }
   double cap[BPL], rcap[BPL], asg[BPL], occ[BPL], rem[BPL];
@@ -206,6 +220,7 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     }
   }
   if (a.trace && rep == 0 && lane == 0) a.trace[15] = clock64();
+  done();
 #pragma unroll
   for (int i = 0; i < BPL; ++i) {
     const int j = lane + 32 * i;
@@ -219,6 +234,9 @@ __device__ __forceinline__ void greedy_warp(const PlanArgs& a, int rep, int64_t 
     }
   }
   if (lane == 0) atomicAdd(viol_out, viol);
+#ifdef SB_TRACE_P3
+  if (a.trace && rep == 0 && lane == 0) a.trace[7] = clock64();
+#endif
 }
 
 }  // namespace sb

@@ -18,6 +18,13 @@ namespace sb {
   } while (0)
 // Sub-phase marks (diagnostics): thread 0's time / the latest warp's time.
 #define SB_MARK(k) SB_PHASE(k)
+#ifdef SB_TRACE_P3  // diagnostics: slots 7-9, 11, 12 mark phase 3's setup / epilogue instead of phases 1 and 5
+#define SB_P3(k) SB_PHASE(k)
+#define SB_P5(x)
+#else
+#define SB_P3(k)
+#define SB_P5(x) x
+#endif
 #define SB_MARK_MAX(k)                                                                                   \
   do {                                                                                                   \
     if (a.trace && (threadIdx.x & 31) == 0)                                                              \
@@ -36,7 +43,7 @@ __host__ __device__ inline int small_pow2(int n) {
 
 struct SmallLayout {  // byte offsets into dynamic shared memory
   size_t ids, lens, w, soff, hi, lo, v, rank, sorted, pick, G, cb, bo, rank_off, rpre, bagcnt, bagcb, bagq,
-      sendcnt, sendoff, reptot, repc, tie, t_boff, t_branks, t_bsize, t_rbag, t_rmem, pergpu, recvoff, q, total;
+      sendcnt, sendoff, reptot, repc, tie, t_boff, t_branks, t_bsize, t_rbag, t_rmem, pergpu, recvoff, q, qcnt, total;
   int T;
 };
 
@@ -81,6 +88,7 @@ __host__ __device__ inline SmallLayout small_layout(int cap, int W, int RM, int 
   L.pergpu = take(8ull * W);  // per-GPU workload: the greedy writes it, WIR reads it
   L.recvoff = take(8ull * W);
   L.q = take(4ull * cap);  // rank of each greedy position inside its bag
+  L.qcnt = take(4ull * M);  // bag counters of the split bag-rank pass (one replica)
   L.total = o;
   return L;
 }
@@ -126,17 +134,46 @@ __device__ void reg_sort_emit(int32_t* sorted_idx, uint64_t* s_hi, uint64_t* s_l
   }
 }
 
+// Each greedy position's rank inside its bag (the stable bag partition,
+// balancer.cpp:178-192): one match_any pass over the picks, `cnt` (M bag
+// counters, zero on entry) running.  Recording it inside the chain cost more
+// per step.
+__device__ __forceinline__ void bag_ranks_pass(const int32_t* pick, int n, int32_t* cnt, int32_t* q) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int p0 = 0; p0 < n; p0 += 32) {
+    const int p = p0 + lane;
+    const bool valid = p < n;
+    const int b = valid ? pick[p] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int rank_in = __popc(peers & lt);
+    const int base = valid ? cnt[b] : 0;
+    __syncwarp();
+    if (valid && rank_in == 0) cnt[b] = base + __popc(peers);
+    __syncwarp();
+    if (valid) q[p] = base + rank_in;
+  }
+}
+
 // The greedy inlined (an out-of-line call gave the same ~150 cycles per step
 // and a larger stack frame that lengthened every launch by ~4 us,
-// tools/plan_latency.py).
+// tools/plan_latency.py).  `qsplit`: the bag ranks are another warp's (it
+// waits on named barrier 4, which this warp arrives at once the picks are
+// stored); else this warp derives them after the per-bag epilogue, with
+// `bagcnt` (this replica's M counts, written by the greedy) as the running
+// counters, restored at the end.
 template <int BPL>
 __device__ __forceinline__ void small_greedy(const PlanArgs& a, int rep, int64_t n, double total_rep, const double* ws,
-                                          int32_t* pick, int32_t* bagcnt, int* viol, int32_t* q) {
-  greedy_warp<BPL, 0>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, pick, bagcnt, viol);
-  // each position's rank inside its bag (the stable bag partition), one
-  // match_any pass after the chain: recording it inside the chain cost more
-  // per step.  `bagcnt` (this replica's M counts, written by the greedy)
-  // serves as the running counters and is restored at the end.
+                                          int32_t* pick, int32_t* bagcnt, int* viol, int32_t* q, bool qsplit) {
+  auto handoff = [qsplit]() {
+    if (qsplit) {
+      __syncwarp();
+      asm volatile("bar.arrive 4, 64;" ::: "memory");
+    }
+  };
+  greedy_warp<BPL, 0>(a, rep, n, total_rep, [ws](int p) { return ws[p]; }, [](int) {}, pick, bagcnt, viol, nullptr,
+                      handoff);
+  if (qsplit) return;
   const int lane = threadIdx.x & 31, M = a.M;
   int32_t* cnt = bagcnt + rep * M;
   __syncwarp();
@@ -148,19 +185,7 @@ __device__ __forceinline__ void small_greedy(const PlanArgs& a, int rep, int64_t
     if (j < M) cnt[j] = 0;
   }
   __syncwarp();
-  const unsigned lt = (1u << lane) - 1u;
-  for (int p0 = 0; p0 < (int)n; p0 += 32) {
-    const int p = p0 + lane;
-    const bool valid = p < (int)n;
-    const int b = valid ? pick[p] : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
-    const int rank_in = __popc(peers & lt);
-    const int base = valid ? cnt[b] : 0;
-    __syncwarp();
-    if (valid && rank_in == 0) cnt[b] = base + __popc(peers);
-    __syncwarp();
-    if (valid) q[p] = base + rank_in;
-  }
+  bag_ranks_pass(pick, (int)n, cnt, q);
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < BPL; ++i)
@@ -358,7 +383,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
           }
           for (; i < n; ++i) s = __dadd_rn(s, wsrc[i]);
         }
-        if (MODE == 0) SB_MARK_MAX(11);  // diagnostics: totals chain done
+        if (MODE == 0) SB_P5(SB_MARK_MAX(11));  // diagnostics: totals chain done
         if (lane == 0) {
           *a.total = s;
           *a.n_seqs = N;
@@ -385,7 +410,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
           a.seq_off[i] = s_soff[i];
         }
         for (int r = lane; r < W; r += 32) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-        if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
+        if (MODE == 0) SB_P5(SB_MARK_MAX(12));  // diagnostics: origin offsets done
       } else if (N <= kSmallScanSeqs) {
         seq_pass(tid - 64, (int)blockDim.x - 64, true);
       } else {
@@ -426,7 +451,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
           a.seq_off[i] = s_soff[i];
         }
         for (int r = t; r < W; r += nt) a.origin_rows[r] = s_rpre[r + 1] - s_rpre[r];
-        if (MODE == 0) SB_MARK_MAX(12);  // diagnostics: origin offsets done
+        if (MODE == 0) SB_P5(SB_MARK_MAX(12));  // diagnostics: origin offsets done
       }
       __syncthreads();
     } else {
@@ -552,14 +577,19 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
   // ---- phase 3: greedy, one warp per replica (balancer.cpp:44-62), beside
   // the duplicate-id check inside each replica (divergence)
   const int ng = R < nw - 2 ? R : nw - 2;
+  // one replica: warp 1 derives the bag ranks from the picks (handed over on
+  // named barrier 4) while warp 0 finishes the per-bag epilogue and the bag
+  // bases; the duplicate check then runs on warps 2..
+  const bool qsplit = MODE == 0 && R == 1 && nw >= 4;
   if (warp < ng) {
     for (int rep = warp; rep < R; rep += ng) {
       const int64_t lo = s_roff[rep * U], n = s_roff[rep * U + U] - lo;
       if constexpr (MODE == 0) {
         const double* ws = s_wsorted + lo;
-        if (M <= 32) small_greedy<1>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
-        else small_greedy<2>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo);
+        if (M <= 32) small_greedy<1>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo, qsplit);
+        else small_greedy<2>(a, rep, n, s_reptot[rep], ws, s_pick + lo, s_bagcnt, &s_viol, s_q + lo, qsplit);
         __syncwarp();
+        if (rep == 0) SB_P3(8);
       }
       // replica-local chunk bases of the bags (chunk order: bag, q, k) and
       // the bags' first slots in the (replica, bag)-grouped sequence list
@@ -581,11 +611,19 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
         a.rep_chunks[rep] = cb;
         if (R == 1) *a.n_chunks = cb;
       }
+      if (rep == 0) SB_P3(9);
     }
+  } else if (qsplit && warp == 1) {
+    int32_t* qc = reinterpret_cast<int32_t*>(sm + L.qcnt);
+    for (int j = lane; j < M; j += 32) qc[j] = 0;
+    __syncwarp();
+    asm volatile("bar.sync 4, 64;" ::: "memory");
+    bag_ranks_pass(s_pick, (int)N, qc, s_q);
   } else if (MODE == 0 && !a.w_in) {  // the hybrid runs k_dup_small beside its greedy kernel
     // open-addressing set per replica in the sort scratch (free now):
     // s_hi and s_lo are contiguous, 2T slots >= 2 * replica size, EMPTY = ~0
-    const int t = tid - 32 * ng, nt = (int)blockDim.x - 32 * ng;
+    const int w0 = ng + (qsplit ? 1 : 0);
+    const int t = tid - 32 * w0, nt = (int)blockDim.x - 32 * w0;
     auto bar = [nt]() { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); };
     for (int rep = 0; rep < R; ++rep) {
       const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
@@ -793,7 +831,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
         a.recv_off[W] = ir;
       }
     }
-    SB_MARK(7);
+    SB_P5(SB_MARK(7));
     if (N > kSmallScanSeqs && 2 * W <= nw) {
       // send[r] = the chunks of source r in chunk order (finalize_manifests,
       // balancer.cpp:84-91): a stable filter of the chunk array by source
@@ -805,7 +843,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       __shared__ int s_run[32];
       if (warp < W) {
         rank_lists(warp, __shfl_sync(kFull, ro_l, warp), __shfl_sync(kFull, so_l, warp));
-        SB_MARK_MAX(8);
+        SB_P5(SB_MARK_MAX(8));
       } else {
         const int t0 = tid - 32 * W, nt = (int)blockDim.x - 32 * W, tw = warp - W, ntw = nw - W;
         auto bar = [nt]() { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); };
@@ -835,11 +873,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
           const int64_t so = __shfl_sync(kFull, so_l, valid ? r : 0);
           if (valid) a.send_idx[so + wc[r] + rank_in] = (int32_t)c;
         }
-        SB_MARK_MAX(9);
+        SB_P5(SB_MARK_MAX(9));
       }
     } else {
       for (int r = warp; r < W; r += nw) rank_lists(r, __shfl_sync(kFull, ro_l, r), __shfl_sync(kFull, so_l, r));
-      SB_MARK_MAX(8);
+      SB_P5(SB_MARK_MAX(8));
       for (int64_t c = rtid; c < n_chunks; c += blockDim.x) emit_chunk(c);
       for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {  // warp-uniform trip count (the shuffle below)
         const int64_t i = b0 + rtid;
@@ -847,7 +885,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
         const int64_t so = __shfl_sync(kFull, so_l, r);
         if (i < N) send_list(i, so);
       }
-      SB_MARK_MAX(9);
+      SB_P5(SB_MARK_MAX(9));
     }
   } else {
     if (warp == 0) {

@@ -47,4 +47,10 @@ for k, i in sub.items():
     if t[i] > 0:
         print(f"  {k:32s} +{int(t[i] - t[0]):8d} cycles from start")
 if t[15] > t[14] > 0:
-    print("greedy chain (replica 0):", int(t[15] - t[14]), "cycles")
+    print("greedy chain (replica 0):", int(t[15] - t[14]), "cycles;", "phase 3 start -> chain",
+          int(t[14] - t[3]), "chain end -> phase 4", int(t[4] - t[15]))
+if os.environ.get("SB_TRACE_P3"):
+    print("P3 setup: phase 3 start -> greedy entry", int(t[11] - t[3]), "-> target divided", int(t[12] - t[11]),
+          "-> chain start", int(t[14] - t[12]))
+    print("P3 epilogue: chain end -> greedy return", int(t[7] - t[15]), "-> q pass", int(t[8] - t[7]),
+          "-> bag bases", int(t[9] - t[8]), "-> phase 4", int(t[4] - t[9]))
