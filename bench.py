@@ -207,10 +207,9 @@ def run_c4(args):
     import paper_2508_06001_b200 as sb
     from paper_2508_06001_b200 import datagen
 
-    rank = int(os.environ.get("RANK", "0"))
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rows = []
