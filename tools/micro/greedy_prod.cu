@@ -2,7 +2,7 @@
 // runs it) timed beside greedy_micro.cu's hand copy of its step on the same
 // sorted workloads (diagnostics).
 //   nvcc -O3 -std=c++17 --expt-relaxed-constexpr -gencode arch=compute_100a,code=sm_100a \
-//        -I../../paper_2508_06001_b200/csrc -o greedy_prod greedy_prod.cu
+//        -I../../paper_2508_06001_b200/csrc -I../../include -o greedy_prod greedy_prod.cu
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -60,6 +60,95 @@ __global__ void __launch_bounds__(32) k_prod_pad(PlanArgs a, const double* sw, i
   const int lane = threadIdx.x;
   for (int i = lane; i < n + 4; i += 32) stage[i] = i < n ? sw[i] : 0.0;
   __syncwarp();
+  const long long t0 = clock64();
+  greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
+                                 a.violations);
+  const long long t1 = clock64();
+  if (lane == 0) *cyc = t1 - t0;
+}
+
+// register budget probes: the same kernel as k_prod_pad under a 128- and a
+// 64-register cap (the fused planner's 512-thread CTA allows 128), and a
+// 512-thread CTA whose warp 0 runs it (warps 1.. exit)
+template <int MINB>
+__global__ void __launch_bounds__(32, MINB) k_prod_cap(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n + 4; i += 32) stage[i] = i < n ? sw[i] : 0.0;
+  __syncwarp();
+  const long long t0 = clock64();
+  greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
+                                 a.violations);
+  const long long t1 = clock64();
+  if (lane == 0) *cyc = t1 - t0;
+}
+__global__ void __launch_bounds__(512, 1) k_prod_512(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n + 4; i += 32) stage[i] = i < n ? sw[i] : 0.0;
+  __syncwarp();
+  const long long t0 = clock64();
+  greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
+                                 a.violations);
+  const long long t1 = clock64();
+  if (lane == 0) *cyc = t1 - t0;
+}
+
+// the fused planner's shape: warps 1.. wait at a CTA barrier while warp 0
+// runs the greedy (SYNC); plus the warp-strided replica loop that makes ptxas
+// guard the REDUX chain with BRA.DIV (STRIDED)
+template <bool STRIDED>
+__global__ void __launch_bounds__(512, 1) k_prod_512sync(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n + 4; i += blockDim.x) stage[i] = i < n ? sw[i] : 0.0;
+  __syncthreads();
+  const int R = a.R, ng = R < 14 ? R : 14;
+  if (warp < ng) {
+    for (int rep = STRIDED ? warp : 0; rep < (STRIDED ? R : 1); rep += ng) {
+      const long long t0 = clock64();
+      greedy_warp<1, 0, false, true>(a, rep, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick,
+                                     nullptr, a.violations);
+      const long long t1 = clock64();
+      if (lane == 0) *cyc = t1 - t0;
+    }
+  }
+  __syncthreads();
+}
+
+// warp 0 by a constant test (ptxas proves convergence: no BRA.DIV) while the
+// others wait at the CTA barrier (W0) / the others exit early (EXIT: control)
+template <int V>
+__global__ void __launch_bounds__(512, 1) k_prod_512w0(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ int flag;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n + 4; i += blockDim.x) stage[i] = i < n ? sw[i] : 0.0;
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  if (warp == 0) {
+    const long long t0 = clock64();
+    greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
+                                   a.violations);
+    const long long t1 = clock64();
+    if (lane == 0) *cyc = t1 - t0;
+    if (V == 1 && lane == 0) atomicExch(&flag, 1);
+  } else if (V == 1) {  // the others sleep-poll a shared flag instead of a barrier
+    while (atomicAdd(&flag, 0) == 0) __nanosleep(2000);
+  }
+  if (V == 0) __syncthreads();
+}
+
+// divergent block-wide work and a barrier first, then warps 1.. exit and
+// warp 0 runs the greedy (a prefix kernel that keeps the greedy)
+__global__ void __launch_bounds__(512, 1) k_prod_512late(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n + 4; i += blockDim.x) stage[i] = i < n ? sw[i] : 0.0;
+  if (lane < (threadIdx.x % 7)) stage[n + 3] = 0.0;  // lane-divergent store
+  __syncthreads();
+  if (warp != 0) return;
   const long long t0 = clock64();
   greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
                                  a.violations);
@@ -125,15 +214,15 @@ int main(int argc, char** argv) {
     a.pick = pick;
     a.violations = viol;
     a.trace = nullptr;
-    auto run = [&](auto kern, const char* name) {
+    auto run = [&](auto kern, const char* name, int threads = 32) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (n + 4) * 8);
       long long c = 0;
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
-      for (int r = 0; r < 3; ++r) kern<<<1, 32, (n + 4) * 8>>>(a, dw, n, dc);
+      for (int r = 0; r < 3; ++r) kern<<<1, threads, (n + 4) * 8>>>(a, dw, n, dc);
       cudaEventRecord(e0);
-      kern<<<1, 32, (n + 4) * 8>>>(a, dw, n, dc);
+      kern<<<1, threads, (n + 4) * 8>>>(a, dw, n, dc);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0.f;
@@ -145,6 +234,14 @@ int main(int argc, char** argv) {
     run(k_prod, "prod");
     run(k_prod_regs, "prod-regs");
     run(k_prod_pad, "prod-padded");
+    run(k_prod_cap<16>, "cap-128reg");
+    run(k_prod_cap<32>, "cap-64reg");
+    run(k_prod_512, "cta-512", 512);
+    run(k_prod_512sync<false>, "512-sync", 512);
+    run(k_prod_512sync<true>, "512-strided", 512);
+    run(k_prod_512w0<0>, "512-w0-bar", 512);
+    run(k_prod_512w0<1>, "512-w0-sleep", 512);
+    run(k_prod_512late, "512-late-exit", 512);
   }
   return 0;
 }
