@@ -1412,14 +1412,11 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
     return;
   }
   if (p->last_path == 3) {
-    // hybrid: prefix (phases 0-2; clears status and violations) -> 32-thread
-    // greedy kernel -> suffix (phases 3-6); the duplicate-id check runs on the
-    // side stream beside the greedy kernel.  (Measured slower: forking the
-    // check before the prefix behind a status memset, 256 sequences 42 vs 37
-    // us, and programmatic dependent launch of the last two kernels.)
-    if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
-    k_plan_small<1><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
-    SB_CHECK_LAUNCH();
+    // hybrid: the duplicate-id check forked on the side stream first (it
+    // reads only the inputs and reports through its own word), the prefix
+    // (phases 0-2, then -- one replica -- the greedy on warp 0 once the other
+    // warps have exited; several replicas: the 32-thread greedy kernel), the
+    // suffix (phases 3-6) after the join.
     {
       const int dsmem = (int)(sizeof(uint64_t) * 2 * small_pow2((int)p->max_seqs));
       static int dset = 0;
@@ -1433,24 +1430,31 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaEventRecord(p->join_ev, p->side));
     }
-    const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 6) +
-                           sizeof(int32_t) * std::max<int64_t>(1, p->max_seqs));
-    static int set_to[2] = {0, 0};
-    const bool wide = p->M > 32;
-    if (smem > set_to[wide]) {
-      if (wide) SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      else SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      set_to[wide] = smem;
-    }
-    if (wide) k_greedy_staged<2, true><<<p->R, 32, smem, s>>>(a);
-    else k_greedy_staged<1, true><<<p->R, 32, smem, s>>>(a);
+    if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
+    k_plan_small<1><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
     SB_CHECK_LAUNCH();
+    if (p->R > 1) {  // several replicas: the 32-thread greedy kernel, one CTA per replica
+      const int smem = (int)(sizeof(double) * (std::max<int64_t>(1, p->max_seqs) + 6) +
+                             sizeof(int32_t) * std::max<int64_t>(1, p->max_seqs));
+      static int set_to[2] = {0, 0};
+      const bool wide = p->M > 32;
+      if (smem > set_to[wide]) {
+        if (wide)
+          SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        else
+          SB_CUDA(cudaFuncSetAttribute(k_greedy_staged<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        set_to[wide] = smem;
+      }
+      if (wide) k_greedy_staged<2, true><<<p->R, 32, smem, s>>>(a);
+      else k_greedy_staged<1, true><<<p->R, 32, smem, s>>>(a);
+      SB_CHECK_LAUNCH();
+    }
     SB_CUDA(cudaStreamWaitEvent(s, p->join_ev, 0));  // duplicate check joined
     k_plan_small<2><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
     SB_CHECK_LAUNCH();
     if (p->timing)
       for (int i = 1; i < 6; ++i) SB_CUDA(cudaEventRecord(p->ev[i], s));
-    count_launch(4);
+    count_launch(p->R > 1 ? 4 : 3);
     return;
   }
   plan_common_prologue(p, s);

@@ -551,9 +551,48 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       }
       __syncthreads();
     }
-    if constexpr (MODE == 1) {  // hand the greedy-order workloads to the greedy kernel
+    if constexpr (MODE == 1) {
+      // one replica: the greedy on warp 0 after every other warp has exited:
+      // only then does ptxas prove the warp converged and schedule the
+      // speculative FP64 work across the REDUX latencies (~105 cycles per step
+      // instead of ~150 with live warps waiting, tools/micro/greedy_prod.cu)
+      // Several replicas: the greedy-order workloads go to the 32-thread greedy
+      // kernel, one CTA per replica (a replica loop here, with bounds ptxas
+      // cannot prove warp-uniform, would bring the guard back).
       for (int64_t p = tid; p < N; p += blockDim.x) a.sorted_w[p] = s_wsorted[p];
-      SB_PHASE(12);  // trace: prefix end (the hybrid's kernels run on different SMs)
+      SB_PHASE(12);  // trace: phases 0-2 done
+      if (R != 1 || warp != 0) return;
+      const int rep = 0;
+      const int64_t lo = 0;
+      const int n = (int)(s_roff[rep * U + U] - lo);
+      const double* ws = s_wsorted + lo;  // reads up to 3 past the replica's end: unused values
+      int32_t* pk = s_pick + lo;
+      if (M <= 32)
+        greedy_warp<1, 0, false, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, pk,
+                                       nullptr, a.violations);
+      else
+        greedy_warp<2, 0, false, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, pk,
+                                       nullptr, a.violations);
+      // each position's rank inside its bag (match_any pass), picks and ranks out
+      int32_t* cnt = s_bagcnt + rep * M;
+      for (int j = lane; j < M; j += 32) cnt[j] = 0;
+      __syncwarp();
+      const unsigned lt = (1u << lane) - 1u;
+      for (int p0 = 0; p0 < n; p0 += 32) {
+        const int p = p0 + lane;
+        const bool valid = p < n;
+        const int b = valid ? pk[p] : -1;
+        const unsigned peers = __match_any_sync(kFull, b);
+        const int rank_in = __popc(peers & lt);
+        const int base = valid ? cnt[b] : 0;
+        __syncwarp();
+        if (valid && rank_in == 0) cnt[b] = base + __popc(peers);
+        __syncwarp();
+        if (valid) {
+          a.pick[lo + p] = b;
+          a.greedy_q[lo + p] = base + rank_in;
+        }
+      }
       return;
     }
   } else {  // hybrid suffix
@@ -571,6 +610,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       s_q[i] = a.greedy_q[i];
     }
     for (int e = tid; e < R * M; e += blockDim.x) s_bagcnt[e] = a.bag_count[e];
+    if (tid == 0 && !a.w_in && a.sentinel[0]) atomicOr(a.status, ST_DUP_ID);  // k_dup_small's result
     __syncthreads();
   }
   SB_PHASE(3);
@@ -933,7 +973,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_dup_small(PlanArgs a, int cap
   __shared__ unsigned n_empty;
   __shared__ int flag;
   const int64_t N = a.rank_off[a.W];
-  if (N > cap || a.w_in) return;
+  if (N > cap || a.w_in) {
+    if (threadIdx.x == 0) a.sentinel[0] = 0;
+    return;
+  }
   const int tsz = 2 * small_pow2(cap);
   if (threadIdx.x == 0) flag = 0;
   for (int rep = 0; rep < a.R; ++rep) {
@@ -960,7 +1003,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_dup_small(PlanArgs a, int cap
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0 && flag) atomicOr(a.status, ST_DUP_ID);
+  // its own result word (sentinel[0], unused by this path otherwise): the
+  // hybrid runs this kernel beside the prefix, which resets the status word;
+  // the suffix folds it in
+  if (threadIdx.x == 0) a.sentinel[0] = flag;
 }
 
 }  // namespace sb

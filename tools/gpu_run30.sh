@@ -1,2 +1,1 @@
-# greedy register-budget probes (tools/micro/greedy_prod, built here)
-cd tools/micro && ./greedy_prod
+cd tools/micro && timeout 120 ./greedy_prod

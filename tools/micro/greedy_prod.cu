@@ -156,6 +156,35 @@ __global__ void __launch_bounds__(512, 1) k_prod_512late(PlanArgs a, const doubl
   if (lane == 0) *cyc = t1 - t0;
 }
 
+// warps 1.. do other work and exit while warp 0 runs the greedy (the hybrid
+// prefix with the greedy and the duplicate check side by side)
+__global__ void __launch_bounds__(512, 1) k_prod_512work(PlanArgs a, const double* sw, int n, long long* cyc) {
+  extern __shared__ __align__(16) double stage[];
+  __shared__ unsigned long long table[1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n + 4; i += blockDim.x) stage[i] = i < n ? sw[i] : 0.0;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) table[i] = ~0ull;
+  __syncthreads();
+  if (warp != 0) {  // open-addressing inserts (the duplicate check's shape)
+    for (int i = threadIdx.x - 32; i < (n < 512 ? n : 512); i += blockDim.x - 32) {
+      const unsigned long long id = __double_as_longlong(stage[i]);
+      unsigned slot = (unsigned)(id * 0x9E3779B97F4A7C15ull >> 54);
+      for (;;) {
+        const unsigned long long old = atomicCAS(&table[slot], ~0ull, id);
+        if (old == ~0ull || old == id) break;
+        slot = (slot + 1) & 1023u;
+      }
+    }
+    if (threadIdx.x == 32 && table[0] == 12345ull) a.pick[0] = -1;
+    return;
+  }
+  const long long t0 = clock64();
+  greedy_warp<1, 0, false, true>(a, 0, n, *a.total, [&](int p) { return stage[p]; }, [](int) {}, a.pick, nullptr,
+                                 a.violations);
+  const long long t1 = clock64();
+  if (lane == 0) *cyc = t1 - t0;
+}
+
 int main(int argc, char** argv) {
   std::vector<int64_t> lens;
   if (argc > 1) {
@@ -242,6 +271,7 @@ int main(int argc, char** argv) {
     run(k_prod_512w0<0>, "512-w0-bar", 512);
     run(k_prod_512w0<1>, "512-w0-sleep", 512);
     run(k_prod_512late, "512-late-exit", 512);
+    run(k_prod_512work, "512-work-exit", 512);
   }
   return 0;
 }
