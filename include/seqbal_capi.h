@@ -151,8 +151,9 @@ typedef struct sb_plan_host {
 SB_API sb_status sb_plan_download(sb_planner* p, sb_plan_host* out, sb_stream stream);
 
 /* Planner pipeline: 0 = auto (by capacity: the single-CTA fused planner for
- * small batches, the hybrid -- fused prefix, 32-thread greedy kernel, fused
- * suffix -- up to 2048 sequences, else the multi-kernel pipeline), 1 = force
+ * small batches, the hybrid -- fused prefix with the greedy (one replica) or
+ * the 32-thread greedy kernel (several), fused suffix -- for 384-1152
+ * sequences, else the multi-kernel pipeline), 1 = force
  * the fused planner, 2 = force the multi-kernel pipeline, 3 = force the
  * hybrid.  All are bit-exact. */
 SB_API sb_status sb_planner_set_path(sb_planner* p, int path);

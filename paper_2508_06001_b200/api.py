@@ -283,7 +283,7 @@ class Planner:
 
     def set_path(self, path: str):
         """'auto' | 'small' (fused single-CTA planner) | 'large' (multi-kernel) |
-        'hybrid' (fused prefix, 32-thread greedy kernel, fused suffix)."""
+        'hybrid' (fused prefix with the greedy or the 32-thread greedy kernel, fused suffix)."""
         call("sb_planner_set_path", self._h, {"auto": 0, "small": 1, "large": 2, "hybrid": 3}[path])
 
     def last_path(self) -> str:
