@@ -152,7 +152,8 @@ SB_API sb_status sb_plan_download(sb_planner* p, sb_plan_host* out, sb_stream st
 
 /* Planner pipeline: 0 = auto (by capacity: the single-CTA fused planner for
  * small batches, the hybrid -- fused prefix with the greedy (one replica) or
- * the 32-thread greedy kernel (several), fused suffix -- for 384-1152
+ * the 32-thread greedy kernel (several), fused suffix as a programmatic
+ * dependent launch -- for 256-1152
  * sequences, else the multi-kernel pipeline), 1 = force
  * the fused planner, 2 = force the multi-kernel pipeline, 3 = force the
  * hybrid.  All are bit-exact. */

@@ -1265,7 +1265,7 @@ static void plan_common_prologue(sb_planner* p, cudaStream_t s) {
 constexpr int64_t kSmallChunks = 8192;
 
 constexpr int64_t kSmallAutoSeqsOneBag = 640;   // one bag per replica (no greedy chain)
-constexpr int64_t kHybridAutoSeqs = 384;        // hybrid from here (see choose_path) ...
+constexpr int64_t kHybridAutoSeqs = 256;        // hybrid from here (see choose_path) ...
 constexpr int64_t kHybridAutoMaxSeqs = 1152;    // ... up to here, multi-kernel above
 
 // 1 = fused single CTA, 2 = multi-kernel, 3 = hybrid (fused prefix, 32-thread
@@ -1412,24 +1412,11 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
     return;
   }
   if (p->last_path == 3) {
-    // hybrid: the duplicate-id check forked on the side stream first (it
-    // reads only the inputs and reports through its own word), the prefix
-    // (phases 0-2, then -- one replica -- the greedy on warp 0 once the other
-    // warps have exited; several replicas: the 32-thread greedy kernel), the
-    // suffix (phases 3-6) after the join.
-    {
-      const int dsmem = (int)(sizeof(uint64_t) * 2 * small_pow2((int)p->max_seqs));
-      static int dset = 0;
-      if (dsmem > 48 * 1024 && dsmem > dset) {
-        SB_CUDA(cudaFuncSetAttribute(k_dup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, dsmem));
-        dset = dsmem;
-      }
-      SB_CUDA(cudaEventRecord(p->fork_ev, s));
-      SB_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
-      k_dup_small<<<1, kSmallThreads, dsmem, p->side>>>(a, (int)p->max_seqs);
-      SB_CHECK_LAUNCH();
-      SB_CUDA(cudaEventRecord(p->join_ev, p->side));
-    }
+    // hybrid: the prefix (phases 0-2, then -- one replica -- the greedy on
+    // warp 0 once the other warps have exited; several replicas: the 32-thread
+    // greedy kernel), then the suffix (phases 3-6) as a programmatic dependent
+    // launch: its prologue (tables, ids, the duplicate-id check) runs under the
+    // greedy chain and it waits on the grid dependency before the rest.
     if (p->timing) SB_CUDA(cudaEventRecord(p->ev[0], s));
     k_plan_small<1><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
     SB_CHECK_LAUNCH();
@@ -1449,12 +1436,23 @@ static void run_plan(sb_planner* p, cudaStream_t s) {
       else k_greedy_staged<1, true><<<p->R, 32, smem, s>>>(a);
       SB_CHECK_LAUNCH();
     }
-    SB_CUDA(cudaStreamWaitEvent(s, p->join_ev, 0));  // duplicate check joined
-    k_plan_small<2><<<1, kSmallThreads, p->small_smem, s>>>(a, (int)p->max_seqs);
-    SB_CHECK_LAUNCH();
+    {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(1);
+      cfg.blockDim = dim3(kSmallThreads);
+      cfg.dynamicSmemBytes = p->small_smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      SB_CUDA(cudaLaunchKernelEx(&cfg, k_plan_small<2>, a, (int)p->max_seqs));
+      SB_CHECK_LAUNCH();
+    }
     if (p->timing)
       for (int i = 1; i < 6; ++i) SB_CUDA(cudaEventRecord(p->ev[i], s));
-    count_launch(p->R > 1 ? 4 : 3);
+    count_launch(p->R > 1 ? 3 : 2);
     return;
   }
   plan_common_prologue(p, s);

@@ -254,6 +254,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
   int64_t* s_repc = reinterpret_cast<int64_t*>(sm + L.repc);
   int32_t* s_q = reinterpret_cast<int32_t*>(sm + L.q);
 
+  // the hybrid prefix lets its suffix launch at once: the suffix's prologue
+  // reads inputs only and waits on the grid dependency before the rest
+  if constexpr (MODE == 1) asm volatile("griddepcontrol.launch_dependents;");
   if (MODE != 2) SB_PHASE(0);
   // ---- phase 0: rank offsets, topology tables
   for (int r = tid; r <= W; r += blockDim.x) s_roff[r] = a.rank_off[r];
@@ -312,6 +315,39 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
     if (a.w_in) return a.w_in[i];
     const int64_t len = a.lens[i];
     return gamma_weighted_workload(len < 0 ? 0 : len, a.d_model, a.gamma);
+  };
+  // duplicate sample ids inside each replica (divergence):
+  // open-addressing set in the sort scratch (s_hi and s_lo are contiguous,
+  // 2T slots >= 2 * replica size, EMPTY = ~0) on threads [t0 .. t0 + nt) of
+  // this CTA (named barrier 2); sets s_flag, reads s_ids and s_roff only
+  auto dup_check = [&](int t, int nt) {
+    auto bar = [nt]() { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); };
+    for (int rep = 0; rep < R; ++rep) {
+      const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
+      const int tsz = 2 * L.T;
+      for (int i = t; i < tsz; i += nt) s_hi[i] = ~0ull;
+      if (t == 0) s_v[0] = 0;  // count of ids equal to the EMPTY marker
+      bar();
+      for (int64_t i = lo + t; i < hi; i += nt) {
+        const uint64_t id = s_ids[i];
+        if (id == ~0ull) {
+          if (atomicAdd(&s_v[0], 1u) > 0) s_flag = 1;
+          continue;
+        }
+        uint32_t slot = (uint32_t)(hash_slot(id) & (uint64_t)(tsz - 1));
+        for (;;) {
+          const unsigned long long old =
+              atomicCAS(reinterpret_cast<unsigned long long*>(&s_hi[slot]), ~0ull, (unsigned long long)id);
+          if (old == ~0ull) break;
+          if (old == id) {
+            s_flag = 1;
+            break;
+          }
+          slot = (slot + 1) & (uint32_t)(tsz - 1);
+        }
+      }
+      bar();
+    }
   };
   if constexpr (MODE != 2) {  // phases 1-2 (fused, hybrid prefix)
     SB_PHASE(1);
@@ -597,12 +633,21 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
     }
   } else {  // hybrid suffix
     SB_PHASE(11);  // trace: suffix start
-    // ---- MODE 2: reload what phases 0-2 and the greedy kernel left in global memory
+    // ---- MODE 2, launched as a programmatic dependent of the prefix (or of the
+    // greedy kernel): until the grid dependency resolves it touches inputs only
+    // -- phase 0 above, the ids and lengths, and the duplicate-id check, all
+    // under the prefix's greedy chain
     for (int64_t i = tid; i < N; i += blockDim.x) {
       const int64_t len = a.lens[i] < 0 ? 0 : a.lens[i];
       if (len >= (int64_t)1 << 26) s_biglen = 1;
       s_ids[i] = a.ids[i];
       s_lens[i] = len;
+    }
+    __syncthreads();
+    if (!a.w_in) dup_check(tid, (int)blockDim.x);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // then what phases 0-2 and the greedy left in global memory
+    for (int64_t i = tid; i < N; i += blockDim.x) {
       s_rank[i] = a.seq_rank[i];
       s_soff[i] = a.seq_off[i];
       s_sorted[i] = a.sorted_idx[i];
@@ -610,7 +655,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       s_q[i] = a.greedy_q[i];
     }
     for (int e = tid; e < R * M; e += blockDim.x) s_bagcnt[e] = a.bag_count[e];
-    if (tid == 0 && !a.w_in && a.sentinel[0]) atomicOr(a.status, ST_DUP_ID);  // k_dup_small's result
+    if (tid == 0 && s_flag) atomicOr(a.status, ST_DUP_ID);  // after the prefix reset the status word
     __syncthreads();
   }
   SB_PHASE(3);
@@ -659,38 +704,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
     __syncwarp();
     asm volatile("bar.sync 4, 64;" ::: "memory");
     bag_ranks_pass(s_pick, (int)N, qc, s_q);
-  } else if (MODE == 0 && !a.w_in) {  // the hybrid runs k_dup_small beside its greedy kernel
-    // open-addressing set per replica in the sort scratch (free now):
-    // s_hi and s_lo are contiguous, 2T slots >= 2 * replica size, EMPTY = ~0
+  } else if (MODE == 0 && !a.w_in) {  // the hybrid's suffix runs it before its grid dependency
     const int w0 = ng + (qsplit ? 1 : 0);
-    const int t = tid - 32 * w0, nt = (int)blockDim.x - 32 * w0;
-    auto bar = [nt]() { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); };
-    for (int rep = 0; rep < R; ++rep) {
-      const int64_t lo = s_roff[rep * U], hi = s_roff[rep * U + U];
-      const int tsz = 2 * L.T;
-      for (int i = t; i < tsz; i += nt) s_hi[i] = ~0ull;
-      if (t == 0) s_v[0] = 0;  // count of ids equal to the EMPTY marker
-      bar();
-      for (int64_t i = lo + t; i < hi; i += nt) {
-        const uint64_t id = s_ids[i];
-        if (id == ~0ull) {
-          if (atomicAdd(&s_v[0], 1u) > 0) s_flag = 1;
-          continue;
-        }
-        uint32_t slot = (uint32_t)(hash_slot(id) & (uint64_t)(tsz - 1));
-        for (;;) {
-          const unsigned long long old =
-              atomicCAS(reinterpret_cast<unsigned long long*>(&s_hi[slot]), ~0ull, (unsigned long long)id);
-          if (old == ~0ull) break;
-          if (old == id) {
-            s_flag = 1;
-            break;
-          }
-          slot = (slot + 1) & (uint32_t)(tsz - 1);
-        }
-      }
-      bar();
-    }
+    const int t = tid - 32 * w0;
+    dup_check(t, (int)blockDim.x - 32 * w0);
     if (s_flag && t == 0) atomicOr(a.status, ST_DUP_ID);
   }
   __syncthreads();
@@ -963,50 +980,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       fix_rev_ties(a.rev_recv_idx, a.send_idx, a.c_seq, a.c_start, s_sendoff[r], s_sendoff[r + 1] - s_sendoff[r], stk);
     }
   SB_PHASE(13);
-}
-
-// Hybrid path: the duplicate-id check inside each replica (divergence, see
-// DESIGN.md) on a side stream beside the greedy kernel -- the same
-// open-addressing set as phase 3 of k_plan_small, in its own shared memory.
-__global__ void __launch_bounds__(kSmallThreads) k_dup_small(PlanArgs a, int cap) {
-  extern __shared__ __align__(16) unsigned long long tab[];  // 2T slots
-  __shared__ unsigned n_empty;
-  __shared__ int flag;
-  const int64_t N = a.rank_off[a.W];
-  if (N > cap || a.w_in) {
-    if (threadIdx.x == 0) a.sentinel[0] = 0;
-    return;
-  }
-  const int tsz = 2 * small_pow2(cap);
-  if (threadIdx.x == 0) flag = 0;
-  for (int rep = 0; rep < a.R; ++rep) {
-    const int64_t lo = a.rank_off[rep * a.U], hi = a.rank_off[rep * a.U + a.U];
-    for (int i = threadIdx.x; i < tsz; i += blockDim.x) tab[i] = ~0ull;
-    if (threadIdx.x == 0) n_empty = 0;
-    __syncthreads();
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const uint64_t id = a.ids[i];
-      if (id == ~0ull) {
-        if (atomicAdd(&n_empty, 1u) > 0) flag = 1;
-        continue;
-      }
-      uint32_t slot = (uint32_t)(hash_slot(id) & (uint64_t)(tsz - 1));
-      for (;;) {
-        const unsigned long long old = atomicCAS(&tab[slot], ~0ull, (unsigned long long)id);
-        if (old == ~0ull) break;
-        if (old == id) {
-          flag = 1;
-          break;
-        }
-        slot = (slot + 1) & (uint32_t)(tsz - 1);
-      }
-    }
-    __syncthreads();
-  }
-  // its own result word (sentinel[0], unused by this path otherwise): the
-  // hybrid runs this kernel beside the prefix, which resets the status word;
-  // the suffix folds it in
-  if (threadIdx.x == 0) a.sentinel[0] = flag;
 }
 
 }  // namespace sb
