@@ -590,8 +590,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
     if constexpr (MODE == 1) {
       // one replica: the greedy on warp 0 after every other warp has exited:
       // only then does ptxas prove the warp converged and schedule the
-      // speculative FP64 work across the REDUX latencies (~105 cycles per step
-      // instead of ~150 with live warps waiting, tools/micro/greedy_prod.cu)
+      // speculative FP64 work across the REDUX latencies (~107 cycles per step
+      // instead of ~140-150 with live warps waiting, tools/micro/greedy_prod.cu)
       // Several replicas: the greedy-order workloads go to the 32-thread greedy
       // kernel, one CTA per replica (a replica loop here, with bounds ptxas
       // cannot prove warp-uniform, would bring the guard back).
@@ -609,7 +609,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_plan_small(PlanArgs a_in, 
       else
         greedy_warp<2, 0, false, true>(a, rep, n, s_reptot[rep], [ws](int p) { return ws[p]; }, [](int) {}, pk,
                                        nullptr, a.violations);
-      // each position's rank inside its bag (match_any pass), picks and ranks out
+      // each position's rank inside its bag (match_any pass), picks and ranks
+      // out in the same pass (bag_ranks_pass plus a separate pick loop measured
+      // 1-2 us slower per plan)
       int32_t* cnt = s_bagcnt + rep * M;
       for (int j = lane; j < M; j += 32) cnt[j] = 0;
       __syncwarp();
